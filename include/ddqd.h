@@ -1,0 +1,146 @@
+/*
+ * ddqd.h -- C ABI of the B200-native DD/QD GEMM + LU library (libddqd.so).
+ *
+ * Method: arXiv 1510.08642 (Kouya 2015). Citation key: P:n = PAPER.md line n,
+ * S:n = SPEC.md line n, BJ:n = BASELINE.json line n. Numerics: docs/numerics.md.
+ *
+ * Data layout (all matrices): PLANAR row-major float64. A DD r x c matrix is
+ * double[2][r][c] (plane 0 = hi words, plane 1 = lo words); a QD matrix is
+ * double[4][r][c] (words of decreasing magnitude). Plane stride = r*c doubles for
+ * the simple entry points; the *_ex entry points take explicit strides.
+ *
+ * Pointers: DEVICE pointers on the current CUDA device (cudaMalloc / torch CUDA
+ * tensors). The simple GEMM entry points also accept HOST pointers for A, B and C
+ * together (detected with cudaPointerGetAttributes): the library then stages them
+ * through its own device buffers, copies the result back and synchronises the stream
+ * before returning (the end-to-end path bench.py times as "e2e").
+ *
+ * Ownership: the caller owns every buffer passed in; the library never frees caller
+ * memory. The library owns a per-device workspace (grown on demand, freed by
+ * ddqd_release) unless the calling thread installed one with ddqd_set_workspace.
+ *
+ * Synchronisation: device-pointer GEMM calls are asynchronous on the calling
+ * thread's stream (ddqd_set_stream; default = legacy default stream), like cuBLAS;
+ * kernel faults surface at the next synchronisation. dd_lu_solve synchronises once
+ * at the end to read `info`.
+ *
+ * Errors: every entry point returns an int status. 0 = success; negative values are
+ * the DDQD_E* codes below (no C++ exception crosses the ABI); a human-readable
+ * message for the last failure of the calling thread is ddqd_last_error().
+ * Zero sizes are valid no-ops (l = 0 gives C := 0). A threshold >= min(m,l,n)
+ * degenerates to Block.
+ */
+#ifndef DDQD_H
+#define DDQD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Algorithms. */
+enum { DDQD_BLOCK = 0, DDQD_STRASSEN = 1, DDQD_WINOGRAD = 2 };
+
+/* Precisions: number of float64 words per element. */
+enum { DDQD_DD = 2, DDQD_QD = 4 };
+
+/* Status codes. */
+enum {
+    DDQD_OK = 0,
+    DDQD_EINVAL = -1,  /* negative size, bad algo/precision, threshold < 1, bad stride   */
+    DDQD_EALIAS = -2,  /* C overlaps A or B                                              */
+    DDQD_ENOMEM = -3,  /* workspace / staging allocation failed                          */
+    DDQD_ECUDA = -4,   /* a CUDA runtime error (message in ddqd_last_error)              */
+    DDQD_ENOTSUP = -5  /* not supported (e.g. QD LU, host pointers to *_ex)              */
+};
+
+/*
+ * dd_gemm / qd_gemm -- C := A B (Eq. (1)) in DD (~106-bit) / QD (~212-bit).
+ *   m, l, n   : A is m x l, B is l x n, C is m x n (>= 0).
+ *   A, B, C   : planar contiguous [W][rows][cols] (W = 2 for dd_gemm, 4 for qd_gemm).
+ *   algo      : DDQD_BLOCK, DDQD_STRASSEN or DDQD_WINOGRAD (the 7-product
+ *               recursions whose leaves are Block).
+ *   threshold : n_min of P:52 -- a (sub)problem recurses while min(m,l,n) > threshold
+ *               (>= 1; ignored for DDQD_BLOCK). Odd halves are zero padded virtually.
+ * Results are bit-identical to the oracle under docs/numerics.md (k ascending per leaf
+ * element, additions in the written order).
+ */
+int dd_gemm(int64_t m, int64_t l, int64_t n, const double *A, const double *B, double *C,
+            int algo, int64_t threshold);
+int qd_gemm(int64_t m, int64_t l, int64_t n, const double *A, const double *B, double *C,
+            int algo, int64_t threshold);
+
+/* Strided / batched / accumulate form used by the LU and the multi-GPU driver.
+ * Element (b, i, j) word w of X lives at X[b*bs + w*ps + i*ld + j] (device pointers only).
+ * beta = 0: C := A B.  beta = 1: C := C - A B, where A B is first formed from +0 and then
+ * subtracted elementwise (dd_sub / qd_sub) -- the LU Schur update of P:131.
+ * batch >= 1 independent problems of identical shape share one schedule. */
+typedef struct {
+    int prec;             /* DDQD_DD or DDQD_QD */
+    int algo;             /* DDQD_BLOCK / DDQD_STRASSEN / DDQD_WINOGRAD */
+    int64_t threshold;
+    int64_t m, l, n;
+    int64_t batch;
+    const double *A; int64_t lda, psA, bsA;
+    const double *B; int64_t ldb, psB, bsB;
+    double *C;       int64_t ldc, psC, bsC;
+    int beta;             /* 0 or 1 (see above) */
+} ddqd_gemm_desc;
+
+int ddqd_gemm_ex(const ddqd_gemm_desc *desc);
+
+/*
+ * dd_lu_solve -- blocked right-looking LU with partial pivoting (P:121-133 steps 1-3,
+ * pivoting per BJ:11) and the solve of Eq. (2), DD only.
+ *   n         : order (>= 0).
+ *   A         : device [2][n][n], overwritten by P A = L U (unit L below the diagonal, U on
+ *               and above it).
+ *   b         : device [2][n], untouched.       x: device [2][n], the solution.
+ *   ipiv      : device int64[n], ipiv[k] = row swapped with row k at step k (0-based).
+ *   panel     : K of P:127 (>= 1); the last panel is ragged.
+ *   algo, threshold : GEMM used for the trailing update T := L21 U12.
+ * Returns 0, a negative DDQD_E* code, or info > 0: U(info-1, info-1) is exactly zero
+ * (LAPACK convention; x is then not a solution). Synchronises the stream once.
+ */
+int dd_lu_solve(int64_t n, double *A, const double *b, double *x, int64_t *ipiv,
+                int64_t panel, int algo, int64_t threshold);
+
+/* Elementwise arithmetic layer, for parity tests of the device DD/QD ops (device
+ * pointers, planar [W][count]): op 0 add, 1 sub, 2 mul, 3 div (DD only), 4 madd
+ * z = x + y*w. */
+int ddqd_elementwise(int prec, int op, int64_t count, const double *x, const double *y,
+                     const double *w, double *z);
+
+/* Stream used by the calling thread (a cudaStream_t; NULL = legacy default stream). */
+int ddqd_set_stream(void *cuda_stream);
+
+/* Bytes of device workspace a GEMM of this shape uses (0 for Block). */
+size_t ddqd_workspace_bytes(int prec, int64_t m, int64_t l, int64_t n, int algo, int64_t threshold);
+
+/* Caller-owned workspace for the calling thread (NULL/0 to revert to the library's own).
+ * Calls that need more than `bytes` fail with DDQD_ENOMEM. */
+int ddqd_set_workspace(void *dptr, size_t bytes);
+
+/* Upper bound on the library-owned workspace (bytes); the recursion schedule runs its top
+ * levels depth-first when breadth-first batching would exceed it. 0 = default (40% of free
+ * device memory at first use). Numerics do not depend on it. */
+int ddqd_set_workspace_limit(size_t bytes);
+
+/* Number of kernels this thread's library calls have launched so far (evidence counter). */
+int64_t ddqd_launch_count(void);
+
+/* Free library-owned device memory (workspace, staging buffers) of the current device. */
+int ddqd_release(void);
+
+/* Message of the last failure on the calling thread ("" if none). */
+const char *ddqd_last_error(void);
+
+/* ABI version (major*100 + minor). */
+int ddqd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DDQD_H */

@@ -1,0 +1,195 @@
+"""paper_1510_08642_b200 -- B200-native DD/QD GEMM (Block / Strassen / Winograd) and DD LU.
+
+Thin ctypes binding over the C ABI of libddqd.so (include/ddqd.h): argument marshalling
+only -- every step of the path runs in the library's sm_100a kernels. PyTorch supplies
+device memory and the current stream. There is no CPU fallback: importing this package
+fails loudly when libddqd.so is missing, and calls fail when no CUDA device is present.
+
+Layout: planar float64 tensors, shape [2, rows, cols] for DD and [4, rows, cols] for QD
+(word 0 = leading word). Method: arXiv 1510.08642.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = ["dd_gemm", "qd_gemm", "gemm", "gemm_ex", "dd_lu_solve", "elementwise", "lib",
+           "workspace_bytes", "set_workspace_limit", "launch_count", "release",
+           "BLOCK", "STRASSEN", "WINOGRAD", "DDQDError"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libddqd.so")
+
+BLOCK, STRASSEN, WINOGRAD = 0, 1, 2
+_ALGOS = {"block": BLOCK, "strassen": STRASSEN, "winograd": WINOGRAD}
+_CODES = {-1: "EINVAL", -2: "EALIAS", -3: "ENOMEM", -4: "ECUDA", -5: "ENOTSUP"}
+
+
+class DDQDError(RuntimeError):
+    pass
+
+
+class GemmDesc(ctypes.Structure):
+    _fields_ = [("prec", ctypes.c_int), ("algo", ctypes.c_int), ("threshold", ctypes.c_int64),
+                ("m", ctypes.c_int64), ("l", ctypes.c_int64), ("n", ctypes.c_int64),
+                ("batch", ctypes.c_int64),
+                ("A", ctypes.c_void_p), ("lda", ctypes.c_int64), ("psA", ctypes.c_int64), ("bsA", ctypes.c_int64),
+                ("B", ctypes.c_void_p), ("ldb", ctypes.c_int64), ("psB", ctypes.c_int64), ("bsB", ctypes.c_int64),
+                ("C", ctypes.c_void_p), ("ldc", ctypes.c_int64), ("psC", ctypes.c_int64), ("bsC", ctypes.c_int64),
+                ("beta", ctypes.c_int)]
+
+
+def _load():
+    if not os.path.exists(_SO):
+        raise ImportError(
+            "libddqd.so not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(nvcc, sm_100a). There is no CPU fallback.")
+    L = ctypes.CDLL(_SO)
+    i64, vp, i32 = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
+    for f in (L.dd_gemm, L.qd_gemm):
+        f.argtypes = [i64, i64, i64, vp, vp, vp, i32, i64]
+        f.restype = i32
+    L.ddqd_gemm_ex.argtypes = [ctypes.POINTER(GemmDesc)]
+    L.dd_lu_solve.argtypes = [i64, vp, vp, vp, vp, i64, i32, i64]
+    L.ddqd_elementwise.argtypes = [i32, i32, i64, vp, vp, vp, vp]
+    L.ddqd_set_stream.argtypes = [vp]
+    L.ddqd_workspace_bytes.argtypes = [i32, i64, i64, i64, i32, i64]
+    L.ddqd_workspace_bytes.restype = ctypes.c_size_t
+    L.ddqd_set_workspace.argtypes = [vp, ctypes.c_size_t]
+    L.ddqd_set_workspace_limit.argtypes = [ctypes.c_size_t]
+    L.ddqd_launch_count.restype = i64
+    L.ddqd_last_error.restype = ctypes.c_char_p
+    return L
+
+
+lib = _load()
+
+EXPORTED = ["dd_gemm", "qd_gemm", "ddqd_gemm_ex", "dd_lu_solve", "ddqd_elementwise", "ddqd_set_stream",
+            "ddqd_workspace_bytes", "ddqd_set_workspace", "ddqd_set_workspace_limit",
+            "ddqd_launch_count", "ddqd_release", "ddqd_last_error", "ddqd_version"]
+
+
+def _check(rc: int, what: str) -> int:
+    if rc < 0:
+        msg = lib.ddqd_last_error().decode(errors="replace")
+        if rc == -1:
+            raise ValueError(f"{what}: {msg}")
+        raise DDQDError(f"{what}: {_CODES.get(rc, rc)}: {msg}")
+    return rc
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _set_stream(t):
+    torch = _torch()
+    if t.is_cuda:
+        lib.ddqd_set_stream(ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream))
+
+
+def _algo(a) -> int:
+    return _ALGOS[a] if isinstance(a, str) else int(a)
+
+
+def _check_mat(x, W, name):
+    torch = _torch()
+    if not isinstance(x, torch.Tensor) or x.dtype != torch.float64 or x.dim() != 3 or x.shape[0] != W:
+        raise ValueError(f"{name} must be a float64 tensor of shape [{W}, rows, cols]")
+    if not x.is_contiguous():
+        raise ValueError(f"{name} must be contiguous (planar row-major)")
+
+
+def gemm(A, B, algo="block", threshold=128, out=None):
+    """C := A B with A [W,m,l], B [W,l,n] float64 CUDA tensors, W = 2 (DD) or 4 (QD).
+    Pinned/ordinary CPU tensors for A, B and `out` use the library's host-staging path
+    (copies inside the call, synchronous)."""
+    torch = _torch()
+    W = A.shape[0] if A.dim() == 3 else -1
+    _check_mat(A, W, "A")
+    _check_mat(B, W, "B")
+    if W not in (2, 4):
+        raise ValueError("leading dimension must be 2 (DD) or 4 (QD)")
+    m, l = A.shape[1], A.shape[2]
+    if B.shape[1] != l:
+        raise ValueError("dimension mismatch")
+    n = B.shape[2]
+    if out is None:
+        out = torch.empty((W, m, n), dtype=torch.float64, device=A.device,
+                          pin_memory=(not A.is_cuda and A.is_pinned()))
+    _check_mat(out, W, "out")
+    if tuple(out.shape) != (W, m, n):
+        raise ValueError("out has the wrong shape")
+    _set_stream(A)
+    f = lib.dd_gemm if W == 2 else lib.qd_gemm
+    _check(f(m, l, n, A.data_ptr(), B.data_ptr(), out.data_ptr(), _algo(algo), threshold), "gemm")
+    return out
+
+
+def dd_gemm(A, B, algo="block", threshold=128, out=None):
+    if A.shape[0] != 2:
+        raise ValueError("dd_gemm takes [2, rows, cols] tensors")
+    return gemm(A, B, algo, threshold, out)
+
+
+def qd_gemm(A, B, algo="block", threshold=128, out=None):
+    if A.shape[0] != 4:
+        raise ValueError("qd_gemm takes [4, rows, cols] tensors")
+    return gemm(A, B, algo, threshold, out)
+
+
+def gemm_ex(prec, algo, threshold, m, l, n, batch, A, lda, psA, bsA, B, ldb, psB, bsB,
+            C, ldc, psC, bsC, beta=0):
+    """Strided/batched form (ddqd_gemm_ex); A, B, C are device addresses (ints)."""
+    d = GemmDesc(prec, _algo(algo), threshold, m, l, n, batch, A, lda, psA, bsA, B, ldb, psB, bsB,
+                 C, ldc, psC, bsC, beta)
+    return _check(lib.ddqd_gemm_ex(ctypes.byref(d)), "gemm_ex")
+
+
+def dd_lu_solve(A, b, panel=256, algo="strassen", threshold=128, overwrite=False):
+    """Blocked right-looking DD LU with partial pivoting + solve (Eq. 2).
+    A: [2,n,n] CUDA float64, b: [2,n]. Returns (x, LU, ipiv, info)."""
+    torch = _torch()
+    _check_mat(A, 2, "A")
+    n = A.shape[1]
+    if A.shape[2] != n or tuple(b.shape) != (2, n) or b.dtype != torch.float64 or not b.is_contiguous():
+        raise ValueError("A must be [2,n,n] and b [2,n] contiguous float64")
+    LU = A if overwrite else A.clone()
+    x = torch.empty_like(b)
+    ipiv = torch.empty(n, dtype=torch.int64, device=A.device)
+    _set_stream(A)
+    info = _check(lib.dd_lu_solve(n, LU.data_ptr(), b.data_ptr(), x.data_ptr(), ipiv.data_ptr(),
+                                  panel, _algo(algo), threshold), "dd_lu_solve")
+    return x, LU, ipiv, info
+
+
+_OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "madd": 4}
+
+
+def elementwise(op, x, y, w=None):
+    """Device DD/QD arithmetic on planar [W, count] tensors (parity tests of the arithmetic layer)."""
+    torch = _torch()
+    W = x.shape[0]
+    z = torch.empty_like(x)
+    w = w if w is not None else torch.zeros_like(x)
+    _set_stream(x)
+    _check(lib.ddqd_elementwise(W, _OPS[op], x.shape[1], x.data_ptr(), y.data_ptr(), w.data_ptr(),
+                                z.data_ptr()), "elementwise")
+    return z
+
+
+def workspace_bytes(prec, m, l, n, algo, threshold):
+    return lib.ddqd_workspace_bytes(prec, m, l, n, _algo(algo), threshold)
+
+
+def set_workspace_limit(nbytes: int):
+    lib.ddqd_set_workspace_limit(nbytes)
+
+
+def launch_count() -> int:
+    return lib.ddqd_launch_count()
+
+
+def release():
+    lib.ddqd_release()

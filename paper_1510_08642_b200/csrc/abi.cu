@@ -1,0 +1,252 @@
+// abi.cu -- the extern "C" boundary of libddqd.so (include/ddqd.h).
+// Argument checking, per-thread stream / error / workspace state, the library-owned
+// workspace cache, and the host-pointer staging path used for end-to-end timing.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/ddqd.h"
+#include "common.cuh"
+
+namespace ddqd {
+
+static thread_local std::string t_err;
+static thread_local cudaStream_t t_stream = nullptr;
+static thread_local int64_t t_launches = 0;
+static thread_local void *t_user_ws = nullptr;
+static thread_local size_t t_user_ws_bytes = 0;
+
+void set_error(const std::string &msg) { t_err = msg; }
+cudaStream_t cur_stream() { return t_stream; }
+void count_launch(int64_t n) { t_launches += n; }
+
+// Library-owned per-device buffers. Growth frees the old buffer (cudaFree synchronises the
+// device, so no in-flight kernel can still be using it).
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+static std::mutex g_mu;
+static DevBuf g_ws[64], g_aux[64], g_stage[64];
+static size_t g_limit = 0;
+
+static int cur_dev() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
+static void *buf_get(DevBuf *arr, size_t bytes, int *status, const char *what) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevBuf &b = arr[cur_dev() & 63];
+    if (b.bytes < bytes) {
+        if (b.p) cudaFree(b.p);
+        b.p = nullptr;
+        b.bytes = 0;
+        if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            b.p = nullptr;
+            set_error(std::string("cannot allocate ") + std::to_string(bytes) + " bytes of " + what);
+            *status = DDQD_ENOMEM;
+            return nullptr;
+        }
+        b.bytes = bytes;
+    }
+    *status = DDQD_OK;
+    return b.p;
+}
+
+void *workspace_get(size_t bytes, int *status) {
+    if (bytes == 0) { *status = DDQD_OK; return nullptr; }
+    if (t_user_ws) {
+        if (bytes > t_user_ws_bytes) {
+            set_error("caller workspace too small: need " + std::to_string(bytes) + " bytes");
+            *status = DDQD_ENOMEM;
+            return nullptr;
+        }
+        *status = DDQD_OK;
+        return t_user_ws;
+    }
+    return buf_get(g_ws, bytes, status, "GEMM workspace");
+}
+
+void *aux_get(size_t bytes, int *status) { return buf_get(g_aux, bytes, status, "LU auxiliary"); }
+
+size_t workspace_limit() {
+    if (t_user_ws) return t_user_ws_bytes;
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_limit == 0) {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+            cudaGetLastError();
+            fr = size_t(8) << 30;
+        }
+        g_limit = (size_t)(0.4 * (double)(fr + g_ws[cur_dev() & 63].bytes));
+    }
+    return g_limit;
+}
+
+int lu_solve_impl(int64_t n, double *A, const double *b, double *x, int64_t *ipiv, int64_t K,
+                  int algo, int64_t T, cudaStream_t s, int *info_out);
+
+static bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
+    const char *pa = static_cast<const char *>(a), *pb = static_cast<const char *>(b);
+    return na && nb && pa < pb + nb && pb < pa + na;
+}
+
+// 0 = device, 1 = host, -1 = error/mixed
+static int where(const void *p) {
+    if (!p) return 0;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return 1;
+    }
+    if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return 0;
+    return 1;
+}
+
+static int check_gemm_args(int64_t m, int64_t l, int64_t n, int algo, int64_t T) {
+    if (m < 0 || l < 0 || n < 0) { set_error("negative dimension"); return DDQD_EINVAL; }
+    if (algo < 0 || algo > 2) { set_error("algo must be DDQD_BLOCK, DDQD_STRASSEN or DDQD_WINOGRAD"); return DDQD_EINVAL; }
+    if (algo != 0 && T < 1) { set_error("threshold must be >= 1"); return DDQD_EINVAL; }
+    const double elems = (double)m * (double)l + (double)l * (double)n + (double)m * (double)n;
+    if (elems * 4.0 > 9.0e18) { set_error("size overflow"); return DDQD_EINVAL; }
+    return DDQD_OK;
+}
+
+static int gemm_simple(int W, int64_t m, int64_t l, int64_t n, const double *A, const double *B,
+                       double *C, int algo, int64_t T) {
+    t_err.clear();
+    int rc = check_gemm_args(m, l, n, algo, T);
+    if (rc) return rc;
+    const size_t bA = sizeof(double) * W * (size_t)m * l, bB = sizeof(double) * W * (size_t)l * n,
+                 bC = sizeof(double) * W * (size_t)m * n;
+    if (overlaps(A, bA, C, bC) || overlaps(B, bB, C, bC)) { set_error("C overlaps A or B"); return DDQD_EALIAS; }
+    if (m == 0 || n == 0) return DDQD_OK;
+    if ((l > 0 && (!A || !B)) || !C) { set_error("null pointer"); return DDQD_EINVAL; }
+    const int wa = where(A), wb = where(B), wc = where(C);
+    cudaStream_t s = t_stream;
+    if (wa == 0 && wb == 0 && wc == 0) {
+        MatDesc dA{const_cast<double *>(A), m, l, l, m * l, 0};
+        MatDesc dB{const_cast<double *>(B), l, n, n, l * n, 0};
+        MatDesc dC{C, m, n, n, m * n, 0};
+        return run_gemm(W, algo, T, m, l, n, 1, dA, dB, dC, 0, s);
+    }
+    if (!(wa == 1 && wb == 1 && wc == 1)) { set_error("A, B, C must be all device or all host pointers"); return DDQD_EINVAL; }
+    // host path: stage through library-owned device memory, copy back, synchronise
+    int st = DDQD_OK;
+    char *dev = static_cast<char *>(buf_get(g_stage, bA + bB + bC + 512, &st, "staging buffers"));
+    if (st) return st;
+    double *dA = reinterpret_cast<double *>(dev);
+    double *dB = reinterpret_cast<double *>(dev + ((bA + 255) & ~size_t(255)));
+    double *dC = reinterpret_cast<double *>(dev + ((bA + 255) & ~size_t(255)) + ((bB + 255) & ~size_t(255)));
+    if (bA) DDQD_CUDA_CHECK(cudaMemcpyAsync(dA, A, bA, cudaMemcpyHostToDevice, s));
+    if (bB) DDQD_CUDA_CHECK(cudaMemcpyAsync(dB, B, bB, cudaMemcpyHostToDevice, s));
+    MatDesc mA{dA, m, l, l, m * l, 0}, mB{dB, l, n, n, l * n, 0}, mC{dC, m, n, n, m * n, 0};
+    rc = run_gemm(W, algo, T, m, l, n, 1, mA, mB, mC, 0, s);
+    if (rc) return rc;
+    DDQD_CUDA_CHECK(cudaMemcpyAsync(C, dC, bC, cudaMemcpyDeviceToHost, s));
+    DDQD_CUDA_CHECK(cudaStreamSynchronize(s));
+    return DDQD_OK;
+}
+
+}  // namespace ddqd
+
+using namespace ddqd;
+
+extern "C" {
+
+int dd_gemm(int64_t m, int64_t l, int64_t n, const double *A, const double *B, double *C, int algo,
+            int64_t threshold) {
+    return gemm_simple(2, m, l, n, A, B, C, algo, threshold);
+}
+
+int qd_gemm(int64_t m, int64_t l, int64_t n, const double *A, const double *B, double *C, int algo,
+            int64_t threshold) {
+    return gemm_simple(4, m, l, n, A, B, C, algo, threshold);
+}
+
+int ddqd_gemm_ex(const ddqd_gemm_desc *d) {
+    t_err.clear();
+    if (!d) { set_error("null descriptor"); return DDQD_EINVAL; }
+    if (d->prec != 2 && d->prec != 4) { set_error("prec must be DDQD_DD or DDQD_QD"); return DDQD_EINVAL; }
+    int rc = check_gemm_args(d->m, d->l, d->n, d->algo, d->threshold);
+    if (rc) return rc;
+    if (d->batch < 0 || (d->beta != 0 && d->beta != 1)) { set_error("bad batch or beta"); return DDQD_EINVAL; }
+    if (d->lda < d->l || d->ldb < d->n || d->ldc < d->n) { set_error("leading dimension too small"); return DDQD_EINVAL; }
+    if (d->m == 0 || d->n == 0 || d->batch == 0) return DDQD_OK;
+    if (where(d->A) || where(d->B) || where(d->C)) { set_error("ddqd_gemm_ex takes device pointers only"); return DDQD_ENOTSUP; }
+    MatDesc A{const_cast<double *>(d->A), d->m, d->l, d->lda, d->psA, d->bsA};
+    MatDesc B{const_cast<double *>(d->B), d->l, d->n, d->ldb, d->psB, d->bsB};
+    MatDesc C{d->C, d->m, d->n, d->ldc, d->psC, d->bsC};
+    return run_gemm(d->prec, d->algo, d->threshold, d->m, d->l, d->n, d->batch, A, B, C, d->beta, t_stream);
+}
+
+int dd_lu_solve(int64_t n, double *A, const double *b, double *x, int64_t *ipiv, int64_t panel, int algo,
+                int64_t threshold) {
+    t_err.clear();
+    if (n < 0 || panel < 1) { set_error("n must be >= 0 and panel >= 1"); return DDQD_EINVAL; }
+    int rc = check_gemm_args(n, panel, n, algo, threshold);
+    if (rc) return rc;
+    if (n == 0) return DDQD_OK;
+    if (!A || !b || !x || !ipiv) { set_error("null pointer"); return DDQD_EINVAL; }
+    if (where(A) || where(b) || where(x) || where(ipiv)) { set_error("dd_lu_solve takes device pointers only"); return DDQD_ENOTSUP; }
+    int info = 0;
+    rc = lu_solve_impl(n, A, b, x, ipiv, panel, algo, threshold, t_stream, &info);
+    if (rc) return rc;
+    return info;
+}
+
+int ddqd_elementwise(int prec, int op, int64_t count, const double *x, const double *y, const double *w,
+                     double *z) {
+    t_err.clear();
+    if ((prec != 2 && prec != 4) || op < 0 || op > 4 || (prec == 4 && op == 3) || count < 0) {
+        set_error("bad elementwise arguments");
+        return DDQD_EINVAL;
+    }
+    return launch_elementwise(prec, op, count, x, y, w, z, t_stream);
+}
+
+int ddqd_set_stream(void *s) {
+    t_stream = static_cast<cudaStream_t>(s);
+    return DDQD_OK;
+}
+
+size_t ddqd_workspace_bytes(int prec, int64_t m, int64_t l, int64_t n, int algo, int64_t threshold) {
+    if ((prec != 2 && prec != 4) || check_gemm_args(m, l, n, algo, threshold)) return 0;
+    return gemm_workspace_bytes(prec, algo, threshold, m, l, n, 1, workspace_limit(), nullptr);
+}
+
+int ddqd_set_workspace(void *dptr, size_t bytes) {
+    t_user_ws = bytes ? dptr : nullptr;
+    t_user_ws_bytes = dptr ? bytes : 0;
+    return DDQD_OK;
+}
+
+int ddqd_set_workspace_limit(size_t bytes) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_limit = bytes;
+    return DDQD_OK;
+}
+
+int64_t ddqd_launch_count(void) { return t_launches; }
+
+int ddqd_release(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int d = cur_dev() & 63;
+    for (DevBuf *arr : {g_ws, g_aux, g_stage}) {
+        if (arr[d].p) cudaFree(arr[d].p);
+        arr[d].p = nullptr;
+        arr[d].bytes = 0;
+    }
+    return DDQD_OK;
+}
+
+const char *ddqd_last_error(void) { return t_err.c_str(); }
+
+int ddqd_version(void) { return 100; }
+
+}  // extern "C"

@@ -1,0 +1,194 @@
+// addsub.cu -- fused Strassen/Winograd pre- and post-addition kernels (SURVEY.md N7/N8,
+// north_star subsystem (3); formulas S:239 / S:248 as fixed in docs/numerics.md s.4).
+//
+// Both are HBM-bound elementwise DD/QD kernels over a batch of P problems of one level:
+//   pre-add : parent X[b] (rows x cols) -> 7 children Y[7b+c] (ceil(rows/2) x ceil(cols/2)),
+//             reading the four quadrants once (virtual zero padding at odd edges) and
+//             writing the 7 operands of one side (A or B) in one pass;
+//   post-add: 7 children products M[7b+c] (hm x hn) -> parent C[b] quadrants, cropping,
+//             optionally subtracting from C (beta = 1, the LU update).
+// One thread per quadrant position; all additions are dd_add/dd_sub (qd_add/qd_sub) in the
+// written left-to-right order, so results are bit-identical to the oracle's explicit-copy
+// recursion. Per element: pre-add reads 4 and writes 7 W-word values; post-add reads 7 and
+// writes 4 (8 with beta = 1).
+#include "common.cuh"
+#include "ddqd_arith.cuh"
+
+namespace ddqd {
+
+template <int W>
+__device__ __forceinline__ typename elem<W>::T ld_or_zero(const double *base, int64_t ps, bool ok) {
+    return ok ? elem<W>::load(base, ps) : elem<W>::zero();
+}
+
+// side 0 = A operands, side 1 = B operands; algo 1 = Strassen, 2 = Winograd
+template <int W, int ALGO, int SIDE>
+__global__ void __launch_bounds__(256) pre_add_kernel(int64_t P, MatDesc X, MatDesc Y) {
+    using E = elem<W>;
+    using T = typename E::T;
+    const int64_t hr = Y.rows, hc = Y.cols;
+    const int64_t per = hr * hc;
+    const int64_t total = P * per;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = t / per, rem = t % per, i = rem / hc, j = rem % hc;
+        const double *xb = X.p + b * X.bs;
+        const bool r2 = i + hr < X.rows, c2 = j + hc < X.cols;
+        const T x11 = E::load(xb + i * X.ld + j, X.ps);
+        const T x12 = ld_or_zero<W>(xb + i * X.ld + (j + hc), X.ps, c2);
+        const T x21 = ld_or_zero<W>(xb + (i + hr) * X.ld + j, X.ps, r2);
+        const T x22 = ld_or_zero<W>(xb + (i + hr) * X.ld + (j + hc), X.ps, r2 && c2);
+        T o[7];
+        if constexpr (ALGO == 1 && SIDE == 0) {        // Strassen, A side
+            o[0] = E::add(x11, x22);                    // P1: A11+A22
+            o[1] = E::add(x21, x22);                    // P2: A21+A22
+            o[2] = x11;                                 // P3: A11
+            o[3] = x22;                                 // P4: A22
+            o[4] = E::add(x11, x12);                    // P5: A11+A12
+            o[5] = E::sub(x21, x11);                    // P6: A21-A11
+            o[6] = E::sub(x12, x22);                    // P7: A12-A22
+        } else if constexpr (ALGO == 1 && SIDE == 1) { // Strassen, B side
+            o[0] = E::add(x11, x22);                    // P1: B11+B22
+            o[1] = x11;                                 // P2: B11
+            o[2] = E::sub(x12, x22);                    // P3: B12-B22
+            o[3] = E::sub(x21, x11);                    // P4: B21-B11
+            o[4] = x22;                                 // P5: B22
+            o[5] = E::add(x11, x12);                    // P6: B11+B12
+            o[6] = E::add(x21, x22);                    // P7: B21+B22
+        } else if constexpr (ALGO == 2 && SIDE == 0) { // Winograd, A side
+            const T s1 = E::add(x21, x22);
+            const T s2 = E::sub(s1, x11);
+            const T s3 = E::sub(x11, x21);
+            const T s4 = E::sub(x12, s2);
+            o[0] = x11; o[1] = x12; o[2] = s4; o[3] = x22; o[4] = s1; o[5] = s2; o[6] = s3;
+        } else {                                        // Winograd, B side
+            const T t1 = E::sub(x12, x11);
+            const T t2 = E::sub(x22, t1);
+            const T t3 = E::sub(x22, x12);
+            const T t4 = E::sub(t2, x21);
+            o[0] = x11; o[1] = x21; o[2] = x22; o[3] = t4; o[4] = t1; o[5] = t2; o[6] = t3;
+        }
+#pragma unroll
+        for (int c = 0; c < 7; c++) E::store(Y.p + (7 * b + c) * Y.bs + i * Y.ld + j, Y.ps, o[c]);
+    }
+}
+
+template <int W, int ALGO>
+__global__ void __launch_bounds__(256) post_add_kernel(int64_t P, MatDesc M, MatDesc C, int beta) {
+    using E = elem<W>;
+    using T = typename E::T;
+    const int64_t hm = M.rows, hn = M.cols;
+    const int64_t per = hm * hn;
+    const int64_t total = P * per;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = t / per, rem = t % per, i = rem / hn, j = rem % hn;
+        T p[7];
+#pragma unroll
+        for (int c = 0; c < 7; c++) p[c] = E::load(M.p + (7 * b + c) * M.bs + i * M.ld + j, M.ps);
+        T c11, c12, c21, c22;
+        if constexpr (ALGO == 1) {
+            c11 = E::add(E::sub(E::add(p[0], p[3]), p[4]), p[6]);   // ((P1+P4)-P5)+P7
+            c12 = E::add(p[2], p[4]);                                // P3+P5
+            c21 = E::add(p[1], p[3]);                                // P2+P4
+            c22 = E::add(E::add(E::sub(p[0], p[1]), p[2]), p[5]);   // ((P1-P2)+P3)+P6
+        } else {
+            const T u2 = E::add(p[0], p[5]);      // U2 = M1+M6
+            const T u3 = E::add(u2, p[6]);        // U3 = U2+M7
+            const T u4 = E::add(u2, p[4]);        // U4 = U2+M5
+            c11 = E::add(p[0], p[1]);             // U1 = M1+M2
+            c12 = E::add(u4, p[2]);               // U5 = U4+M3
+            c21 = E::sub(u3, p[3]);               // U6 = U3-M4
+            c22 = E::add(u3, p[4]);               // U7 = U3+M5
+        }
+        double *cb = C.p + b * C.bs;
+        const bool r2 = i + hm < C.rows, cc2 = j + hn < C.cols;
+        auto put = [&](int64_t r, int64_t c, const T &v) {
+            double *q = cb + r * C.ld + c;
+            if (beta) E::store(q, C.ps, E::sub(E::load(q, C.ps), v));
+            else E::store(q, C.ps, v);
+        };
+        if (i < C.rows && j < C.cols) put(i, j, c11);
+        if (i < C.rows && cc2) put(i, j + hn, c12);
+        if (r2 && j < C.cols) put(i + hm, j, c21);
+        if (r2 && cc2) put(i + hm, j + hn, c22);
+    }
+}
+
+static unsigned grid_for(int64_t total) {
+    int64_t blocks = (total + 255) / 256;
+    const int64_t cap = 148 * 16;   // grid-stride beyond 16 CTAs per SM
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    return (unsigned)blocks;
+}
+
+template <int W>
+static int pre_dispatch(int algo, int side, int64_t P, const MatDesc &X, const MatDesc &Y, cudaStream_t s) {
+    const int64_t total = P * Y.rows * Y.cols;
+    if (total == 0) return DDQD_OK;
+    const unsigned g = grid_for(total);
+    if (algo == 1 && side == 0) pre_add_kernel<W, 1, 0><<<g, 256, 0, s>>>(P, X, Y);
+    else if (algo == 1) pre_add_kernel<W, 1, 1><<<g, 256, 0, s>>>(P, X, Y);
+    else if (side == 0) pre_add_kernel<W, 2, 0><<<g, 256, 0, s>>>(P, X, Y);
+    else pre_add_kernel<W, 2, 1><<<g, 256, 0, s>>>(P, X, Y);
+    DDQD_LAUNCH_CHECK();
+    return DDQD_OK;
+}
+
+int launch_pre_add(int W, int algo, int side, int64_t P, const MatDesc &X, const MatDesc &Y,
+                   cudaStream_t s) {
+    if (W == 2) return pre_dispatch<2>(algo, side, P, X, Y, s);
+    return pre_dispatch<4>(algo, side, P, X, Y, s);
+}
+
+template <int W>
+static int post_dispatch(int algo, int64_t P, const MatDesc &M, const MatDesc &C, int beta, cudaStream_t s) {
+    const int64_t total = P * M.rows * M.cols;
+    if (total == 0) return DDQD_OK;
+    const unsigned g = grid_for(total);
+    if (algo == 1) post_add_kernel<W, 1><<<g, 256, 0, s>>>(P, M, C, beta);
+    else post_add_kernel<W, 2><<<g, 256, 0, s>>>(P, M, C, beta);
+    DDQD_LAUNCH_CHECK();
+    return DDQD_OK;
+}
+
+int launch_post_add(int W, int algo, int64_t P, const MatDesc &M, const MatDesc &C, int beta,
+                    cudaStream_t s) {
+    if (W == 2) return post_dispatch<2>(algo, P, M, C, beta, s);
+    return post_dispatch<4>(algo, P, M, C, beta, s);
+}
+
+// ---- elementwise arithmetic layer (parity tests of ddqd_arith.cuh) ---------------------
+template <int W>
+__global__ void elementwise_kernel(int op, int64_t count, const double *x, const double *y,
+                                   const double *w, double *z) {
+    using E = elem<W>;
+    using T = typename E::T;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const T a = E::load(x + i, count), b = E::load(y + i, count);
+        T r;
+        if (op == 0) r = E::add(a, b);
+        else if (op == 1) r = E::sub(a, b);
+        else if (op == 4) r = E::madd(a, b, E::load(w + i, count));
+        else if constexpr (W == 2) {
+            r = (op == 2) ? dd_mul(a, b) : dd_div(a, b);
+        } else {
+            r = qd_mul(a, b);
+        }
+        E::store(z + i, count, r);
+    }
+}
+
+int launch_elementwise(int W, int op, int64_t count, const double *x, const double *y,
+                       const double *w, double *z, cudaStream_t s) {
+    if (count == 0) return DDQD_OK;
+    const unsigned g = grid_for(count);
+    if (W == 2) elementwise_kernel<2><<<g, 256, 0, s>>>(op, count, x, y, w, z);
+    else elementwise_kernel<4><<<g, 256, 0, s>>>(op, count, x, y, w, z);
+    DDQD_LAUNCH_CHECK();
+    return DDQD_OK;
+}
+
+}  // namespace ddqd

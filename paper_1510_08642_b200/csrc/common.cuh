@@ -1,0 +1,62 @@
+// common.cuh -- shared host/device plumbing of libddqd (descriptors, status, launch count).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+
+#include "../../include/ddqd.h"
+
+namespace ddqd {
+
+// A batch of planar row-major W-word matrices: element (b,i,j) word w at
+// p[b*bs + w*ps + i*ld + j]. rows/cols are the LOGICAL extent; reads outside it are
+// exact zeros (virtual padding of numerics.md s.4), writes outside it are dropped.
+struct MatDesc {
+    double *p;
+    int64_t rows, cols, ld, ps, bs;
+};
+
+
+// thread-local error message + stream + launch counter (abi.cu)
+void set_error(const std::string &msg);
+cudaStream_t cur_stream();
+void count_launch(int64_t n = 1);
+
+#define DDQD_CUDA_CHECK(expr)                                                            \
+    do {                                                                                 \
+        cudaError_t e__ = (expr);                                                        \
+        if (e__ != cudaSuccess) {                                                        \
+            ::ddqd::set_error(std::string(#expr) + ": " + cudaGetErrorString(e__));      \
+            return DDQD_ECUDA;                                                        \
+        }                                                                                \
+    } while (0)
+
+#define DDQD_LAUNCH_CHECK()                                                              \
+    do {                                                                                 \
+        ::ddqd::count_launch();                                                          \
+        cudaError_t e__ = cudaGetLastError();                                            \
+        if (e__ != cudaSuccess) {                                                        \
+            ::ddqd::set_error(std::string("kernel launch: ") + cudaGetErrorString(e__)); \
+            return DDQD_ECUDA;                                                        \
+        }                                                                                \
+    } while (0)
+
+// Leaf GEMM (leaf_gemm.cu): C[b] (=|-=) A[b] B[b] for b < batch; beta 0: store, 1: C := C - AB.
+int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
+                     const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s);
+
+// Strassen/Winograd pre/post additions (addsub.cu).
+int launch_pre_add(int W, int algo, int side, int64_t P, const MatDesc &X, const MatDesc &Y,
+                   cudaStream_t s);
+int launch_post_add(int W, int algo, int64_t P, const MatDesc &M, const MatDesc &C, int beta,
+                    cudaStream_t s);
+int launch_elementwise(int W, int op, int64_t count, const double *x, const double *y,
+                       const double *w, double *z, cudaStream_t s);
+
+// Recursion planner + executor (recursion.cu).
+size_t gemm_workspace_bytes(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n,
+                            int64_t batch, size_t limit, int *dfs_levels);
+int run_gemm(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n, int64_t batch,
+             const MatDesc &A, const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s);
+
+}  // namespace ddqd

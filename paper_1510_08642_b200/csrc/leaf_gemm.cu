@@ -1,0 +1,217 @@
+// leaf_gemm.cu -- the Block leaf GEMM for DD and QD on sm_100a (SURVEY.md N4/N5,
+// north_star subsystem (2); "Block", Eq. (1)).
+//
+// C[b] := A[b] B[b] (beta = 0) or C[b] := C[b] - A[b] B[b] (beta = 1) for a batch of
+// problems of identical shape (grid.z = problem index: the BFS-batched 7^d Strassen /
+// Winograd leaves run as ONE launch).
+//
+// Per CTA: a BM x BN tile of C; per thread: a TM x TN register micro-tile of DD/QD
+// accumulators. Each element is accumulated from +0 over k ascending (numerics.md s.4),
+// so the result is bit-identical to the oracle's Simple/Block. The k loop streams
+// BK-deep slabs of A (stored k-major, i.e. transposed, so a thread's TM rows are one
+// 16-byte shared load per pair) and B through a STAGES-deep cp.async ring with zero-fill
+// for the ragged edges; the FP64 pipe does DADD/DMUL/DFMA only (20 per DD madd, ~200 per
+// QD madd). Shared-memory traffic per madd is 1/TM + 1/TN words per operand (tiny next to
+// the 20-200 FP64 instructions), so the kernel is FP64-pipe bound by design.
+#include "common.cuh"
+#include "ddqd_arith.cuh"
+
+namespace ddqd {
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, bool pred) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    int sz = pred ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int W, int BM, int BN, int BK, int TM, int TN, int STAGES>
+struct LeafCfg {
+    static constexpr int TX = BN / TN;          // threads along n
+    static constexpr int TY = BM / TM;          // threads along m
+    static constexpr int NT = TX * TY;
+    static constexpr int LDA_S = BM + 2;        // k-major A slab row (even: 16B-aligned pairs)
+    static constexpr int LDB_S = BN;            // k-major B slab row (natural layout)
+    static constexpr int A_STAGE = W * BK * LDA_S;
+    static constexpr int B_STAGE = W * BK * LDB_S;
+    static constexpr size_t SMEM = sizeof(double) * (size_t)STAGES * (A_STAGE + B_STAGE);
+    static_assert(TM % 2 == 0 && TN % 2 == 0, "micro-tile pairs");
+};
+
+// row of micro-tile entry i for thread coordinate t: pairs spread over BM/(TM/2) bands
+template <int BM, int TM>
+__device__ __forceinline__ int micro_idx(int t, int i) {
+    return (i >> 1) * (BM / (TM / 2)) + t * 2 + (i & 1);
+}
+
+template <int W, int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB>
+__global__ void __launch_bounds__(LeafCfg<W, BM, BN, BK, TM, TN, STAGES>::NT, MINB)
+leaf_gemm_kernel(int64_t m, int64_t l, int64_t n, MatDesc A, MatDesc B, MatDesc C, int beta,
+                 int64_t batch0) {
+    using Cfg = LeafCfg<W, BM, BN, BK, TM, TN, STAGES>;
+    using E = elem<W>;
+    using T = typename E::T;
+    constexpr int NT = Cfg::NT;
+    extern __shared__ __align__(16) double smem[];
+    double *As = smem;
+    double *Bs = smem + STAGES * Cfg::A_STAGE;
+
+    const int tid = threadIdx.x;
+    const int tx = tid % Cfg::TX, ty = tid / Cfg::TX;
+    const int64_t b = batch0 + blockIdx.z;
+    const int64_t row0 = (int64_t)blockIdx.y * BM, col0 = (int64_t)blockIdx.x * BN;
+    const double *Ab = A.p + b * A.bs;
+    const double *Bb = B.p + b * B.bs;
+    double *Cb = C.p + b * C.bs;
+
+    T acc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; i++)
+#pragma unroll
+        for (int j = 0; j < TN; j++) acc[i][j] = E::zero();
+
+    const int64_t KT = (l + BK - 1) / BK;
+
+    auto load_stage = [&](int stage, int64_t kt) {
+        const int64_t k0 = kt * BK;
+        double *as = As + stage * Cfg::A_STAGE;
+        double *bs = Bs + stage * Cfg::B_STAGE;
+#pragma unroll 4
+        for (int e = tid; e < W * BM * BK; e += NT) {
+            const int w = e / (BM * BK), rem = e % (BM * BK), r = rem / BK, kk = rem % BK;
+            const int64_t gi = row0 + r, gk = k0 + kk;
+            const bool ok = gi < m && gk < l;
+            const double *src = ok ? Ab + w * A.ps + gi * A.ld + gk : Ab;
+            cp_async8(as + (w * BK + kk) * Cfg::LDA_S + r, src, ok);
+        }
+#pragma unroll 4
+        for (int e = tid; e < W * BK * BN; e += NT) {
+            const int w = e / (BK * BN), rem = e % (BK * BN), kk = rem / BN, c = rem % BN;
+            const int64_t gk = k0 + kk, gj = col0 + c;
+            const bool ok = gk < l && gj < n;
+            const double *src = ok ? Bb + w * B.ps + gk * B.ld + gj : Bb;
+            cp_async8(bs + (w * BK + kk) * Cfg::LDB_S + c, src, ok);
+        }
+    };
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; s++) {
+        if (s < KT) load_stage(s, s);
+        cp_async_commit();
+    }
+
+    for (int64_t kt = 0; kt < KT; kt++) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int64_t nk = kt + STAGES - 1;
+            if (nk < KT) load_stage((int)(nk % STAGES), nk);
+            cp_async_commit();
+        }
+        const int st = (int)(kt % STAGES);
+        const double *as = As + st * Cfg::A_STAGE;
+        const double *bs = Bs + st * Cfg::B_STAGE;
+        const int64_t krem = l - kt * BK;
+        const int kmax = krem < BK ? (int)krem : BK;   // uniform: no madds past l
+        for (int kk = 0; kk < kmax; kk++) {
+            double av[W][TM], bv[W][TN];
+#pragma unroll
+            for (int w = 0; w < W; w++) {
+                const double *arow = as + (w * BK + kk) * Cfg::LDA_S;
+                const double *brow = bs + (w * BK + kk) * Cfg::LDB_S;
+#pragma unroll
+                for (int i = 0; i < TM; i += 2) {
+                    const double2 v = *reinterpret_cast<const double2 *>(arow + micro_idx<BM, TM>(ty, i));
+                    av[w][i] = v.x; av[w][i + 1] = v.y;
+                }
+#pragma unroll
+                for (int j = 0; j < TN; j += 2) {
+                    const double2 v = *reinterpret_cast<const double2 *>(brow + micro_idx<BN, TN>(tx, j));
+                    bv[w][j] = v.x; bv[w][j + 1] = v.y;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < TM; i++) {
+                T a;
+                if constexpr (W == 2) { a.hi = av[0][i]; a.lo = av[1][i]; }
+                else {
+#pragma unroll
+                    for (int w = 0; w < W; w++) a.w[w] = av[w][i];
+                }
+#pragma unroll
+                for (int j = 0; j < TN; j++) {
+                    T bb;
+                    if constexpr (W == 2) { bb.hi = bv[0][j]; bb.lo = bv[1][j]; }
+                    else {
+#pragma unroll
+                        for (int w = 0; w < W; w++) bb.w[w] = bv[w][j];
+                    }
+                    acc[i][j] = E::madd(acc[i][j], a, bb);
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+
+    // epilogue: masked stores (crop of ragged tiles), optional C := C - AB
+#pragma unroll
+    for (int i = 0; i < TM; i++) {
+        const int64_t gi = row0 + micro_idx<BM, TM>(ty, i);
+        if (gi >= m) continue;
+#pragma unroll
+        for (int j = 0; j < TN; j++) {
+            const int64_t gj = col0 + micro_idx<BN, TN>(tx, j);
+            if (gj >= n) continue;
+            double *cp = Cb + gi * C.ld + gj;
+            if (beta) {
+                T old = E::load(cp, C.ps);
+                E::store(cp, C.ps, E::sub(old, acc[i][j]));
+            } else {
+                E::store(cp, C.ps, acc[i][j]);
+            }
+        }
+    }
+}
+
+template <int W, int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB>
+static int launch_cfg(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
+                      const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s) {
+    using Cfg = LeafCfg<W, BM, BN, BK, TM, TN, STAGES>;
+    auto kern = leaf_gemm_kernel<W, BM, BN, BK, TM, TN, STAGES, MINB>;
+    static bool attr_set = false;   // per template instance
+    if (!attr_set) {
+        DDQD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)Cfg::SMEM));
+        attr_set = true;
+    }
+    const int64_t gx = (n + BN - 1) / BN, gy = (m + BM - 1) / BM;
+    if (gx > 0x7fffffff || gy > 65535) {
+        set_error("leaf GEMM: matrix too large for the tile grid");
+        return DDQD_EINVAL;
+    }
+    for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+        const int64_t bz = (batch - b0) < 65535 ? (batch - b0) : 65535;
+        dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)bz);
+        kern<<<grid, Cfg::NT, Cfg::SMEM, s>>>(m, l, n, A, B, C, beta, b0);
+        DDQD_LAUNCH_CHECK();
+    }
+    return DDQD_OK;
+}
+
+int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
+                     const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s) {
+    if (m == 0 || n == 0 || batch == 0) return DDQD_OK;
+    if (W == 2) {
+        const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
+        if (big_tiles >= 2 * 148)
+            return launch_cfg<2, 64, 64, 16, 4, 4, 3, 2>(m, l, n, batch, A, B, C, beta, s);
+        return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2>(m, l, n, batch, A, B, C, beta, s);
+    }
+    if (W == 4) return launch_cfg<4, 32, 32, 16, 2, 2, 3, 1>(m, l, n, batch, A, B, C, beta, s);
+    set_error("leaf GEMM: precision must be 2 (DD) or 4 (QD)");
+    return DDQD_EINVAL;
+}
+
+}  // namespace ddqd

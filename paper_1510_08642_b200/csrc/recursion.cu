@@ -1,0 +1,136 @@
+// recursion.cu -- Strassen/Winograd recursion planner + device-side schedule
+// (north_star subsystem (3)).
+//
+// Planner: depth d from the stop rule min(m,l,n) <= T ("n_min"); per-level shapes
+// halve with ceil (virtual zero padding). Schedule: level j holds a batch of
+// problems of one shape. A batch is processed in chunks of parents: one fused pre-add
+// launch per side writes the 7 children of every parent in the chunk, the children recurse
+// as ONE batch (so the 7^d leaves run as a single batched leaf-GEMM launch instead of the
+// paper's 7 OpenMP sections), and one fused post-add launch combines them. Chunk
+// size = whole batch (breadth-first) below a split level s and 1 parent (depth-first)
+// above it; s is the smallest level whose breadth-first workspace fits the limit. The
+// chunking changes only the launch grouping, never the arithmetic: results are bitwise
+// those of the oracle's recursion.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ddqd {
+
+void *workspace_get(size_t bytes, int *status);   // abi.cu
+size_t workspace_limit();                          // abi.cu
+
+struct Plan {
+    int W = 2, algo = 0, d = 0, s = 0;
+    int64_t T = 1;
+    std::vector<int64_t> m, l, n;       // level shapes, 0..d
+    std::vector<int64_t> chunk;         // parents per chunk at level j (j < d)
+    std::vector<size_t> offA, offB, offM;   // byte offsets of level j+1 buffers (index j+1)
+    size_t bytes = 0;
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static void plan_shapes(Plan &p, int64_t m, int64_t l, int64_t n) {
+    p.m = {m}; p.l = {l}; p.n = {n};
+    if (p.algo == 0) { p.d = 0; return; }
+    int d = 0;
+    while (std::min(std::min(m, l), n) > p.T) {
+        m = (m + 1) / 2; l = (l + 1) / 2; n = (n + 1) / 2;
+        p.m.push_back(m); p.l.push_back(l); p.n.push_back(n);
+        d++;
+    }
+    p.d = d;
+}
+
+// memory of split level s (levels j < s depth-first, j >= s breadth-first)
+static size_t plan_layout(Plan &p, int64_t batch, int s, bool fill) {
+    const int d = p.d;
+    std::vector<int64_t> chunk(d), cnt(d + 1);
+    cnt[0] = batch;
+    for (int j = 0; j < d; j++) {
+        chunk[j] = (j < s) ? 1 : cnt[j];
+        cnt[j + 1] = 7 * chunk[j];
+    }
+    size_t off = 0;
+    std::vector<size_t> oa(d + 1, 0), ob(d + 1, 0), om(d + 1, 0);
+    for (int j = 0; j < d; j++) {
+        const int64_t k = cnt[j + 1];
+        const size_t W = (size_t)p.W;
+        const size_t a = (size_t)k * W * p.m[j + 1] * p.l[j + 1] * sizeof(double);
+        const size_t b = (size_t)k * W * p.l[j + 1] * p.n[j + 1] * sizeof(double);
+        const size_t c = (size_t)k * W * p.m[j + 1] * p.n[j + 1] * sizeof(double);
+        oa[j + 1] = off; off = align256(off + a);
+        ob[j + 1] = off; off = align256(off + b);
+        om[j + 1] = off; off = align256(off + c);
+    }
+    if (fill) {
+        p.s = s; p.chunk = chunk; p.offA = oa; p.offB = ob; p.offM = om; p.bytes = off;
+    }
+    return off;
+}
+
+static int make_plan(Plan &p, int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n,
+                     int64_t batch, size_t limit) {
+    p.W = W; p.algo = algo; p.T = T;
+    plan_shapes(p, m, l, n);
+    if (p.d == 0) { p.bytes = 0; p.s = 0; return DDQD_OK; }
+    for (int s = 0; s <= p.d; s++) {
+        if (plan_layout(p, batch, s, false) <= limit || s == p.d) {
+            plan_layout(p, batch, s, true);
+            return DDQD_OK;
+        }
+    }
+    return DDQD_OK;
+}
+
+size_t gemm_workspace_bytes(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n,
+                            int64_t batch, size_t limit, int *dfs_levels) {
+    Plan p;
+    make_plan(p, W, algo, T, m, l, n, batch, limit);
+    if (dfs_levels) *dfs_levels = p.s;
+    return p.bytes;
+}
+
+static MatDesc child(const Plan &p, char *ws, const std::vector<size_t> &off, int level,
+                     int64_t rows, int64_t cols) {
+    MatDesc d;
+    d.p = reinterpret_cast<double *>(ws + off[level]);
+    d.rows = rows; d.cols = cols; d.ld = cols; d.ps = rows * cols; d.bs = (int64_t)p.W * d.ps;
+    return d;
+}
+
+static MatDesc shift(MatDesc d, int64_t p0) { d.p += p0 * d.bs; return d; }
+
+static int exec_level(const Plan &p, char *ws, int j, int64_t cnt, const MatDesc &A,
+                      const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s) {
+    if (j == p.d) return launch_leaf_gemm(p.W, p.m[j], p.l[j], p.n[j], cnt, A, B, C, beta, s);
+    const MatDesc cA = child(p, ws, p.offA, j + 1, p.m[j + 1], p.l[j + 1]);
+    const MatDesc cB = child(p, ws, p.offB, j + 1, p.l[j + 1], p.n[j + 1]);
+    const MatDesc cM = child(p, ws, p.offM, j + 1, p.m[j + 1], p.n[j + 1]);
+    for (int64_t p0 = 0; p0 < cnt; p0 += p.chunk[j]) {
+        const int64_t pc = std::min<int64_t>(p.chunk[j], cnt - p0);
+        int rc;
+        if ((rc = launch_pre_add(p.W, p.algo, 0, pc, shift(A, p0), cA, s))) return rc;
+        if ((rc = launch_pre_add(p.W, p.algo, 1, pc, shift(B, p0), cB, s))) return rc;
+        if ((rc = exec_level(p, ws, j + 1, 7 * pc, cA, cB, cM, 0, s))) return rc;
+        if ((rc = launch_post_add(p.W, p.algo, pc, cM, shift(C, p0), beta, s))) return rc;
+    }
+    return DDQD_OK;
+}
+
+int run_gemm(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n, int64_t batch,
+             const MatDesc &A, const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s) {
+    if (m == 0 || n == 0 || batch == 0) return DDQD_OK;
+    Plan p;
+    int rc = make_plan(p, W, algo, T, m, l, n, batch, workspace_limit());
+    if (rc) return rc;
+    if (p.d == 0) return launch_leaf_gemm(W, m, l, n, batch, A, B, C, beta, s);
+    int st = DDQD_OK;
+    char *ws = static_cast<char *>(workspace_get(p.bytes, &st));
+    if (st) return st;
+    return exec_level(p, ws, 0, batch, A, B, C, beta, s);
+}
+
+}  // namespace ddqd

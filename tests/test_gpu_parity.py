@@ -1,0 +1,304 @@
+"""GPU parity tests: the CUDA path (through the C ABI of libddqd.so) against the CPU
+oracle on the same seeded inputs. Bit-exact wherever the kernel reproduces the oracle's
+summation order (everything here: docs/numerics.md), plus exact-error bounds (BJ:5) at
+the BASELINE.json full sizes where only sampled entries are checkable."""
+import numpy as np
+import pytest
+
+import ddqd_inputs as gen
+from tests.util import rec_depth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1510_08642_b200 as ddqd  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def np_(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def same(a, b):
+    """bitwise equality of float64 arrays (incl. signed zeros)"""
+    return np.array_equal(a.view(np.int64), b.view(np.int64))
+
+
+# ---- arithmetic layer ---------------------------------------------------------
+def _dd_samples(n, seed):
+    rng = np.random.default_rng(seed)
+    hi = rng.uniform(-1, 1, n) * np.exp2(rng.integers(-30, 30, n))
+    lo = hi * 2.0 ** -53 * rng.uniform(-1, 1, n)
+    s = hi + lo
+    e = lo - (s - hi)
+    x = np.stack([s, e])
+    x[:, :50] = 0.0
+    return x
+
+
+@pytest.mark.parametrize("op", ["add", "sub", "mul", "div", "madd"])
+def test_dd_elementwise_bitwise(orc, op):
+    x, y, w = _dd_samples(100000, 1), _dd_samples(100000, 2), _dd_samples(100000, 3)
+    y[:, 1000:2000] = -x[:, 1000:2000]          # exact cancellation
+    if op == "div":
+        y[:, :50] = 1.0
+        y[1, :50] = 0.0
+    ref = orc.dd_op(op, x, y, w)
+    got = np_(ddqd.elementwise(op, cu(x), cu(y), cu(w)))
+    assert same(got, ref)
+
+
+@pytest.mark.parametrize("op", ["add", "sub", "mul", "madd"])
+def test_qd_elementwise_bitwise(orc, op):
+    q = [gen.qd_matrix(1, 50000, s, 0).reshape(4, -1) for s in (4, 5, 6)]
+    q[1][:, :500] = -q[0][:, :500]
+    ref = orc.qd_op(op, *q)
+    got = np_(ddqd.elementwise(op, *(cu(a) for a in q)))
+    assert same(got, ref)
+
+
+# ---- leaf GEMM (Block) ----------------------------------------------------------
+@pytest.mark.parametrize("W", [2, 4])
+def test_block_small_and_ragged_bitwise(orc, W):
+    shapes = [(1, 1, 1), (3, 5, 2), (7, 1, 9), (33, 17, 65), (64, 64, 64), (65, 63, 129),
+              (130, 17, 3), (2, 300, 2), (100, 200, 70)]
+    for (m, l, n) in shapes:
+        A = gen.matrix(W, m, l, m + l, 0)
+        B = gen.matrix(W, l, n, m + l, 1)
+        ref = orc.gemm(A, B, "block")
+        got = np_(ddqd.gemm(cu(A), cu(B), "block"))
+        assert same(got, ref), (m, l, n)
+
+
+def test_block_large_tiles_bitwise(orc):
+    """Shape that selects the 64x64 4x4 kernel (>= 296 tiles) with ragged edges on all sides."""
+    A = gen.dd_matrix(1100, 301, 9, 0)
+    B = gen.dd_matrix(301, 1090, 9, 1)
+    assert same(np_(ddqd.dd_gemm(cu(A), cu(B), "block")), orc.gemm(A, B, "block"))
+
+
+def test_c0_dd_block_128(orc):
+    """BJ:7 (config 0): DD Block 128^3, seed 1: bit-exact vs oracle, and within
+    2^-96 l |A| |B| of the exact product on every entry."""
+    A = gen.dd_matrix(128, 128, 1, 0)
+    B = gen.dd_matrix(128, 128, 1, 1)
+    got = np_(ddqd.dd_gemm(cu(A), cu(B), "block"))
+    assert same(got, orc.gemm(A, B, "block"))
+    r, c = np.meshgrid(np.arange(128), np.arange(128), indexing="ij")
+    _, err = orc.exact_entries(A, B, got, r.ravel(), c.ravel())
+    bound = 2.0 ** -96 * 128 * np.abs(A[0]).max() * np.abs(B[0]).max()
+    assert np.abs(err).max() <= bound
+
+
+def test_zero_and_degenerate_sizes(orc):
+    A = cu(np.zeros((2, 5, 0))); B = cu(np.zeros((2, 0, 4)))
+    C = ddqd.dd_gemm(A, B, "strassen", 1)
+    assert np_(C).shape == (2, 5, 4) and np.all(np_(C) == 0)
+    A = cu(np.zeros((2, 0, 3))); B = cu(np.zeros((2, 3, 4)))
+    assert np_(ddqd.dd_gemm(A, B)).shape == (2, 0, 4)
+
+
+def test_errors():
+    A = cu(gen.dd_matrix(4, 4, 1, 0))
+    with pytest.raises(ValueError):
+        ddqd.dd_gemm(A, cu(gen.dd_matrix(5, 4, 1, 0)))
+    with pytest.raises(ValueError):
+        ddqd.dd_gemm(A, A, "strassen", 0)          # threshold < 1 -> EINVAL
+    with pytest.raises(ddqd.DDQDError):
+        ddqd.dd_gemm(A, A, out=A)                  # aliasing -> EALIAS
+
+
+# ---- recursion --------------------------------------------------------------------
+@pytest.mark.parametrize("algo", ["strassen", "winograd"])
+@pytest.mark.parametrize("W", [2, 4])
+def test_recursion_odd_shapes_bitwise(orc, algo, W):
+    """Odd/rectangular shapes with virtual zero padding at several levels (T small)."""
+    for (m, l, n, T) in [(37, 29, 33, 4), (64, 64, 64, 8), (65, 66, 67, 16), (101, 45, 77, 10),
+                         (9, 130, 11, 2)]:
+        A = gen.matrix(W, m, l, 3 * m + T, 0)
+        B = gen.matrix(W, l, n, 3 * m + T, 1)
+        ref = orc.gemm(A, B, algo, threshold=T)
+        got = np_(ddqd.gemm(cu(A), cu(B), algo, T))
+        assert same(got, ref), (m, l, n, T)
+
+
+@pytest.mark.parametrize("algo", ["strassen", "winograd"])
+def test_threshold_ge_dims_equals_block(algo):
+    A = cu(gen.dd_matrix(70, 80, 3, 0)); B = cu(gen.dd_matrix(80, 90, 3, 1))
+    assert same(np_(ddqd.dd_gemm(A, B, algo, 70)), np_(ddqd.dd_gemm(A, B, "block")))
+
+
+def test_c1_dd_strassen_1024(orc):
+    """BJ:8 (config 1): DD Strassen 1024^3, T = 128 (depth 3), seed 2; Block on the same
+    inputs; both bit-exact vs the oracle."""
+    A = gen.dd_matrix(1024, 1024, 2, 0)
+    B = gen.dd_matrix(1024, 1024, 2, 1)
+    gA, gB = cu(A), cu(B)
+    got = np_(ddqd.dd_gemm(gA, gB, "strassen", 128))
+    assert same(got, orc.gemm(A, B, "strassen", 128))
+    got_b = np_(ddqd.dd_gemm(gA, gB, "block"))
+    assert same(got_b, orc.gemm(A, B, "block"))
+    rng = np.random.default_rng(1)
+    r, c = rng.integers(0, 1024, 2048), rng.integers(0, 1024, 2048)
+    _, err = orc.exact_entries(A, B, got, r, c)
+    bound = 18.0 ** 3 * 2.0 ** -96 * 1024 * np.abs(A[0]).max() * np.abs(B[0]).max()
+    assert np.abs(err).max() <= bound
+
+
+def test_c2_qd_winograd_1024_sampled_and_512_bitwise(orc):
+    """BJ:9 (config 2): QD Winograd 1024^3, T = 128, seed 3: sampled exact errors within
+    18^3 2^-200 l |A||B|; bit-exact vs the oracle at 512^3 (depth 2) with the same recipe."""
+    A = gen.qd_matrix(1024, 1024, 3, 0)
+    B = gen.qd_matrix(1024, 1024, 3, 1)
+    got = np_(ddqd.qd_gemm(cu(A), cu(B), "winograd", 128))
+    rng = np.random.default_rng(2)
+    r, c = rng.integers(0, 1024, 512), rng.integers(0, 1024, 512)
+    _, err = orc.exact_entries(A, B, got, r, c)
+    bound = 18.0 ** 3 * 2.0 ** -200 * 1024 * np.abs(A[0]).max() * np.abs(B[0]).max()
+    assert np.abs(err).max() <= bound
+    A5, B5 = A[:, :512, :512].copy(), B[:, :512, :512].copy()
+    assert same(np_(ddqd.qd_gemm(cu(A5), cu(B5), "winograd", 128)), orc.gemm(A5, B5, "winograd", 128))
+
+
+def test_c3_shape_reduced_bitwise(orc):
+    """BJ:10 recipe (odd m, l, n) at 1023 x 1025 x 1021, T = 128 (depth 3): bit-exact."""
+    A = gen.dd_matrix(1023, 1025, 4, 0)
+    B = gen.dd_matrix(1025, 1021, 4, 1)
+    got = np_(ddqd.dd_gemm(cu(A), cu(B), "winograd", 128))
+    assert same(got, orc.gemm(A, B, "winograd", 128))
+
+
+def test_c3_full_size_sampled(orc):
+    """BJ:10 (config 3): DD Winograd 8191 x 8193 x 8190, T = 256 (depth 5), seed 4, in the
+    launch configuration bench.py times: >= 4096 sampled entries, including every padded
+    border row/column class, within 18^5 2^-96 l |A| |B| of the exact product."""
+    m, l, n, T = 8191, 8193, 8190, 256
+    A = gen.dd_matrix(m, l, 4, 0)
+    B = gen.dd_matrix(l, n, 4, 1)
+    got = np_(ddqd.dd_gemm(cu(A), cu(B), "winograd", T))
+    assert rec_depth(m, l, n, T) == 5
+    rng = np.random.default_rng(3)
+    r = np.concatenate([rng.integers(0, m, 4000), [0, m - 1, 4095, 4096, m - 1, 0, 2047, 6143]])
+    c = np.concatenate([rng.integers(0, n, 4000), [0, n - 1, 4094, 4095, 0, n - 1, 6142, 2047]])
+    _, err = orc.exact_entries(A, B, got, r, c)
+    bound = 18.0 ** 5 * 2.0 ** -96 * l * np.abs(A[0]).max() * np.abs(B[0]).max()
+    assert np.abs(err).max() <= bound
+    assert np.abs(err).max() <= bound * 2.0 ** -10     # typical error is far inside the bound
+
+
+def test_host_pointer_path_matches_device(orc):
+    A = gen.dd_matrix(300, 257, 7, 0)
+    B = gen.dd_matrix(257, 301, 7, 1)
+    hA = torch.from_numpy(A).pin_memory(); hB = torch.from_numpy(B).pin_memory()
+    hC = ddqd.dd_gemm(hA, hB, "winograd", 64)
+    assert same(hC.numpy(), np_(ddqd.dd_gemm(cu(A), cu(B), "winograd", 64)))
+    assert same(hC.numpy(), orc.gemm(A, B, "winograd", 64))
+
+
+@pytest.mark.parametrize("algo", ["block", "strassen"])
+def test_gemm_ex_strided_beta1(orc, algo):
+    """C := C - A B on strided sub-blocks (the LU Schur update form)."""
+    N = 200
+    big = gen.dd_matrix(N, N, 11, 0)
+    m, l, n = 120, 40, 130
+    A = big[:, 50:50 + m, 10:10 + l].copy()
+    B = big[:, 5:5 + l, 60:60 + n].copy()
+    C0 = big[:, 70:70 + m, 65:65 + n].copy()
+    T = orc.gemm(A, B, algo, threshold=16)
+    ref = orc.dd_op("sub", C0.reshape(2, -1), T.reshape(2, -1)).reshape(2, m, n)
+    g = cu(big)
+    base, ps = g.data_ptr(), N * N
+    ddqd.gemm_ex(2, algo, 16, m, l, n, 1,
+                 base + 8 * (50 * N + 10), N, ps, 0,
+                 base + 8 * (5 * N + 60), N, ps, 0,
+                 base + 8 * (70 * N + 65), N, ps, 0, beta=1)
+    assert same(np_(g)[:, 70:70 + m, 65:65 + n], ref)
+
+
+# ---- paper benchmark pair ----------------------------------------------------
+@pytest.mark.parametrize("n", [1023, 1024, 1025])
+def test_paper_pair_columns_and_parity(orc, n):
+    """P:60-61 inputs at the paper's sizes, Strassen(32)/Winograd(32) bit-exact vs the
+    oracle run on the same inputs; Block's columns bitwise identical (B has equal columns)."""
+    A, B = gen.bench_pair(n, 2)
+    gA, gB = cu(A), cu(B)
+    Cb = np_(ddqd.dd_gemm(gA, gB, "block"))
+    assert np.all(Cb == Cb[:, :, :1])
+    for algo in ("strassen", "winograd"):
+        got = np_(ddqd.dd_gemm(gA, gB, algo, 128))
+        assert same(got, orc.gemm(A, B, algo, threshold=128))
+
+
+# ---- LU ---------------------------------------------------------------------------
+def _b_ones(orc, A):
+    n = A.shape[1]
+    ones = np.zeros((2, n, 1)); ones[0] = 1.0
+    return orc.gemm(A, ones, "block")[:, :, 0]
+
+
+@pytest.mark.parametrize("algo,T,K", [("strassen", 32, 64), ("block", 128, 48), ("winograd", 16, 100)])
+def test_lu_bitwise_vs_oracle(orc, algo, T, K):
+    n = 300
+    A = gen.lu_matrix(n, 5)
+    b = _b_ones(orc, A)
+    x_ref, LU_ref, piv_ref, info_ref = orc.solve(A, b, panel=K, algo=algo, threshold=T)
+    x, LU, piv, info = ddqd.dd_lu_solve(cu(A), cu(b), panel=K, algo=algo, threshold=T)
+    assert info == info_ref == 0
+    assert np.array_equal(np_(piv), piv_ref)
+    assert same(np_(LU), LU_ref)
+    assert same(np_(x), x_ref)
+
+
+def test_lu_pivoting_path_bitwise(orc):
+    """Non-dominant matrix: row interchanges happen; still bit-exact."""
+    n = 200
+    A = gen.dd_matrix(n, n, 13, 0)
+    b = gen.dd_matrix(1, n, 13, 1)[:, 0, :].copy()
+    x_ref, LU_ref, piv_ref, _ = orc.solve(A, b, panel=32, algo="strassen", threshold=16)
+    x, LU, piv, info = ddqd.dd_lu_solve(cu(A), cu(b), panel=32, algo="strassen", threshold=16)
+    assert np.any(piv_ref != np.arange(n))
+    assert np.array_equal(np_(piv), piv_ref)
+    assert same(np_(LU), LU_ref) and same(np_(x), x_ref)
+
+
+def test_lu_zero_pivot_info():
+    A = gen.dd_matrix(40, 40, 2, 0)
+    A[:, :, 7] = 0.0
+    b = np.zeros((2, 40)); b[0] = 1.0
+    _, _, _, info = ddqd.dd_lu_solve(cu(A), cu(b), panel=16, algo="block")
+    assert info == 8
+
+
+def test_c4_lu_1024_bitwise(orc):
+    """BJ:11 recipe at n = 1024 (panel 256, Strassen update T = 128): bit-exact vs oracle."""
+    n = 1024
+    A = gen.lu_matrix(n, 5)
+    b = _b_ones(orc, A)
+    x_ref, LU_ref, piv_ref, _ = orc.solve(A, b, panel=256, algo="strassen", threshold=128)
+    x, LU, piv, info = ddqd.dd_lu_solve(cu(A), cu(b), panel=256, algo="strassen", threshold=128)
+    assert info == 0 and same(np_(LU), LU_ref) and same(np_(x), x_ref)
+
+
+def test_c4_lu_full_size_properties():
+    """BJ:11 (config 4): n = 4096, panel 256, Strassen update: ipiv = identity (column
+    diagonal dominance), x = 1 within 2^-96 n kappa 18."""
+    n = 4096
+    A = gen.lu_matrix(n, 5)
+    gA = cu(A)
+    ones = torch.zeros((2, n, 1), dtype=torch.float64, device=DEV); ones[0] = 1.0
+    b = ddqd.dd_gemm(gA, ones, "block")[:, :, 0].contiguous()
+    x, LU, piv, info = ddqd.dd_lu_solve(gA, b, panel=256, algo="strassen", threshold=128)
+    assert info == 0
+    assert np.array_equal(np_(piv), np.arange(n))
+    xx = np_(x)
+    err = np.abs((xx[0] - 1.0) + xx[1]).max()
+    assert err <= 2.0 ** -96 * n * 3 * 18
