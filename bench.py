@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""bench.py -- DD/QD GEMM effective GFLOPS (2mln/s) and FP64-pipe roofline on B200 (BJ:2).
+
+Step = one C := A B through the library's public C ABI (dd_gemm/qd_gemm) for the named
+workload: pre-additions, the batched leaf GEMM and post-additions of every recursion level
+(all SURVEY.md s.8(a) GEMM rows). Default workload: BASELINE.json configs[3] -- DD Winograd
+8191 x 8193 x 8190, threshold 256 (depth 5) -- the config the metric's 1/2/4/8-GPU numbers
+are quoted on (DESIGN.md s.7 explains the choice). Inputs are the seeded synthetic matrices
+of BJ:10 (ddqd_inputs), resident in HBM before the timed region; each operand (1.07 GB) is
+larger than L2 (126 MB), so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1|c2|c3] [--impl reference]
+
+N > 1 runs under torchrun (one process per GPU, NCCL) with the multi-GPU schedule of
+paper_1510_08642_b200.mgpu; rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c1": dict(W=2, algo="strassen", T=128, m=1024, l=1024, n=1024, seed=2,
+               name="BJ configs[1]: DD Strassen GEMM 1024^3, threshold 128 (depth 3), seed 2"),
+    "c2": dict(W=4, algo="winograd", T=128, m=1024, l=1024, n=1024, seed=3,
+               name="BJ configs[2]: QD Winograd GEMM 1024^3, threshold 128 (depth 3), seed 3"),
+    "c3": dict(W=2, algo="winograd", T=256, m=8191, l=8193, n=8190, seed=4,
+               name="BJ configs[3]: DD Winograd GEMM 8191x8193x8190, threshold 256 (depth 5), seed 4"),
+}
+# FP64-pipe lane-instructions per multiply-add (docs/numerics.md: DD 3 DMUL + 1 DFMA + 16 DADD;
+# QD common path 118 (qd_mul) + 82 (qd_add)).
+OPS_PER_MADD = {2: 20, 4: 200}
+MAD_DTYPE = {2: "f64x2 (double-double)", 4: "f64x4 (quad-double)"}
+
+
+def rec_shapes(m, l, n, T):
+    shapes = [(m, l, n)]
+    while min(m, l, n) > T:
+        m, l, n = (m + 1) // 2, (l + 1) // 2, (n + 1) // 2
+        shapes.append((m, l, n))
+    return shapes
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ---- clocks sampler (nvidia-smi during the timed region) ------------------------------
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.5)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons, power = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0])); mx = float(f[1]); power.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(power) if power else None}
+
+
+# ---- CPU oracle sample (cpu_baseline and --impl reference) ----------------------------
+def oracle_sample(wl):
+    """Bounded sample of the workload for the oracle: the leading (m/4, l/4, n/4) block
+    (same recipe, same algorithm and threshold) for c3; the full problem for c1; the leading
+    (m/2, l/2, n/2) block for c2. Returns (A, B, shape, description)."""
+    import ddqd_inputs as gen
+    m, l, n = wl["m"], wl["l"], wl["n"]
+    div = {"c3": 4, "c2": 2, "c1": 1}[wl["key"]]
+    ms, ls, ns = (m + div - 1) // div, (l + div - 1) // div, (n + div - 1) // div
+    A = gen.matrix(wl["W"], ms, ls, wl["seed"], 0)
+    B = gen.matrix(wl["W"], ls, ns, wl["seed"], 1)
+    desc = (f"oracle {wl['algo']}(T={wl['T']}) on a {ms}x{ls}x{ns} problem with the workload's "
+            f"input recipe ({'full problem' if div == 1 else f'1/{div} of each dimension'})")
+    return A, B, (ms, ls, ns), desc
+
+
+def run_oracle_once(orc, wl, A, B):
+    t0 = time.perf_counter()
+    orc.gemm(A, B, wl["algo"], threshold=wl["T"])
+    return time.perf_counter() - t0
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count()
+
+
+def reference_arm(args, wl, rank, world):
+    if rank != 0:
+        return 0
+    import oracle as orc
+    orc.build()
+    A, B, (ms, ls, ns), desc = oracle_sample(wl)
+    for _ in range(args.warmup):
+        run_oracle_once(orc, wl, A, B)
+    tot = sum(run_oracle_once(orc, wl, A, B) for _ in range(args.steps))
+    value = 2.0 * ms * ls * ns * args.steps / tot / 1e9
+    cores = cpu_cores()
+    line = {
+        "impl": "reference", "metric": "effective GFLOPS (2mln/s)", "value": value, "unit": "GFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": MAD_DTYPE[wl["W"]], "data": "synthetic (seeded, BJ recipe)",
+        "config": {"workload": wl["name"], "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---- our arm ------------------------------------------------------------------------
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    wl = dict(WORKLOADS[args.workload])
+    wl["key"] = args.workload
+    if args.impl == "reference":
+        return reference_arm(args, wl, rank, world)
+
+    import numpy as np
+    import torch
+
+    import ddqd_inputs as gen
+    import paper_1510_08642_b200 as ddqd
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    W, algo, T, m, l, n = wl["W"], wl["algo"], wl["T"], wl["m"], wl["l"], wl["n"]
+    flops_per_step = 2.0 * m * l * n
+
+    # inputs: every rank builds the same seeded matrices (rank 0's are the ones broadcast in
+    # the multi-GPU schedule); resident in HBM before the timed region
+    A_h = torch.from_numpy(gen.matrix(W, m, l, wl["seed"], 0))
+    B_h = torch.from_numpy(gen.matrix(W, l, n, wl["seed"], 1))
+    A = A_h.to(dev)
+    B = B_h.to(dev)
+    C = torch.empty((W, m, n), dtype=torch.float64, device=dev)
+
+    peak_dadd, _ = ddqd.fp64_peak("dadd")
+    peak_dfma, _ = ddqd.fp64_peak("dfma")
+    peak = max(peak_dadd, peak_dfma)
+
+    if world > 1:
+        from paper_1510_08642_b200 import mgpu
+        sched = mgpu.DistributedGemm(W, algo, T, m, l, n, dist, dev)
+
+        def step():
+            sched(A, B, C)
+    else:
+        def step():
+            ddqd.gemm(A, B, algo, T, out=C)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    clocks.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    n0 = ddqd.launch_count()
+    ddqd.profile_start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    prof = ddqd.profile_stop()
+    launches = ddqd.launch_count() - n0
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = flops_per_step * args.steps / (ms * 1e-3) / 1e9     # whole job, GFLOP/s
+
+    # roofline of the dominant kernel: the batched leaf GEMM (FP64-pipe bound)
+    leaf_ms, leaf_n, leaf_madds = prof["leaf"]
+    ops = OPS_PER_MADD[W]
+    leaf_avg_s = (leaf_ms / leaf_n) * 1e-3 if leaf_n else float("nan")
+    leaf_ops_per_launch = ops * leaf_madds / leaf_n if leaf_n else 0.0
+    achieved = leaf_ops_per_launch / leaf_avg_s / 1e12 if leaf_n else 0.0
+    roofline = {
+        "bound": "alu", "achieved": achieved, "peak": peak / 1e12, "unit": "TFLOP/s",
+        "frac": achieved / (peak / 1e12),
+        "flop_def": f"one FP64-pipe lane op (DADD/DMUL/DFMA); {ops} per {'DD' if W == 2 else 'QD'} madd",
+        "peak_source": "measured live by ddqd_fp64_peak (DADD/DFMA stream, 148 SMs); "
+                       "MEASURED_PEAKS.json has no FP64 figure",
+        "peak_dadd": peak_dadd / 1e12, "peak_dfma": peak_dfma / 1e12,
+        "kernel": "leaf_gemm_kernel", "launches": int(leaf_n),
+        "avg_launch_ms": leaf_avg_s * 1e3, "share_of_step": leaf_ms / ms if ms else None,
+        "traffic": None,
+        "pre_add": {"ms": prof["pre"][0], "launches": int(prof["pre"][1]),
+                    "GB_per_s": prof["pre"][2] / (prof["pre"][0] * 1e-3) / 1e9 if prof["pre"][0] else None},
+        "post_add": {"ms": prof["post"][0], "launches": int(prof["post"][1]),
+                     "GB_per_s": prof["post"][2] / (prof["post"][0] * 1e-3) / 1e9 if prof["post"][0] else None},
+    }
+    shapes = rec_shapes(m, l, n, T)
+    d = len(shapes) - 1
+    leaf_madds_step = (7 ** d) * shapes[-1][0] * shapes[-1][1] * shapes[-1][2]
+    classical = ops * m * l * n / (ms_per_step * 1e-3) / peak   # BJ:5's literal formula (may be > 1)
+
+    e2e = None
+    if not args.no_e2e and world == 1:
+        hA = A_h.pin_memory()
+        hB = B_h.pin_memory()
+        hC = torch.empty((W, m, n), dtype=torch.float64).pin_memory()
+        ddqd.gemm(hA, hB, algo, T, out=hC)            # warm the staging buffers
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            ddqd.gemm(hA, hB, algo, T, out=hC)        # H2D + compute + D2H, synchronous
+        e1.record()
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        e2e = {"value": flops_per_step * args.steps / (ems * 1e-3) / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(hA.numel() * 8 + hB.numel() * 8),
+               "d2h_bytes_per_step": int(hC.numel() * 8),
+               "ms_per_step": ems / args.steps,
+               "path": "dd_gemm/qd_gemm with pinned HOST pointers (library stages H2D/D2H inside the call)"}
+        del hA, hB, hC
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle as orc
+        orc.build()
+        sA, sB, (ms_, ls_, ns_), desc = oracle_sample(wl)
+        t = run_oracle_once(orc, wl, sA, sB)
+        cpu = {"value": 2.0 * ms_ * ls_ * ns_ / t / 1e9, "unit": "GFLOP/s", "cores": cpu_cores(),
+               "kind": "oracle", "sample": desc, "seconds": t}
+
+    if rank == 0:
+        line = {
+            "metric": "DD/QD GEMM effective GFLOPS (2mln/s) and % FP64-pipe roofline",
+            "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": MAD_DTYPE[W],
+            "data": "synthetic (seeded SplitMix64, BASELINE.json recipe)",
+            "config": {"workload": wl["name"], "m": m, "l": l, "n": n, "algo": algo, "threshold": T,
+                       "depth": d, "leaf_shape": list(shapes[-1]), "leaf_madds_per_step": leaf_madds_step,
+                       "l2": "no flush: each operand (%.2f GB) exceeds the 126 MB L2" % (A.numel() * 8 / 1e9),
+                       "parallelism": f"{world} GPU" + ("s, depth-k product distribution" if world > 1 else "")},
+            "roofline": roofline,
+            "fp64_roofline_fraction": {
+                "algorithmic_leaf": roofline["frac"],
+                "classical_normalised": classical,
+                "note": "classical = ops_per_madd*m*l*n/(P64*t) (BJ:5 literal; > 1 possible for Strassen/Winograd)"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -131,6 +131,18 @@ int ddqd_set_workspace_limit(size_t bytes);
 /* Number of kernels this thread's library calls have launched so far (evidence counter). */
 int64_t ddqd_launch_count(void);
 
+/* Live kernel timing (CUDA events on the launching stream) for bench.py's roofline:
+ * between start and stop every leaf-GEMM / pre-add / post-add launch is bracketed by
+ * events. stop() synchronises and writes, for class c = 0 leaf GEMM, 1 pre-add, 2 post-add,
+ * out[3c+0] = total ms, out[3c+1] = launches, out[3c+2] = work (madds for c = 0,
+ * algorithmic bytes for c = 1, 2); cap = number of doubles in out (>= 9). */
+int ddqd_profile_start(void);
+int ddqd_profile_stop(double *out, int cap);
+
+/* FP64-pipe throughput probe: op 0 = DFMA, 1 = DADD stream; returns lane-operations per
+ * second on the current device (and the per-launch ms). Roofline denominator of the leaf. */
+int ddqd_fp64_peak(int op, double *lane_ops_per_s, double *ms);
+
 /* Free library-owned device memory (workspace, staging buffers) of the current device. */
 int ddqd_release(void);
 

@@ -15,6 +15,7 @@ import os
 
 __all__ = ["dd_gemm", "qd_gemm", "gemm", "gemm_ex", "dd_lu_solve", "elementwise", "lib",
            "workspace_bytes", "set_workspace_limit", "launch_count", "release",
+           "profile_start", "profile_stop", "fp64_peak",
            "BLOCK", "STRASSEN", "WINOGRAD", "DDQDError"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -59,6 +60,8 @@ def _load():
     L.ddqd_set_workspace_limit.argtypes = [ctypes.c_size_t]
     L.ddqd_launch_count.restype = i64
     L.ddqd_last_error.restype = ctypes.c_char_p
+    L.ddqd_profile_stop.argtypes = [ctypes.POINTER(ctypes.c_double), i32]
+    L.ddqd_fp64_peak.argtypes = [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
     return L
 
 
@@ -66,7 +69,8 @@ lib = _load()
 
 EXPORTED = ["dd_gemm", "qd_gemm", "ddqd_gemm_ex", "dd_lu_solve", "ddqd_elementwise", "ddqd_set_stream",
             "ddqd_workspace_bytes", "ddqd_set_workspace", "ddqd_set_workspace_limit",
-            "ddqd_launch_count", "ddqd_release", "ddqd_last_error", "ddqd_version"]
+            "ddqd_launch_count", "ddqd_release", "ddqd_last_error", "ddqd_version",
+            "ddqd_profile_start", "ddqd_profile_stop", "ddqd_fp64_peak"]
 
 
 def _check(rc: int, what: str) -> int:
@@ -193,3 +197,22 @@ def launch_count() -> int:
 
 def release():
     lib.ddqd_release()
+
+
+def profile_start():
+    lib.ddqd_profile_start()
+
+
+def profile_stop():
+    """-> {"leaf": (ms, launches, madds), "pre": (ms, launches, bytes), "post": (...)}"""
+    buf = (ctypes.c_double * 9)()
+    _check(lib.ddqd_profile_stop(buf, 9), "profile_stop")
+    v = list(buf)
+    return {"leaf": tuple(v[0:3]), "pre": tuple(v[3:6]), "post": tuple(v[6:9])}
+
+
+def fp64_peak(op="dfma"):
+    """Measured FP64-pipe lane-operations per second (DFMA or DADD stream)."""
+    r, ms = ctypes.c_double(), ctypes.c_double()
+    _check(lib.ddqd_fp64_peak(0 if op == "dfma" else 1, ctypes.byref(r), ctypes.byref(ms)), "fp64_peak")
+    return r.value, ms.value

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/ddqd.h"
 #include "common.cuh"
@@ -19,6 +20,30 @@ static thread_local void *t_user_ws = nullptr;
 static thread_local size_t t_user_ws_bytes = 0;
 
 void set_error(const std::string &msg) { t_err = msg; }
+
+struct ProfRec {
+    int cls;
+    double work;
+    cudaEvent_t e0, e1;
+};
+static thread_local bool t_prof = false;
+static thread_local std::vector<ProfRec> t_recs;
+static thread_local cudaEvent_t t_open = nullptr;
+
+void prof_begin(int cls, cudaStream_t s) {
+    (void)cls;
+    if (!t_prof) return;
+    cudaEventCreate(&t_open);
+    cudaEventRecord(t_open, s);
+}
+void prof_end(int cls, double work, cudaStream_t s) {
+    if (!t_prof || !t_open) return;
+    cudaEvent_t e1;
+    cudaEventCreate(&e1);
+    cudaEventRecord(e1, s);
+    t_recs.push_back(ProfRec{cls, work, t_open, e1});
+    t_open = nullptr;
+}
 cudaStream_t cur_stream() { return t_stream; }
 void count_launch(int64_t n) { t_launches += n; }
 
@@ -233,6 +258,37 @@ int ddqd_set_workspace_limit(size_t bytes) {
 }
 
 int64_t ddqd_launch_count(void) { return t_launches; }
+
+int ddqd_profile_start(void) {
+    t_prof = true;
+    t_recs.clear();
+    return DDQD_OK;
+}
+
+int ddqd_profile_stop(double *out, int cap) {
+    t_prof = false;
+    for (int i = 0; i < cap; i++) out[i] = 0.0;
+    for (auto &r : t_recs) {
+        cudaEventSynchronize(r.e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.e0, r.e1);
+        if (3 * r.cls + 2 < cap) {
+            out[3 * r.cls + 0] += ms;
+            out[3 * r.cls + 1] += 1.0;
+            out[3 * r.cls + 2] += r.work;
+        }
+        cudaEventDestroy(r.e0);
+        cudaEventDestroy(r.e1);
+    }
+    t_recs.clear();
+    DDQD_CUDA_CHECK(cudaGetLastError());
+    return DDQD_OK;
+}
+
+int ddqd_fp64_peak(int op, double *lane_ops_per_s, double *ms) {
+    t_err.clear();
+    return fp64_peak(op, lane_ops_per_s, ms, t_stream);
+}
 
 int ddqd_release(void) {
     std::lock_guard<std::mutex> lk(g_mu);

@@ -128,11 +128,13 @@ static int pre_dispatch(int algo, int side, int64_t P, const MatDesc &X, const M
     const int64_t total = P * Y.rows * Y.cols;
     if (total == 0) return DDQD_OK;
     const unsigned g = grid_for(total);
+    prof_begin(1, s);
     if (algo == 1 && side == 0) pre_add_kernel<W, 1, 0><<<g, 256, 0, s>>>(P, X, Y);
     else if (algo == 1) pre_add_kernel<W, 1, 1><<<g, 256, 0, s>>>(P, X, Y);
     else if (side == 0) pre_add_kernel<W, 2, 0><<<g, 256, 0, s>>>(P, X, Y);
     else pre_add_kernel<W, 2, 1><<<g, 256, 0, s>>>(P, X, Y);
     DDQD_LAUNCH_CHECK();
+    prof_end(1, (double)total * W * 8.0 * 11.0, s);   // 4 quadrant reads + 7 operand writes
     return DDQD_OK;
 }
 
@@ -147,9 +149,11 @@ static int post_dispatch(int algo, int64_t P, const MatDesc &M, const MatDesc &C
     const int64_t total = P * M.rows * M.cols;
     if (total == 0) return DDQD_OK;
     const unsigned g = grid_for(total);
+    prof_begin(2, s);
     if (algo == 1) post_add_kernel<W, 1><<<g, 256, 0, s>>>(P, M, C, beta);
     else post_add_kernel<W, 2><<<g, 256, 0, s>>>(P, M, C, beta);
     DDQD_LAUNCH_CHECK();
+    prof_end(2, (double)total * W * 8.0 * (beta ? 15.0 : 11.0), s);   // 7 product reads + 4 (8) C
     return DDQD_OK;
 }
 

@@ -22,6 +22,13 @@ void set_error(const std::string &msg);
 cudaStream_t cur_stream();
 void count_launch(int64_t n = 1);
 
+// Live per-class kernel timing for bench.py (CUDA events on the launching stream), active
+// only between ddqd_profile_start/stop. Classes: 0 leaf GEMM (work = madds), 1 pre-add
+// (work = algorithmic bytes), 2 post-add (bytes), 3 LU kernels.
+void prof_begin(int cls, cudaStream_t s);
+void prof_end(int cls, double work, cudaStream_t s);
+int fp64_peak(int op, double *lane_ops_per_s, double *ms, cudaStream_t s);
+
 #define DDQD_CUDA_CHECK(expr)                                                            \
     do {                                                                                 \
         cudaError_t e__ = (expr);                                                        \

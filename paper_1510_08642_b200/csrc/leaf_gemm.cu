@@ -191,12 +191,14 @@ static int launch_cfg(int64_t m, int64_t l, int64_t n, int64_t batch, const MatD
         set_error("leaf GEMM: matrix too large for the tile grid");
         return DDQD_EINVAL;
     }
+    prof_begin(0, s);
     for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
         const int64_t bz = (batch - b0) < 65535 ? (batch - b0) : 65535;
         dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)bz);
         kern<<<grid, Cfg::NT, Cfg::SMEM, s>>>(m, l, n, A, B, C, beta, b0);
         DDQD_LAUNCH_CHECK();
     }
+    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s);
     return DDQD_OK;
 }
 
