@@ -91,6 +91,24 @@ typedef struct {
 
 int ddqd_gemm_ex(const ddqd_gemm_desc *desc);
 
+/* One recursion level's fused additions, exported for the multi-GPU schedule (which runs
+ * the top k levels itself and distributes the 7^k products). A batch of matrices: element
+ * (b, i, j) word w at p[b*bs + w*ps + i*ld + j]; rows/cols are the logical extent.
+ *   ddqd_pre_add : P parents X (rows x cols) -> 7P children Y (ceil(rows/2) x ceil(cols/2)),
+ *                  child c of parent b at batch index 7b + c, for side 0 (A operands) or
+ *                  side 1 (B operands) of Strassen / Winograd in the child
+ *                  order of docs/numerics.md s.4; missing quadrant rows/cols read as zero.
+ *   ddqd_post_add: 7P products M -> P parents C (cropped to C's rows x cols); beta = 1
+ *                  subtracts from C instead of storing.
+ * Device pointers only; asynchronous on the thread's stream. */
+typedef struct {
+    double *p;
+    int64_t rows, cols, ld, ps, bs;
+} ddqd_mat;
+
+int ddqd_pre_add(int prec, int algo, int side, int64_t P, const ddqd_mat *X, const ddqd_mat *Y);
+int ddqd_post_add(int prec, int algo, int64_t P, const ddqd_mat *M, const ddqd_mat *C, int beta);
+
 /*
  * dd_lu_solve -- blocked right-looking LU with partial pivoting (P:121-133 steps 1-3,
  * pivoting per BJ:11) and the solve of Eq. (2), DD only.

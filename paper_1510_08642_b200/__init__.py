@@ -30,6 +30,11 @@ class DDQDError(RuntimeError):
     pass
 
 
+class Mat(ctypes.Structure):
+    _fields_ = [("p", ctypes.c_void_p), ("rows", ctypes.c_int64), ("cols", ctypes.c_int64),
+                ("ld", ctypes.c_int64), ("ps", ctypes.c_int64), ("bs", ctypes.c_int64)]
+
+
 class GemmDesc(ctypes.Structure):
     _fields_ = [("prec", ctypes.c_int), ("algo", ctypes.c_int), ("threshold", ctypes.c_int64),
                 ("m", ctypes.c_int64), ("l", ctypes.c_int64), ("n", ctypes.c_int64),
@@ -60,6 +65,8 @@ def _load():
     L.ddqd_set_workspace_limit.argtypes = [ctypes.c_size_t]
     L.ddqd_launch_count.restype = i64
     L.ddqd_last_error.restype = ctypes.c_char_p
+    L.ddqd_pre_add.argtypes = [i32, i32, i32, i64, ctypes.POINTER(Mat), ctypes.POINTER(Mat)]
+    L.ddqd_post_add.argtypes = [i32, i32, i64, ctypes.POINTER(Mat), ctypes.POINTER(Mat), i32]
     L.ddqd_profile_stop.argtypes = [ctypes.POINTER(ctypes.c_double), i32]
     L.ddqd_fp64_peak.argtypes = [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
     return L
@@ -70,7 +77,7 @@ lib = _load()
 EXPORTED = ["dd_gemm", "qd_gemm", "ddqd_gemm_ex", "dd_lu_solve", "ddqd_elementwise", "ddqd_set_stream",
             "ddqd_workspace_bytes", "ddqd_set_workspace", "ddqd_set_workspace_limit",
             "ddqd_launch_count", "ddqd_release", "ddqd_last_error", "ddqd_version",
-            "ddqd_profile_start", "ddqd_profile_stop", "ddqd_fp64_peak"]
+            "ddqd_profile_start", "ddqd_profile_stop", "ddqd_fp64_peak", "ddqd_pre_add", "ddqd_post_add"]
 
 
 def _check(rc: int, what: str) -> int:
@@ -149,6 +156,44 @@ def gemm_ex(prec, algo, threshold, m, l, n, batch, A, lda, psA, bsA, B, ldb, psB
     d = GemmDesc(prec, _algo(algo), threshold, m, l, n, batch, A, lda, psA, bsA, B, ldb, psB, bsB,
                  C, ldc, psC, bsC, beta)
     return _check(lib.ddqd_gemm_ex(ctypes.byref(d)), "gemm_ex")
+
+
+def batch_mat(t):
+    """Mat descriptor of a contiguous [batch, W, rows, cols] (or [W, rows, cols]) CUDA tensor."""
+    if t.dim() == 3:
+        W, r, c = t.shape
+        return Mat(t.data_ptr(), r, c, c, r * c, W * r * c)
+    B, W, r, c = t.shape
+    return Mat(t.data_ptr(), r, c, c, r * c, W * r * c)
+
+
+def pre_add(algo, side, X, Y):
+    """One level's fused pre-additions: X [P,W,r,c] -> Y [7P,W,ceil(r/2),ceil(c/2)]."""
+    P = 1 if X.dim() == 3 else X.shape[0]
+    W = X.shape[-3]
+    _set_stream(X)
+    x, y = batch_mat(X), batch_mat(Y)
+    _check(lib.ddqd_pre_add(W, _algo(algo), side, P, ctypes.byref(x), ctypes.byref(y)), "pre_add")
+
+
+def post_add(algo, M, C, beta=0):
+    """One level's fused post-additions: M [7P,W,h,h'] -> C [P,W,r,c]."""
+    P = 1 if C.dim() == 3 else C.shape[0]
+    W = C.shape[-3]
+    _set_stream(C)
+    mm, cc = batch_mat(M), batch_mat(C)
+    _check(lib.ddqd_post_add(W, _algo(algo), P, ctypes.byref(mm), ctypes.byref(cc), beta), "post_add")
+
+
+def gemm_batched(A, B, C, algo, threshold, beta=0):
+    """C[b] := A[b] B[b] for contiguous [batch, W, .., ..] CUDA tensors (one library schedule)."""
+    batch, W, m, l = A.shape
+    n = B.shape[3]
+    _set_stream(A)
+    return gemm_ex(W, algo, threshold, m, l, n, batch,
+                   A.data_ptr(), l, m * l, W * m * l,
+                   B.data_ptr(), n, l * n, W * l * n,
+                   C.data_ptr(), n, m * n, W * m * n, beta)
 
 
 def dd_lu_solve(A, b, panel=256, algo="strassen", threshold=128, overwrite=False):

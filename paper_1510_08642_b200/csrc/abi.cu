@@ -225,6 +225,34 @@ int dd_lu_solve(int64_t n, double *A, const double *b, double *x, int64_t *ipiv,
     return info;
 }
 
+static MatDesc to_desc(const ddqd_mat *x) { return MatDesc{x->p, x->rows, x->cols, x->ld, x->ps, x->bs}; }
+
+int ddqd_pre_add(int prec, int algo, int side, int64_t P, const ddqd_mat *X, const ddqd_mat *Y) {
+    t_err.clear();
+    if ((prec != 2 && prec != 4) || (algo != 1 && algo != 2) || (side != 0 && side != 1) || P < 0 || !X || !Y) {
+        set_error("bad pre_add arguments");
+        return DDQD_EINVAL;
+    }
+    if (Y->rows != (X->rows + 1) / 2 || Y->cols != (X->cols + 1) / 2) {
+        set_error("pre_add: child shape must be ceil(parent/2)");
+        return DDQD_EINVAL;
+    }
+    return launch_pre_add(prec, algo, side, P, to_desc(X), to_desc(Y), t_stream);
+}
+
+int ddqd_post_add(int prec, int algo, int64_t P, const ddqd_mat *M, const ddqd_mat *C, int beta) {
+    t_err.clear();
+    if ((prec != 2 && prec != 4) || (algo != 1 && algo != 2) || P < 0 || !M || !C || (beta != 0 && beta != 1)) {
+        set_error("bad post_add arguments");
+        return DDQD_EINVAL;
+    }
+    if (M->rows != (C->rows + 1) / 2 || M->cols != (C->cols + 1) / 2) {
+        set_error("post_add: product shape must be ceil(parent/2)");
+        return DDQD_EINVAL;
+    }
+    return launch_post_add(prec, algo, P, to_desc(M), to_desc(C), beta, t_stream);
+}
+
 int ddqd_elementwise(int prec, int op, int64_t count, const double *x, const double *y, const double *w,
                      double *z) {
     t_err.clear();

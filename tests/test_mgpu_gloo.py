@@ -1,0 +1,149 @@
+"""Multi-process (world size 2, gloo, CPU) tests of the multi-GPU schedule's host logic
+(paper_1510_08642_b200/mgpu.py): depth-k product distribution and C row-slab tiling must
+reproduce the single-process recursion bit for bit. The compute backend here is built
+from the oracle (tests only); on GPUs the same schedule drives libddqd.so over NCCL."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import ddqd_inputs as gen
+
+# mgpu.py imports nothing from the CUDA package at module level
+from paper_1510_08642_b200 import mgpu as _mgpu_probe  # noqa: F401  (needs libddqd.so built)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class OracleBackend:
+    """CPU stand-in for the library kernels, written from docs/numerics.md s.4 with oracle ops."""
+
+    def __init__(self, W):
+        import oracle
+        self.o = oracle
+        self.W = W
+        self.op = oracle.dd_op if W == 2 else oracle.qd_op
+
+    def empty(self, shape, like):
+        return torch.empty(shape, dtype=torch.float64)
+
+    def _ew(self, name, x, y):
+        W = self.W
+        shp = x.shape
+        return self.op(name, x.reshape(W, -1), y.reshape(W, -1)).reshape(shp)
+
+    def _quads(self, X, hr, hc):
+        W, r, c = X.shape
+        P = np.zeros((W, 2 * hr, 2 * hc))
+        P[:, :r, :c] = X
+        return P[:, :hr, :hc], P[:, :hr, hc:], P[:, hr:, :hc], P[:, hr:, hc:]
+
+    def pre_add(self, algo, side, X, Y):
+        Xn = X.numpy().reshape((-1,) + tuple(X.shape[-3:]))
+        hr, hc = Y.shape[-2], Y.shape[-1]
+        add = lambda a, b: self._ew("add", a, b)   # noqa: E731
+        sub = lambda a, b: self._ew("sub", a, b)   # noqa: E731
+        for b in range(Xn.shape[0]):
+            x11, x12, x21, x22 = self._quads(Xn[b], hr, hc)
+            if algo == "strassen" and side == 0:
+                o = [add(x11, x22), add(x21, x22), x11, x22, add(x11, x12), sub(x21, x11), sub(x12, x22)]
+            elif algo == "strassen":
+                o = [add(x11, x22), x11, sub(x12, x22), sub(x21, x11), x22, add(x11, x12), add(x21, x22)]
+            elif side == 0:
+                s1 = add(x21, x22); s2 = sub(s1, x11); s3 = sub(x11, x21); s4 = sub(x12, s2)
+                o = [x11, x12, s4, x22, s1, s2, s3]
+            else:
+                t1 = sub(x12, x11); t2 = sub(x22, t1); t3 = sub(x22, x12); t4 = sub(t2, x21)
+                o = [x11, x21, x22, t4, t1, t2, t3]
+            for c in range(7):
+                Y[7 * b + c] = torch.from_numpy(np.ascontiguousarray(o[c]))
+
+    def post_add(self, algo, M, C):
+        add = lambda a, b: self._ew("add", a, b)   # noqa: E731
+        sub = lambda a, b: self._ew("sub", a, b)   # noqa: E731
+        Cv = C if C.dim() == 4 else C.unsqueeze(0)
+        hm, hn = M.shape[-2], M.shape[-1]
+        for b in range(Cv.shape[0]):
+            p = [M[7 * b + c].numpy() for c in range(7)]
+            if algo == "strassen":
+                c11 = add(sub(add(p[0], p[3]), p[4]), p[6]); c12 = add(p[2], p[4])
+                c21 = add(p[1], p[3]); c22 = add(add(sub(p[0], p[1]), p[2]), p[5])
+            else:
+                u2 = add(p[0], p[5]); u3 = add(u2, p[6]); u4 = add(u2, p[4])
+                c11 = add(p[0], p[1]); c12 = add(u4, p[2]); c21 = sub(u3, p[3]); c22 = add(u3, p[4])
+            full = np.zeros((self.W, 2 * hm, 2 * hn))
+            full[:, :hm, :hn] = c11; full[:, :hm, hn:] = c12; full[:, hm:, :hn] = c21; full[:, hm:, hn:] = c22
+            r, c = Cv.shape[-2], Cv.shape[-1]
+            Cv[b] = torch.from_numpy(np.ascontiguousarray(full[:, :r, :c]))
+
+    def gemm_batched(self, A, B, C, algo, T):
+        for b in range(A.shape[0]):
+            C[b] = torch.from_numpy(self.o.gemm(A[b].numpy(), B[b].numpy(), algo, threshold=T))
+
+    def gemm_rows(self, A, B, r0, r1, out, algo, T):
+        out[:, : r1 - r0, :] = torch.from_numpy(
+            self.o.gemm(np.ascontiguousarray(A[:, r0:r1, :].numpy()), B.numpy(), algo, threshold=T))
+
+
+def _worker(rank, world, port, cfg, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1510_08642_b200.mgpu import DistributedGemm
+        W, algo, T, m, l, n, k = cfg
+        A = torch.from_numpy(gen.matrix(W, m, l, 21, 0)) if rank == 0 else torch.zeros((W, m, l), dtype=torch.float64)
+        B = torch.from_numpy(gen.matrix(W, l, n, 21, 1)) if rank == 0 else torch.zeros((W, l, n), dtype=torch.float64)
+        C = torch.zeros((W, m, n), dtype=torch.float64)
+        dg = DistributedGemm(W, algo, T, m, l, n, dist, k=k, backend=OracleBackend(W))
+        dg(A, B, C)
+        dg(A, B, C)    # buffers are reused across steps
+        if rank == 0:
+            q.put((dg.k, C.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(cfg, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    k, C = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return k, C
+
+
+@pytest.mark.parametrize("cfg", [
+    (2, "winograd", 4, 37, 29, 33, None),     # odd shapes, k chosen by the balancer (k = 2)
+    (2, "strassen", 5, 40, 41, 42, 1),
+    (4, "winograd", 3, 19, 23, 17, 2),       # QD
+    (2, "block", 8, 31, 20, 25, None),       # C row-slab tiling
+])
+def test_distributed_matches_single_process(orc, cfg):
+    W, algo, T, m, l, n, _ = cfg
+    k, C = _run(cfg)
+    ref = orc.gemm(gen.matrix(W, m, l, 21, 0), gen.matrix(W, l, n, 21, 1), algo, threshold=T)
+    assert np.array_equal(C.view(np.int64), ref.view(np.int64))
+    if algo != "block":
+        assert k >= 1
+
+
+def test_balancer():
+    from paper_1510_08642_b200.mgpu import balanced_slices, choose_depth
+    assert balanced_slices(49, 8)[0] == (0, 7) and balanced_slices(49, 8)[-1] == (43, 49)
+    assert choose_depth(5, 8) == 3 and choose_depth(5, 4) == 2 and choose_depth(5, 2) == 2
+    assert choose_depth(5, 7) == 1 and choose_depth(0, 8) == 0
