@@ -34,6 +34,9 @@ WORKLOADS = {
                name="BJ configs[2]: QD Winograd GEMM 1024^3, threshold 128 (depth 3), seed 3"),
     "c3": dict(W=2, algo="winograd", T=256, m=8191, l=8193, n=8190, seed=4,
                name="BJ configs[3]: DD Winograd GEMM 8191x8193x8190, threshold 256 (depth 5), seed 4"),
+    "c4": dict(W=2, algo="strassen", T=128, n=4096, panel=256, seed=5, lu=True,
+               name="BJ configs[4]: DD blocked right-looking LU with partial pivoting, n=4096, panel 256, "
+                    "Strassen update (threshold 128), A = R + nI, b = A*1, seed 5"),
 }
 # FP64-pipe lane-instructions per multiply-add (docs/numerics.md: DD 3 DMUL + 1 DFMA + 16 DADD;
 # QD common path 118 (qd_mul) + 82 (qd_add)).
@@ -55,6 +58,7 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--k", type=int, default=None, help="multi-GPU product depth (default: balancer)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -137,6 +141,8 @@ def reference_arm(args, wl, rank, world):
         return 0
     import oracle as orc
     orc.build()
+    if wl.get("lu"):
+        return reference_lu(args, wl, orc)
     A, B, (ms, ls, ns), desc = oracle_sample(wl)
     for _ in range(args.warmup):
         run_oracle_once(orc, wl, A, B)
@@ -156,6 +162,123 @@ def reference_arm(args, wl, rank, world):
     return 0
 
 
+def reference_lu(args, wl, orc):
+    """Oracle LU + solve on a 1024 x 1024 matrix with the c4 recipe (bounded sample)."""
+    import numpy as np
+
+    import ddqd_inputs as gen
+    n = 1024
+    A = gen.lu_matrix(n, wl["seed"])
+    ones = np.zeros((2, n, 1)); ones[0] = 1.0
+    b = orc.gemm(A, ones, "block")[:, :, 0].copy()
+    run = lambda: orc.solve(A, b, panel=wl["panel"], algo=wl["algo"], threshold=wl["T"])  # noqa: E731
+    for _ in range(args.warmup):
+        run()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run()
+    tot = time.perf_counter() - t0
+    value = 2.0 / 3.0 * n ** 3 * args.steps / tot / 1e9
+    desc = f"oracle LU+solve, n={n} (c4 recipe, panel {wl['panel']}, {wl['algo']} T={wl['T']})"
+    print(json.dumps({
+        "impl": "reference", "metric": "DD LU effective GFLOPS (2n^3/3 per solve / s)", "value": value,
+        "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": MAD_DTYPE[2], "data": "synthetic (seeded, BJ recipe)",
+        "config": {"workload": wl["name"], "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cpu_cores(), "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
+    return 0
+
+
+# ---- LU (c4) ----------------------------------------------------------------------------
+def lu_bench(args, wl, rank, world, local):
+    """c4: one step = dd_lu_solve (factor + solve) of a fresh copy of A. Multi-GPU: replicas
+    only (DESIGN.md s.8: the LU's panel chain does not shard at this size); value = total
+    work of all replicas / max-over-ranks time."""
+    import numpy as np
+    import torch
+
+    import ddqd_inputs as gen
+    import paper_1510_08642_b200 as ddqd
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    n, K, algo, T = wl["n"], wl["panel"], wl["algo"], wl["T"]
+    A0 = torch.from_numpy(gen.lu_matrix(n, wl["seed"])).to(dev)
+    ones = torch.zeros((2, n, 1), dtype=torch.float64, device=dev)
+    ones[0] = 1.0
+    b = ddqd.dd_gemm(A0, ones, "block")[:, :, 0].contiguous()     # b = A*1 on the device
+    A = torch.empty_like(A0)
+    x = torch.empty_like(b)
+    ipiv = torch.empty(n, dtype=torch.int64, device=dev)
+
+    def step():
+        A.copy_(A0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ddqd._set_stream(A)
+        info = ddqd.lib.dd_lu_solve(n, A.data_ptr(), b.data_ptr(), x.data_ptr(), ipiv.data_ptr(),
+                                     K, ddqd._algo(algo), T)
+        e1.record()
+        torch.cuda.synchronize()
+        assert info == 0, info
+        return e0.elapsed_time(e1)
+
+    for _ in range(args.warmup):
+        step()
+    peak = max(ddqd.fp64_peak("dadd")[0], ddqd.fp64_peak("dfma")[0])
+    clocks = Clocks(local)
+    clocks.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    n0 = ddqd.launch_count()
+    ddqd.profile_start()
+    ms = sum(step() for _ in range(args.steps))
+    prof = ddqd.profile_stop()
+    launches = ddqd.launch_count() - n0
+    clk = clocks.stop()
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    flops = 2.0 / 3.0 * n ** 3
+    value = flops * world * args.steps / (ms * 1e-3) / 1e9
+    xx = x.cpu().numpy()
+    err = float(np.abs((xx[0] - 1.0) + xx[1]).max())
+    leaf_ms, leaf_n, leaf_madds = prof["leaf"]
+    achieved = 20.0 * leaf_madds / (leaf_ms * 1e-3) / 1e12 if leaf_ms else 0.0
+    shares = {k: v[0] / ms for k, v in prof.items()}
+    dominant = max(shares, key=shares.get)
+    if rank == 0:
+        line = {
+            "metric": "DD LU effective GFLOPS (2n^3/3 per solve / s)", "value": value, "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+            "dtype": MAD_DTYPE[2], "data": "synthetic (seeded SplitMix64, BASELINE.json recipe)",
+            "config": {"workload": wl["name"], "n": n, "panel": K, "algo": algo, "threshold": T,
+                       "parallelism": f"{world} GPU replica(s)",
+                       "l2": "A (268 MB) exceeds L2; fresh copy of A before each step, outside the events"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak / 1e12, "unit": "TFLOP/s",
+                         "frac": achieved / (peak / 1e12) if peak else None,
+                         "kernel": "leaf_gemm_kernel (Schur update)", "traffic": None,
+                         "note": "LU time is dominated by '%s' (share %.2f); panel steps are latency-bound"
+                                 % (dominant, shares[dominant])},
+            "time_shares": shares,
+            "max_abs_err_x_minus_1": err,
+            "cpu_baseline": None, "e2e": None, "gpu_launches": int(launches), "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
 # ---- our arm ------------------------------------------------------------------------
 def main():
     args = parse_args()
@@ -166,6 +289,8 @@ def main():
     wl["key"] = args.workload
     if args.impl == "reference":
         return reference_arm(args, wl, rank, world)
+    if wl.get("lu"):
+        return lu_bench(args, wl, rank, world, local)
 
     import numpy as np
     import torch
@@ -197,7 +322,7 @@ def main():
 
     if world > 1:
         from paper_1510_08642_b200 import mgpu
-        sched = mgpu.DistributedGemm(W, algo, T, m, l, n, dist, dev)
+        sched = mgpu.DistributedGemm(W, algo, T, m, l, n, dist, dev, k=args.k)
 
         def step():
             sched(A, B, C)

@@ -152,8 +152,9 @@ int64_t ddqd_launch_count(void);
 /* Live kernel timing (CUDA events on the launching stream) for bench.py's roofline:
  * between start and stop every leaf-GEMM / pre-add / post-add launch is bracketed by
  * events. stop() synchronises and writes, for class c = 0 leaf GEMM, 1 pre-add, 2 post-add,
- * out[3c+0] = total ms, out[3c+1] = launches, out[3c+2] = work (madds for c = 0,
- * algorithmic bytes for c = 1, 2); cap = number of doubles in out (>= 9). */
+ * 3 LU panel factorisation, 4 LU TRSM, 5 LU solve: out[3c+0] = total ms, out[3c+1] =
+ * bracketed regions, out[3c+2] = work (madds for c = 0, 3, 4; algorithmic bytes for c = 1, 2;
+ * n^2 for c = 5); cap = number of doubles in out (18 for all classes). */
 int ddqd_profile_start(void);
 int ddqd_profile_stop(double *out, int cap);
 

@@ -250,10 +250,11 @@ def profile_start():
 
 def profile_stop():
     """-> {"leaf": (ms, launches, madds), "pre": (ms, launches, bytes), "post": (...)}"""
-    buf = (ctypes.c_double * 9)()
-    _check(lib.ddqd_profile_stop(buf, 9), "profile_stop")
+    buf = (ctypes.c_double * 18)()
+    _check(lib.ddqd_profile_stop(buf, 18), "profile_stop")
     v = list(buf)
-    return {"leaf": tuple(v[0:3]), "pre": tuple(v[3:6]), "post": tuple(v[6:9])}
+    names = ["leaf", "pre", "post", "lu_panel", "lu_trsm", "lu_solve"]
+    return {nm: tuple(v[3 * i:3 * i + 3]) for i, nm in enumerate(names)}
 
 
 def fp64_peak(op="dfma"):

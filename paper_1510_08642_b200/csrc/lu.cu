@@ -238,6 +238,7 @@ int lu_solve_impl(int64_t n, double *A, const double *b, double *x, int64_t *ipi
 
     for (int64_t p = 0; p < n; p += K) {
         const int64_t kb = std::min(K, n - p);
+        prof_begin(3, s);
         for (int64_t k = p; k < p + kb; k++) {
             lu_pivot_kernel<<<1, 1024, 0, s>>>(A, n, k, ipiv, aux);
             DDQD_LAUNCH_CHECK();
@@ -249,6 +250,7 @@ int lu_solve_impl(int64_t n, double *A, const double *b, double *x, int64_t *ipi
                 DDQD_LAUNCH_CHECK();
             }
         }
+        prof_end(3, (double)kb * (double)(n - p) * (double)kb / 2.0, s);   // panel madds (approx.)
         const int64_t n2 = n - p - kb;
         if (n2 <= 0) continue;
         int cw = (int)std::max<int64_t>(1, std::min<int64_t>(32, 6144 / kb));
@@ -256,8 +258,10 @@ int lu_solve_impl(int64_t n, double *A, const double *b, double *x, int64_t *ipi
         if (smem > 48 * 1024)
             DDQD_CUDA_CHECK(cudaFuncSetAttribute(lu_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem));
+        prof_begin(4, s);
         lu_trsm_kernel<<<(unsigned)((n2 + cw - 1) / cw), 256, smem, s>>>(A, n, p, kb, p + kb, cw);
         DDQD_LAUNCH_CHECK();
+        prof_end(4, (double)kb * (double)kb / 2.0 * (double)n2, s);
         MatDesc L21{A + (p + kb) * n + p, n2, kb, n, n * n, 0};
         MatDesc U12{A + p * n + (p + kb), kb, n2, n, n * n, 0};
         MatDesc A22{A + (p + kb) * n + (p + kb), n2, n2, n, n * n, 0};
@@ -271,6 +275,7 @@ int lu_solve_impl(int64_t n, double *A, const double *b, double *x, int64_t *ipi
     if (psmem > 48 * 1024)
         DDQD_CUDA_CHECK(cudaFuncSetAttribute(lu_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)psmem));
+    prof_begin(5, s);
     lu_perm_kernel<<<1, 1024, psmem, s>>>(b, y, ipiv, n, use_smem);
     DDQD_LAUNCH_CHECK();
     const int NB = 256;
@@ -294,6 +299,7 @@ int lu_solve_impl(int64_t n, double *A, const double *b, double *x, int64_t *ipi
             DDQD_LAUNCH_CHECK();
         }
     }
+    prof_end(5, (double)n * (double)n, s);
     int info_h = 0;
     DDQD_CUDA_CHECK(cudaMemcpyAsync(&info_h, &aux->info, sizeof(int), cudaMemcpyDeviceToHost, s));
     DDQD_CUDA_CHECK(cudaStreamSynchronize(s));

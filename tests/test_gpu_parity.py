@@ -302,3 +302,26 @@ def test_c4_lu_full_size_properties():
     xx = np_(x)
     err = np.abs((xx[0] - 1.0) + xx[1]).max()
     assert err <= 2.0 ** -96 * n * 3 * 18
+
+
+# ---- multi-GPU schedule's CUDA backend, world size 1 (one GPU available) ---------------
+@pytest.mark.parametrize("algo,k", [("winograd", 2), ("strassen", 1), ("block", 0)])
+def test_mgpu_schedule_cuda_backend_world1(orc, algo, k):
+    """The depth-k product schedule (pre-adds, batched slice GEMM, gather, post-adds) through
+    the library's ddqd_pre_add / ddqd_gemm_ex / ddqd_post_add on one GPU: bit-exact."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1510_08642_b200.mgpu import DistributedGemm
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    try:
+        m, l, n, T = 301, 257, 299, 32
+        A = gen.dd_matrix(m, l, 17, 0); B = gen.dd_matrix(l, n, 17, 1)
+        C = torch.empty((2, m, n), dtype=torch.float64, device=DEV)
+        dg = DistributedGemm(2, algo, T, m, l, n, dist, DEV, k=k)
+        dg(cu(A), cu(B), C)
+        assert same(np_(C), orc.gemm(A, B, algo, threshold=T))
+    finally:
+        dist.destroy_process_group()
