@@ -2,6 +2,8 @@
 oracle on the same seeded inputs. Bit-exact wherever the kernel reproduces the oracle's
 summation order (everything here: docs/numerics.md), plus exact-error bounds (BJ:5) at
 the BASELINE.json full sizes where only sampled entries are checkable."""
+import os
+
 import numpy as np
 import pytest
 
@@ -17,6 +19,7 @@ if not torch.cuda.is_available():
 import paper_1510_08642_b200 as ddqd  # noqa: E402
 
 DEV = torch.device("cuda:0")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def cu(a):
@@ -325,3 +328,22 @@ def test_mgpu_schedule_cuda_backend_world1(orc, algo, k):
         assert same(np_(C), orc.gemm(A, B, algo, threshold=T))
     finally:
         dist.destroy_process_group()
+
+
+def test_lu_per_column_path_bitwise(tmp_path):
+    """The per-column two-kernel panel schedule (DDQD_LU_PANEL=steps) gives the same bits as
+    the cooperative panel kernel (run in a subprocess: the switch is read once per process)."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, ddqd_inputs as gen, paper_1510_08642_b200 as d\n"
+        "A = gen.dd_matrix(300, 300, 13, 0); b = gen.dd_matrix(1, 300, 13, 1)[:, 0, :].copy()\n"
+        "x, LU, piv, info = d.dd_lu_solve(torch.from_numpy(A).cuda(), torch.from_numpy(b).cuda(), 64, 'strassen', 32)\n"
+        "np.save(r'%s', np.concatenate([LU.cpu().numpy().ravel(), x.cpu().numpy().ravel(), piv.cpu().numpy().astype(np.float64)]))\n")
+    outs = []
+    for mode in ("steps", "coop"):
+        f = tmp_path / f"{mode}.npy"
+        env = dict(os.environ, DDQD_LU_PANEL=mode)
+        subprocess.check_call([sys.executable, "-c", code % f], env=env, cwd=ROOT)
+        outs.append(np.load(f))
+    assert same(outs[0], outs[1])
