@@ -81,9 +81,12 @@ __device__ __forceinline__ void three_sum2(double &a, double &b, double c) {
     two_sum(c, t1, a, t3);
     b = __dadd_rn(t2, t3);
 }
-// IEEE "x != 0" on the bit pattern (keeps the compare off the FP64 pipe; -0 == 0).
+// IEEE "x != 0" on the bit pattern (-0 == 0). The move goes through inline PTX so nvcc
+// cannot fold it back into a DSETP: the test runs on the integer pipe, not the FP64 pipe.
 __device__ __forceinline__ bool nz(double x) {
-    return (static_cast<unsigned long long>(__double_as_longlong(x)) << 1) != 0ull;
+    unsigned long long u;
+    asm("mov.b64 %0, %1;" : "=l"(u) : "d"(x));
+    return (u << 1) != 0ull;
 }
 
 __device__ __forceinline__ qd qd_renorm(double c0, double c1, double c2, double c3, double c4) {

@@ -211,7 +211,7 @@ int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, cons
             return launch_cfg<2, 64, 64, 16, 4, 4, 3, 2>(m, l, n, batch, A, B, C, beta, s);
         return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2>(m, l, n, batch, A, B, C, beta, s);
     }
-    if (W == 4) return launch_cfg<4, 32, 32, 16, 2, 2, 3, 1>(m, l, n, batch, A, B, C, beta, s);
+    if (W == 4) return launch_cfg<4, 32, 32, 16, 2, 2, 3, 2>(m, l, n, batch, A, B, C, beta, s);
     set_error("leaf GEMM: precision must be 2 (DD) or 4 (QD)");
     return DDQD_EINVAL;
 }
