@@ -13,6 +13,8 @@
 // for the ragged edges; the FP64 pipe does DADD/DMUL/DFMA only (20 per DD madd, ~200 per
 // QD madd). Shared-memory traffic per madd is 1/TM + 1/TN words per operand (tiny next to
 // the 20-200 FP64 instructions), so the kernel is FP64-pipe bound by design.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ddqd_arith.cuh"
 
@@ -202,13 +204,38 @@ static int launch_cfg(int64_t m, int64_t l, int64_t n, int64_t batch, const MatD
     return DDQD_OK;
 }
 
+// DDQD_LEAF_CFG selects an alternative tile configuration (tuning experiments only;
+// tools/tune_leaf.py). Every configuration computes the same bits.
+static int leaf_cfg_override() {
+    static int v = -2;
+    if (v == -2) {
+        const char *e = getenv("DDQD_LEAF_CFG");
+        v = e ? atoi(e) : -1;
+    }
+    return v;
+}
+
 int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
                      const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s) {
     if (m == 0 || n == 0 || batch == 0) return DDQD_OK;
+    switch (leaf_cfg_override()) {
+    case 0: return launch_cfg<2, 64, 64, 16, 4, 4, 3, 2>(m, l, n, batch, A, B, C, beta, s);
+    case 1: return launch_cfg<2, 64, 64, 8, 4, 4, 4, 2>(m, l, n, batch, A, B, C, beta, s);
+    case 2: return launch_cfg<2, 32, 64, 16, 2, 4, 3, 3>(m, l, n, batch, A, B, C, beta, s);
+    case 3: return launch_cfg<2, 64, 32, 16, 4, 2, 3, 3>(m, l, n, batch, A, B, C, beta, s);
+    case 4: return launch_cfg<2, 64, 64, 16, 4, 4, 2, 2>(m, l, n, batch, A, B, C, beta, s);
+    case 5: return launch_cfg<2, 32, 32, 16, 2, 2, 3, 4>(m, l, n, batch, A, B, C, beta, s);
+    case 6: return launch_cfg<2, 64, 64, 32, 4, 4, 2, 1>(m, l, n, batch, A, B, C, beta, s);
+    case 10: return launch_cfg<4, 32, 32, 16, 2, 2, 3, 2>(m, l, n, batch, A, B, C, beta, s);
+    case 11: return launch_cfg<4, 32, 32, 8, 2, 2, 4, 2>(m, l, n, batch, A, B, C, beta, s);
+    case 12: return launch_cfg<4, 16, 32, 16, 2, 2, 3, 4>(m, l, n, batch, A, B, C, beta, s);
+    case 13: return launch_cfg<4, 32, 64, 8, 2, 4, 3, 1>(m, l, n, batch, A, B, C, beta, s);
+    default: break;
+    }
     if (W == 2) {
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
-        if (big_tiles >= 2 * 148)
-            return launch_cfg<2, 64, 64, 16, 4, 4, 3, 2>(m, l, n, batch, A, B, C, beta, s);
+        if (big_tiles >= 2 * 148)   // tools/tune_leaf.py: BK = 8 x 4 stages is the fastest DD tile
+            return launch_cfg<2, 64, 64, 8, 4, 4, 4, 2>(m, l, n, batch, A, B, C, beta, s);
         return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2>(m, l, n, batch, A, B, C, beta, s);
     }
     if (W == 4) return launch_cfg<4, 32, 32, 16, 2, 2, 3, 2>(m, l, n, batch, A, B, C, beta, s);
