@@ -129,6 +129,25 @@ def run_oracle_once(orc, wl, A, B):
     return time.perf_counter() - t0
 
 
+def ncu_leaf_traffic(workload):
+    """DRAM bytes (read + write) per leaf launch from the newest committed `ncu --set full`
+    capture of this workload's leaf kernel (profiles/rNN/ncu_full_leaf_<wl>_raw.csv)."""
+    import csv
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_full_leaf_{workload}_raw.csv")))
+    if not files:
+        return None, None
+    rows = list(csv.reader(open(files[-1])))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tot = 0.0
+    for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        i = hdr.index(name)
+        tot += float(vals[i].replace(",", "")) * scale.get(units[i], 1)
+    grid = vals[hdr.index("launch__grid_size")] if "launch__grid_size" in hdr else None
+    return tot, f"{os.path.relpath(files[-1], ROOT)} (grid {grid})"
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -376,6 +395,7 @@ def main():
         "kernel": "leaf_gemm_kernel", "launches": int(leaf_n),
         "avg_launch_ms": leaf_avg_s * 1e3, "share_of_step": leaf_ms / ms if ms else None,
         "traffic": None,
+        "algorithmic_bytes_per_launch": None,
         "pre_add": {"ms": prof["pre"][0], "launches": int(prof["pre"][1]),
                     "GB_per_s": prof["pre"][2] / (prof["pre"][0] * 1e-3) / 1e9 if prof["pre"][0] else None},
         "post_add": {"ms": prof["post"][0], "launches": int(prof["post"][1]),
@@ -383,6 +403,14 @@ def main():
     }
     shapes = rec_shapes(m, l, n, T)
     d = len(shapes) - 1
+    if leaf_n:
+        lm, ll, ln = shapes[-1]
+        per_launch_leaves = leaf_madds / leaf_n / (lm * ll * ln)
+        roofline["algorithmic_bytes_per_launch"] = per_launch_leaves * W * 8.0 * (lm * ll + ll * ln + lm * ln)
+        tr, src = ncu_leaf_traffic(args.workload)
+        if tr is not None:
+            roofline["traffic"] = tr
+            roofline["traffic_source"] = src
     leaf_madds_step = (7 ** d) * shapes[-1][0] * shapes[-1][1] * shapes[-1][2]
     classical = ops * m * l * n / (ms_per_step * 1e-3) / peak   # BJ:5's literal formula (may be > 1)
 

@@ -233,8 +233,9 @@ int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, cons
     default: break;
     }
     if (W == 2) {
+        // 64x64 tiles when the grid fills the GPU and the leaf is not smaller than a tile
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
-        if (big_tiles >= 2 * 148)   // tools/tune_leaf.py: BK = 8 x 4 stages is the fastest DD tile
+        if (big_tiles >= 2 * 148 && m > 32 && n > 32)   // tools/tune_leaf.py: BK = 8 x 4 stages is the fastest DD tile
             return launch_cfg<2, 64, 64, 8, 4, 4, 4, 2>(m, l, n, batch, A, B, C, beta, s);
         return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2>(m, l, n, batch, A, B, C, beta, s);
     }

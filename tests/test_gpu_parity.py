@@ -237,8 +237,9 @@ def test_paper_pair_columns_and_parity(orc, n):
     Cb = np_(ddqd.dd_gemm(gA, gB, "block"))
     assert np.all(Cb == Cb[:, :, :1])
     for algo in ("strassen", "winograd"):
-        got = np_(ddqd.dd_gemm(gA, gB, algo, 128))
-        assert same(got, orc.gemm(A, B, algo, threshold=128))
+        for T in ((128, 32) if n == 1025 else (128,)):     # the paper's n_min = 32 too
+            got = np_(ddqd.dd_gemm(gA, gB, algo, T))
+            assert same(got, orc.gemm(A, B, algo, threshold=T))
 
 
 # ---- LU ---------------------------------------------------------------------------

@@ -1,0 +1,101 @@
+"""Paper benchmark workload on one B200 side by side with PAPER.md Tables 1-2 (SURVEY.md
+s.8(f) row f2). Inputs: the paper's pair A = [sqrt5 (i+j-1)], B = [sqrt3 (n-i)] at
+n = 1023, 1024, 1025; algorithms Block, Strassen(n_min), Winograd(n_min) with the paper's
+n_min = 32 and with this build's default threshold 128; DD and QD. Every result is checked
+against the closed form c_ij = sqrt(15) * S(i, n) within 4 n eps 18^d.
+Times are CUDA-event medians of 5 runs (inputs resident). Paper times: 1 and 8 OpenMP
+threads on a Xeon E5-2620 v2, context only.
+
+    python tools/paper_tables.py [--out profiles/r01/paper_tables.md]
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+from fractions import Fraction
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+PAPER = {  # (prec, algo, n) -> (1PE s, 8PE s)
+    ("DD", "block", 1023): (20.8, 3.2), ("DD", "block", 1024): (20.3, 3.2), ("DD", "block", 1025): (22.3, 4.1),
+    ("DD", "strassen", 1023): (11.7, 3.2), ("DD", "strassen", 1024): (11.7, 3.1), ("DD", "strassen", 1025): (11.7, 3.2),
+    ("DD", "winograd", 1023): (11.7, 3.2), ("DD", "winograd", 1024): (11.6, 3.1), ("DD", "winograd", 1025): (11.7, 3.2),
+    ("QD", "block", 1023): (249.0, 32.5), ("QD", "block", 1024): (247.6, 32.6), ("QD", "block", 1025): (272.4, 42.8),
+    ("QD", "strassen", 1023): (134.5, 17.8), ("QD", "strassen", 1024): (134.3, 17.2), ("QD", "strassen", 1025): (135.0, 18.9),
+    ("QD", "winograd", 1023): (134.7, 17.8), ("QD", "winograd", 1024): (134.5, 17.2), ("QD", "winograd", 1025): (134.9, 18.9),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01", "paper_tables.md"))
+    args = ap.parse_args()
+    import numpy as np
+    import torch
+
+    import ddqd_inputs as gen
+    import paper_1510_08642_b200 as ddqd
+
+    r15 = Fraction(math.isqrt(15 << 1200), 1 << 600)
+    rows, recs = [], []
+    for W, prec in ((2, "DD"), (4, "QD")):
+        eps = Fraction(1, 2 ** 104) if W == 2 else Fraction(1, 2 ** 209)
+        for n in (1023, 1024, 1025):
+            A, B = gen.bench_pair(n, W)
+            gA, gB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+            C = torch.empty((W, n, n), dtype=torch.float64, device="cuda")
+            for algo, T in (("block", 32), ("strassen", 32), ("winograd", 32), ("strassen", 128), ("winograd", 128)):
+                ddqd.gemm(gA, gB, algo, T, out=C)
+                ts = []
+                for _ in range(5):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    ddqd.gemm(gA, gB, algo, T, out=C)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    ts.append(e0.elapsed_time(e1) * 1e-3)
+                t = statistics.median(ts)
+                Ch = C.cpu().numpy()
+                d = 0
+                if algo != "block":
+                    mm = n
+                    while mm > T:
+                        mm = (mm + 1) // 2
+                        d += 1
+                worst = Fraction(0)
+                for i in range(0, n, max(1, n // 64)):
+                    ex = r15 * gen.bench_pair_exact(n, i + 1)
+                    for j in (0, n // 2, n - 1):
+                        got = sum((Fraction(float(w)) for w in Ch[:, i, j]), Fraction(0))
+                        if ex:
+                            worst = max(worst, abs(got - ex) / abs(ex))
+                bound = 4 * n * eps * 18 ** d
+                ok = worst <= bound
+                p1, p8 = PAPER[(prec, algo, n)]
+                label = f"{algo.capitalize()}({T})" if algo != "block" else "Block"
+                rec = {"prec": prec, "n": n, "algo": algo, "T": T, "depth": d, "gpu_s": t,
+                       "gflops": 2.0 * n ** 3 / t / 1e9, "paper_1pe_s": p1, "paper_8pe_s": p8,
+                       "speedup_vs_8pe": p8 / t, "max_rel_err_vs_closed_form": float(worst),
+                       "bound": float(bound), "closed_form_ok": bool(ok)}
+                recs.append(rec)
+                rows.append(f"| {prec} | {n} | {label} | {t * 1e3:.3f} | {rec['gflops']:.1f} | {p1} | {p8} | "
+                            f"{rec['speedup_vs_8pe']:.0f}x | {float(worst):.2e} | {'ok' if ok else 'FAIL'} |")
+                print(json.dumps(rec), flush=True)
+    hdr = ("| prec | n | algorithm | B200 ms | GFLOP/s | paper 1PE s | paper 8PE s | vs 8PE | max rel err "
+           "(closed form) | check |\n|---|---|---|---|---|---|---|---|---|---|")
+    txt = ("# Paper benchmark workload (P:61) on one B200 vs PAPER.md Tables 1-2\n\n"
+           "Paper column 'Block' is Block(32); Strassen/Winograd(32) use the paper's n_min; (128) is this "
+           "build's default threshold. Paper hardware: Xeon E5-2620 v2, 1 / 8 OpenMP threads (context only).\n\n"
+           + hdr + "\n" + "\n".join(rows) + "\n")
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    with open(args.out, "w") as f:
+        f.write(txt)
+    print(txt)
+    assert all(r["closed_form_ok"] for r in recs)
+
+
+if __name__ == "__main__":
+    main()
