@@ -125,8 +125,19 @@ int ddqd_post_add(int prec, int algo, int64_t P, const ddqd_mat *M, const ddqd_m
 int dd_lu_solve(int64_t n, double *A, const double *b, double *x, int64_t *ipiv,
                 int64_t panel, int algo, int64_t threshold);
 
+/* QD (4-word) LU with partial pivoting + solve; arguments as dd_lu_solve with [4][n][n] /
+ * [4][n] planes (divisions are qd_div of docs/numerics.md s.3). */
+int qd_lu_solve(int64_t n, double *A, const double *b, double *x, int64_t *ipiv,
+                int64_t panel, int algo, int64_t threshold);
+
+/* General form: prec = DDQD_DD / DDQD_QD; pivot = 1 partial pivoting (BJ:11), 0 = the paper's
+ * pivot-free LU ("none of the LU decomposition involves pivoting"; ipiv[k] = k, a zero
+ * pivot returns info = k+1). Other arguments and return values as dd_lu_solve. */
+int ddqd_lu_solve(int prec, int pivot, int64_t n, double *A, const double *b, double *x,
+                  int64_t *ipiv, int64_t panel, int algo, int64_t threshold);
+
 /* Elementwise arithmetic layer, for parity tests of the device DD/QD ops (device
- * pointers, planar [W][count]): op 0 add, 1 sub, 2 mul, 3 div (DD only), 4 madd
+ * pointers, planar [W][count]): op 0 add, 1 sub, 2 mul, 3 div, 4 madd
  * z = x + y*w. */
 int ddqd_elementwise(int prec, int op, int64_t count, const double *x, const double *y,
                      const double *w, double *z);

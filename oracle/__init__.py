@@ -52,8 +52,9 @@ def lib():
         L.or_qd_renorm.argtypes = [i64, P, P]
         L.or_dd_abs_gt.argtypes = [P, P]
         L.or_gemm.argtypes = [ctypes.c_int, ctypes.c_int, i64, i64, i64, i64, i64, P, P, P, ctypes.c_int]
-        L.or_lu.argtypes = [i64, P, PI, i64, ctypes.c_int, i64, ctypes.c_int]
-        L.or_lu_solve.argtypes = [i64, P, PI, P, P]
+        L.or_lu.argtypes = [ctypes.c_int, ctypes.c_int, i64, P, PI, i64, ctypes.c_int, i64, ctypes.c_int]
+        L.or_lu_solve.argtypes = [ctypes.c_int, i64, P, PI, P, P]
+        L.or_qd_div.argtypes = [i64, P, P, P]
         L.or_counter_madds.restype = i64
         L.or_counter_block_adds.restype = i64
         L.or_exact_entries.argtypes = [ctypes.c_int, i64, i64, i64, P, P, P, i64, PI, PI, P, P]
@@ -156,13 +157,14 @@ def reset_counters():
 
 
 # ---- LU ----------------------------------------------------------------------
-def lu(A, panel=256, algo="strassen", threshold=128, nthreads=0):
-    """Blocked right-looking LU with partial pivoting (numerics.md s.5).
-    Returns (LU [2,n,n], ipiv int64[n], info)."""
+def lu(A, panel=256, algo="strassen", threshold=128, nthreads=0, pivot=True):
+    """Blocked right-looking LU (numerics.md s.5) of a [W,n,n] DD (W=2) or QD (W=4) matrix,
+    with partial pivoting or (pivot=False) the paper's pivot-free variant.
+    Returns (LU [W,n,n], ipiv int64[n], info)."""
     LU = _f64(A).copy()
-    n = LU.shape[1]
+    W, n = LU.shape[0], LU.shape[1]
     ipiv = np.zeros(n, dtype=np.int64)
-    info = lib().or_lu(n, _p(LU), _pi(ipiv), panel, ALGOS[algo], threshold, nthreads)
+    info = lib().or_lu(W, 1 if pivot else 0, n, _p(LU), _pi(ipiv), panel, ALGOS[algo], threshold, nthreads)
     if info < 0:
         raise ValueError("or_lu: invalid arguments")
     return LU, ipiv, info
@@ -172,13 +174,21 @@ def lu_solve(LU, ipiv, b):
     LU, b = _f64(LU), _f64(b)
     ipiv = np.ascontiguousarray(ipiv, dtype=np.int64)
     x = np.empty_like(b)
-    lib().or_lu_solve(LU.shape[1], _p(LU), _pi(ipiv), _p(b), _p(x))
+    lib().or_lu_solve(LU.shape[0], LU.shape[1], _p(LU), _pi(ipiv), _p(b), _p(x))
     return x
 
 
-def solve(A, b, panel=256, algo="strassen", threshold=128, nthreads=0):
-    LU, ipiv, info = lu(A, panel, algo, threshold, nthreads)
+def solve(A, b, panel=256, algo="strassen", threshold=128, nthreads=0, pivot=True):
+    LU, ipiv, info = lu(A, panel, algo, threshold, nthreads, pivot)
     return lu_solve(LU, ipiv, b), LU, ipiv, info
+
+
+def qd_div(x, y):
+    """QD division (numerics.md s.3) on [4, n] arrays."""
+    x, y = _f64(x), _f64(y)
+    z = np.empty_like(x)
+    lib().or_qd_div(x.shape[1], _p(x), _p(y), _p(z))
+    return z
 
 
 # ---- exact reference -----------------------------------------------------------

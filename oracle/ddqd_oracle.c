@@ -493,22 +493,79 @@ int or_gemm(int W, int algo, int64_t T, int64_t bs, int64_t m, int64_t l, int64_
 }
 
 /* ------------------------------------------------------------------------- */
-/* numerics.md s.5: blocked right-looking LU with partial pivoting            */
-/* (P:121-133 steps 1-3; pivoting per BJ:11), DD only.                         */
-/* A is n x n planar [2][n][n], overwritten by L\U; ipiv[k] = pivot row.       */
-/* Returns info: 0, or k+1 for the first exactly-zero pivot.                   */
+/* numerics.md s.3: qd_div and the QD magnitude order (LU) */
 /* ------------------------------------------------------------------------- */
-static dd_t ld_dd(const double *A, int64_t n, int64_t i, int64_t j) {
-    dd_t r = { A[i * n + j], A[n * n + i * n + j] };
-    return r;
-}
-static void st_dd(double *A, int64_t n, int64_t i, int64_t j, dd_t v) {
-    A[i * n + j] = v.hi; A[n * n + i * n + j] = v.lo;
+static qd_t qd_div(qd_t a, qd_t b) {
+    qd_t r = a, t;
+    double q[4];
+    for (int i = 0; i < 3; i++) {
+        q[i] = r.w[0] / b.w[0];
+        t.w[0] = q[i]; t.w[1] = 0.0; t.w[2] = 0.0; t.w[3] = 0.0;
+        r = qd_sub(r, qd_mul(b, t));
+    }
+    q[3] = r.w[0] / b.w[0];
+    return qd_renorm(q[0], q[1], q[2], q[3], 0.0);
 }
 
-int or_lu(int64_t n, double *A, int64_t *ipiv, int64_t K, int algo, int64_t T, int nthreads) {
+static int qd_abs_gt(qd_t x, qd_t y) {
+    qd_t ax = x.w[0] >= 0.0 ? x : qd_neg(x);
+    qd_t ay = y.w[0] >= 0.0 ? y : qd_neg(y);
+    for (int i = 0; i < 4; i++)
+        if (ax.w[i] != ay.w[i]) return ax.w[i] > ay.w[i];
+    return 0;
+}
+
+void or_qd_div(int64_t n, const double *x, const double *y, double *z) {
+    for (int64_t i = 0; i < n; i++) {
+        qd_t a, b, r;
+        for (int k = 0; k < 4; k++) { a.w[k] = x[k * n + i]; b.w[k] = y[k * n + i]; }
+        r = qd_div(a, b);
+        for (int k = 0; k < 4; k++) z[k * n + i] = r.w[k];
+    }
+}
+
+/* A W-word scalar for the LU (DD when W = 2, QD when W = 4). */
+typedef struct { double w[4]; } sc_t;
+
+static sc_t sc_from_dd(dd_t v) { sc_t r = { { v.hi, v.lo, 0.0, 0.0 } }; return r; }
+static dd_t sc_dd(sc_t v) { dd_t r = { v.w[0], v.w[1] }; return r; }
+static qd_t sc_qd(sc_t v) { qd_t r; for (int i = 0; i < 4; i++) r.w[i] = v.w[i]; return r; }
+static sc_t sc_from_qd(qd_t v) { sc_t r; for (int i = 0; i < 4; i++) r.w[i] = v.w[i]; return r; }
+
+static sc_t sc_sub(int W, sc_t x, sc_t y) {
+    return W == 2 ? sc_from_dd(dd_sub(sc_dd(x), sc_dd(y))) : sc_from_qd(qd_sub(sc_qd(x), sc_qd(y)));
+}
+static sc_t sc_mul(int W, sc_t x, sc_t y) {
+    return W == 2 ? sc_from_dd(dd_mul(sc_dd(x), sc_dd(y))) : sc_from_qd(qd_mul(sc_qd(x), sc_qd(y)));
+}
+static sc_t sc_div(int W, sc_t x, sc_t y) {
+    return W == 2 ? sc_from_dd(dd_div(sc_dd(x), sc_dd(y))) : sc_from_qd(qd_div(sc_qd(x), sc_qd(y)));
+}
+static int sc_abs_gt(int W, sc_t x, sc_t y) {
+    return W == 2 ? dd_abs_gt(sc_dd(x), sc_dd(y)) : qd_abs_gt(sc_qd(x), sc_qd(y));
+}
+static sc_t sc_one(void) { sc_t r = { { 1.0, 0.0, 0.0, 0.0 } }; return r; }
+
+/* element (i,j) of a planar [W][n][n] matrix */
+static sc_t ld_sc(int W, const double *A, int64_t n, int64_t i, int64_t j) {
+    sc_t r = { { 0.0, 0.0, 0.0, 0.0 } };
+    for (int w = 0; w < W; w++) r.w[w] = A[w * n * n + i * n + j];
+    return r;
+}
+static void st_sc(int W, double *A, int64_t n, int64_t i, int64_t j, sc_t v) {
+    for (int w = 0; w < W; w++) A[w * n * n + i * n + j] = v.w[w];
+}
+
+/* ------------------------------------------------------------------------- */
+/* numerics.md s.5: blocked right-looking LU (P:121-133 steps 1-3); partial  */
+/* pivoting per BJ:11 (pivot = 1) or the paper's pivot-free LU (pivot = 0,   */
+/* P:121). A is n x n planar [W][n][n], overwritten by L\U; ipiv[k] = pivot  */
+/* row. Returns info: 0, or k+1 for the first exactly-zero pivot.            */
+/* ------------------------------------------------------------------------- */
+int or_lu(int W, int pivot, int64_t n, double *A, int64_t *ipiv, int64_t K, int algo, int64_t T,
+          int nthreads) {
     int info = 0;
-    if (n < 0 || K < 1) return -1;
+    if ((W != 2 && W != 4) || n < 0 || K < 1) return -1;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
 #endif
@@ -517,28 +574,29 @@ int or_lu(int64_t n, double *A, int64_t *ipiv, int64_t K, int algo, int64_t T, i
         /* step 1: panel factorisation, column by column */
         for (int64_t k = p; k < p + kb; k++) {
             int64_t r = k;
-            dd_t best = ld_dd(A, n, k, k);
-            for (int64_t i = k + 1; i < n; i++) {
-                dd_t v = ld_dd(A, n, i, k);
-                if (dd_abs_gt(v, best)) { best = v; r = i; }
+            if (pivot) {
+                sc_t best = ld_sc(W, A, n, k, k);
+                for (int64_t i = k + 1; i < n; i++) {
+                    sc_t v = ld_sc(W, A, n, i, k);
+                    if (sc_abs_gt(W, v, best)) { best = v; r = i; }
+                }
             }
             ipiv[k] = r;
             if (r != k)
                 for (int64_t j = 0; j < n; j++) {
-                    dd_t t = ld_dd(A, n, k, j);
-                    st_dd(A, n, k, j, ld_dd(A, n, r, j));
-                    st_dd(A, n, r, j, t);
+                    sc_t t = ld_sc(W, A, n, k, j);
+                    st_sc(W, A, n, k, j, ld_sc(W, A, n, r, j));
+                    st_sc(W, A, n, r, j, t);
                 }
-            dd_t piv = ld_dd(A, n, k, k);
-            if (piv.hi == 0.0) { if (!info) info = (int)(k + 1); continue; }
-            dd_t one = { 1.0, 0.0 };
-            dd_t rinv = dd_div(one, piv);
+            sc_t piv = ld_sc(W, A, n, k, k);
+            if (piv.w[0] == 0.0) { if (!info) info = (int)(k + 1); continue; }
+            sc_t rinv = sc_div(W, sc_one(), piv);
 #pragma omp parallel for schedule(static)
             for (int64_t i = k + 1; i < n; i++) {
-                dd_t lik = dd_mul(ld_dd(A, n, i, k), rinv);
-                st_dd(A, n, i, k, lik);
+                sc_t lik = sc_mul(W, ld_sc(W, A, n, i, k), rinv);
+                st_sc(W, A, n, i, k, lik);
                 for (int64_t j = k + 1; j < p + kb; j++)
-                    st_dd(A, n, i, j, dd_sub(ld_dd(A, n, i, j), dd_mul(lik, ld_dd(A, n, k, j))));
+                    st_sc(W, A, n, i, j, sc_sub(W, ld_sc(W, A, n, i, j), sc_mul(W, lik, ld_sc(W, A, n, k, j))));
             }
         }
         int64_t n2 = n - p - kb;
@@ -547,29 +605,26 @@ int or_lu(int64_t n, double *A, int64_t *ipiv, int64_t K, int algo, int64_t T, i
         for (int64_t i = p; i < p + kb; i++)
 #pragma omp parallel for schedule(static)
             for (int64_t r = i + 1; r < p + kb; r++) {
-                dd_t lri = ld_dd(A, n, r, i);
+                sc_t lri = ld_sc(W, A, n, r, i);
                 for (int64_t j = p + kb; j < n; j++)
-                    st_dd(A, n, r, j, dd_sub(ld_dd(A, n, r, j), dd_mul(lri, ld_dd(A, n, i, j))));
+                    st_sc(W, A, n, r, j, sc_sub(W, ld_sc(W, A, n, r, j), sc_mul(W, lri, ld_sc(W, A, n, i, j))));
             }
         /* step 3: A22 := A22 - L21 U12, T := gemm(L21, U12) first (the underlined term) */
-        mat_t L21 = mat_alloc(2, n2, kb), U12 = mat_alloc(2, kb, n2), Tm = mat_alloc(2, n2, n2);
-        for (int64_t i = 0; i < n2; i++)
-            for (int64_t j = 0; j < kb; j++) {
-                dd_t v = ld_dd(A, n, p + kb + i, p + j);
-                set_w(&L21, 0, i, j, v.hi); set_w(&L21, 1, i, j, v.lo);
-            }
-        for (int64_t i = 0; i < kb; i++)
-            for (int64_t j = 0; j < n2; j++) {
-                dd_t v = ld_dd(A, n, p + i, p + kb + j);
-                set_w(&U12, 0, i, j, v.hi); set_w(&U12, 1, i, j, v.lo);
-            }
+        mat_t L21 = mat_alloc(W, n2, kb), U12 = mat_alloc(W, kb, n2), Tm = mat_alloc(W, n2, n2);
+        for (int w = 0; w < W; w++) {
+            for (int64_t i = 0; i < n2; i++)
+                for (int64_t j = 0; j < kb; j++) set_w(&L21, w, i, j, A[w * n * n + (p + kb + i) * n + p + j]);
+            for (int64_t i = 0; i < kb; i++)
+                for (int64_t j = 0; j < n2; j++) set_w(&U12, w, i, j, A[w * n * n + (p + i) * n + p + kb + j]);
+        }
         gemm_any(algo, T, &L21, &U12, &Tm);
 #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n2; i++)
             for (int64_t j = 0; j < n2; j++) {
-                dd_t t = { get_w(&Tm, 0, i, j), get_w(&Tm, 1, i, j) };
+                sc_t t = { { 0.0, 0.0, 0.0, 0.0 } };
+                for (int w = 0; w < W; w++) t.w[w] = get_w(&Tm, w, i, j);
                 int64_t gi = p + kb + i, gj = p + kb + j;
-                st_dd(A, n, gi, gj, dd_sub(ld_dd(A, n, gi, gj), t));
+                st_sc(W, A, n, gi, gj, sc_sub(W, ld_sc(W, A, n, gi, gj), t));
             }
         mat_free(&L21); mat_free(&U12); mat_free(&Tm);
     }
@@ -577,34 +632,31 @@ int or_lu(int64_t n, double *A, int64_t *ipiv, int64_t K, int algo, int64_t T, i
 }
 
 /* Solve with the factors of or_lu (numerics.md s.5): y := P b; forward (unit L,
- * j ascending); backward (j descending, x_j = dd_div(y_j, u_jj)). b, x: [2][n]. */
-void or_lu_solve(int64_t n, const double *LU, const int64_t *ipiv, const double *b, double *x) {
-    double *y = (double *)malloc((size_t)(2 * (n > 0 ? n : 1)) * sizeof(double));
-    for (int64_t i = 0; i < n; i++) { y[i] = b[i]; y[n + i] = b[n + i]; }
+ * j ascending); backward (j descending, x_j = div(y_j, u_jj)). b, x: [W][n]. */
+void or_lu_solve(int W, int64_t n, const double *LU, const int64_t *ipiv, const double *b, double *x) {
+    double *y = (double *)malloc((size_t)(W * (n > 0 ? n : 1)) * sizeof(double));
+    for (int64_t i = 0; i < W * n; i++) y[i] = b[i];
     for (int64_t k = 0; k < n; k++) {
         int64_t r = ipiv[k];
-        if (r != k) {
-            double t0 = y[k], t1 = y[n + k];
-            y[k] = y[r]; y[n + k] = y[n + r]; y[r] = t0; y[n + r] = t1;
-        }
+        if (r != k)
+            for (int w = 0; w < W; w++) {
+                double t = y[w * n + k];
+                y[w * n + k] = y[w * n + r];
+                y[w * n + r] = t;
+            }
     }
+#define YV(i) ({ sc_t v_ = { { 0.0, 0.0, 0.0, 0.0 } }; for (int w_ = 0; w_ < W; w_++) v_.w[w_] = y[w_ * n + (i)]; v_; })
+#define YS(i, v) do { sc_t s_ = (v); for (int w_ = 0; w_ < W; w_++) y[w_ * n + (i)] = s_.w[w_]; } while (0)
     for (int64_t j = 0; j < n; j++) {
-        dd_t yj = { y[j], y[n + j] };
-        for (int64_t i = j + 1; i < n; i++) {
-            dd_t yi = { y[i], y[n + i] };
-            yi = dd_sub(yi, dd_mul(ld_dd(LU, n, i, j), yj));
-            y[i] = yi.hi; y[n + i] = yi.lo;
-        }
+        sc_t yj = YV(j);
+        for (int64_t i = j + 1; i < n; i++) YS(i, sc_sub(W, YV(i), sc_mul(W, ld_sc(W, LU, n, i, j), yj)));
     }
     for (int64_t j = n - 1; j >= 0; j--) {
-        dd_t yj = { y[j], y[n + j] };
-        dd_t xj = dd_div(yj, ld_dd(LU, n, j, j));
-        x[j] = xj.hi; x[n + j] = xj.lo;
-        for (int64_t i = 0; i < j; i++) {
-            dd_t yi = { y[i], y[n + i] };
-            yi = dd_sub(yi, dd_mul(ld_dd(LU, n, i, j), xj));
-            y[i] = yi.hi; y[n + i] = yi.lo;
-        }
+        sc_t xj = sc_div(W, YV(j), ld_sc(W, LU, n, j, j));
+        for (int w = 0; w < W; w++) x[w * n + j] = xj.w[w];
+        for (int64_t i = 0; i < j; i++) YS(i, sc_sub(W, YV(i), sc_mul(W, ld_sc(W, LU, n, i, j), xj)));
     }
+#undef YV
+#undef YS
     free(y);
 }

@@ -13,7 +13,7 @@ from __future__ import annotations
 import ctypes
 import os
 
-__all__ = ["dd_gemm", "qd_gemm", "gemm", "gemm_ex", "dd_lu_solve", "elementwise", "lib",
+__all__ = ["dd_gemm", "qd_gemm", "gemm", "gemm_ex", "dd_lu_solve", "qd_lu_solve", "lu_solve", "elementwise", "lib",
            "workspace_bytes", "set_workspace_limit", "launch_count", "release",
            "profile_start", "profile_stop", "fp64_peak",
            "BLOCK", "STRASSEN", "WINOGRAD", "DDQDError"]
@@ -57,6 +57,8 @@ def _load():
         f.restype = i32
     L.ddqd_gemm_ex.argtypes = [ctypes.POINTER(GemmDesc)]
     L.dd_lu_solve.argtypes = [i64, vp, vp, vp, vp, i64, i32, i64]
+    L.qd_lu_solve.argtypes = [i64, vp, vp, vp, vp, i64, i32, i64]
+    L.ddqd_lu_solve.argtypes = [i32, i32, i64, vp, vp, vp, vp, i64, i32, i64]
     L.ddqd_elementwise.argtypes = [i32, i32, i64, vp, vp, vp, vp]
     L.ddqd_set_stream.argtypes = [vp]
     L.ddqd_workspace_bytes.argtypes = [i32, i64, i64, i64, i32, i64]
@@ -74,7 +76,7 @@ def _load():
 
 lib = _load()
 
-EXPORTED = ["dd_gemm", "qd_gemm", "ddqd_gemm_ex", "dd_lu_solve", "ddqd_elementwise", "ddqd_set_stream",
+EXPORTED = ["dd_gemm", "qd_gemm", "ddqd_gemm_ex", "dd_lu_solve", "qd_lu_solve", "ddqd_lu_solve", "ddqd_elementwise", "ddqd_set_stream",
             "ddqd_workspace_bytes", "ddqd_set_workspace", "ddqd_set_workspace_limit",
             "ddqd_launch_count", "ddqd_release", "ddqd_last_error", "ddqd_version",
             "ddqd_profile_start", "ddqd_profile_stop", "ddqd_fp64_peak", "ddqd_pre_add", "ddqd_post_add"]
@@ -196,21 +198,39 @@ def gemm_batched(A, B, C, algo, threshold, beta=0):
                    C.data_ptr(), n, m * n, W * m * n, beta)
 
 
-def dd_lu_solve(A, b, panel=256, algo="strassen", threshold=128, overwrite=False):
-    """Blocked right-looking DD LU with partial pivoting + solve (Eq. 2).
-    A: [2,n,n] CUDA float64, b: [2,n]. Returns (x, LU, ipiv, info)."""
+def lu_solve(A, b, panel=256, algo="strassen", threshold=128, pivot=True, overwrite=False):
+    """Blocked right-looking DD/QD LU (partial pivoting, or the paper's pivot-free variant with
+    pivot=False) + solve (Eq. 2). A: [W,n,n] CUDA float64, b: [W,n], W = 2 or 4.
+    Returns (x, LU, ipiv, info)."""
     torch = _torch()
-    _check_mat(A, 2, "A")
+    W = A.shape[0]
+    if W not in (2, 4):
+        raise ValueError("A must be [2|4, n, n]")
+    _check_mat(A, W, "A")
     n = A.shape[1]
-    if A.shape[2] != n or tuple(b.shape) != (2, n) or b.dtype != torch.float64 or not b.is_contiguous():
-        raise ValueError("A must be [2,n,n] and b [2,n] contiguous float64")
+    if A.shape[2] != n or tuple(b.shape) != (W, n) or b.dtype != torch.float64 or not b.is_contiguous():
+        raise ValueError("A must be [W,n,n] and b [W,n] contiguous float64")
     LU = A if overwrite else A.clone()
     x = torch.empty_like(b)
     ipiv = torch.empty(n, dtype=torch.int64, device=A.device)
     _set_stream(A)
-    info = _check(lib.dd_lu_solve(n, LU.data_ptr(), b.data_ptr(), x.data_ptr(), ipiv.data_ptr(),
-                                  panel, _algo(algo), threshold), "dd_lu_solve")
+    info = _check(lib.ddqd_lu_solve(W, 1 if pivot else 0, n, LU.data_ptr(), b.data_ptr(), x.data_ptr(),
+                                    ipiv.data_ptr(), panel, _algo(algo), threshold), "lu_solve")
     return x, LU, ipiv, info
+
+
+def dd_lu_solve(A, b, panel=256, algo="strassen", threshold=128, overwrite=False):
+    """DD LU with partial pivoting + solve (BJ:11). Returns (x, LU, ipiv, info)."""
+    if A.shape[0] != 2:
+        raise ValueError("dd_lu_solve takes [2, n, n]")
+    return lu_solve(A, b, panel, algo, threshold, True, overwrite)
+
+
+def qd_lu_solve(A, b, panel=256, algo="strassen", threshold=128, overwrite=False):
+    """QD LU with partial pivoting + solve. Returns (x, LU, ipiv, info)."""
+    if A.shape[0] != 4:
+        raise ValueError("qd_lu_solve takes [4, n, n]")
+    return lu_solve(A, b, panel, algo, threshold, True, overwrite)
 
 
 _OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "madd": 4}

@@ -113,8 +113,8 @@ size_t workspace_limit() {
     return g_limit;
 }
 
-int lu_solve_impl(int64_t n, double *A, const double *b, double *x, int64_t *ipiv, int64_t K,
-                  int algo, int64_t T, cudaStream_t s, int *info_out);
+int lu_solve_impl(int W, int pivot, int64_t n, double *A, const double *b, double *x, int64_t *ipiv,
+                  int64_t K, int algo, int64_t T, cudaStream_t s, int *info_out);
 
 static bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
     const char *pa = static_cast<const char *>(a), *pb = static_cast<const char *>(b);
@@ -210,19 +210,31 @@ int ddqd_gemm_ex(const ddqd_gemm_desc *d) {
     return run_gemm(d->prec, d->algo, d->threshold, d->m, d->l, d->n, d->batch, A, B, C, d->beta, t_stream);
 }
 
-int dd_lu_solve(int64_t n, double *A, const double *b, double *x, int64_t *ipiv, int64_t panel, int algo,
-                int64_t threshold) {
+int ddqd_lu_solve(int prec, int pivot, int64_t n, double *A, const double *b, double *x, int64_t *ipiv,
+                  int64_t panel, int algo, int64_t threshold) {
     t_err.clear();
+    if (prec != 2 && prec != 4) { set_error("prec must be DDQD_DD or DDQD_QD"); return DDQD_EINVAL; }
+    if (pivot != 0 && pivot != 1) { set_error("pivot must be 0 or 1"); return DDQD_EINVAL; }
     if (n < 0 || panel < 1) { set_error("n must be >= 0 and panel >= 1"); return DDQD_EINVAL; }
     int rc = check_gemm_args(n, panel, n, algo, threshold);
     if (rc) return rc;
     if (n == 0) return DDQD_OK;
     if (!A || !b || !x || !ipiv) { set_error("null pointer"); return DDQD_EINVAL; }
-    if (where(A) || where(b) || where(x) || where(ipiv)) { set_error("dd_lu_solve takes device pointers only"); return DDQD_ENOTSUP; }
+    if (where(A) || where(b) || where(x) || where(ipiv)) { set_error("LU takes device pointers only"); return DDQD_ENOTSUP; }
     int info = 0;
-    rc = lu_solve_impl(n, A, b, x, ipiv, panel, algo, threshold, t_stream, &info);
+    rc = lu_solve_impl(prec, pivot, n, A, b, x, ipiv, panel, algo, threshold, t_stream, &info);
     if (rc) return rc;
     return info;
+}
+
+int dd_lu_solve(int64_t n, double *A, const double *b, double *x, int64_t *ipiv, int64_t panel, int algo,
+                int64_t threshold) {
+    return ddqd_lu_solve(2, 1, n, A, b, x, ipiv, panel, algo, threshold);
+}
+
+int qd_lu_solve(int64_t n, double *A, const double *b, double *x, int64_t *ipiv, int64_t panel, int algo,
+                int64_t threshold) {
+    return ddqd_lu_solve(4, 1, n, A, b, x, ipiv, panel, algo, threshold);
 }
 
 static MatDesc to_desc(const ddqd_mat *x) { return MatDesc{x->p, x->rows, x->cols, x->ld, x->ps, x->bs}; }
@@ -256,7 +268,7 @@ int ddqd_post_add(int prec, int algo, int64_t P, const ddqd_mat *M, const ddqd_m
 int ddqd_elementwise(int prec, int op, int64_t count, const double *x, const double *y, const double *w,
                      double *z) {
     t_err.clear();
-    if ((prec != 2 && prec != 4) || op < 0 || op > 4 || (prec == 4 && op == 3) || count < 0) {
+    if ((prec != 2 && prec != 4) || op < 0 || op > 4 || count < 0) {
         set_error("bad elementwise arguments");
         return DDQD_EINVAL;
     }

@@ -179,7 +179,7 @@ __global__ void elementwise_kernel(int op, int64_t count, const double *x, const
         else if constexpr (W == 2) {
             r = (op == 2) ? dd_mul(a, b) : dd_div(a, b);
         } else {
-            r = qd_mul(a, b);
+            r = (op == 2) ? qd_mul(a, b) : qd_div(a, b);
         }
         E::store(z + i, count, r);
     }

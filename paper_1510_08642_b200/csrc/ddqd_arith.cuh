@@ -176,6 +176,29 @@ __device__ __forceinline__ qd qd_madd(const qd &c, const qd &a, const qd &b) {
     return qd_add(c, qd_mul(a, b));
 }
 
+// qd_div (numerics.md s.3): long division with three correction steps, then renorm.
+__device__ __forceinline__ qd qd_div(const qd &a, const qd &b) {
+    qd r = a, t;
+    double q[4];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        q[i] = __ddiv_rn(r.w[0], b.w[0]);
+        t.w[0] = q[i]; t.w[1] = 0.0; t.w[2] = 0.0; t.w[3] = 0.0;
+        r = qd_sub(r, qd_mul(b, t));
+    }
+    q[3] = __ddiv_rn(r.w[0], b.w[0]);
+    return qd_renorm(q[0], q[1], q[2], q[3], 0.0);
+}
+// |x| > |y| in the QD magnitude order (words compared lexicographically after the sign fold)
+__device__ __forceinline__ bool qd_abs_gt(const qd &x, const qd &y) {
+    const qd ax = x.w[0] >= 0.0 ? x : qd_neg(x);
+    const qd ay = y.w[0] >= 0.0 ? y : qd_neg(y);
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+        if (ax.w[i] != ay.w[i]) return ax.w[i] > ay.w[i];
+    return false;
+}
+
 // ---- width-generic element type: W = 2 (DD) or 4 (QD) -----------------------------
 template <int W> struct elem;
 template <> struct elem<2> {
@@ -187,6 +210,11 @@ template <> struct elem<2> {
     static __device__ __forceinline__ T load(const double *p, int64_t ps) { return dd{p[0], p[ps]}; }
     static __device__ __forceinline__ void store(double *p, int64_t ps, T v) { p[0] = v.hi; p[ps] = v.lo; }
     static __device__ __forceinline__ double word(const T &v, int w) { return w == 0 ? v.hi : v.lo; }
+    static __device__ __forceinline__ void set_word(T &v, int w, double x) { if (w == 0) v.hi = x; else v.lo = x; }
+    static __device__ __forceinline__ T one() { return dd{1.0, 0.0}; }
+    static __device__ __forceinline__ T mul(T x, T y) { return dd_mul(x, y); }
+    static __device__ __forceinline__ T div(T x, T y) { return dd_div(x, y); }
+    static __device__ __forceinline__ bool abs_gt(T x, T y) { return dd_abs_gt(x, y); }
 };
 template <> struct elem<4> {
     using T = qd;
@@ -200,6 +228,12 @@ template <> struct elem<4> {
     static __device__ __forceinline__ void store(double *p, int64_t ps, const T &v) {
         p[0] = v.w[0]; p[ps] = v.w[1]; p[2 * ps] = v.w[2]; p[3 * ps] = v.w[3];
     }
+    static __device__ __forceinline__ double word(const T &v, int w) { return v.w[w]; }
+    static __device__ __forceinline__ void set_word(T &v, int w, double x) { v.w[w] = x; }
+    static __device__ __forceinline__ T one() { qd r; r.w[0] = 1.0; r.w[1] = r.w[2] = r.w[3] = 0.0; return r; }
+    static __device__ __forceinline__ T mul(const T &x, const T &y) { return qd_mul(x, y); }
+    static __device__ __forceinline__ T div(const T &x, const T &y) { return qd_div(x, y); }
+    static __device__ __forceinline__ bool abs_gt(const T &x, const T &y) { return qd_abs_gt(x, y); }
 };
 
 }  // namespace ddqd

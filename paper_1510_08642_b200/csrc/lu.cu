@@ -1,13 +1,17 @@
-// lu.cu -- blocked right-looking DD LU with partial pivoting and the triangular solves
-// (north_star subsystem (5); PAPER.md P:121-133 steps 1-3, Eq. (2)
-// P:124-126; pivoting per BJ:11). Op sequences: docs/numerics.md s.5.
+// lu.cu -- blocked right-looking DD/QD LU (partial pivoting, or the paper's pivot-free
+// variant) and the triangular solves (north_star subsystem (5), NEXT row f1;
+// PAPER.md P:121-133 steps 1-3, Eq. (2); pivoting per BJ:11).
+// Op sequences: docs/numerics.md s.5. Templated on W = 2 (DD) / 4 (QD) words.
 //
-// Per panel of width K: for each column k a single-CTA kernel does the DD argmax (ties to
-// the lowest row), the full-row interchange, the reciprocal of the pivot and the scaling
-// of the column; a 2-D kernel does the rank-1 update of the rest of the panel. U12 is
-// formed by a shared-memory forward substitution (one CTA per column strip), and the
-// Schur update A22 := A22 - L21 U12 (the underlined term of P:131) is the library GEMM
-// (Block/Strassen/Winograd) with beta = 1. Nothing returns to the host until the end.
+// Per panel of width K: a persistent cooperative kernel factors the panel (rows held in
+// shared memory across all SMs, one grid barrier per column: DD/QD argmax with ties to the
+// lowest row, interchange, reciprocal, column scaling, rank-1 update); when the panel does not
+// fit in shared memory a per-column pair of kernels does the same steps. Interchanges of the
+// columns outside the panel are applied afterwards (they commute with the panel's column
+// operations). U12 is formed by a shared-memory forward substitution (one CTA per column
+// strip), and the Schur update A22 := A22 - L21 U12 (the underlined term of P:131) is the
+// library GEMM (Block/Strassen/Winograd) with beta = 1. Nothing returns to the host until
+// the end.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -21,393 +25,267 @@ namespace ddqd {
 
 void *aux_get(size_t bytes, int *status);   // abi.cu (separate from the GEMM workspace)
 
-__device__ __forceinline__ dd ldA(const double *A, int64_t n, int64_t i, int64_t j) {
-    return dd{A[i * n + j], A[n * n + i * n + j]};
+template <int W>
+__device__ __forceinline__ typename elem<W>::T ldA(const double *A, int64_t n, int64_t i, int64_t j) {
+    return elem<W>::load(A + i * n + j, n * n);
 }
-__device__ __forceinline__ void stA(double *A, int64_t n, int64_t i, int64_t j, dd v) {
-    A[i * n + j] = v.hi;
-    A[n * n + i * n + j] = v.lo;
+template <int W>
+__device__ __forceinline__ void stA(double *A, int64_t n, int64_t i, int64_t j, const typename elem<W>::T &v) {
+    elem<W>::store(A + i * n + j, n * n, v);
+}
+// planar shared-memory arrays: word w of entry e at s[w * stride + e]
+template <int W>
+__device__ __forceinline__ typename elem<W>::T lds(const double *s, int stride, int e) {
+    typename elem<W>::T v;
+#pragma unroll
+    for (int w = 0; w < W; w++) elem<W>::set_word(v, w, s[w * stride + e]);
+    return v;
+}
+template <int W>
+__device__ __forceinline__ void sts(double *s, int stride, int e, const typename elem<W>::T &v) {
+#pragma unroll
+    for (int w = 0; w < W; w++) s[w * stride + e] = elem<W>::word(v, w);
 }
 
 struct LuAux {
     int info;
     int skip;
-    double rinv_hi, rinv_lo;
+    double rinv[4];
 };
 
-// argmax |a_ik| over i >= k (first index on ties), swap rows k <-> r over all n columns,
-// rinv = 1 / a_kk (dd_div), a_ik := a_ik * rinv for i > k.
-__global__ void __launch_bounds__(1024) lu_pivot_kernel(double *A, int64_t n, int64_t k,
-                                                        int64_t *ipiv, LuAux *aux) {
-    __shared__ double sh_hi[1024], sh_lo[1024];
-    __shared__ int64_t sh_idx[1024];
-    __shared__ int sh_skip;
-    __shared__ double sh_r[2];
-    const int tid = threadIdx.x;
-    dd best{0.0, 0.0};
-    int64_t bidx = -1;
-    for (int64_t i = k + tid; i < n; i += blockDim.x) {
-        dd v = ldA(A, n, i, k);
-        if (bidx < 0 || dd_abs_gt(v, best)) { best = v; bidx = i; }
+// is candidate (a, ia) preferred over (b, ib)? larger magnitude; ties -> lower row; -1 = none
+template <int W>
+__device__ __forceinline__ bool cand_better(const typename elem<W>::T &a, long long ia,
+                                            const typename elem<W>::T &b, long long ib) {
+    if (ia < 0) return false;
+    if (ib < 0) return true;
+    if (elem<W>::abs_gt(a, b)) return true;
+    if (elem<W>::abs_gt(b, a)) return false;
+    return ia < ib;
+}
+
+template <int W>
+__device__ __forceinline__ typename elem<W>::T shfl_down(const typename elem<W>::T &v, int off) {
+    typename elem<W>::T r;
+#pragma unroll
+    for (int w = 0; w < W; w++) elem<W>::set_word(r, w, __shfl_down_sync(0xffffffffu, elem<W>::word(v, w), off));
+    return r;
+}
+
+// block-wide argmax (ties -> lower row); result in slot 0 of (rv [W][32], ri); all threads call
+template <int W>
+__device__ __forceinline__ void block_argmax(typename elem<W>::T v, long long i, double *rv, long long *ri) {
+    using T = typename elem<W>::T;
+    for (int off = 16; off > 0; off >>= 1) {
+        const T ov = shfl_down<W>(v, off);
+        const long long oi = __shfl_down_sync(0xffffffffu, i, off);
+        if (cand_better<W>(ov, oi, v, i)) { v = ov; i = oi; }
     }
-    sh_hi[tid] = best.hi; sh_lo[tid] = best.lo; sh_idx[tid] = bidx;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    __syncthreads();   // slots may still be read from the previous use
+    if (lane == 0) { sts<W>(rv, 32, warp, v); ri[warp] = i; }
     __syncthreads();
-    for (int off = blockDim.x / 2; off > 0; off >>= 1) {
-        if (tid < off) {
-            const int64_t oi = sh_idx[tid + off];
-            if (oi >= 0) {
-                const dd o{sh_hi[tid + off], sh_lo[tid + off]};
-                const dd me{sh_hi[tid], sh_lo[tid]};
-                const int64_t mi = sh_idx[tid];
-                bool take;
-                if (mi < 0) take = true;
-                else if (dd_abs_gt(o, me)) take = true;
-                else if (dd_abs_gt(me, o)) take = false;
-                else take = oi < mi;
-                if (take) { sh_hi[tid] = o.hi; sh_lo[tid] = o.lo; sh_idx[tid] = oi; }
-            }
+    if (warp == 0) {
+        v = lane < nw ? lds<W>(rv, 32, lane) : elem<W>::zero();
+        i = lane < nw ? ri[lane] : -1;
+        for (int off = 16; off > 0; off >>= 1) {
+            const T ov = shfl_down<W>(v, off);
+            const long long oi = __shfl_down_sync(0xffffffffu, i, off);
+            if (cand_better<W>(ov, oi, v, i)) { v = ov; i = oi; }
         }
-        __syncthreads();
+        if (lane == 0) { sts<W>(rv, 32, 0, v); ri[0] = i; }
     }
-    const int64_t r = sh_idx[0];
+    __syncthreads();
+}
+
+// ---- per-column path ---------------------------------------------------------------------
+// pivot row r (argmax over i >= k, or r = k without pivoting), swap rows k <-> r over all n
+// columns, rinv = 1 / a_kk, a_ik := a_ik * rinv for i > k.
+template <int W>
+__global__ void __launch_bounds__(1024) lu_pivot_kernel(double *A, int64_t n, int64_t k, int pivot,
+                                                        int64_t *ipiv, LuAux *aux) {
+    using E = elem<W>;
+    using T = typename E::T;
+    __shared__ double rv[W * 32];
+    __shared__ long long ri[32];
+    __shared__ int sh_skip;
+    __shared__ double sh_r[4];
+    const int tid = threadIdx.x;
+    int64_t r = k;
+    if (pivot) {
+        T best = E::zero();
+        long long bidx = -1;
+        for (int64_t i = k + tid; i < n; i += blockDim.x) {
+            const T v = ldA<W>(A, n, i, k);
+            if (cand_better<W>(v, i, best, bidx)) { best = v; bidx = i; }
+        }
+        block_argmax<W>(best, bidx, rv, ri);
+        r = ri[0];
+    }
     if (r != k) {
         for (int64_t j = tid; j < n; j += blockDim.x) {
-            const dd a = ldA(A, n, k, j), c = ldA(A, n, r, j);
-            stA(A, n, k, j, c);
-            stA(A, n, r, j, a);
+            const T a = ldA<W>(A, n, k, j), c = ldA<W>(A, n, r, j);
+            stA<W>(A, n, k, j, c);
+            stA<W>(A, n, r, j, a);
         }
     }
     __syncthreads();
     if (tid == 0) {
         ipiv[k] = r;
-        const dd piv = ldA(A, n, k, k);
-        if (piv.hi == 0.0) {
+        const T piv = ldA<W>(A, n, k, k);
+        if (E::word(piv, 0) == 0.0) {
             if (aux->info == 0) aux->info = (int)(k + 1);
             sh_skip = 1;
         } else {
-            const dd rv = dd_div(dd{1.0, 0.0}, piv);
-            sh_r[0] = rv.hi; sh_r[1] = rv.lo;
+            const T rvv = E::div(E::one(), piv);
+            for (int w = 0; w < W; w++) sh_r[w] = E::word(rvv, w);
             sh_skip = 0;
         }
         aux->skip = sh_skip;
-        aux->rinv_hi = sh_r[0]; aux->rinv_lo = sh_r[1];
     }
     __syncthreads();
     if (sh_skip) return;
-    const dd rinv{sh_r[0], sh_r[1]};
-    for (int64_t i = k + 1 + tid; i < n; i += blockDim.x) stA(A, n, i, k, dd_mul(ldA(A, n, i, k), rinv));
+    const T rinv = lds<W>(sh_r, 1, 0);
+    for (int64_t i = k + 1 + tid; i < n; i += blockDim.x) stA<W>(A, n, i, k, E::mul(ldA<W>(A, n, i, k), rinv));
 }
 
 // a_ij := a_ij - l_ik * a_kj for i in (k, n), j in (k, jend)
+template <int W>
 __global__ void lu_rank1_kernel(double *A, int64_t n, int64_t k, int64_t jend, const LuAux *aux) {
+    using E = elem<W>;
     if (aux->skip) return;
     const int64_t j = k + 1 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t i = k + 1 + (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
     if (j >= jend || i >= n) return;
-    stA(A, n, i, j, dd_sub(ldA(A, n, i, j), dd_mul(ldA(A, n, i, k), ldA(A, n, k, j))));
+    stA<W>(A, n, i, j, E::sub(ldA<W>(A, n, i, j), E::mul(ldA<W>(A, n, i, k), ldA<W>(A, n, k, j))));
 }
 
-// U12 := L11^{-1} A12 (unit lower, forward substitution in row order), one CTA per strip
-// of cw columns held in shared memory; thread r owns panel row r and prefetches its next
-// multiplier l_{r,i+1} during step i (row-major, so consecutive i are contiguous).
-__global__ void __launch_bounds__(1024) lu_trsm_kernel(double *A, int64_t n, int64_t p, int64_t kb,
-                                                       int64_t c0, int cw) {
-    extern __shared__ double tile[];   // [2][kb][cw]
-    const int64_t col0 = c0 + (int64_t)blockIdx.x * cw;
-    const int ncols = (int)((n - col0) < cw ? (n - col0) : cw);
-    for (int64_t e = threadIdx.x; e < kb * cw; e += blockDim.x) {
-        const int64_t r = e / cw, c = e % cw;
-        if (c < ncols) {
-            const dd v = ldA(A, n, p + r, col0 + c);
-            tile[r * cw + c] = v.hi;
-            tile[kb * cw + r * cw + c] = v.lo;
-        }
-    }
-    const int64_t r = threadIdx.x;   // blockDim.x >= kb (host guarantees)
-    dd lnext{0.0, 0.0};
-    if (r > 0 && r < kb) lnext = ldA(A, n, p + r, p);
-    for (int64_t i = 0; i < kb; i++) {
-        __syncthreads();
-        const dd l = lnext;
-        if (i + 1 < r && r < kb) lnext = ldA(A, n, p + r, p + i + 1);
-        if (r > i && r < kb) {
-            for (int c = 0; c < ncols; c++) {
-                const dd u{tile[i * cw + c], tile[kb * cw + i * cw + c]};
-                dd a{tile[r * cw + c], tile[kb * cw + r * cw + c]};
-                a = dd_sub(a, dd_mul(l, u));
-                tile[r * cw + c] = a.hi;
-                tile[kb * cw + r * cw + c] = a.lo;
-            }
-        }
-    }
-    __syncthreads();
-    for (int64_t e = threadIdx.x; e < kb * cw; e += blockDim.x) {
-        const int64_t rr = e / cw, c = e % cw;
-        if (c < ncols) stA(A, n, p + rr, col0 + c, dd{tile[rr * cw + c], tile[kb * cw + rr * cw + c]});
-    }
-}
-
-// y := P b (ipiv swaps applied in order), in shared memory when it fits.
-__global__ void __launch_bounds__(1024) lu_perm_kernel(const double *b, double *y, const int64_t *ipiv,
-                                                       int64_t n, int use_smem) {
-    extern __shared__ double sy[];
-    double *buf = use_smem ? sy : y;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) { buf[i] = b[i]; buf[n + i] = b[n + i]; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int64_t k = 0; k < n; k++) {
-            const int64_t r = ipiv[k];
-            if (r != k) {
-                double t0 = buf[k], t1 = buf[n + k];
-                buf[k] = buf[r]; buf[n + k] = buf[n + r];
-                buf[r] = t0; buf[n + r] = t1;
-            }
-        }
-    }
-    __syncthreads();
-    if (use_smem)
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) { y[i] = sy[i]; y[n + i] = sy[n + i]; }
-}
-
-// Forward (unit L, j ascending) diagonal block [J, J+nb): one thread per row of the block.
-__global__ void __launch_bounds__(1024) trsv_fwd_diag(const double *A, int64_t n, double *y, int64_t J, int nb) {
-    __shared__ double yh[1024], yl[1024];
-    const int s = threadIdx.x;
-    if (s < nb) { yh[s] = y[J + s]; yl[s] = y[n + J + s]; }
-    dd lnext{0.0, 0.0};
-    if (s > 0 && s < nb) lnext = ldA(A, n, J + s, J);
-    for (int t = 0; t < nb; t++) {
-        __syncthreads();
-        const dd l = lnext;
-        if (t + 1 < s && s < nb) lnext = ldA(A, n, J + s, J + t + 1);   // prefetch
-        if (s > t && s < nb) {
-            dd v{yh[s], yl[s]};
-            v = dd_sub(v, dd_mul(l, dd{yh[t], yl[t]}));
-            yh[s] = v.hi; yl[s] = v.lo;
-        }
-    }
-    __syncthreads();
-    if (s < nb) { y[J + s] = yh[s]; y[n + J + s] = yl[s]; }
-}
-
-// rows i >= J+nb: y_i := y_i - l_ij y_j for j in [J, J+nb) ascending
-__global__ void trsv_fwd_update(const double *A, int64_t n, double *y, int64_t J, int nb) {
-    __shared__ double yh[1024], yl[1024];
-    for (int t = threadIdx.x; t < nb; t += blockDim.x) { yh[t] = y[J + t]; yl[t] = y[n + J + t]; }
-    __syncthreads();
-    const int64_t i = J + nb + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    dd v{y[i], y[n + i]};
-    for (int t = 0; t < nb; t++) v = dd_sub(v, dd_mul(ldA(A, n, i, J + t), dd{yh[t], yl[t]}));
-    y[i] = v.hi; y[n + i] = v.lo;
-}
-
-// Backward diagonal block: for t descending, x_t = y_t / u_tt, then rows s < t update.
-__global__ void __launch_bounds__(1024) trsv_bwd_diag(const double *A, int64_t n, double *y, double *x,
-                                                      int64_t J, int nb) {
-    __shared__ double yh[1024], yl[1024];
-    const int s = threadIdx.x;
-    if (s < nb) { yh[s] = y[J + s]; yl[s] = y[n + J + s]; }
-    // thread s < nb holds u_{s,t} for the current t (prefetched one step ahead; u_ss is the
-    // divisor when t == s)
-    dd unext{0.0, 0.0};
-    if (s < nb) unext = ldA(A, n, J + s, J + nb - 1);
-    for (int t = nb - 1; t >= 0; t--) {
-        __syncthreads();
-        const dd u = unext;
-        if (s < nb && t - 1 >= s) unext = ldA(A, n, J + s, J + t - 1);
-        if (s == t) {
-            const dd xv = dd_div(dd{yh[t], yl[t]}, u);
-            yh[t] = xv.hi; yl[t] = xv.lo;   // slot t now holds x_t
-        }
-        __syncthreads();
-        if (s < t) {
-            dd v{yh[s], yl[s]};
-            v = dd_sub(v, dd_mul(u, dd{yh[t], yl[t]}));
-            yh[s] = v.hi; yl[s] = v.lo;
-        }
-    }
-    __syncthreads();
-    if (s < nb) { x[J + s] = yh[s]; x[n + J + s] = yl[s]; }
-}
-
-// rows i < J: y_i := y_i - u_ij x_j for j in [J, J+nb) descending
-__global__ void trsv_bwd_update(const double *A, int64_t n, double *y, const double *x, int64_t J, int nb) {
-    __shared__ double xh[1024], xl[1024];
-    for (int t = threadIdx.x; t < nb; t += blockDim.x) { xh[t] = x[J + t]; xl[t] = x[n + J + t]; }
-    __syncthreads();
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= J) return;
-    dd v{y[i], y[n + i]};
-    for (int t = nb - 1; t >= 0; t--) v = dd_sub(v, dd_mul(ldA(A, n, i, J + t), dd{xh[t], xl[t]}));
-    y[i] = v.hi; y[n + i] = v.lo;
-}
-
-// ---- persistent cooperative panel factorisation ------------------------------------------
+// ---- persistent cooperative panel factorisation --------------------------------------------
 // One launch per panel. CTA b owns rows [p + b*rows_per, ...) of the panel (n-p rows x kb
-// columns) in shared memory. Per column: local DD argmax -> candidate (value, row, the row's
-// kb words) published to a double-buffered global scratch -> ONE grid-wide barrier -> every
-// CTA reduces the G candidates identically (ties -> lowest row), applies the row interchange
-// to the rows it owns, forms rinv = 1/u_kk, scales its column entries and does its part of the
-// rank-1 update. Rows outside the panel are interchanged afterwards by lu_laswp_kernel (the
-// swaps commute with the panel's column operations), so results equal the per-step
-// full-row-swap order of numerics.md s.5 bit for bit.
-__device__ __forceinline__ bool cand_better(double h1, double l1, long long i1, double h2, double l2,
-                                            long long i2) {
-    // is candidate 1 preferred over candidate 2? (larger DD magnitude; ties -> lower row; -1 = none)
-    if (i1 < 0) return false;
-    if (i2 < 0) return true;
-    const dd a{h1, l1}, b{h2, l2};
-    if (dd_abs_gt(a, b)) return true;
-    if (dd_abs_gt(b, a)) return false;
-    return i1 < i2;
-}
-
-// block-wide DD argmax (ties -> lower row); result in slot 0 of (rh, rl, ri); all threads call
-__device__ __forceinline__ void block_argmax(double h, double l, long long i, double *rh, double *rl,
-                                             long long *ri) {
-    for (int off = 16; off > 0; off >>= 1) {
-        const double oh = __shfl_down_sync(0xffffffffu, h, off);
-        const double ol = __shfl_down_sync(0xffffffffu, l, off);
-        const long long oi = __shfl_down_sync(0xffffffffu, i, off);
-        if (cand_better(oh, ol, oi, h, l, i)) { h = oh; l = ol; i = oi; }
-    }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-    __syncthreads();   // slots may still be read from the previous use
-    if (lane == 0) { rh[warp] = h; rl[warp] = l; ri[warp] = i; }
-    __syncthreads();
-    if (warp == 0) {
-        h = lane < nw ? rh[lane] : 0.0;
-        l = lane < nw ? rl[lane] : 0.0;
-        i = lane < nw ? ri[lane] : -1;
-        for (int off = 16; off > 0; off >>= 1) {
-            const double oh = __shfl_down_sync(0xffffffffu, h, off);
-            const double ol = __shfl_down_sync(0xffffffffu, l, off);
-            const long long oi = __shfl_down_sync(0xffffffffu, i, off);
-            if (cand_better(oh, ol, oi, h, l, i)) { h = oh; l = ol; i = oi; }
-        }
-        if (lane == 0) { rh[0] = h; rl[0] = l; ri[0] = i; }
-    }
-    __syncthreads();
-}
-
+// columns) in shared memory. Per column: local argmax -> candidate (value, row, the row's kb
+// entries) published to a double-buffered global scratch -> ONE grid barrier -> every CTA
+// reduces the G candidates identically, interchanges the rows it owns, forms rinv = 1/u_kk,
+// scales its column entries and does its part of the rank-1 update.
+template <int W>
 __global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n, int64_t p, int kb,
-                                                            int rows_per, int64_t *ipiv, LuAux *aux,
-                                                            double *scr) {
+                                                            int rows_per, int pivot, int64_t *ipiv,
+                                                            LuAux *aux, double *scr) {
+    using E = elem<W>;
+    using T = typename E::T;
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double sm[];
     const int G = gridDim.x;
     const int tid = threadIdx.x;
-    double *Sh = sm;                              // [rows_per][kb]
-    double *Sl = Sh + (size_t)rows_per * kb;
-    double *Uh = Sl + (size_t)rows_per * kb;      // new row k (pivot row)
-    double *Ul = Uh + kb;
-    double *Lh = Ul + kb;                          // l_ik of owned rows
-    double *Ll = Lh + rows_per;
-    __shared__ double rh[256], rl[256];
-    __shared__ long long ri[256];
-    __shared__ double s_rinv[2];
-    __shared__ long long s_r;
-    __shared__ int s_w, s_skip;
+    const int SS = rows_per * kb;                 // plane stride of the slab
+    double *S = sm;                               // [W][rows_per][kb]
+    double *U = S + (size_t)W * SS;               // [W][kb] new row k (pivot row)
+    double *L = U + (size_t)W * kb;               // [W][rows_per] multipliers of owned rows
+    __shared__ double rv[W * 32];
+    __shared__ long long ri[32];
+    __shared__ double s_rinv[4];
+    __shared__ int s_skip;
 
     const int64_t r0 = p + (int64_t)blockIdx.x * rows_per;
     const int64_t left = n - r0;
     const int nrows = left <= 0 ? 0 : (int)(left < rows_per ? left : rows_per);
-    // scratch layout per buffer parity: cand (h, l, idx) [G] x 3, cand rows [G][2][kb], krow [2][kb]
-    const size_t per_buf = (size_t)G * 3 + (size_t)G * 2 * kb + 2 * (size_t)kb;
+    // scratch per buffer parity: cand value [W][G], cand idx [G], cand rows [G][W][kb], krow [W][kb]
+    const size_t per_buf = (size_t)G * (W + 1) + (size_t)G * W * kb + (size_t)W * kb;
 
     for (int e = tid; e < nrows * kb; e += blockDim.x) {
         const int li = e / kb, j = e % kb;
-        const dd v = ldA(A, n, r0 + li, p + j);
-        Sh[e] = v.hi; Sl[e] = v.lo;
+        sts<W>(S, SS, e, ldA<W>(A, n, r0 + li, p + j));
     }
     __syncthreads();
 
     for (int kk = 0; kk < kb; kk++) {
         const int64_t k = p + kk;
         double *buf = scr + (size_t)(kk & 1) * per_buf;
-        double *cand_h = buf, *cand_l = buf + G;
-        long long *cand_i = reinterpret_cast<long long *>(buf + 2 * G);
-        double *cand_rows = buf + 3 * G;                 // [G][2][kb]
-        double *krow = cand_rows + (size_t)G * 2 * kb;   // [2][kb]
+        double *cand_v = buf;                                            // [W][G]
+        long long *cand_i = reinterpret_cast<long long *>(buf + (size_t)W * G);
+        double *cand_rows = buf + (size_t)(W + 1) * G;                   // [G][W][kb]
+        double *krow = cand_rows + (size_t)G * W * kb;                   // [W][kb]
 
-        // 1. local argmax of column kk over owned rows >= k
-        double bh = 0.0, bl = 0.0;
+        // 1. local candidate of column kk over owned rows >= k (row k only without pivoting)
+        T best = E::zero();
         long long bi = -1;
         for (int li = tid; li < nrows; li += blockDim.x) {
             const int64_t gi = r0 + li;
-            if (gi < k) continue;
-            const double h = Sh[li * kb + kk], l = Sl[li * kb + kk];
-            if (cand_better(h, l, gi, bh, bl, bi)) { bh = h; bl = l; bi = gi; }
+            if (gi < k || (!pivot && gi != k)) continue;
+            const T v = lds<W>(S, SS, li * kb + kk);
+            if (cand_better<W>(v, gi, best, bi)) { best = v; bi = gi; }
         }
-        block_argmax(bh, bl, bi, rh, rl, ri);
+        block_argmax<W>(best, bi, rv, ri);
         const long long lbi = ri[0];
-        if (tid == 0) { cand_h[blockIdx.x] = rh[0]; cand_l[blockIdx.x] = rl[0]; cand_i[blockIdx.x] = lbi; }
+        if (tid == 0) {
+            for (int w = 0; w < W; w++) cand_v[(size_t)w * G + blockIdx.x] = rv[w * 32];
+            cand_i[blockIdx.x] = lbi;
+        }
         if (lbi >= 0) {
             const int li = (int)(lbi - r0);
-            for (int j = tid; j < kb; j += blockDim.x) {
-                cand_rows[((size_t)blockIdx.x * 2 + 0) * kb + j] = Sh[li * kb + j];
-                cand_rows[((size_t)blockIdx.x * 2 + 1) * kb + j] = Sl[li * kb + j];
-            }
+            for (int j = tid; j < kb; j += blockDim.x)
+                for (int w = 0; w < W; w++) cand_rows[((size_t)blockIdx.x * W + w) * kb + j] = S[w * SS + li * kb + j];
         }
         const bool own_k = k >= r0 && k < r0 + nrows;
         if (own_k) {
             const int li = (int)(k - r0);
-            for (int j = tid; j < kb; j += blockDim.x) { krow[j] = Sh[li * kb + j]; krow[kb + j] = Sl[li * kb + j]; }
+            for (int j = tid; j < kb; j += blockDim.x)
+                for (int w = 0; w < W; w++) krow[(size_t)w * kb + j] = S[w * SS + li * kb + j];
         }
         __threadfence();
         grid.sync();
 
-        // 2. global pivot (identical reduction in every CTA): candidates are rows, so the
-        // winning CTA is recovered from the winning row index
+        // 2. global pivot, identical in every CTA; the winning CTA follows from the row index
         {
-            double h = 0.0, l = 0.0;
+            T v = E::zero();
             long long i = -1;
             for (int g = tid; g < G; g += blockDim.x) {
-                const double ch = cand_h[g], cl = cand_l[g];
-                const long long ci = cand_i[g];
-                if (cand_better(ch, cl, ci, h, l, i)) { h = ch; l = cl; i = ci; }
+                T cv;
+                for (int w = 0; w < W; w++) E::set_word(cv, w, __ldcg(cand_v + (size_t)w * G + g));
+                const long long ci = __ldcg(cand_i + g);
+                if (cand_better<W>(cv, ci, v, i)) { v = cv; i = ci; }
             }
-            block_argmax(h, l, i, rh, rl, ri);
-            if (tid == 0) { s_r = ri[0]; s_w = (int)((ri[0] - p) / rows_per); }
+            block_argmax<W>(v, i, rv, ri);
         }
-        __syncthreads();
-        const int64_t r = s_r;
-        const double *prow = cand_rows + (size_t)s_w * 2 * kb;
-        for (int j = tid; j < kb; j += blockDim.x) { Uh[j] = prow[j]; Ul[j] = prow[kb + j]; }
+        const int64_t r = ri[0];
+        const int wc = (int)((r - p) / rows_per);
+        const double *prow = cand_rows + (size_t)wc * W * kb;
+        for (int j = tid; j < kb; j += blockDim.x)
+            for (int w = 0; w < W; w++) U[w * kb + j] = __ldcg(prow + (size_t)w * kb + j);
         __syncthreads();
         if (r != k) {
             if (own_k) {
                 const int li = (int)(k - r0);
-                for (int j = tid; j < kb; j += blockDim.x) { Sh[li * kb + j] = Uh[j]; Sl[li * kb + j] = Ul[j]; }
+                for (int j = tid; j < kb; j += blockDim.x)
+                    for (int w = 0; w < W; w++) S[w * SS + li * kb + j] = U[w * kb + j];
             }
             if (r >= r0 && r < r0 + nrows) {
                 const int li = (int)(r - r0);
-                for (int j = tid; j < kb; j += blockDim.x) { Sh[li * kb + j] = krow[j]; Sl[li * kb + j] = krow[kb + j]; }
+                for (int j = tid; j < kb; j += blockDim.x)
+                    for (int w = 0; w < W; w++) S[w * SS + li * kb + j] = __ldcg(krow + (size_t)w * kb + j);
             }
         }
         if (tid == 0) {
-            const dd piv{Uh[kk], Ul[kk]};
+            const T piv = lds<W>(U, kb, kk);
             if (blockIdx.x == 0) ipiv[k] = r;
-            if (piv.hi == 0.0) {
+            if (E::word(piv, 0) == 0.0) {
                 s_skip = 1;
                 if (blockIdx.x == 0 && aux->info == 0) aux->info = (int)(k + 1);
             } else {
-                const dd rv = dd_div(dd{1.0, 0.0}, piv);
-                s_rinv[0] = rv.hi; s_rinv[1] = rv.lo;
+                const T rvv = E::div(E::one(), piv);
+                for (int w = 0; w < W; w++) s_rinv[w] = E::word(rvv, w);
                 s_skip = 0;
             }
         }
         __syncthreads();
         if (s_skip) continue;
         // 3. l_ik = a_ik * rinv for owned rows i > k
-        const dd rinv{s_rinv[0], s_rinv[1]};
+        const T rinv = lds<W>(s_rinv, 1, 0);
         for (int li = tid; li < nrows; li += blockDim.x) {
             if (r0 + li <= k) continue;
-            const dd lv = dd_mul(dd{Sh[li * kb + kk], Sl[li * kb + kk]}, rinv);
-            Sh[li * kb + kk] = lv.hi; Sl[li * kb + kk] = lv.lo;
-            Lh[li] = lv.hi; Ll[li] = lv.lo;
+            const T lv = E::mul(lds<W>(S, SS, li * kb + kk), rinv);
+            sts<W>(S, SS, li * kb + kk, lv);
+            sts<W>(L, rows_per, li, lv);
         }
         __syncthreads();
         // 4. rank-1 update a_ij -= l_ik u_kj, j in (kk, kb)
@@ -416,24 +294,23 @@ __global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n
             for (int e = tid; e < nrows * ncol; e += blockDim.x) {
                 const int li = e / ncol, j = kk + 1 + e % ncol;
                 if (r0 + li <= k) continue;
-                const dd a{Sh[li * kb + j], Sl[li * kb + j]};
-                const dd v = dd_sub(a, dd_mul(dd{Lh[li], Ll[li]}, dd{Uh[j], Ul[j]}));
-                Sh[li * kb + j] = v.hi; Sl[li * kb + j] = v.lo;
+                const T a = lds<W>(S, SS, li * kb + j);
+                sts<W>(S, SS, li * kb + j, E::sub(a, E::mul(lds<W>(L, rows_per, li), lds<W>(U, kb, j))));
             }
         }
         __syncthreads();
     }
     for (int e = tid; e < nrows * kb; e += blockDim.x) {
         const int li = e / kb, j = e % kb;
-        stA(A, n, r0 + li, p + j, dd{Sh[e], Sl[e]});
+        stA<W>(A, n, r0 + li, p + j, lds<W>(S, SS, e));
     }
 }
 
 // Apply the panel's interchanges (in order) to the columns outside the panel.
-__global__ void lu_laswp_kernel(double *A, int64_t n, int64_t p, int64_t kb, const int64_t *ipiv) {
+__global__ void lu_laswp_kernel(double *A, int W, int64_t n, int64_t p, int64_t kb, const int64_t *ipiv) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t ncols = n - kb;
-    if (t >= 2 * ncols) return;
+    if (t >= (int64_t)W * ncols) return;
     const int plane = (int)(t / ncols);
     int64_t j = t % ncols;
     if (j >= p) j += kb;
@@ -448,6 +325,154 @@ __global__ void lu_laswp_kernel(double *A, int64_t n, int64_t p, int64_t kb, con
     }
 }
 
+// ---- U12 := L11^{-1} A12 (unit lower, forward substitution in row order) ------------------
+// One CTA per strip of cw columns held in shared memory; thread r owns panel row r and
+// prefetches its next multiplier l_{r,i+1} during step i.
+template <int W>
+__global__ void __launch_bounds__(1024) lu_trsm_kernel(double *A, int64_t n, int64_t p, int64_t kb,
+                                                       int64_t c0, int cw) {
+    using E = elem<W>;
+    using T = typename E::T;
+    extern __shared__ double tile[];   // [W][kb][cw]
+    const int TS = (int)(kb * cw);
+    const int64_t col0 = c0 + (int64_t)blockIdx.x * cw;
+    const int ncols = (int)((n - col0) < cw ? (n - col0) : cw);
+    for (int64_t e = threadIdx.x; e < kb * cw; e += blockDim.x) {
+        const int64_t r = e / cw, c = e % cw;
+        if (c < ncols) sts<W>(tile, TS, (int)e, ldA<W>(A, n, p + r, col0 + c));
+    }
+    const int64_t r = threadIdx.x;   // blockDim.x >= kb (host guarantees)
+    T lnext = E::zero();
+    if (r > 0 && r < kb) lnext = ldA<W>(A, n, p + r, p);
+    for (int64_t i = 0; i < kb; i++) {
+        __syncthreads();
+        const T l = lnext;
+        if (i + 1 < r && r < kb) lnext = ldA<W>(A, n, p + r, p + i + 1);
+        if (r > i && r < kb) {
+            for (int c = 0; c < ncols; c++) {
+                const T u = lds<W>(tile, TS, (int)(i * cw + c));
+                const T a = lds<W>(tile, TS, (int)(r * cw + c));
+                sts<W>(tile, TS, (int)(r * cw + c), E::sub(a, E::mul(l, u)));
+            }
+        }
+    }
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < kb * cw; e += blockDim.x) {
+        const int64_t rr = e / cw, c = e % cw;
+        if (c < ncols) stA<W>(A, n, p + rr, col0 + c, lds<W>(tile, TS, (int)e));
+    }
+}
+
+// ---- solves ----------------------------------------------------------------------------------
+// y := P b (ipiv swaps applied in order), in shared memory when it fits.
+__global__ void __launch_bounds__(1024) lu_perm_kernel(const double *b, double *y, const int64_t *ipiv,
+                                                       int W, int64_t n, int use_smem) {
+    extern __shared__ double sy[];
+    double *buf = use_smem ? sy : y;
+    for (int64_t i = threadIdx.x; i < (int64_t)W * n; i += blockDim.x) buf[i] = b[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int64_t k = 0; k < n; k++) {
+            const int64_t r = ipiv[k];
+            if (r != k)
+                for (int w = 0; w < W; w++) {
+                    const double t = buf[w * n + k];
+                    buf[w * n + k] = buf[w * n + r];
+                    buf[w * n + r] = t;
+                }
+        }
+    }
+    __syncthreads();
+    if (use_smem)
+        for (int64_t i = threadIdx.x; i < (int64_t)W * n; i += blockDim.x) y[i] = sy[i];
+}
+
+// y vectors: planar [W][n]
+template <int W>
+__device__ __forceinline__ typename elem<W>::T ldv(const double *y, int64_t n, int64_t i) {
+    return elem<W>::load(y + i, n);
+}
+template <int W>
+__device__ __forceinline__ void stv(double *y, int64_t n, int64_t i, const typename elem<W>::T &v) {
+    elem<W>::store(y + i, n, v);
+}
+
+// Forward (unit L, j ascending) diagonal block [J, J+nb): one thread per row of the block.
+template <int W>
+__global__ void __launch_bounds__(1024) trsv_fwd_diag(const double *A, int64_t n, double *y, int64_t J, int nb) {
+    using E = elem<W>;
+    using T = typename E::T;
+    __shared__ double ys[W * 256];
+    const int s = threadIdx.x;
+    if (s < nb) sts<W>(ys, 256, s, ldv<W>(y, n, J + s));
+    T lnext = E::zero();
+    if (s > 0 && s < nb) lnext = ldA<W>(A, n, J + s, J);
+    for (int t = 0; t < nb; t++) {
+        __syncthreads();
+        const T l = lnext;
+        if (t + 1 < s && s < nb) lnext = ldA<W>(A, n, J + s, J + t + 1);   // prefetch
+        if (s > t && s < nb) sts<W>(ys, 256, s, E::sub(lds<W>(ys, 256, s), E::mul(l, lds<W>(ys, 256, t))));
+    }
+    __syncthreads();
+    if (s < nb) stv<W>(y, n, J + s, lds<W>(ys, 256, s));
+}
+
+// rows i >= J+nb: y_i := y_i - l_ij y_j for j in [J, J+nb) ascending
+template <int W>
+__global__ void trsv_fwd_update(const double *A, int64_t n, double *y, int64_t J, int nb) {
+    using E = elem<W>;
+    using T = typename E::T;
+    __shared__ double ys[W * 256];
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) sts<W>(ys, 256, t, ldv<W>(y, n, J + t));
+    __syncthreads();
+    const int64_t i = J + nb + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    T v = ldv<W>(y, n, i);
+    for (int t = 0; t < nb; t++) v = E::sub(v, E::mul(ldA<W>(A, n, i, J + t), lds<W>(ys, 256, t)));
+    stv<W>(y, n, i, v);
+}
+
+// Backward diagonal block: for t descending, x_t = y_t / u_tt, then rows s < t update.
+template <int W>
+__global__ void __launch_bounds__(1024) trsv_bwd_diag(const double *A, int64_t n, double *y, double *x,
+                                                      int64_t J, int nb) {
+    using E = elem<W>;
+    using T = typename E::T;
+    __shared__ double ys[W * 256];
+    const int s = threadIdx.x;
+    if (s < nb) sts<W>(ys, 256, s, ldv<W>(y, n, J + s));
+    // thread s < nb holds u_{s,t} for the current t (prefetched one step ahead; u_ss is the
+    // divisor when t == s)
+    T unext = E::zero();
+    if (s < nb) unext = ldA<W>(A, n, J + s, J + nb - 1);
+    for (int t = nb - 1; t >= 0; t--) {
+        __syncthreads();
+        const T u = unext;
+        if (s < nb && t - 1 >= s) unext = ldA<W>(A, n, J + s, J + t - 1);
+        if (s == t) sts<W>(ys, 256, t, E::div(lds<W>(ys, 256, t), u));   // slot t now holds x_t
+        __syncthreads();
+        if (s < t) sts<W>(ys, 256, s, E::sub(lds<W>(ys, 256, s), E::mul(u, lds<W>(ys, 256, t))));
+    }
+    __syncthreads();
+    if (s < nb) stv<W>(x, n, J + s, lds<W>(ys, 256, s));
+}
+
+// rows i < J: y_i := y_i - u_ij x_j for j in [J, J+nb) descending
+template <int W>
+__global__ void trsv_bwd_update(const double *A, int64_t n, double *y, const double *x, int64_t J, int nb) {
+    using E = elem<W>;
+    using T = typename E::T;
+    __shared__ double xs[W * 256];
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) sts<W>(xs, 256, t, ldv<W>(x, n, J + t));
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= J) return;
+    T v = ldv<W>(y, n, i);
+    for (int t = nb - 1; t >= 0; t--) v = E::sub(v, E::mul(ldA<W>(A, n, i, J + t), lds<W>(xs, 256, t)));
+    stv<W>(y, n, i, v);
+}
+
+// ---- host driver -------------------------------------------------------------------------------
 static int g_coop_sms = -1;
 
 // DDQD_LU_PANEL=steps forces the per-column two-kernel path (kept as the reference schedule)
@@ -461,7 +486,8 @@ static bool use_coop_panel() {
 }
 
 // returns 1 if the cooperative path was launched, 0 if the caller should use the per-column path
-static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int64_t *ipiv, LuAux *aux,
+template <int W>
+static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot, int64_t *ipiv, LuAux *aux,
                           double *scr, size_t scr_bytes, cudaStream_t s, int *rc) {
     *rc = DDQD_OK;
     const int64_t R = n - p;
@@ -476,34 +502,35 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int64_t *
     int G = (int)std::min<int64_t>(g_coop_sms, R);
     const int rows_per = (int)((R + G - 1) / G);
     G = (int)((R + rows_per - 1) / rows_per);
-    const size_t smem = sizeof(double) * (2 * (size_t)rows_per * kb + 2 * (size_t)kb + 2 * (size_t)rows_per);
+    const size_t smem = sizeof(double) * W * ((size_t)rows_per * kb + (size_t)kb + (size_t)rows_per);
     if (smem > 200 * 1024) return 0;
-    const size_t per_buf = (size_t)G * 3 + (size_t)G * 2 * kb + 2 * (size_t)kb;
+    const size_t per_buf = (size_t)G * (W + 1) + (size_t)G * W * kb + (size_t)W * kb;
     if (2 * per_buf * sizeof(double) > scr_bytes) return 0;
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
-        if (cudaFuncSetAttribute(lu_panel_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess) {
+        if (cudaFuncSetAttribute(lu_panel_coop_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess) {
             cudaGetLastError();
             return 0;
         }
         attr = smem;
     }
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lu_panel_coop_kernel, 256, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lu_panel_coop_kernel<W>, 256, smem);
     if (occ < 1 || G > occ * g_coop_sms) return 0;
     int kbi = (int)kb;
-    void *args[] = {&A, &n, &p, &kbi, (void *)&rows_per, &ipiv, &aux, &scr};
-    cudaError_t e = cudaLaunchCooperativeKernel((void *)lu_panel_coop_kernel, dim3(G), dim3(256), args, smem, s);
+    int piv = pivot;
+    void *args[] = {&A, &n, &p, &kbi, (void *)&rows_per, &piv, &ipiv, &aux, &scr};
+    cudaError_t e = cudaLaunchCooperativeKernel((void *)lu_panel_coop_kernel<W>, dim3(G), dim3(256), args, smem, s);
     count_launch();
     if (e != cudaSuccess) {
         set_error(std::string("cooperative panel launch: ") + cudaGetErrorString(e));
         *rc = DDQD_ECUDA;
         return 1;
     }
-    if (n - kb > 0) {
-        const int64_t threads = 2 * (n - kb);
-        lu_laswp_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(A, n, p, kb, ipiv);
+    if (pivot && n - kb > 0) {
+        const int64_t threads = (int64_t)W * (n - kb);
+        lu_laswp_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(A, W, n, p, kb, ipiv);
         count_launch();
         e = cudaGetLastError();
         if (e != cudaSuccess) {
@@ -514,14 +541,15 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int64_t *
     return 1;
 }
 
-int lu_solve_impl(int64_t n, double *A, const double *b, double *x, int64_t *ipiv, int64_t K,
-                  int algo, int64_t T, cudaStream_t s, int *info_out) {
+template <int W>
+static int lu_solve_w(int64_t n, int pivot, double *A, const double *b, double *x, int64_t *ipiv, int64_t K,
+                      int algo, int64_t T, cudaStream_t s, int *info_out) {
     *info_out = 0;
     if (n == 0) return DDQD_OK;
     int st = DDQD_OK;
-    // aux: LuAux | y [2n] | cooperative-panel scratch (2 buffers of G*(3 + 2K) + 2K doubles)
-    const size_t ybytes = (sizeof(double) * 2 * (size_t)n + 255) & ~size_t(255);
-    const size_t scr_bytes = sizeof(double) * 2 * ((size_t)160 * (3 + 2 * (size_t)K) + 2 * (size_t)K);
+    // aux: LuAux | y [W n] | cooperative-panel scratch (2 buffers)
+    const size_t ybytes = (sizeof(double) * W * (size_t)n + 255) & ~size_t(255);
+    const size_t scr_bytes = sizeof(double) * 2 * ((size_t)160 * (W + 1 + W * (size_t)K) + W * (size_t)K);
     const size_t aux_bytes = 256 + ybytes + scr_bytes;
     char *aux_mem = static_cast<char *>(aux_get(aux_bytes, &st));
     if (st) return st;
@@ -534,16 +562,16 @@ int lu_solve_impl(int64_t n, double *A, const double *b, double *x, int64_t *ipi
         const int64_t kb = std::min(K, n - p);
         prof_begin(3, s);
         int crc = DDQD_OK;
-        const bool coop = use_coop_panel() && try_panel_coop(A, n, p, kb, ipiv, aux, scr, scr_bytes, s, &crc);
+        const bool coop = use_coop_panel() && try_panel_coop<W>(A, n, p, kb, pivot, ipiv, aux, scr, scr_bytes, s, &crc);
         if (crc) return crc;
         for (int64_t k = p; !coop && k < p + kb; k++) {
-            lu_pivot_kernel<<<1, 1024, 0, s>>>(A, n, k, ipiv, aux);
+            lu_pivot_kernel<W><<<1, 1024, 0, s>>>(A, n, k, pivot, ipiv, aux);
             DDQD_LAUNCH_CHECK();
             const int64_t nc = p + kb - (k + 1), nr = n - (k + 1);
             if (nc > 0 && nr > 0) {
                 dim3 blk(32, 8);
                 dim3 grd((unsigned)((nc + 31) / 32), (unsigned)((nr + 7) / 8));
-                lu_rank1_kernel<<<grd, blk, 0, s>>>(A, n, k, p + kb, aux);
+                lu_rank1_kernel<W><<<grd, blk, 0, s>>>(A, n, k, p + kb, aux);
                 DDQD_LAUNCH_CHECK();
             }
         }
@@ -551,52 +579,52 @@ int lu_solve_impl(int64_t n, double *A, const double *b, double *x, int64_t *ipi
         const int64_t n2 = n - p - kb;
         if (n2 <= 0) continue;
         // one CTA per SM when possible: cw = ceil(n2 / 148), capped by shared memory
-        const int64_t cw_smem = std::max<int64_t>(1, (int64_t)(200 * 1024) / (16 * kb));
+        const int64_t cw_smem = std::max<int64_t>(1, (int64_t)(200 * 1024) / (8 * W * kb));
         int cw = (int)std::max<int64_t>(1, std::min<int64_t>(cw_smem, (n2 + 147) / 148));
-        const size_t smem = sizeof(double) * 2 * (size_t)kb * cw;
+        const size_t smem = sizeof(double) * W * (size_t)kb * cw;
         if (smem > 48 * 1024)
-            DDQD_CUDA_CHECK(cudaFuncSetAttribute(lu_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            DDQD_CUDA_CHECK(cudaFuncSetAttribute(lu_trsm_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem));
         prof_begin(4, s);
         if (kb > 1024) { set_error("panel > 1024 not supported by the TRSM kernel"); return DDQD_ENOTSUP; }
         const int tthreads = (int)(((kb + 31) / 32) * 32);
-        lu_trsm_kernel<<<(unsigned)((n2 + cw - 1) / cw), tthreads, smem, s>>>(A, n, p, kb, p + kb, cw);
+        lu_trsm_kernel<W><<<(unsigned)((n2 + cw - 1) / cw), tthreads, smem, s>>>(A, n, p, kb, p + kb, cw);
         DDQD_LAUNCH_CHECK();
         prof_end(4, (double)kb * (double)kb / 2.0 * (double)n2, s);
         MatDesc L21{A + (p + kb) * n + p, n2, kb, n, n * n, 0};
         MatDesc U12{A + p * n + (p + kb), kb, n2, n, n * n, 0};
         MatDesc A22{A + (p + kb) * n + (p + kb), n2, n2, n, n * n, 0};
-        const int rc = run_gemm(2, algo, T, n2, kb, n2, 1, L21, U12, A22, 1, s);
+        const int rc = run_gemm(W, algo, T, n2, kb, n2, 1, L21, U12, A22, 1, s);
         if (rc) return rc;
     }
 
     // solve: y = P b; L y' = y (j ascending); U x = y' (j descending)
-    const int use_smem = (2 * n * (int64_t)sizeof(double) <= 200 * 1024) ? 1 : 0;
-    const size_t psmem = use_smem ? 2 * n * sizeof(double) : 0;
+    const int use_smem = ((int64_t)W * n * (int64_t)sizeof(double) <= 200 * 1024) ? 1 : 0;
+    const size_t psmem = use_smem ? (size_t)W * n * sizeof(double) : 0;
     if (psmem > 48 * 1024)
         DDQD_CUDA_CHECK(cudaFuncSetAttribute(lu_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)psmem));
     prof_begin(5, s);
-    lu_perm_kernel<<<1, 1024, psmem, s>>>(b, y, ipiv, n, use_smem);
+    lu_perm_kernel<<<1, 1024, psmem, s>>>(b, y, ipiv, W, n, use_smem);
     DDQD_LAUNCH_CHECK();
     const int NB = 256;
     for (int64_t J = 0; J < n; J += NB) {
         const int nb = (int)std::min<int64_t>(NB, n - J);
-        trsv_fwd_diag<<<1, 1024, 0, s>>>(A, n, y, J, nb);
+        trsv_fwd_diag<W><<<1, 256, 0, s>>>(A, n, y, J, nb);
         DDQD_LAUNCH_CHECK();
         const int64_t rows = n - J - nb;
         if (rows > 0) {
-            trsv_fwd_update<<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(A, n, y, J, nb);
+            trsv_fwd_update<W><<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(A, n, y, J, nb);
             DDQD_LAUNCH_CHECK();
         }
     }
     const int64_t last = ((n - 1) / NB) * NB;
     for (int64_t J = last; J >= 0; J -= NB) {
         const int nb = (int)std::min<int64_t>(NB, n - J);
-        trsv_bwd_diag<<<1, 1024, 0, s>>>(A, n, y, x, J, nb);
+        trsv_bwd_diag<W><<<1, 256, 0, s>>>(A, n, y, x, J, nb);
         DDQD_LAUNCH_CHECK();
         if (J > 0) {
-            trsv_bwd_update<<<(unsigned)((J + 127) / 128), 128, 0, s>>>(A, n, y, x, J, nb);
+            trsv_bwd_update<W><<<(unsigned)((J + 127) / 128), 128, 0, s>>>(A, n, y, x, J, nb);
             DDQD_LAUNCH_CHECK();
         }
     }
@@ -606,6 +634,12 @@ int lu_solve_impl(int64_t n, double *A, const double *b, double *x, int64_t *ipi
     DDQD_CUDA_CHECK(cudaStreamSynchronize(s));
     *info_out = info_h;
     return DDQD_OK;
+}
+
+int lu_solve_impl(int W, int pivot, int64_t n, double *A, const double *b, double *x, int64_t *ipiv, int64_t K,
+                  int algo, int64_t T, cudaStream_t s, int *info_out) {
+    if (W == 2) return lu_solve_w<2>(n, pivot, A, b, x, ipiv, K, algo, T, s, info_out);
+    return lu_solve_w<4>(n, pivot, A, b, x, ipiv, K, algo, T, s, info_out);
 }
 
 }  // namespace ddqd

@@ -60,11 +60,12 @@ def test_dd_elementwise_bitwise(orc, op):
     assert same(got, ref)
 
 
-@pytest.mark.parametrize("op", ["add", "sub", "mul", "madd"])
+@pytest.mark.parametrize("op", ["add", "sub", "mul", "madd", "div"])
 def test_qd_elementwise_bitwise(orc, op):
     q = [gen.qd_matrix(1, 50000, s, 0).reshape(4, -1) for s in (4, 5, 6)]
-    q[1][:, :500] = -q[0][:, :500]
-    ref = orc.qd_op(op, *q)
+    if op != "div":
+        q[1][:, :500] = -q[0][:, :500]
+    ref = orc.qd_div(q[0], q[1]) if op == "div" else orc.qd_op(op, *q)
     got = np_(ddqd.elementwise(op, *(cu(a) for a in q)))
     assert same(got, ref)
 
@@ -340,7 +341,10 @@ def test_lu_per_column_path_bitwise(tmp_path):
         "import numpy as np, torch, ddqd_inputs as gen, paper_1510_08642_b200 as d\n"
         "A = gen.dd_matrix(300, 300, 13, 0); b = gen.dd_matrix(1, 300, 13, 1)[:, 0, :].copy()\n"
         "x, LU, piv, info = d.dd_lu_solve(torch.from_numpy(A).cuda(), torch.from_numpy(b).cuda(), 64, 'strassen', 32)\n"
-        "np.save(r'%s', np.concatenate([LU.cpu().numpy().ravel(), x.cpu().numpy().ravel(), piv.cpu().numpy().astype(np.float64)]))\n")
+        "q = gen.qd_matrix(200, 200, 3, 0); qb = gen.qd_matrix(1, 200, 3, 1)[:, 0, :].copy()\n"
+        "qx, qLU, qp, qi = d.qd_lu_solve(torch.from_numpy(q).cuda(), torch.from_numpy(qb).cuda(), 48, 'winograd', 16)\n"
+        "np.save(r'%s', np.concatenate([LU.cpu().numpy().ravel(), x.cpu().numpy().ravel(), piv.cpu().numpy().astype(np.float64),"
+        " qLU.cpu().numpy().ravel(), qx.cpu().numpy().ravel()]))\n")
     outs = []
     for mode in ("steps", "coop"):
         f = tmp_path / f"{mode}.npy"
@@ -348,3 +352,35 @@ def test_lu_per_column_path_bitwise(tmp_path):
         subprocess.check_call([sys.executable, "-c", code % f], env=env, cwd=ROOT)
         outs.append(np.load(f))
     assert same(outs[0], outs[1])
+
+
+# ---- QD LU and the paper's pivot-free LU -----------------------
+def _qd_lu_matrix(n, seed):
+    A = gen.qd_matrix(n, n, seed, 0)
+    A[0, np.arange(n), np.arange(n)] += n
+    return A
+
+
+@pytest.mark.parametrize("pivot", [True, False])
+@pytest.mark.parametrize("W", [2, 4])
+def test_lu_qd_and_pivot_free_bitwise(orc, W, pivot):
+    """DD/QD LU with and without pivoting (the paper's pivot-free LU), Winograd update,
+    on a random non-dominant matrix (pivoting path) and bit-exact vs the oracle."""
+    n = 200
+    A = gen.matrix(W, n, n, 23, 0)
+    b = gen.matrix(W, 1, n, 23, 1)[:, 0, :].copy()
+    x_ref, LU_ref, piv_ref, info_ref = orc.solve(A, b, panel=48, algo="winograd", threshold=16, pivot=pivot)
+    x, LU, piv, info = ddqd.lu_solve(cu(A), cu(b), panel=48, algo="winograd", threshold=16, pivot=pivot)
+    assert info == info_ref == 0
+    assert np.array_equal(np_(piv), piv_ref)
+    assert same(np_(LU), LU_ref) and same(np_(x), x_ref)
+
+
+def test_qd_lu_c4_recipe_512_bitwise(orc):
+    n = 512
+    A = _qd_lu_matrix(n, 5)
+    ones = np.zeros((4, n, 1)); ones[0] = 1.0
+    b = orc.gemm(A, ones, "block")[:, :, 0].copy()
+    x_ref, LU_ref, _, _ = orc.solve(A, b, panel=128, algo="strassen", threshold=64)
+    x, LU, piv, info = ddqd.qd_lu_solve(cu(A), cu(b), panel=128, algo="strassen", threshold=64)
+    assert info == 0 and same(np_(LU), LU_ref) and same(np_(x), x_ref)

@@ -129,3 +129,76 @@ def test_tie_lowest_index(orc):
     A = np.zeros((2, 3, 3)); A[0] = [[1, 0, 0], [-2, 1, 0], [2, 0, 1]]
     _, ipiv, _ = orc.lu(A, panel=3, algo="block")
     assert ipiv[0] == 1
+
+
+# ---- QD LU and the paper's pivot-free mode ---------------------
+def test_qd_div(orc):
+    """mul(div(1,7),7) within 16 eps_qd of 1; random quotients (calibrated 2^-205)."""
+    from tests.util import EPS_QD
+    one = np.zeros((4, 1)); one[0] = 1.0
+    seven = np.zeros((4, 1)); seven[0] = 7.0
+    q = orc.qd_div(one, seven)
+    assert abs(frac(orc.qd_op("mul", q, seven)[:, 0]) - 1) <= 16 * EPS_QD
+    assert abs(frac(q[:, 0]) - Fraction(1, 7)) <= 4 * EPS_QD
+    x = gen.qd_matrix(1, 400, 3, 0).reshape(4, -1)
+    y = gen.qd_matrix(1, 400, 4, 0).reshape(4, -1)
+    z = orc.qd_div(x, y)
+    for i in range(400):
+        X, Y = frac(x[:, i]), frac(y[:, i])
+        assert abs(frac(z[:, i]) - X / Y) <= Fraction(1, 2 ** 205) * abs(X / Y)
+
+
+def _qd_lu_matrix(n, seed, shift=True):
+    A = gen.qd_matrix(n, n, seed, 0)
+    if shift:
+        A[0, np.arange(n), np.arange(n)] += n     # exact: |w0| < 1 and n a small integer
+    return A
+
+
+def test_qd_lu_identity_and_2x2(orc):
+    n = 9
+    A = np.zeros((4, n, n)); A[0] = np.eye(n)
+    b = gen.qd_matrix(1, n, 3, 1)[:, 0, :]
+    x, LU, ipiv, info = orc.solve(A, b, panel=4, algo="winograd", threshold=1)
+    assert info == 0 and np.array_equal(x, b)
+    A2 = np.zeros((4, 2, 2)); A2[0] = [[4, 3], [6, 3]]
+    LU, ipiv, info = orc.lu(A2, panel=1, algo="block")
+    assert list(ipiv) == [1, 1]
+    from tests.util import EPS_QD
+    assert abs(frac(LU[:, 1, 0]) - Fraction(2, 3)) <= 2 * EPS_QD
+
+
+def test_qd_lu_residual_and_solution(orc):
+    """QD LU with a Winograd update: ||PA - LU|| (exact) <= 100 n eps_qd ||A||; x = 1 within
+    2^-200 n kappa 18."""
+    n = 48
+    A = _qd_lu_matrix(n, 7)
+    ones = np.zeros((4, n, 1)); ones[0] = 1.0
+    b = orc.gemm(A, ones, "block")[:, :, 0].copy()
+    x, LU, ipiv, info = orc.solve(A, b, panel=16, algo="winograd", threshold=4)
+    assert info == 0 and np.array_equal(ipiv, np.arange(n))
+    L, U = _split_LU(LU)
+    L[1:, np.arange(n), np.arange(n)] = 0.0
+    r, c = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    _, err = orc.exact_entries(L, U, _perm_rows(A, ipiv), r.ravel(), c.ravel())
+    normA = np.abs(A[0]).sum(axis=1).max()
+    assert np.abs(err).reshape(n, n).sum(axis=1).max() <= 100 * n * 2.0 ** -209 * normA
+    err_x = max(abs(frac(x[:, i]) - 1) for i in range(n))
+    assert err_x <= Fraction(1, 2 ** 200) * n * 3 * 18
+
+
+def test_pivot_free_mode(orc):
+    """P:121 pivot-free LU: ipiv = identity always; on a diagonally dominant matrix it equals
+    the pivoted factorisation bitwise (no interchange happens there either)."""
+    for W in (2, 4):
+        n = 40
+        A = gen.lu_matrix(n, 3) if W == 2 else _qd_lu_matrix(n, 3)
+        LUp, pp, _ = orc.lu(A, panel=8, algo="strassen", threshold=4, pivot=True)
+        LUf, pf, _ = orc.lu(A, panel=8, algo="strassen", threshold=4, pivot=False)
+        assert np.array_equal(pf, np.arange(n)) and np.array_equal(LUp, LUf)
+    # a random (non-dominant) matrix: pivot-free still factors it, with |l_ij| > 1 somewhere
+    A = gen.dd_matrix(30, 30, 12, 0)
+    LU, piv, info = orc.lu(A, panel=8, algo="block", pivot=False)
+    assert info == 0 and np.array_equal(piv, np.arange(30))
+    assert np.abs(LU[0][np.tril(np.ones((30, 30), bool), -1)]).max() > 1.0
+    assert _residual_ok(orc, A, LU, piv, factor=1e6)[0]
