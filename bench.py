@@ -62,6 +62,9 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--madd", default="canonical", choices=["canonical", "fused"],
+                    help="DD multiply-add: the paper's QD-library sequence (20 FP64 ops) or the "
+                         "fused variant of numerics.md s.2 (15 ops; row f3)")
     return ap.parse_args()
 
 
@@ -347,7 +350,7 @@ def main():
             sched(A, B, C)
     else:
         def step():
-            ddqd.gemm(A, B, algo, T, out=C)
+            ddqd.gemm(A, B, algo, T, out=C, madd=args.madd)
 
     for _ in range(args.warmup):
         step()
@@ -381,7 +384,7 @@ def main():
 
     # roofline of the dominant kernel: the batched leaf GEMM (FP64-pipe bound)
     leaf_ms, leaf_n, leaf_madds = prof["leaf"]
-    ops = OPS_PER_MADD[W]
+    ops = OPS_PER_MADD[W] if args.madd == "canonical" else 15
     leaf_avg_s = (leaf_ms / leaf_n) * 1e-3 if leaf_n else float("nan")
     leaf_ops_per_launch = ops * leaf_madds / leaf_n if leaf_n else 0.0
     achieved = leaf_ops_per_launch / leaf_avg_s / 1e12 if leaf_n else 0.0
@@ -419,12 +422,12 @@ def main():
         hA = A_h.pin_memory()
         hB = B_h.pin_memory()
         hC = torch.empty((W, m, n), dtype=torch.float64).pin_memory()
-        ddqd.gemm(hA, hB, algo, T, out=hC)            # warm the staging buffers
+        ddqd.gemm(hA, hB, algo, T, out=hC, madd=args.madd)   # warm the staging buffers
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            ddqd.gemm(hA, hB, algo, T, out=hC)        # H2D + compute + D2H, synchronous
+            ddqd.gemm(hA, hB, algo, T, out=hC, madd=args.madd)   # H2D + compute + D2H, synchronous
         e1.record()
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
@@ -452,6 +455,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": MAD_DTYPE[W],
             "data": "synthetic (seeded SplitMix64, BASELINE.json recipe)",
             "config": {"workload": wl["name"], "m": m, "l": l, "n": n, "algo": algo, "threshold": T,
+                       "madd": args.madd,
                        "depth": d, "leaf_shape": list(shapes[-1]), "leaf_madds_per_step": leaf_madds_step,
                        "l2": "no flush: each operand (%.2f GB) exceeds the 126 MB L2" % (A.numel() * 8 / 1e9),
                        "parallelism": f"{world} GPU" + ("s, depth-k product distribution" if world > 1 else "")},

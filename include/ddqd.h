@@ -43,6 +43,12 @@ extern "C" {
 /* Algorithms. */
 enum { DDQD_BLOCK = 0, DDQD_STRASSEN = 1, DDQD_WINOGRAD = 2 };
 
+/* Flag OR-ed into `algo` (DD only): the leaf uses the fused DD multiply-add of
+ * docs/numerics.md s.2 (15 FP64 instructions instead of the QD-library dd_add(c, dd_mul(a,b))
+ * = 20). Results are then bit-identical to the oracle's fused
+ * variant, not to the canonical one. QD with this flag returns DDQD_ENOTSUP. */
+enum { DDQD_MADD_FUSED = 0x100 };
+
 /* Precisions: number of float64 words per element. */
 enum { DDQD_DD = 2, DDQD_QD = 4 };
 
@@ -137,8 +143,8 @@ int ddqd_lu_solve(int prec, int pivot, int64_t n, double *A, const double *b, do
                   int64_t *ipiv, int64_t panel, int algo, int64_t threshold);
 
 /* Elementwise arithmetic layer, for parity tests of the device DD/QD ops (device
- * pointers, planar [W][count]): op 0 add, 1 sub, 2 mul, 3 div, 4 madd
- * z = x + y*w. */
+ * pointers, planar [W][count]): op 0 add, 1 sub, 2 mul, 3 div, 4 madd z = x + y*w,
+ * 5 fused madd (DD only, DDQD_MADD_FUSED's operation). */
 int ddqd_elementwise(int prec, int op, int64_t count, const double *x, const double *y,
                      const double *w, double *z);
 

@@ -97,7 +97,8 @@ def two_prod(a, b):
     return _eft("or_two_prod", a, b)
 
 
-_OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "madd": 4}
+_OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "madd": 4, "madd_fused": 5}
+MADD_FUSED = 0x100
 
 
 def dd_op(op: str, x, y, w=None):
@@ -132,15 +133,17 @@ def dd_abs_gt(x, y) -> bool:
 
 
 # ---- GEMM --------------------------------------------------------------------
-def gemm(A, B, algo="block", threshold=32, bs=0, nthreads=0):
-    """C := A B for planar [W, m, l] x [W, l, n] arrays (numerics.md s.4)."""
+def gemm(A, B, algo="block", threshold=32, bs=0, nthreads=0, madd="canonical"):
+    """C := A B for planar [W, m, l] x [W, l, n] arrays (numerics.md s.4); madd='fused'
+    selects the fused DD multiply-add variant (numerics.md s.2)."""
     A, B = _f64(A), _f64(B)
     W, m, l = A.shape
     W2, l2, n = B.shape
     if W != W2 or l != l2:
         raise ValueError("dimension mismatch")
     C = np.empty((W, m, n))
-    rc = lib().or_gemm(W, ALGOS[algo] if isinstance(algo, str) else algo, threshold, bs,
+    a = (ALGOS[algo] if isinstance(algo, str) else algo) | (MADD_FUSED if madd == "fused" else 0)
+    rc = lib().or_gemm(W, a, threshold, bs,
                        m, l, n, _p(A), _p(B), _p(C), nthreads)
     if rc:
         raise ValueError("or_gemm: invalid arguments")
@@ -157,14 +160,15 @@ def reset_counters():
 
 
 # ---- LU ----------------------------------------------------------------------
-def lu(A, panel=256, algo="strassen", threshold=128, nthreads=0, pivot=True):
+def lu(A, panel=256, algo="strassen", threshold=128, nthreads=0, pivot=True, madd="canonical"):
     """Blocked right-looking LU (numerics.md s.5) of a [W,n,n] DD (W=2) or QD (W=4) matrix,
     with partial pivoting or (pivot=False) the paper's pivot-free variant.
     Returns (LU [W,n,n], ipiv int64[n], info)."""
     LU = _f64(A).copy()
     W, n = LU.shape[0], LU.shape[1]
     ipiv = np.zeros(n, dtype=np.int64)
-    info = lib().or_lu(W, 1 if pivot else 0, n, _p(LU), _pi(ipiv), panel, ALGOS[algo], threshold, nthreads)
+    a = ALGOS[algo] | (MADD_FUSED if madd == "fused" else 0)
+    info = lib().or_lu(W, 1 if pivot else 0, n, _p(LU), _pi(ipiv), panel, a, threshold, nthreads)
     if info < 0:
         raise ValueError("or_lu: invalid arguments")
     return LU, ipiv, info
@@ -178,8 +182,8 @@ def lu_solve(LU, ipiv, b):
     return x
 
 
-def solve(A, b, panel=256, algo="strassen", threshold=128, nthreads=0, pivot=True):
-    LU, ipiv, info = lu(A, panel, algo, threshold, nthreads, pivot)
+def solve(A, b, panel=256, algo="strassen", threshold=128, nthreads=0, pivot=True, madd="canonical"):
+    LU, ipiv, info = lu(A, panel, algo, threshold, nthreads, pivot, madd)
     return lu_solve(LU, ipiv, b), LU, ipiv, info
 
 

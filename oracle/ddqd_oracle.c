@@ -80,6 +80,23 @@ static dd_t dd_mul(dd_t x, dd_t y) {
 
 static dd_t dd_madd(dd_t c, dd_t a, dd_t b) { return dd_add(c, dd_mul(a, b)); }
 
+/* numerics.md s.2 fused variant (DDQD_MADD_FUSED) */
+static dd_t dd_madd_fused(dd_t c, dd_t a, dd_t b) {
+    double p = a.hi * b.hi, e, s, t;
+    dd_t r;
+    e = fma(a.hi, b.hi, -p);
+    e = fma(a.hi, b.lo, e);
+    e = fma(a.lo, b.hi, e);
+    two_sum(c.hi, p, &s, &t);
+    t = t + (c.lo + e);
+    fast_two_sum(s, t, &r.hi, &r.lo);
+    return r;
+}
+
+static int g_madd_fused = 0;   /* set per call by or_gemm / or_lu from the algo flag 0x100 */
+
+static dd_t dd_madd_v(dd_t c, dd_t a, dd_t b) { return g_madd_fused ? dd_madd_fused(c, a, b) : dd_madd(c, a, b); }
+
 static dd_t dd_div(dd_t x, dd_t y) {
     dd_t q1d, r, out;
     double q1 = x.hi / y.hi, q2;
@@ -226,6 +243,7 @@ void or_dd_op(int op, int64_t n, const double *x, const double *y, const double 
         case 1: r = dd_sub(a, b); break;
         case 2: r = dd_mul(a, b); break;
         case 3: r = dd_div(a, b); break;
+        case 5: { dd_t c = { w[i], w[n + i] }; r = dd_madd_fused(a, b, c); break; }
         default: { dd_t c = { w[i], w[n + i] }; r = dd_madd(a, b, c); }
         }
         z[i] = r.hi; z[n + i] = r.lo;
@@ -340,7 +358,7 @@ static void gemm_simple(const mat_t *A, const mat_t *B, mat_t *C) {
                 for (int64_t j = 0; j < n; j++) {
                     dd_t c = { acc[j], acc[n + j] };
                     dd_t b = { get_w(B, 0, k, j), get_w(B, 1, k, j) };
-                    c = dd_madd(c, a, b);
+                    c = dd_madd_v(c, a, b);
                     acc[j] = c.hi; acc[n + j] = c.lo;
                 }
             } else {
@@ -380,7 +398,7 @@ static void gemm_block(const mat_t *A, const mat_t *B, mat_t *C, int64_t bs) {
                                 dd_t a = { get_w(A, 0, i, k), get_w(A, 1, i, k) };
                                 dd_t b = { get_w(B, 0, k, j), get_w(B, 1, k, j) };
                                 dd_t c = { get_w(C, 0, i, j), get_w(C, 1, i, j) };
-                                c = dd_madd(c, a, b);
+                                c = dd_madd_v(c, a, b);
                                 set_w(C, 0, i, j, c.hi); set_w(C, 1, i, j, c.lo);
                             } else {
                                 qd_t a, b, c;
@@ -481,7 +499,10 @@ static void gemm_any(int algo, int64_t T, const mat_t *A, const mat_t *B, mat_t 
  * bs > 0 selects the explicitly tiled Block(bs) loop nest (for the Block == Simple pin). */
 int or_gemm(int W, int algo, int64_t T, int64_t bs, int64_t m, int64_t l, int64_t n,
             const double *A, const double *B, double *C, int nthreads) {
+    g_madd_fused = (algo & 0x100) ? 1 : 0;
+    algo &= 0xff;
     if ((W != 2 && W != 4) || algo < 0 || algo > 2 || m < 0 || l < 0 || n < 0) return -1;
+    if (g_madd_fused && W != 2) return -1;
     if (algo != 0 && T < 1) return -1;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -565,7 +586,9 @@ static void st_sc(int W, double *A, int64_t n, int64_t i, int64_t j, sc_t v) {
 int or_lu(int W, int pivot, int64_t n, double *A, int64_t *ipiv, int64_t K, int algo, int64_t T,
           int nthreads) {
     int info = 0;
-    if ((W != 2 && W != 4) || n < 0 || K < 1) return -1;
+    g_madd_fused = (algo & 0x100) ? 1 : 0;
+    algo &= 0xff;
+    if ((W != 2 && W != 4) || n < 0 || K < 1 || (g_madd_fused && W != 2)) return -1;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
 #endif

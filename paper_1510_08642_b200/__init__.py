@@ -22,6 +22,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libddqd.so")
 
 BLOCK, STRASSEN, WINOGRAD = 0, 1, 2
+MADD_FUSED = 0x100   # DDQD_MADD_FUSED: fused DD multiply-add in the leaf (docs/numerics.md s.2)
 _ALGOS = {"block": BLOCK, "strassen": STRASSEN, "winograd": WINOGRAD}
 _CODES = {-1: "EINVAL", -2: "EALIAS", -3: "ENOMEM", -4: "ECUDA", -5: "ENOTSUP"}
 
@@ -102,8 +103,12 @@ def _set_stream(t):
         lib.ddqd_set_stream(ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream))
 
 
-def _algo(a) -> int:
-    return _ALGOS[a] if isinstance(a, str) else int(a)
+def _algo(a, madd="canonical") -> int:
+    """'block' | 'strassen' | 'winograd' (or the int); madd='fused' ORs in DDQD_MADD_FUSED."""
+    v = _ALGOS[a] if isinstance(a, str) else int(a)
+    if madd not in ("canonical", "fused"):
+        raise ValueError("madd must be 'canonical' or 'fused'")
+    return v | (MADD_FUSED if madd == "fused" else 0)
 
 
 def _check_mat(x, W, name):
@@ -114,7 +119,7 @@ def _check_mat(x, W, name):
         raise ValueError(f"{name} must be contiguous (planar row-major)")
 
 
-def gemm(A, B, algo="block", threshold=128, out=None):
+def gemm(A, B, algo="block", threshold=128, out=None, madd="canonical"):
     """C := A B with A [W,m,l], B [W,l,n] float64 CUDA tensors, W = 2 (DD) or 4 (QD).
     Pinned/ordinary CPU tensors for A, B and `out` use the library's host-staging path
     (copies inside the call, synchronous)."""
@@ -136,7 +141,7 @@ def gemm(A, B, algo="block", threshold=128, out=None):
         raise ValueError("out has the wrong shape")
     _set_stream(A)
     f = lib.dd_gemm if W == 2 else lib.qd_gemm
-    _check(f(m, l, n, A.data_ptr(), B.data_ptr(), out.data_ptr(), _algo(algo), threshold), "gemm")
+    _check(f(m, l, n, A.data_ptr(), B.data_ptr(), out.data_ptr(), _algo(algo, madd), threshold), "gemm")
     return out
 
 
@@ -153,9 +158,9 @@ def qd_gemm(A, B, algo="block", threshold=128, out=None):
 
 
 def gemm_ex(prec, algo, threshold, m, l, n, batch, A, lda, psA, bsA, B, ldb, psB, bsB,
-            C, ldc, psC, bsC, beta=0):
+            C, ldc, psC, bsC, beta=0, madd="canonical"):
     """Strided/batched form (ddqd_gemm_ex); A, B, C are device addresses (ints)."""
-    d = GemmDesc(prec, _algo(algo), threshold, m, l, n, batch, A, lda, psA, bsA, B, ldb, psB, bsB,
+    d = GemmDesc(prec, _algo(algo, madd), threshold, m, l, n, batch, A, lda, psA, bsA, B, ldb, psB, bsB,
                  C, ldc, psC, bsC, beta)
     return _check(lib.ddqd_gemm_ex(ctypes.byref(d)), "gemm_ex")
 
@@ -187,7 +192,7 @@ def post_add(algo, M, C, beta=0):
     _check(lib.ddqd_post_add(W, _algo(algo), P, ctypes.byref(mm), ctypes.byref(cc), beta), "post_add")
 
 
-def gemm_batched(A, B, C, algo, threshold, beta=0):
+def gemm_batched(A, B, C, algo, threshold, beta=0, madd="canonical"):
     """C[b] := A[b] B[b] for contiguous [batch, W, .., ..] CUDA tensors (one library schedule)."""
     batch, W, m, l = A.shape
     n = B.shape[3]
@@ -195,10 +200,11 @@ def gemm_batched(A, B, C, algo, threshold, beta=0):
     return gemm_ex(W, algo, threshold, m, l, n, batch,
                    A.data_ptr(), l, m * l, W * m * l,
                    B.data_ptr(), n, l * n, W * l * n,
-                   C.data_ptr(), n, m * n, W * m * n, beta)
+                   C.data_ptr(), n, m * n, W * m * n, beta, madd)
 
 
-def lu_solve(A, b, panel=256, algo="strassen", threshold=128, pivot=True, overwrite=False):
+def lu_solve(A, b, panel=256, algo="strassen", threshold=128, pivot=True, overwrite=False,
+             madd="canonical"):
     """Blocked right-looking DD/QD LU (partial pivoting, or the paper's pivot-free variant with
     pivot=False) + solve (Eq. 2). A: [W,n,n] CUDA float64, b: [W,n], W = 2 or 4.
     Returns (x, LU, ipiv, info)."""
@@ -215,7 +221,7 @@ def lu_solve(A, b, panel=256, algo="strassen", threshold=128, pivot=True, overwr
     ipiv = torch.empty(n, dtype=torch.int64, device=A.device)
     _set_stream(A)
     info = _check(lib.ddqd_lu_solve(W, 1 if pivot else 0, n, LU.data_ptr(), b.data_ptr(), x.data_ptr(),
-                                    ipiv.data_ptr(), panel, _algo(algo), threshold), "lu_solve")
+                                    ipiv.data_ptr(), panel, _algo(algo, madd), threshold), "lu_solve")
     return x, LU, ipiv, info
 
 
@@ -233,7 +239,7 @@ def qd_lu_solve(A, b, panel=256, algo="strassen", threshold=128, overwrite=False
     return lu_solve(A, b, panel, algo, threshold, True, overwrite)
 
 
-_OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "madd": 4}
+_OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "madd": 4, "madd_fused": 5}
 
 
 def elementwise(op, x, y, w=None):

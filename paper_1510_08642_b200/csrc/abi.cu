@@ -135,6 +135,8 @@ static int where(const void *p) {
 
 static int check_gemm_args(int64_t m, int64_t l, int64_t n, int algo, int64_t T) {
     if (m < 0 || l < 0 || n < 0) { set_error("negative dimension"); return DDQD_EINVAL; }
+    if (algo & ~(0xff | DDQD_MADD_FUSED)) { set_error("unknown algo flag"); return DDQD_EINVAL; }
+    algo &= 0xff;
     if (algo < 0 || algo > 2) { set_error("algo must be DDQD_BLOCK, DDQD_STRASSEN or DDQD_WINOGRAD"); return DDQD_EINVAL; }
     if (algo != 0 && T < 1) { set_error("threshold must be >= 1"); return DDQD_EINVAL; }
     const double elems = (double)m * (double)l + (double)l * (double)n + (double)m * (double)n;
@@ -147,6 +149,7 @@ static int gemm_simple(int W, int64_t m, int64_t l, int64_t n, const double *A, 
     t_err.clear();
     int rc = check_gemm_args(m, l, n, algo, T);
     if (rc) return rc;
+    if ((algo & DDQD_MADD_FUSED) && W != 2) { set_error("the fused madd variant is DD only"); return DDQD_ENOTSUP; }
     const size_t bA = sizeof(double) * W * (size_t)m * l, bB = sizeof(double) * W * (size_t)l * n,
                  bC = sizeof(double) * W * (size_t)m * n;
     if (overlaps(A, bA, C, bC) || overlaps(B, bB, C, bC)) { set_error("C overlaps A or B"); return DDQD_EALIAS; }
@@ -200,6 +203,7 @@ int ddqd_gemm_ex(const ddqd_gemm_desc *d) {
     if (d->prec != 2 && d->prec != 4) { set_error("prec must be DDQD_DD or DDQD_QD"); return DDQD_EINVAL; }
     int rc = check_gemm_args(d->m, d->l, d->n, d->algo, d->threshold);
     if (rc) return rc;
+    if ((d->algo & DDQD_MADD_FUSED) && d->prec != 2) { set_error("the fused madd variant is DD only"); return DDQD_ENOTSUP; }
     if (d->batch < 0 || (d->beta != 0 && d->beta != 1)) { set_error("bad batch or beta"); return DDQD_EINVAL; }
     if (d->lda < d->l || d->ldb < d->n || d->ldc < d->n) { set_error("leading dimension too small"); return DDQD_EINVAL; }
     if (d->m == 0 || d->n == 0 || d->batch == 0) return DDQD_OK;
@@ -218,6 +222,7 @@ int ddqd_lu_solve(int prec, int pivot, int64_t n, double *A, const double *b, do
     if (n < 0 || panel < 1) { set_error("n must be >= 0 and panel >= 1"); return DDQD_EINVAL; }
     int rc = check_gemm_args(n, panel, n, algo, threshold);
     if (rc) return rc;
+    if ((algo & DDQD_MADD_FUSED) && prec != 2) { set_error("the fused madd variant is DD only"); return DDQD_ENOTSUP; }
     if (n == 0) return DDQD_OK;
     if (!A || !b || !x || !ipiv) { set_error("null pointer"); return DDQD_EINVAL; }
     if (where(A) || where(b) || where(x) || where(ipiv)) { set_error("LU takes device pointers only"); return DDQD_ENOTSUP; }
@@ -268,7 +273,7 @@ int ddqd_post_add(int prec, int algo, int64_t P, const ddqd_mat *M, const ddqd_m
 int ddqd_elementwise(int prec, int op, int64_t count, const double *x, const double *y, const double *w,
                      double *z) {
     t_err.clear();
-    if ((prec != 2 && prec != 4) || op < 0 || op > 4 || count < 0) {
+    if ((prec != 2 && prec != 4) || op < 0 || op > 5 || (op == 5 && prec != 2) || count < 0) {
         set_error("bad elementwise arguments");
         return DDQD_EINVAL;
     }

@@ -176,6 +176,7 @@ __global__ void elementwise_kernel(int op, int64_t count, const double *x, const
         if (op == 0) r = E::add(a, b);
         else if (op == 1) r = E::sub(a, b);
         else if (op == 4) r = E::madd(a, b, E::load(w + i, count));
+        else if (op == 5) r = E::madd_fused(a, b, E::load(w + i, count));
         else if constexpr (W == 2) {
             r = (op == 2) ? dd_mul(a, b) : dd_div(a, b);
         } else {

@@ -50,7 +50,7 @@ int fp64_peak(int op, double *lane_ops_per_s, double *ms, cudaStream_t s);
 
 // Leaf GEMM (leaf_gemm.cu): C[b] (=|-=) A[b] B[b] for b < batch; beta 0: store, 1: C := C - AB.
 int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
-                     const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s);
+                     const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s);
 
 // Strassen/Winograd pre/post additions (addsub.cu).
 int launch_pre_add(int W, int algo, int side, int64_t P, const MatDesc &X, const MatDesc &Y,
@@ -63,6 +63,7 @@ int launch_elementwise(int W, int op, int64_t count, const double *x, const doub
 // Recursion planner + executor (recursion.cu).
 size_t gemm_workspace_bytes(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n,
                             int64_t batch, size_t limit, int *dfs_levels);
+// algo may carry DDQD_MADD_FUSED (bit 8): the leaf then uses the fused DD madd
 int run_gemm(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n, int64_t batch,
              const MatDesc &A, const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s);
 

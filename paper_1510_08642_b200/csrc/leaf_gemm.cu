@@ -48,7 +48,7 @@ __device__ __forceinline__ int micro_idx(int t, int i) {
     return (i >> 1) * (BM / (TM / 2)) + t * 2 + (i & 1);
 }
 
-template <int W, int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB>
+template <int W, int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int MV>
 __global__ void __launch_bounds__(LeafCfg<W, BM, BN, BK, TM, TN, STAGES>::NT, MINB)
 leaf_gemm_kernel(int64_t m, int64_t l, int64_t n, MatDesc A, MatDesc B, MatDesc C, int beta,
                  int64_t batch0) {
@@ -150,7 +150,7 @@ leaf_gemm_kernel(int64_t m, int64_t l, int64_t n, MatDesc A, MatDesc B, MatDesc 
 #pragma unroll
                         for (int w = 0; w < W; w++) bb.w[w] = bv[w][j];
                     }
-                    acc[i][j] = E::madd(acc[i][j], a, bb);
+                    acc[i][j] = MV ? E::madd_fused(acc[i][j], a, bb) : E::madd(acc[i][j], a, bb);
                 }
             }
         }
@@ -177,11 +177,11 @@ leaf_gemm_kernel(int64_t m, int64_t l, int64_t n, MatDesc A, MatDesc B, MatDesc 
     }
 }
 
-template <int W, int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB>
+template <int W, int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int MV = 0>
 static int launch_cfg(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
                       const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s) {
     using Cfg = LeafCfg<W, BM, BN, BK, TM, TN, STAGES>;
-    auto kern = leaf_gemm_kernel<W, BM, BN, BK, TM, TN, STAGES, MINB>;
+    auto kern = leaf_gemm_kernel<W, BM, BN, BK, TM, TN, STAGES, MINB, MV>;
     static bool attr_set = false;   // per template instance
     if (!attr_set) {
         DDQD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -216,8 +216,15 @@ static int leaf_cfg_override() {
 }
 
 int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
-                     const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s) {
+                     const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s) {
     if (m == 0 || n == 0 || batch == 0) return DDQD_OK;
+    if (mv) {   // fused DD madd (numerics.md s.2, row f3)
+        if (W != 2) { set_error("the fused madd variant is DD only"); return DDQD_ENOTSUP; }
+        const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
+        if (big_tiles >= 2 * 148 && m > 32 && n > 32)
+            return launch_cfg<2, 64, 64, 8, 4, 4, 4, 2, 1>(m, l, n, batch, A, B, C, beta, s);
+        return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2, 1>(m, l, n, batch, A, B, C, beta, s);
+    }
     switch (leaf_cfg_override()) {
     case 0: return launch_cfg<2, 64, 64, 16, 4, 4, 3, 2>(m, l, n, batch, A, B, C, beta, s);
     case 1: return launch_cfg<2, 64, 64, 8, 4, 4, 4, 2>(m, l, n, batch, A, B, C, beta, s);

@@ -22,7 +22,7 @@ void *workspace_get(size_t bytes, int *status);   // abi.cu
 size_t workspace_limit();                          // abi.cu
 
 struct Plan {
-    int W = 2, algo = 0, d = 0, s = 0;
+    int W = 2, algo = 0, d = 0, s = 0, mv = 0;
     int64_t T = 1;
     std::vector<int64_t> m, l, n;       // level shapes, 0..d
     std::vector<int64_t> chunk;         // parents per chunk at level j (j < d)
@@ -87,6 +87,7 @@ static int make_plan(Plan &p, int W, int algo, int64_t T, int64_t m, int64_t l, 
 
 size_t gemm_workspace_bytes(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n,
                             int64_t batch, size_t limit, int *dfs_levels) {
+    algo &= 0xff;
     Plan p;
     make_plan(p, W, algo, T, m, l, n, batch, limit);
     if (dfs_levels) *dfs_levels = p.s;
@@ -105,7 +106,7 @@ static MatDesc shift(MatDesc d, int64_t p0) { d.p += p0 * d.bs; return d; }
 
 static int exec_level(const Plan &p, char *ws, int j, int64_t cnt, const MatDesc &A,
                       const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s) {
-    if (j == p.d) return launch_leaf_gemm(p.W, p.m[j], p.l[j], p.n[j], cnt, A, B, C, beta, s);
+    if (j == p.d) return launch_leaf_gemm(p.W, p.m[j], p.l[j], p.n[j], cnt, A, B, C, beta, p.mv, s);
     const MatDesc cA = child(p, ws, p.offA, j + 1, p.m[j + 1], p.l[j + 1]);
     const MatDesc cB = child(p, ws, p.offB, j + 1, p.l[j + 1], p.n[j + 1]);
     const MatDesc cM = child(p, ws, p.offM, j + 1, p.m[j + 1], p.n[j + 1]);
@@ -123,10 +124,13 @@ static int exec_level(const Plan &p, char *ws, int j, int64_t cnt, const MatDesc
 int run_gemm(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n, int64_t batch,
              const MatDesc &A, const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s) {
     if (m == 0 || n == 0 || batch == 0) return DDQD_OK;
+    const int mv = (algo & DDQD_MADD_FUSED) ? 1 : 0;
+    algo &= 0xff;
     Plan p;
     int rc = make_plan(p, W, algo, T, m, l, n, batch, workspace_limit());
     if (rc) return rc;
-    if (p.d == 0) return launch_leaf_gemm(W, m, l, n, batch, A, B, C, beta, s);
+    p.mv = mv;
+    if (p.d == 0) return launch_leaf_gemm(W, m, l, n, batch, A, B, C, beta, mv, s);
     int st = DDQD_OK;
     char *ws = static_cast<char *>(workspace_get(p.bytes, &st));
     if (st) return st;

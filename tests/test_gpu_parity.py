@@ -384,3 +384,30 @@ def test_qd_lu_c4_recipe_512_bitwise(orc):
     x_ref, LU_ref, _, _ = orc.solve(A, b, panel=128, algo="strassen", threshold=64)
     x, LU, piv, info = ddqd.qd_lu_solve(cu(A), cu(b), panel=128, algo="strassen", threshold=64)
     assert info == 0 and same(np_(LU), LU_ref) and same(np_(x), x_ref)
+
+
+# ---- fused DD madd variant (DDQD_MADD_FUSED) --------------------
+def test_dd_madd_fused_elementwise_bitwise(orc):
+    x, y, w = _dd_samples(100000, 4), _dd_samples(100000, 5), _dd_samples(100000, 6)
+    assert same(np_(ddqd.elementwise("madd_fused", cu(x), cu(y), cu(w))), orc.dd_op("madd_fused", x, y, w))
+
+
+@pytest.mark.parametrize("algo", ["block", "strassen", "winograd"])
+def test_fused_madd_gemm_bitwise(orc, algo):
+    for (m, l, n, T) in [(65, 66, 67, 16), (301, 257, 299, 64), (1024, 1024, 1024, 128)]:
+        A = gen.dd_matrix(m, l, 31, 0)
+        B = gen.dd_matrix(l, n, 31, 1)
+        got = np_(ddqd.gemm(cu(A), cu(B), algo, T, madd="fused"))
+        assert same(got, orc.gemm(A, B, algo, threshold=T, madd="fused")), (m, l, n)
+
+
+def test_fused_madd_lu_and_qd_rejected(orc):
+    n = 160
+    A = gen.lu_matrix(n, 5)
+    b = _b_ones(orc, A)
+    x_ref, LU_ref, _, _ = orc.solve(A, b, panel=32, algo="strassen", threshold=16, madd="fused")
+    x, LU, piv, info = ddqd.lu_solve(cu(A), cu(b), panel=32, algo="strassen", threshold=16, madd="fused")
+    assert info == 0 and same(np_(LU), LU_ref) and same(np_(x), x_ref)
+    Q = cu(gen.qd_matrix(8, 8, 1, 0))
+    with pytest.raises(ddqd.DDQDError):
+        ddqd.gemm(Q, Q, "block", madd="fused")

@@ -241,3 +241,28 @@ def test_strassen_c1_shape_error_vs_exact_sampled(orc):
         bound = 18.0 ** d * 2.0 ** -96 * n * nA * nB
         assert np.max(np.abs(err)) <= bound
         assert np.max(np.abs(err)) <= bound * 2.0 ** -8
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_fused_madd_gemm_vs_exact(orc, algo):
+    """Fused-madd variant (row f3): every algorithm within 18^d 2^-96 l |A||B| of the exact
+    product; integer inputs still exact; it changes bits relative to the canonical madd."""
+    cases = [(13, 11, 15, 3), (16, 16, 16, 2), (7, 9, 5, 1)]
+    for (m, l, n, T) in cases:
+        A = gen.dd_matrix(m, l, m + 7, 0)
+        B = gen.dd_matrix(l, n, m + 7, 1)
+        C = orc.gemm(A, B, algo, threshold=T, madd="fused")
+        E = exact_product(A, B)
+        d = 0 if algo == "block" else rec_depth(m, l, n, T)
+        nA = max(abs(frac(A[:, i, k])) for i in range(m) for k in range(l))
+        nB = max(abs(frac(B[:, k, j])) for k in range(l) for j in range(n))
+        bound = Fraction(18) ** d * Fraction(1, 2 ** 96) * l * nA * nB
+        for i in range(m):
+            for j in range(n):
+                assert abs(frac(C[:, i, j]) - E[i][j]) <= bound
+    A = gen.dd_matrix(40, 40, 3, 0)
+    assert not np.array_equal(orc.gemm(A, A, algo, 8, madd="fused"), orc.gemm(A, A, algo, 8))
+    rng = np.random.default_rng(3)
+    Ai = _int_mat(2, 17, 9, rng)
+    Bi = _int_mat(2, 9, 13, rng)
+    assert np.array_equal(orc.gemm(Ai, Bi, algo, 2, madd="fused")[0], Ai[0] @ Bi[0])
