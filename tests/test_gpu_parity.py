@@ -411,3 +411,68 @@ def test_fused_madd_lu_and_qd_rejected(orc):
     Q = cu(gen.qd_matrix(8, 8, 1, 0))
     with pytest.raises(ddqd.DDQDError):
         ddqd.gemm(Q, Q, "block", madd="fused")
+
+
+# ---- schedule / plumbing robustness ---------------------------------------------------------
+def test_batch_beyond_grid_z_limit(orc):
+    """> 65535 problems in one batched call (the leaf splits grid.z)."""
+    batch, m = 70000, 3
+    A = gen.dd_matrix(batch * m, m, 41, 0).reshape(2, batch, m, m).transpose(1, 0, 2, 3).copy()
+    B = gen.dd_matrix(batch * m, m, 41, 1).reshape(2, batch, m, m).transpose(1, 0, 2, 3).copy()
+    C = torch.empty((batch, 2, m, m), dtype=torch.float64, device=DEV)
+    ddqd.gemm_batched(cu(A), cu(B), C, "block", 1)
+    got = np_(C)
+    for b in (0, 1, 65534, 65535, 65536, batch - 1):
+        assert same(got[b], orc.gemm(A[b], B[b], "block"))
+
+
+@pytest.mark.parametrize("limit_mb", [1, 40])
+def test_depth_first_schedule_same_bits(orc, limit_mb):
+    """A small workspace limit forces depth-first top levels (chunked batches); results are
+    bitwise those of the breadth-first schedule and the oracle."""
+    A = gen.dd_matrix(515, 517, 43, 0)
+    B = gen.dd_matrix(517, 513, 43, 1)
+    ref = orc.gemm(A, B, "winograd", threshold=32)
+    try:
+        ddqd.set_workspace_limit(limit_mb << 20)
+        got = np_(ddqd.dd_gemm(cu(A), cu(B), "winograd", 32))
+    finally:
+        ddqd.set_workspace_limit(0)
+        ddqd.release()
+    assert same(got, ref)
+
+
+def test_caller_workspace_and_stream(orc):
+    """Caller-owned workspace (ddqd_set_workspace) and a non-default torch stream."""
+    import ctypes
+    A = gen.dd_matrix(300, 280, 44, 0)
+    B = gen.dd_matrix(280, 290, 44, 1)
+    need = ddqd.workspace_bytes(2, 300, 280, 290, "strassen", 40)
+    assert need > 0
+    ws = torch.empty(need // 8 + 1, dtype=torch.float64, device=DEV)
+    s = torch.cuda.Stream()
+    try:
+        ddqd.lib.ddqd_set_workspace(ctypes.c_void_p(ws.data_ptr()), need)
+        with torch.cuda.stream(s):
+            gA, gB = cu(A), cu(B)
+            C = ddqd.dd_gemm(gA, gB, "strassen", 40)
+        s.synchronize()
+        got = C.cpu().numpy()
+        # too small a caller workspace -> ENOMEM, not a crash
+        ddqd.lib.ddqd_set_workspace(ctypes.c_void_p(ws.data_ptr()), 1024)
+        with pytest.raises(ddqd.DDQDError):
+            ddqd.dd_gemm(gA, gB, "strassen", 40)
+    finally:
+        ddqd.lib.ddqd_set_workspace(None, 0)
+    assert same(got, orc.gemm(A, B, "strassen", threshold=40))
+
+
+def test_launch_count_and_profile():
+    A = cu(gen.dd_matrix(256, 256, 1, 0))
+    n0 = ddqd.launch_count()
+    ddqd.profile_start()
+    ddqd.dd_gemm(A, A, "strassen", 64)
+    prof = ddqd.profile_stop()
+    assert ddqd.launch_count() - n0 == 7   # BFS: 2 pre-adds per level x 2 + 1 batched leaf + 2 post-adds
+    assert prof["leaf"][1] == 1 and prof["leaf"][2] == 49 * 64 ** 3
+    assert prof["pre"][1] == 4 and prof["post"][1] == 2
