@@ -215,9 +215,29 @@ static int leaf_cfg_override() {
     return v;
 }
 
+int try_leaf_tma(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A, const MatDesc &B,
+                 const MatDesc &C, int beta, int mv, cudaStream_t s, int *rc);   // leaf_tma.cu
+
+// DDQD_LEAF_TMA=0 disables the TMA + mbarrier DD leaf (A/B comparisons); default on
+static bool tma_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_LEAF_TMA");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
                      const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s) {
     if (m == 0 || n == 0 || batch == 0) return DDQD_OK;
+    if (W == 2 && tma_enabled() && leaf_cfg_override() < 0) {
+        const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
+        if (big_tiles >= 2 * 148 && m > 32 && n > 32) {
+            int rc = DDQD_OK;
+            if (try_leaf_tma(m, l, n, batch, A, B, C, beta, mv, s, &rc)) return rc;
+        }
+    }
     if (mv) {   // fused DD madd (numerics.md s.2, row f3)
         if (W != 2) { set_error("the fused madd variant is DD only"); return DDQD_ENOTSUP; }
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;

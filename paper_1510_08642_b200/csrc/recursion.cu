@@ -31,6 +31,8 @@ struct Plan {
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+// workspace leading dimension: even, so every row starts 16-byte aligned (TMA tensor maps)
+static int64_t ws_ld(int64_t cols) { return (cols + 1) & ~int64_t(1); }
 
 static void plan_shapes(Plan &p, int64_t m, int64_t l, int64_t n) {
     p.m = {m}; p.l = {l}; p.n = {n};
@@ -58,9 +60,9 @@ static size_t plan_layout(Plan &p, int64_t batch, int s, bool fill) {
     for (int j = 0; j < d; j++) {
         const int64_t k = cnt[j + 1];
         const size_t W = (size_t)p.W;
-        const size_t a = (size_t)k * W * p.m[j + 1] * p.l[j + 1] * sizeof(double);
-        const size_t b = (size_t)k * W * p.l[j + 1] * p.n[j + 1] * sizeof(double);
-        const size_t c = (size_t)k * W * p.m[j + 1] * p.n[j + 1] * sizeof(double);
+        const size_t a = (size_t)k * W * p.m[j + 1] * ws_ld(p.l[j + 1]) * sizeof(double);
+        const size_t b = (size_t)k * W * p.l[j + 1] * ws_ld(p.n[j + 1]) * sizeof(double);
+        const size_t c = (size_t)k * W * p.m[j + 1] * ws_ld(p.n[j + 1]) * sizeof(double);
         oa[j + 1] = off; off = align256(off + a);
         ob[j + 1] = off; off = align256(off + b);
         om[j + 1] = off; off = align256(off + c);
@@ -98,7 +100,7 @@ static MatDesc child(const Plan &p, char *ws, const std::vector<size_t> &off, in
                      int64_t rows, int64_t cols) {
     MatDesc d;
     d.p = reinterpret_cast<double *>(ws + off[level]);
-    d.rows = rows; d.cols = cols; d.ld = cols; d.ps = rows * cols; d.bs = (int64_t)p.W * d.ps;
+    d.rows = rows; d.cols = cols; d.ld = ws_ld(cols); d.ps = rows * d.ld; d.bs = (int64_t)p.W * d.ps;
     return d;
 }
 
