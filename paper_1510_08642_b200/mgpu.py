@@ -7,11 +7,13 @@ One process per GPU (torchrun), torch.distributed over NCCL for the plumbing:
     2. every rank forms the top-k levels of pre-additions locally (fused library kernels),
        giving the 7^k operand pairs of depth k (the paper's 7 "sections" of P:33, k levels
        deep);
-    3. rank r multiplies a contiguous, balanced slice of those 7^k products with ONE batched
-       library call (the recursion continues below depth k on the GPU);
-    4. the products are gathered to rank 0 (NCCL gather), which runs the top-k post-
-       additions into C. DD/QD sums cannot use NCCL reductions (adding hi and lo planes
-       separately is not DD addition), so the combine is the library's post-add kernel.
+       -- pruned to the ancestors of the rank's own products;
+    3. rank r multiplies a contiguous, balanced slice of those 7^k products with batched
+       library calls (the recursion continues below depth k on the GPU), in ~6 chunks;
+    4. each finished chunk is sent to rank 0 (NCCL point-to-point on its own stream) while
+       the next chunk computes; rank 0 receives straight into its level-k product buffer and
+       runs the top-k post-additions into C. DD/QD sums cannot use NCCL reductions (adding hi
+       and lo planes separately is not DD addition), so the combine is the library's post-add.
   Block (or d = 0): C row-slab tiling -- rank r computes rows [r0, r1) of C from the same
     A row slab and all of B, and the slabs are gathered to rank 0.
 
@@ -92,7 +94,7 @@ class CudaBackend:
 class DistributedGemm:
     """C := A B across the process group `dist` (rank 0 holds the operands and the result)."""
 
-    def __init__(self, W, algo, T, m, l, n, dist, device=None, k=None, backend=None):
+    def __init__(self, W, algo, T, m, l, n, dist, device=None, k=None, backend=None, chunk=None):
         self.W, self.algo, self.T = W, algo, T
         self.m, self.l, self.n = m, l, n
         self.dist = dist
@@ -106,6 +108,8 @@ class DistributedGemm:
             units = 7 ** self.k
             self.slices = balanced_slices(units, self.world)
             self.per = max(hi - lo for lo, hi in self.slices)
+            # products per send: ~6 chunks per rank so communication overlaps compute
+            self.chunk = chunk or max(1, -(-self.per // 6))
         else:
             self.slices = balanced_slices(m, self.world)          # C row slabs
             self.per = max(hi - lo for lo, hi in self.slices)
@@ -125,15 +129,22 @@ class DistributedGemm:
                 bufs["M"].append(bk.empty((7 ** j, W, mj, nj), like))
         if self.k > 0:
             mk, _, nk = self.shapes[self.k]
-            bufs["local"] = bk.empty((self.per, W, mk, nk), like)
-            if self.rank == 0:
-                bufs["gather"] = [bk.empty((self.per, W, mk, nk), like) for _ in range(self.world)]
+            if self.rank != 0:
+                bufs["local"] = bk.empty((self.per, W, mk, nk), like)
         else:
             bufs["local"] = bk.empty((W, self.per, self.n), like)
             if self.rank == 0:
                 bufs["gather"] = [bk.empty((W, self.per, self.n), like) for _ in range(self.world)]
         self._bufs = bufs
         return bufs
+
+    def _ancestor_range(self, j):
+        """Parents at level j (0 <= j < k) whose subtrees contain this rank's products."""
+        lo, hi = self.slices[self.rank]
+        if hi <= lo:
+            return 0, 0
+        span = 7 ** (self.k - j)
+        return lo // span, (hi - 1) // span + 1
 
     def __call__(self, A, B, C):
         dist, W = self.dist, self.W
@@ -143,23 +154,49 @@ class DistributedGemm:
         if self.k == 0:
             return self._row_slabs(A, B, C, bufs)
         bk = self.backend
-        # top-k pre-additions, breadth-first, on every rank
+        # top-k pre-additions, breadth-first, pruned to the ancestors of this rank's products
         X, Y = A, B
         for j in range(self.k):
-            bk.pre_add(self.algo, 0, X, bufs["A"][j])
-            bk.pre_add(self.algo, 1, Y, bufs["B"][j])
+            a, b = self._ancestor_range(j)
+            if b > a:
+                Xs = X if j == 0 else X[a:b]
+                Ys = Y if j == 0 else Y[a:b]
+                bk.pre_add(self.algo, 0, Xs, bufs["A"][j][7 * a:7 * b])
+                bk.pre_add(self.algo, 1, Ys, bufs["B"][j][7 * a:7 * b])
             X, Y = bufs["A"][j], bufs["B"][j]
         lo, hi = self.slices[self.rank]
-        local = bufs["local"]
-        bk.gemm_batched(X[lo:hi], Y[lo:hi], local[: hi - lo], self.algo, self.T)
-        dist.gather(local, bufs.get("gather") if self.rank == 0 else None, dst=0)
+        # this rank's products, in chunks; each finished chunk streams to rank 0 while the next
+        # one computes (point-to-point sends on the NCCL stream overlap the library's stream)
         if self.rank == 0:
             Mk = bufs["M"][self.k - 1]
-            for r, (a, b) in enumerate(self.slices):
-                Mk[a:b].copy_(bufs["gather"][r][: b - a])
+            # receives are posted round by round (chunk c of every peer in one NCCL group), so
+            # the transfers of all peers proceed together as their chunks finish
+            chunks = {r: [(c0, min(self.slices[r][1], c0 + self.chunk))
+                          for c0 in range(self.slices[r][0], self.slices[r][1], self.chunk)]
+                      for r in range(1, self.world)}
+            reqs = []
+            for c in range(max((len(v) for v in chunks.values()), default=0)):
+                ops = [dist.P2POp(dist.irecv, Mk[v[c][0]:v[c][1]], r)
+                       for r, v in chunks.items() if c < len(v)]
+                reqs += dist.batch_isend_irecv(ops)
+            for c0 in range(lo, hi, self.chunk):
+                c1 = min(hi, c0 + self.chunk)
+                bk.gemm_batched(X[c0:c1], Y[c0:c1], Mk[c0:c1], self.algo, self.T)
+            for q in reqs:
+                q.wait()
             for j in range(self.k - 1, -1, -1):
                 target = C if j == 0 else bufs["M"][j - 1]
                 bk.post_add(self.algo, bufs["M"][j], target)
+        else:
+            local = bufs["local"]
+            sends = []
+            for c0 in range(lo, hi, self.chunk):
+                c1 = min(hi, c0 + self.chunk)
+                part = local[c0 - lo:c1 - lo]
+                bk.gemm_batched(X[c0:c1], Y[c0:c1], part, self.algo, self.T)
+                sends += dist.batch_isend_irecv([dist.P2POp(dist.isend, part, 0)])
+            for q in sends:
+                q.wait()
         return C
 
     def _row_slabs(self, A, B, C, bufs):

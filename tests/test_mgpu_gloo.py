@@ -95,7 +95,7 @@ class OracleBackend:
             self.o.gemm(np.ascontiguousarray(A[:, r0:r1, :].numpy()), B.numpy(), algo, threshold=T))
 
 
-def _worker(rank, world, port, cfg, q):
+def _worker(rank, world, port, cfg, q, chunk=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -104,7 +104,7 @@ def _worker(rank, world, port, cfg, q):
         A = torch.from_numpy(gen.matrix(W, m, l, 21, 0)) if rank == 0 else torch.zeros((W, m, l), dtype=torch.float64)
         B = torch.from_numpy(gen.matrix(W, l, n, 21, 1)) if rank == 0 else torch.zeros((W, l, n), dtype=torch.float64)
         C = torch.zeros((W, m, n), dtype=torch.float64)
-        dg = DistributedGemm(W, algo, T, m, l, n, dist, k=k, backend=OracleBackend(W))
+        dg = DistributedGemm(W, algo, T, m, l, n, dist, k=k, backend=OracleBackend(W), chunk=chunk)
         dg(A, B, C)
         dg(A, B, C)    # buffers are reused across steps
         if rank == 0:
@@ -113,11 +113,11 @@ def _worker(rank, world, port, cfg, q):
         dist.destroy_process_group()
 
 
-def _run(cfg, world=2):
+def _run(cfg, world=2, chunk=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q, chunk)) for r in range(world)]
     for p in procs:
         p.start()
     k, C = q.get(timeout=300)
@@ -140,6 +140,15 @@ def test_distributed_matches_single_process(orc, cfg):
     assert np.array_equal(C.view(np.int64), ref.view(np.int64))
     if algo != "block":
         assert k >= 1
+
+
+def test_three_ranks_uneven_chunks(orc):
+    """world size 3: 49 depth-2 products split 17/16/16, sent in chunks of 5 (uneven rounds),
+    pre-additions pruned per rank; still bit-identical to the single-process recursion."""
+    cfg = (2, "winograd", 3, 30, 27, 29, 2)
+    k, C = _run(cfg, world=3, chunk=5)
+    ref = orc.gemm(gen.matrix(2, 30, 27, 21, 0), gen.matrix(2, 27, 29, 21, 1), "winograd", threshold=3)
+    assert k == 2 and np.array_equal(C.view(np.int64), ref.view(np.int64))
 
 
 def test_balancer():
