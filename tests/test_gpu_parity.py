@@ -476,3 +476,17 @@ def test_launch_count_and_profile():
     assert ddqd.launch_count() - n0 == 7   # BFS: 2 pre-adds per level x 2 + 1 batched leaf + 2 post-adds
     assert prof["leaf"][1] == 1 and prof["leaf"][2] == 49 * 64 ** 3
     assert prof["pre"][1] == 4 and prof["post"][1] == 2
+
+
+@pytest.mark.parametrize("W", [2, 4])
+def test_exhaustive_small_shapes_all_algorithms(orc, W):
+    """Every m, l, n in 1..7 with every algorithm at thresholds 1 and 2 (forcing recursion,
+    padding at every odd level): bit-exact vs the oracle."""
+    import itertools
+    for m, l, n in itertools.product(range(1, 8), repeat=3):
+        A = gen.matrix(W, m, l, 100 * m + 10 * l + n, 0)
+        B = gen.matrix(W, l, n, 100 * m + 10 * l + n, 1)
+        gA, gB = cu(A), cu(B)
+        for algo, T in (("block", 1), ("strassen", 1), ("winograd", 1), ("strassen", 2), ("winograd", 2)):
+            got = np_(ddqd.gemm(gA, gB, algo, T))
+            assert same(got, orc.gemm(A, B, algo, threshold=T)), (m, l, n, algo, T)
