@@ -98,6 +98,20 @@ __device__ __forceinline__ void block_argmax(typename elem<W>::T v, long long i,
     __syncthreads();
 }
 
+// warp-wide argmax (ties -> lower row): every lane ends with the warp's winner
+template <int W>
+__device__ __forceinline__ void warp_argmax(typename elem<W>::T &v, long long &i) {
+    using T = typename elem<W>::T;
+    for (int off = 16; off > 0; off >>= 1) {
+        const T ov = shfl_down<W>(v, off);
+        const long long oi = __shfl_down_sync(0xffffffffu, i, off);
+        if (cand_better<W>(ov, oi, v, i)) { v = ov; i = oi; }
+    }
+    i = __shfl_sync(0xffffffffu, i, 0);
+#pragma unroll
+    for (int w = 0; w < W; w++) elem<W>::set_word(v, w, __shfl_sync(0xffffffffu, elem<W>::word(v, w), 0));
+}
+
 // ---- per-column path ---------------------------------------------------------------------
 // pivot row r (argmax over i >= k, or r = k without pivoting), swap rows k <-> r over all n
 // columns, rinv = 1 / a_kk, a_ik := a_ik * rinv for i > k.
@@ -169,7 +183,7 @@ __global__ void lu_rank1_kernel(double *A, int64_t n, int64_t k, int64_t jend, c
 template <int W>
 __global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n, int64_t p, int kb,
                                                             int rows_per, int pivot, int64_t *ipiv,
-                                                            LuAux *aux, double *scr) {
+                                                            LuAux *aux, double *scr, int probe) {
     using E = elem<W>;
     using T = typename E::T;
     namespace cg = cooperative_groups;
@@ -198,28 +212,60 @@ __global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n
     }
     __syncthreads();
 
+    long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tlast = clock64();
+    auto mark = [&](int ph) {   // DDQD_LU_PROBE timing (CTA 0 and G-1 report per-phase cycles)
+        if (probe) {
+            __syncthreads();
+            const long long t = clock64();
+            tph[ph] += t - tlast;
+            tlast = t;
+        }
+    };
     for (int kk = 0; kk < kb; kk++) {
         const int64_t k = p + kk;
+        mark(7);
         double *buf = scr + (size_t)(kk & 1) * per_buf;
         double *cand_v = buf;                                            // [W][G]
         long long *cand_i = reinterpret_cast<long long *>(buf + (size_t)W * G);
         double *cand_rows = buf + (size_t)(W + 1) * G;                   // [G][W][kb]
         double *krow = cand_rows + (size_t)G * W * kb;                   // [W][kb]
 
-        // 1. local candidate of column kk over owned rows >= k (row k only without pivoting)
-        T best = E::zero();
-        long long bi = -1;
-        for (int li = tid; li < nrows; li += blockDim.x) {
-            const int64_t gi = r0 + li;
-            if (gi < k || (!pivot && gi != k)) continue;
-            const T v = lds<W>(S, SS, li * kb + kk);
-            if (cand_better<W>(v, gi, best, bi)) { best = v; bi = gi; }
-        }
-        block_argmax<W>(best, bi, rv, ri);
-        const long long lbi = ri[0];
-        if (tid == 0) {
-            for (int w = 0; w < W; w++) cand_v[(size_t)w * G + blockIdx.x] = rv[w * 32];
-            cand_i[blockIdx.x] = lbi;
+        // 1. local candidate of column kk over owned rows >= k (row k only without pivoting);
+        // one warp suffices when the CTA owns <= 32 rows (one shared-memory barrier)
+        long long lbi;
+        if (nrows <= 32) {
+            if (tid < 32) {
+                T best = E::zero();
+                long long bi = -1;
+                if (tid < nrows) {
+                    const int64_t gi = r0 + tid;
+                    if (gi >= k && (pivot || gi == k)) { best = lds<W>(S, SS, tid * kb + kk); bi = gi; }
+                }
+                warp_argmax<W>(best, bi);
+                if (tid == 0) {
+                    for (int w = 0; w < W; w++) cand_v[(size_t)w * G + blockIdx.x] = E::word(best, w);
+                    cand_i[blockIdx.x] = bi;
+                    ri[0] = bi;
+                }
+            }
+            __syncthreads();
+            lbi = ri[0];
+        } else {
+            T best = E::zero();
+            long long bi = -1;
+            for (int li = tid; li < nrows; li += blockDim.x) {
+                const int64_t gi = r0 + li;
+                if (gi < k || (!pivot && gi != k)) continue;
+                const T v = lds<W>(S, SS, li * kb + kk);
+                if (cand_better<W>(v, gi, best, bi)) { best = v; bi = gi; }
+            }
+            block_argmax<W>(best, bi, rv, ri);
+            lbi = ri[0];
+            if (tid == 0) {
+                for (int w = 0; w < W; w++) cand_v[(size_t)w * G + blockIdx.x] = rv[w * 32];
+                cand_i[blockIdx.x] = lbi;
+            }
         }
         if (lbi >= 0) {
             const int li = (int)(lbi - r0);
@@ -232,8 +278,9 @@ __global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n
             for (int j = tid; j < kb; j += blockDim.x)
                 for (int w = 0; w < W; w++) krow[(size_t)w * kb + j] = S[w * SS + li * kb + j];
         }
-        __threadfence();
-        grid.sync();
+        mark(0);
+        grid.sync();   // grid-wide barrier with memory ordering (bar.sync + fenced arrive)
+        mark(1);
 
         // 2. global pivot, identical in every CTA; the winning CTA follows from the row index
         {
@@ -245,14 +292,25 @@ __global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n
                 const long long ci = __ldcg(cand_i + g);
                 if (cand_better<W>(cv, ci, v, i)) { v = cv; i = ci; }
             }
-            block_argmax<W>(v, i, rv, ri);
+            warp_argmax<W>(v, i);
+            const int warp = tid >> 5, nw = blockDim.x >> 5;
+            if ((tid & 31) == 0) { sts<W>(rv, 32, warp, v); ri[warp] = i; }
+            __syncthreads();
+            // every warp merges the nw per-warp winners itself (no second barrier)
+            v = (tid & 31) < nw ? lds<W>(rv, 32, tid & 31) : E::zero();
+            i = (tid & 31) < nw ? ri[tid & 31] : -1;
+            warp_argmax<W>(v, i);
+            if (tid == 0) ri[0] = i;   // read below only after the next barrier
+            __syncthreads();
         }
+        mark(2);
         const int64_t r = ri[0];
         const int wc = (int)((r - p) / rows_per);
         const double *prow = cand_rows + (size_t)wc * W * kb;
         for (int j = tid; j < kb; j += blockDim.x)
             for (int w = 0; w < W; w++) U[w * kb + j] = __ldcg(prow + (size_t)w * kb + j);
         __syncthreads();
+        mark(3);
         if (r != k) {
             if (own_k) {
                 const int li = (int)(k - r0);
@@ -278,6 +336,7 @@ __global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n
             }
         }
         __syncthreads();
+        mark(4);
         if (s_skip) continue;
         // 3. l_ik = a_ik * rinv for owned rows i > k
         const T rinv = lds<W>(s_rinv, 1, 0);
@@ -288,18 +347,27 @@ __global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n
             sts<W>(L, rows_per, li, lv);
         }
         __syncthreads();
-        // 4. rank-1 update a_ij -= l_ik u_kj, j in (kk, kb)
-        const int ncol = kb - kk - 1;
-        if (ncol > 0) {
-            for (int e = tid; e < nrows * ncol; e += blockDim.x) {
-                const int li = e / ncol, j = kk + 1 + e % ncol;
-                if (r0 + li <= k) continue;
-                const T a = lds<W>(S, SS, li * kb + j);
-                sts<W>(S, SS, li * kb + j, E::sub(a, E::mul(lds<W>(L, rows_per, li), lds<W>(U, kb, j))));
+        mark(5);
+        // 4. rank-1 update a_ij -= l_ik u_kj, j in (kk, kb): thread per column, owned active rows
+        {
+            const int64_t first = k + 1 - r0;                 // first owned row below k
+            const int li0 = first <= 0 ? 0 : (first >= nrows ? nrows : (int)first);
+            // warps take row groups, lanes take columns: every warp stays busy, no division
+            const int nwarp = blockDim.x >> 5, lane = tid & 31, wrp = tid >> 5;
+            for (int j = kk + 1 + lane; j < kb; j += 32) {
+                const T u = lds<W>(U, kb, j);
+                for (int li = li0 + wrp; li < nrows; li += nwarp) {
+                    const T a = lds<W>(S, SS, li * kb + j);
+                    sts<W>(S, SS, li * kb + j, E::sub(a, E::mul(lds<W>(L, rows_per, li), u)));
+                }
             }
         }
         __syncthreads();
+        mark(6);
     }
+    if (probe && tid == 0 && (p == 0 || blockIdx.x == 0 || blockIdx.x == G - 1))
+        printf("LUPROBE p=%lld G=%d rows=%d cta=%d publish %lld sync %lld cand %lld prow %lld swap %lld scale %lld update %lld\n",
+               (long long)p, G, rows_per, blockIdx.x, tph[0], tph[1], tph[2], tph[3], tph[4], tph[5], tph[6]);
     for (int e = tid; e < nrows * kb; e += blockDim.x) {
         const int li = e / kb, j = e % kb;
         stA<W>(A, n, r0 + li, p + j, lds<W>(S, SS, e));
@@ -520,7 +588,12 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
     if (occ < 1 || G > occ * g_coop_sms) return 0;
     int kbi = (int)kb;
     int piv = pivot;
-    void *args[] = {&A, &n, &p, &kbi, (void *)&rows_per, &piv, &ipiv, &aux, &scr};
+    static int probe = -1;   // DDQD_LU_PROBE=1: per-phase clock64 report (timing experiments)
+    if (probe < 0) {
+        const char *e = getenv("DDQD_LU_PROBE");
+        probe = (e && e[0] == '1') ? 1 : 0;
+    }
+    void *args[] = {&A, &n, &p, &kbi, (void *)&rows_per, &piv, &ipiv, &aux, &scr, &probe};
     cudaError_t e = cudaLaunchCooperativeKernel((void *)lu_panel_coop_kernel<W>, dim3(G), dim3(256), args, smem, s);
     count_launch();
     if (e != cudaSuccess) {
