@@ -41,7 +41,8 @@ WORKLOADS = {
 # FP64-pipe lane-instructions per multiply-add (docs/numerics.md: DD 3 DMUL + 1 DFMA + 16 DADD;
 # QD common path 118 (qd_mul) + 82 (qd_add)).
 OPS_PER_MADD = {2: 20, 4: 200}
-MAD_DTYPE = {2: "f64x2 (double-double)", 4: "f64x4 (quad-double)"}
+MAD_DTYPE = {2: "f64", 4: "f64"}          # arithmetic type of the path (FP64 pipe)
+REPR = {2: "double-double (2 x f64, ~106-bit)", 4: "quad-double (4 x f64, ~212-bit)"}
 
 
 def rec_shapes(m, l, n, T):
@@ -62,6 +63,8 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-variant", action="store_true",
+                    help="skip the extra fused-madd measurement reported under 'variants'")
     ap.add_argument("--madd", default="canonical", choices=["canonical", "fused"],
                     help="DD multiply-add: the paper's QD-library sequence (20 FP64 ops) or the "
                          "fused variant of numerics.md s.2 (15 ops; row f3)")
@@ -282,7 +285,7 @@ def lu_bench(args, wl, rank, world, local):
             "metric": "DD LU effective GFLOPS (2n^3/3 per solve / s)", "value": value, "unit": "GFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
-            "dtype": MAD_DTYPE[2], "data": "synthetic (seeded SplitMix64, BASELINE.json recipe)",
+            "dtype": MAD_DTYPE[2], "representation": REPR[2], "data": "synthetic (seeded SplitMix64, BASELINE.json recipe)",
             "config": {"workload": wl["name"], "n": n, "panel": K, "algo": algo, "threshold": T,
                        "parallelism": f"{world} GPU replica(s)",
                        "l2": "A (268 MB) exceeds L2; fresh copy of A before each step, outside the events"},
@@ -417,6 +420,25 @@ def main():
     leaf_madds_step = (7 ** d) * shapes[-1][0] * shapes[-1][1] * shapes[-1][2]
     classical = ops * m * l * n / (ms_per_step * 1e-3) / peak   # BJ:5's literal formula (may be > 1)
 
+    variants = None
+    if W == 2 and args.madd == "canonical" and world == 1 and not args.no_variant:
+        # the fused DD multiply-add of numerics.md s.2 (SURVEY s.8(f) row f3) on the same inputs:
+        # a different (documented) rounding, reported beside the paper-faithful headline
+        def fstep():
+            ddqd.gemm(A, B, algo, T, out=C, madd="fused")
+        fstep()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.steps):
+            fstep()
+        f1.record()
+        torch.cuda.synchronize()
+        fms = f0.elapsed_time(f1)
+        variants = {"madd_fused": {"value": flops_per_step * args.steps / (fms * 1e-3) / 1e9, "unit": "GFLOP/s",
+                                   "ms_per_step": fms / args.steps, "fp64_ops_per_madd": 15,
+                                   "note": "DDQD_MADD_FUSED: bit-exact vs the oracle's fused variant, not the canonical"}}
+
     e2e = None
     if not args.no_e2e and world == 1:
         hA = A_h.pin_memory()
@@ -452,7 +474,7 @@ def main():
             "metric": "DD/QD GEMM effective GFLOPS (2mln/s) and % FP64-pipe roofline",
             "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": MAD_DTYPE[W],
+            "scaling": "strong", "vs_baseline": None, "dtype": MAD_DTYPE[W], "representation": REPR[W],
             "data": "synthetic (seeded SplitMix64, BASELINE.json recipe)",
             "config": {"workload": wl["name"], "m": m, "l": l, "n": n, "algo": algo, "threshold": T,
                        "madd": args.madd,
@@ -466,6 +488,7 @@ def main():
                 "note": "classical = ops_per_madd*m*l*n/(P64*t) (BJ:5 literal; > 1 possible for Strassen/Winograd)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "variants": variants,
             "gpu_launches": int(launches),
             "clocks": clk,
         }

@@ -46,6 +46,11 @@ void prof_end(int cls, double work, cudaStream_t s) {
 }
 cudaStream_t cur_stream() { return t_stream; }
 void count_launch(int64_t n) { t_launches += n; }
+int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & 63;
+}
 
 // Library-owned per-device buffers. Growth frees the old buffer (cudaFree synchronises the
 // device, so no in-flight kernel can still be using it).

@@ -21,6 +21,7 @@ struct MatDesc {
 void set_error(const std::string &msg);
 cudaStream_t cur_stream();
 void count_launch(int64_t n = 1);
+int current_device();   // cudaGetDevice, masked to [0, 64) for per-device caches
 
 // Live per-class kernel timing for bench.py (CUDA events on the launching stream), active
 // only between ddqd_profile_start/stop. Classes: 0 leaf GEMM (work = madds), 1 pre-add

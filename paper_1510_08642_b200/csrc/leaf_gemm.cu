@@ -182,11 +182,12 @@ static int launch_cfg(int64_t m, int64_t l, int64_t n, int64_t batch, const MatD
                       const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s) {
     using Cfg = LeafCfg<W, BM, BN, BK, TM, TN, STAGES>;
     auto kern = leaf_gemm_kernel<W, BM, BN, BK, TM, TN, STAGES, MINB, MV>;
-    static bool attr_set = false;   // per template instance
-    if (!attr_set) {
+    static bool attr_set[64] = {};   // per template instance and device
+    const int dev = current_device();
+    if (!attr_set[dev]) {
         DDQD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)Cfg::SMEM));
-        attr_set = true;
+        attr_set[dev] = true;
     }
     const int64_t gx = (n + BN - 1) / BN, gy = (m + BM - 1) / BM;
     if (gx > 0x7fffffff || gy > 65535) {

@@ -208,13 +208,14 @@ int try_leaf_tma(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &
     CUtensorMap ma, mb;
     if (!make_map(&ma, A, batch, BK, BM) || !make_map(&mb, B, batch, BN, BK)) return 0;
     auto kern = mv ? leaf_tma_kernel<1> : leaf_tma_kernel<0>;
-    static bool attr[2] = {false, false};
-    if (!attr[mv]) {
+    static bool attr_set[2][64] = {};   // per variant and device
+    bool &attr = attr_set[mv][current_device()];
+    if (!attr) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess) {
             cudaGetLastError();
             return 0;
         }
-        attr[mv] = true;
+        attr = true;
     }
     const int64_t gx = (n + BN - 1) / BN, gy = (m + BM - 1) / BM;
     if (gx > 0x7fffffff || gy > 65535) return 0;

@@ -541,7 +541,8 @@ __global__ void trsv_bwd_update(const double *A, int64_t n, double *y, const dou
 }
 
 // ---- host driver -------------------------------------------------------------------------------
-static int g_coop_sms = -1;
+static int g_coop_sms[64];   // per device: SM count if cooperative launch is supported, else 0
+static bool g_coop_init[64];
 
 // DDQD_LU_PANEL=steps forces the per-column two-kernel path (kept as the reference schedule)
 static bool use_coop_panel() {
@@ -559,22 +560,26 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
                           double *scr, size_t scr_bytes, cudaStream_t s, int *rc) {
     *rc = DDQD_OK;
     const int64_t R = n - p;
-    if (g_coop_sms < 0) {
+    const int dv = current_device();
+    if (!g_coop_init[dv]) {
         int dev = 0, coop = 0, sms = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        g_coop_sms = coop ? sms : 0;
+        g_coop_sms[dv] = coop ? sms : 0;
+        g_coop_init[dv] = true;
     }
-    if (g_coop_sms <= 0 || kb > 4096) return 0;
-    int G = (int)std::min<int64_t>(g_coop_sms, R);
+    const int nsm = g_coop_sms[dv];
+    if (nsm <= 0 || kb > 4096) return 0;
+    int G = (int)std::min<int64_t>(nsm, R);
     const int rows_per = (int)((R + G - 1) / G);
     G = (int)((R + rows_per - 1) / rows_per);
     const size_t smem = sizeof(double) * W * ((size_t)rows_per * kb + (size_t)kb + (size_t)rows_per);
     if (smem > 200 * 1024) return 0;
     const size_t per_buf = (size_t)G * (W + 1) + (size_t)G * W * kb + (size_t)W * kb;
     if (2 * per_buf * sizeof(double) > scr_bytes) return 0;
-    static size_t attr = 0;
+    static size_t attr_dev[64];
+    size_t &attr = attr_dev[dv];
     if (smem > 48 * 1024 && smem > attr) {
         if (cudaFuncSetAttribute(lu_panel_coop_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem) != cudaSuccess) {
@@ -585,7 +590,7 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
     }
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lu_panel_coop_kernel<W>, 256, smem);
-    if (occ < 1 || G > occ * g_coop_sms) return 0;
+    if (occ < 1 || G > occ * nsm) return 0;
     int kbi = (int)kb;
     int piv = pivot;
     static int probe = -1;   // DDQD_LU_PROBE=1: per-phase clock64 report (timing experiments)
