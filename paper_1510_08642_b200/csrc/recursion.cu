@@ -12,6 +12,7 @@
 // chunking changes only the launch grouping, never the arithmetic: results are bitwise
 // those of the oracle's recursion.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -31,8 +32,18 @@ struct Plan {
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
-// workspace leading dimension: even, so every row starts 16-byte aligned (TMA tensor maps)
-static int64_t ws_ld(int64_t cols) { return (cols + 1) & ~int64_t(1); }
+// workspace leading dimension: tight by default. DDQD_WS_PAD=1 pads it to even so every row is
+// 16-byte aligned and odd-width leaves qualify for the TMA leaf; measured on c3 this costs
+// more in the pre-additions (row gaps break their contiguous stores: 23.6 vs 20.3 ms/step)
+// than TMA gains in the leaf (equal FP64-pipe rate), so it is off.
+static int64_t ws_ld(int64_t cols) {
+    static int pad = -1;
+    if (pad < 0) {
+        const char *e = getenv("DDQD_WS_PAD");
+        pad = (e && e[0] == '1') ? 1 : 0;
+    }
+    return pad ? ((cols + 1) & ~int64_t(1)) : cols;
+}
 
 static void plan_shapes(Plan &p, int64_t m, int64_t l, int64_t n) {
     p.m = {m}; p.l = {l}; p.n = {n};
