@@ -145,16 +145,16 @@ def gemm(A, B, algo="block", threshold=128, out=None, madd="canonical"):
     return out
 
 
-def dd_gemm(A, B, algo="block", threshold=128, out=None):
+def dd_gemm(A, B, algo="block", threshold=128, out=None, madd="canonical"):
     if A.shape[0] != 2:
         raise ValueError("dd_gemm takes [2, rows, cols] tensors")
-    return gemm(A, B, algo, threshold, out)
+    return gemm(A, B, algo, threshold, out, madd)
 
 
-def qd_gemm(A, B, algo="block", threshold=128, out=None):
+def qd_gemm(A, B, algo="block", threshold=128, out=None, madd="canonical"):
     if A.shape[0] != 4:
         raise ValueError("qd_gemm takes [4, rows, cols] tensors")
-    return gemm(A, B, algo, threshold, out)
+    return gemm(A, B, algo, threshold, out, madd)
 
 
 def gemm_ex(prec, algo, threshold, m, l, n, batch, A, lda, psA, bsA, B, ldb, psB, bsB,

@@ -490,3 +490,26 @@ def test_exhaustive_small_shapes_all_algorithms(orc, W):
         for algo, T in (("block", 1), ("strassen", 1), ("winograd", 1), ("strassen", 2), ("winograd", 2)):
             got = np_(ddqd.gemm(gA, gB, algo, T))
             assert same(got, orc.gemm(A, B, algo, threshold=T)), (m, l, n, algo, T)
+
+
+@pytest.mark.parametrize("W", [2, 4])
+def test_lu_tiny_and_ragged_panels(orc, W):
+    """n in {1, 2, 3, 17, 70} with panels {1, 4, 64} (n < panel, ragged last panel, K = 1):
+    bit-exact vs the oracle, pivoted and pivot-free."""
+    for n in (1, 2, 3, 17, 70):
+        A = gen.matrix(W, n, n, 50 + n, 0)
+        A[0, np.arange(n), np.arange(n)] += 2.0
+        b = gen.matrix(W, 1, n, 50 + n, 1)[:, 0, :].copy()
+        for K in (1, 4, 64):
+            for piv in (True, False):
+                xr, LUr, pr, ir = orc.solve(A, b, panel=K, algo="winograd", threshold=2, pivot=piv)
+                x, LU, p, info = ddqd.lu_solve(cu(A), cu(b), panel=K, algo="winograd", threshold=2, pivot=piv)
+                assert info == ir
+                assert np.array_equal(np_(p), pr) and same(np_(LU), LUr) and same(np_(x), xr), (n, K, piv)
+
+
+def test_qd_host_pointer_path(orc):
+    A = gen.qd_matrix(90, 77, 61, 0)
+    B = gen.qd_matrix(77, 85, 61, 1)
+    hC = ddqd.qd_gemm(torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory(), "strassen", 16)
+    assert same(hC.numpy(), orc.gemm(A, B, "strassen", threshold=16))
