@@ -98,9 +98,11 @@ def _torch():
 
 
 def _set_stream(t):
+    """Make the library use torch's current stream (of t's device; of the current device for
+    host tensors, whose staging copies then run on that stream)."""
     torch = _torch()
-    if t.is_cuda:
-        lib.ddqd_set_stream(ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream))
+    dev = t.device if t.is_cuda else torch.device("cuda", torch.cuda.current_device())
+    lib.ddqd_set_stream(ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
 
 
 def _algo(a, madd="canonical") -> int:

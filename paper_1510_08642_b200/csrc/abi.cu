@@ -149,7 +149,7 @@ static int check_gemm_args(int64_t m, int64_t l, int64_t n, int algo, int64_t T)
     return DDQD_OK;
 }
 
-static int gemm_simple(int W, int64_t m, int64_t l, int64_t n, const double *A, const double *B,
+static int gemm_entry(int W, int64_t m, int64_t l, int64_t n, const double *A, const double *B,
                        double *C, int algo, int64_t T) {
     t_err.clear();
     int rc = check_gemm_args(m, l, n, algo, T);
@@ -194,12 +194,12 @@ extern "C" {
 
 int dd_gemm(int64_t m, int64_t l, int64_t n, const double *A, const double *B, double *C, int algo,
             int64_t threshold) {
-    return gemm_simple(2, m, l, n, A, B, C, algo, threshold);
+    return gemm_entry(2, m, l, n, A, B, C, algo, threshold);
 }
 
 int qd_gemm(int64_t m, int64_t l, int64_t n, const double *A, const double *B, double *C, int algo,
             int64_t threshold) {
-    return gemm_simple(4, m, l, n, A, B, C, algo, threshold);
+    return gemm_entry(4, m, l, n, A, B, C, algo, threshold);
 }
 
 int ddqd_gemm_ex(const ddqd_gemm_desc *d) {
