@@ -41,7 +41,8 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return SO
-    cmd = [NVCC, *NVCC_FLAGS, "-o", SO, *sources()]
+    extra = os.environ.get("DDQD_NVCC_EXTRA", "").split()   # tuning experiments only
+    cmd = [NVCC, *NVCC_FLAGS, *extra, "-o", SO, *sources()]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:

@@ -21,6 +21,68 @@ __device__ __forceinline__ typename elem<W>::T ld_or_zero(const double *base, in
     return ok ? elem<W>::load(base, ps) : elem<W>::zero();
 }
 
+// One level of pre-additions on the four quadrant values of a position: the 7 operands of
+// side 0 (A) or 1 (B); algo 1 = Strassen, 2 = Winograd (numerics.md s.4, S:239 / S:248).
+template <int W, int ALGO, int SIDE>
+__device__ __forceinline__ void pre_ops(const typename elem<W>::T &x11, const typename elem<W>::T &x12,
+                                        const typename elem<W>::T &x21, const typename elem<W>::T &x22,
+                                        typename elem<W>::T o[7]) {
+    using E = elem<W>;
+    using T = typename E::T;
+    if constexpr (ALGO == 1 && SIDE == 0) {        // Strassen, A side
+        o[0] = E::add(x11, x22);                    // P1: A11+A22
+        o[1] = E::add(x21, x22);                    // P2: A21+A22
+        o[2] = x11;                                 // P3: A11
+        o[3] = x22;                                 // P4: A22
+        o[4] = E::add(x11, x12);                    // P5: A11+A12
+        o[5] = E::sub(x21, x11);                    // P6: A21-A11
+        o[6] = E::sub(x12, x22);                    // P7: A12-A22
+    } else if constexpr (ALGO == 1 && SIDE == 1) { // Strassen, B side
+        o[0] = E::add(x11, x22);                    // P1: B11+B22
+        o[1] = x11;                                 // P2: B11
+        o[2] = E::sub(x12, x22);                    // P3: B12-B22
+        o[3] = E::sub(x21, x11);                    // P4: B21-B11
+        o[4] = x22;                                 // P5: B22
+        o[5] = E::add(x11, x12);                    // P6: B11+B12
+        o[6] = E::add(x21, x22);                    // P7: B21+B22
+    } else if constexpr (ALGO == 2 && SIDE == 0) { // Winograd, A side
+        const T s1 = E::add(x21, x22);
+        const T s2 = E::sub(s1, x11);
+        const T s3 = E::sub(x11, x21);
+        const T s4 = E::sub(x12, s2);
+        o[0] = x11; o[1] = x12; o[2] = s4; o[3] = x22; o[4] = s1; o[5] = s2; o[6] = s3;
+    } else {                                        // Winograd, B side
+        const T t1 = E::sub(x12, x11);
+        const T t2 = E::sub(x22, t1);
+        const T t3 = E::sub(x22, x12);
+        const T t4 = E::sub(t2, x21);
+        o[0] = x11; o[1] = x21; o[2] = x22; o[3] = t4; o[4] = t1; o[5] = t2; o[6] = t3;
+    }
+}
+
+// One level of post-additions: 7 products -> the 4 quadrant values of a position.
+template <int W, int ALGO>
+__device__ __forceinline__ void post_ops(const typename elem<W>::T p[7], typename elem<W>::T &c11,
+                                         typename elem<W>::T &c12, typename elem<W>::T &c21,
+                                         typename elem<W>::T &c22) {
+    using E = elem<W>;
+    using T = typename E::T;
+    if constexpr (ALGO == 1) {
+        c11 = E::add(E::sub(E::add(p[0], p[3]), p[4]), p[6]);   // ((P1+P4)-P5)+P7
+        c12 = E::add(p[2], p[4]);                                // P3+P5
+        c21 = E::add(p[1], p[3]);                                // P2+P4
+        c22 = E::add(E::add(E::sub(p[0], p[1]), p[2]), p[5]);   // ((P1-P2)+P3)+P6
+    } else {
+        const T u2 = E::add(p[0], p[5]);      // U2 = M1+M6
+        const T u3 = E::add(u2, p[6]);        // U3 = U2+M7
+        const T u4 = E::add(u2, p[4]);        // U4 = U2+M5
+        c11 = E::add(p[0], p[1]);             // U1 = M1+M2
+        c12 = E::add(u4, p[2]);               // U5 = U4+M3
+        c21 = E::sub(u3, p[3]);               // U6 = U3-M4
+        c22 = E::add(u3, p[4]);               // U7 = U3+M5
+    }
+}
+
 // side 0 = A operands, side 1 = B operands; algo 1 = Strassen, 2 = Winograd
 template <int W, int ALGO, int SIDE>
 __global__ void __launch_bounds__(256) pre_add_kernel(int64_t P, MatDesc X, MatDesc Y) {
@@ -39,37 +101,66 @@ __global__ void __launch_bounds__(256) pre_add_kernel(int64_t P, MatDesc X, MatD
         const T x21 = ld_or_zero<W>(xb + (i + hr) * X.ld + j, X.ps, r2);
         const T x22 = ld_or_zero<W>(xb + (i + hr) * X.ld + (j + hc), X.ps, r2 && c2);
         T o[7];
-        if constexpr (ALGO == 1 && SIDE == 0) {        // Strassen, A side
-            o[0] = E::add(x11, x22);                    // P1: A11+A22
-            o[1] = E::add(x21, x22);                    // P2: A21+A22
-            o[2] = x11;                                 // P3: A11
-            o[3] = x22;                                 // P4: A22
-            o[4] = E::add(x11, x12);                    // P5: A11+A12
-            o[5] = E::sub(x21, x11);                    // P6: A21-A11
-            o[6] = E::sub(x12, x22);                    // P7: A12-A22
-        } else if constexpr (ALGO == 1 && SIDE == 1) { // Strassen, B side
-            o[0] = E::add(x11, x22);                    // P1: B11+B22
-            o[1] = x11;                                 // P2: B11
-            o[2] = E::sub(x12, x22);                    // P3: B12-B22
-            o[3] = E::sub(x21, x11);                    // P4: B21-B11
-            o[4] = x22;                                 // P5: B22
-            o[5] = E::add(x11, x12);                    // P6: B11+B12
-            o[6] = E::add(x21, x22);                    // P7: B21+B22
-        } else if constexpr (ALGO == 2 && SIDE == 0) { // Winograd, A side
-            const T s1 = E::add(x21, x22);
-            const T s2 = E::sub(s1, x11);
-            const T s3 = E::sub(x11, x21);
-            const T s4 = E::sub(x12, s2);
-            o[0] = x11; o[1] = x12; o[2] = s4; o[3] = x22; o[4] = s1; o[5] = s2; o[6] = s3;
-        } else {                                        // Winograd, B side
-            const T t1 = E::sub(x12, x11);
-            const T t2 = E::sub(x22, t1);
-            const T t3 = E::sub(x22, x12);
-            const T t4 = E::sub(t2, x21);
-            o[0] = x11; o[1] = x21; o[2] = x22; o[3] = t4; o[4] = t1; o[5] = t2; o[6] = t3;
-        }
+        pre_ops<W, ALGO, SIDE>(x11, x12, x21, x22, o);
 #pragma unroll
         for (int c = 0; c < 7; c++) E::store(Y.p + (7 * b + c) * Y.bs + i * Y.ld + j, Y.ps, o[c]);
+    }
+}
+
+// The two-level kernels hold 28 DD intermediates per thread (~170 registers unbounded);
+// 128-thread CTAs at <= 170 registers (3 per SM-slot group) keep 12 warps per SM in flight
+// without spilling: measured best of 128x3 / 128x4 (spills) / 256x1 / 64x6 on c3 (pre-adds
+// 11.9 vs 12.0 / 13.9 / 12.7 ms per step).
+#ifndef ADD2_THREADS
+#define ADD2_THREADS 128
+#endif
+#ifndef ADD2_MINB
+#define ADD2_MINB 3
+#endif
+
+// Two recursion levels in one pass (parent X at level j -> 49 grandchildren Y at level
+// j+2, child 49b + 7c1 + c2). A thread owns one level-(j+2) position (i, c): it reads the 16
+// level-j values the position depends on, forms the 7 level-(j+1) operands at each of the 4
+// level-(j+1) positions (i + a*Y.rows, c + e*Y.cols) -- exact zeros where that position is
+// the level-(j+1) padding, as the one-level kernel's zero-filled loads would read them --
+// and then the 7 grandchildren of each. Same operations in the same order as two launches
+// of pre_add_kernel, so bit-identical; the level-(j+1) operands never touch HBM.
+template <int W, int ALGO, int SIDE>
+__global__ void __launch_bounds__(ADD2_THREADS, ADD2_MINB) pre_add2_kernel(int64_t P, MatDesc X, int64_t h1r,
+                                                       int64_t h1c, MatDesc Y) {
+    using E = elem<W>;
+    using T = typename E::T;
+    const int64_t hr = Y.rows, hc = Y.cols;
+    const int64_t per = hr * hc;
+    const int64_t total = P * per;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = t / per, rem = t % per, i = rem / hc, j = rem % hc;
+        const double *xb = X.p + b * X.bs;
+        T y[4][7];
+#pragma unroll
+        for (int sp = 0; sp < 4; sp++) {
+            const int64_t r = i + (sp >> 1) * hr, c = j + (sp & 1) * hc;
+            if (r < h1r && c < h1c) {
+                const bool r2 = r + h1r < X.rows, c2 = c + h1c < X.cols;
+                const T x11 = E::load(xb + r * X.ld + c, X.ps);
+                const T x12 = ld_or_zero<W>(xb + r * X.ld + (c + h1c), X.ps, c2);
+                const T x21 = ld_or_zero<W>(xb + (r + h1r) * X.ld + c, X.ps, r2);
+                const T x22 = ld_or_zero<W>(xb + (r + h1r) * X.ld + (c + h1c), X.ps, r2 && c2);
+                pre_ops<W, ALGO, SIDE>(x11, x12, x21, x22, y[sp]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 7; k++) y[sp][k] = E::zero();
+            }
+        }
+#pragma unroll
+        for (int c1 = 0; c1 < 7; c1++) {
+            T o[7];
+            pre_ops<W, ALGO, SIDE>(y[0][c1], y[1][c1], y[2][c1], y[3][c1], o);
+#pragma unroll
+            for (int c2 = 0; c2 < 7; c2++)
+                E::store(Y.p + (49 * b + 7 * c1 + c2) * Y.bs + i * Y.ld + j, Y.ps, o[c2]);
+        }
     }
 }
 
@@ -87,20 +178,7 @@ __global__ void __launch_bounds__(256) post_add_kernel(int64_t P, MatDesc M, Mat
 #pragma unroll
         for (int c = 0; c < 7; c++) p[c] = E::load(M.p + (7 * b + c) * M.bs + i * M.ld + j, M.ps);
         T c11, c12, c21, c22;
-        if constexpr (ALGO == 1) {
-            c11 = E::add(E::sub(E::add(p[0], p[3]), p[4]), p[6]);   // ((P1+P4)-P5)+P7
-            c12 = E::add(p[2], p[4]);                                // P3+P5
-            c21 = E::add(p[1], p[3]);                                // P2+P4
-            c22 = E::add(E::add(E::sub(p[0], p[1]), p[2]), p[5]);   // ((P1-P2)+P3)+P6
-        } else {
-            const T u2 = E::add(p[0], p[5]);      // U2 = M1+M6
-            const T u3 = E::add(u2, p[6]);        // U3 = U2+M7
-            const T u4 = E::add(u2, p[4]);        // U4 = U2+M5
-            c11 = E::add(p[0], p[1]);             // U1 = M1+M2
-            c12 = E::add(u4, p[2]);               // U5 = U4+M3
-            c21 = E::sub(u3, p[3]);               // U6 = U3-M4
-            c22 = E::add(u3, p[4]);               // U7 = U3+M5
-        }
+        post_ops<W, ALGO>(p, c11, c12, c21, c22);
         double *cb = C.p + b * C.bs;
         const bool r2 = i + hm < C.rows, cc2 = j + hn < C.cols;
         auto put = [&](int64_t r, int64_t c, const T &v) {
@@ -115,9 +193,58 @@ __global__ void __launch_bounds__(256) post_add_kernel(int64_t P, MatDesc M, Mat
     }
 }
 
-static unsigned grid_for(int64_t total) {
-    int64_t blocks = (total + 255) / 256;
-    const int64_t cap = 148 * 16;   // grid-stride beyond 16 CTAs per SM
+// Two recursion levels in one pass (49 level-(j+2) products M, child 49b + 7c1 + c2 -> the
+// level-j parent C[b]). A thread owns one level-(j+2) position: it combines the 7 products of
+// each level-(j+1) child c1 into that child's 4 quadrant values (positions
+// (i + a*M.rows, c + e*M.cols) of the level-(j+1) product), then, at every such position
+// inside the level-(j+1) extent h1m x h1n (the one-level kernel crops the rest away), the
+// 7 children into C's 4 quadrants. Bit-identical to two launches of post_add_kernel; the
+// level-(j+1) products never touch HBM.
+template <int W, int ALGO>
+__global__ void __launch_bounds__(ADD2_THREADS, ADD2_MINB) post_add2_kernel(int64_t P, MatDesc M, int64_t h1m,
+                                                        int64_t h1n, MatDesc C, int beta) {
+    using E = elem<W>;
+    using T = typename E::T;
+    const int64_t hm = M.rows, hn = M.cols;
+    const int64_t per = hm * hn;
+    const int64_t total = P * per;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = t / per, rem = t % per, i = rem / hn, j = rem % hn;
+        T y[4][7];
+#pragma unroll
+        for (int c1 = 0; c1 < 7; c1++) {
+            T p[7];
+#pragma unroll
+            for (int c2 = 0; c2 < 7; c2++)
+                p[c2] = E::load(M.p + (49 * b + 7 * c1 + c2) * M.bs + i * M.ld + j, M.ps);
+            post_ops<W, ALGO>(p, y[0][c1], y[1][c1], y[2][c1], y[3][c1]);
+        }
+        double *cb = C.p + b * C.bs;
+        auto put = [&](int64_t r, int64_t c, const T &v) {
+            double *q = cb + r * C.ld + c;
+            if (beta) E::store(q, C.ps, E::sub(E::load(q, C.ps), v));
+            else E::store(q, C.ps, v);
+        };
+#pragma unroll
+        for (int sp = 0; sp < 4; sp++) {
+            const int64_t r = i + (sp >> 1) * hm, c = j + (sp & 1) * hn;
+            if (r < h1m && c < h1n) {
+                T c11, c12, c21, c22;
+                post_ops<W, ALGO>(y[sp], c11, c12, c21, c22);
+                const bool r2 = r + h1m < C.rows, cc2 = c + h1n < C.cols;
+                if (r < C.rows && c < C.cols) put(r, c, c11);
+                if (r < C.rows && cc2) put(r, c + h1n, c12);
+                if (r2 && c < C.cols) put(r + h1m, c, c21);
+                if (r2 && cc2) put(r + h1m, c + h1n, c22);
+            }
+        }
+    }
+}
+
+static unsigned grid_for(int64_t total, int threads = 256) {
+    int64_t blocks = (total + threads - 1) / threads;
+    const int64_t cap = 148 * 16 * 256 / threads;   // grid-stride beyond 16 CTAs (of 256) per SM
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     return (unsigned)blocks;
@@ -142,6 +269,52 @@ int launch_pre_add(int W, int algo, int side, int64_t P, const MatDesc &X, const
                    cudaStream_t s) {
     if (W == 2) return pre_dispatch<2>(algo, side, P, X, Y, s);
     return pre_dispatch<4>(algo, side, P, X, Y, s);
+}
+
+template <int W>
+static int pre2_dispatch(int algo, int side, int64_t P, const MatDesc &X, int64_t h1r, int64_t h1c,
+                         const MatDesc &Y, cudaStream_t s) {
+    const int64_t total = P * Y.rows * Y.cols;
+    if (total == 0) return DDQD_OK;
+    const unsigned g = grid_for(total, ADD2_THREADS);
+    constexpr int TB = ADD2_THREADS;
+    prof_begin(1, s);
+    if (algo == 1 && side == 0) pre_add2_kernel<W, 1, 0><<<g, TB, 0, s>>>(P, X, h1r, h1c, Y);
+    else if (algo == 1) pre_add2_kernel<W, 1, 1><<<g, TB, 0, s>>>(P, X, h1r, h1c, Y);
+    else if (side == 0) pre_add2_kernel<W, 2, 0><<<g, TB, 0, s>>>(P, X, h1r, h1c, Y);
+    else pre_add2_kernel<W, 2, 1><<<g, TB, 0, s>>>(P, X, h1r, h1c, Y);
+    DDQD_LAUNCH_CHECK();
+    prof_end(1, (double)total * W * 8.0 * 65.0, s);   // 16 level-j reads + 49 level-(j+2) writes
+    return DDQD_OK;
+}
+
+int launch_pre_add2(int W, int algo, int side, int64_t P, const MatDesc &X, int64_t h1r,
+                    int64_t h1c, const MatDesc &Y, cudaStream_t s) {
+    if (W == 2) return pre2_dispatch<2>(algo, side, P, X, h1r, h1c, Y, s);
+    set_error("two-level pre-add: DD only");   // QD: 28 live QD values would spill
+    return DDQD_ENOTSUP;
+}
+
+template <int W>
+static int post2_dispatch(int algo, int64_t P, const MatDesc &M, int64_t h1m, int64_t h1n,
+                          const MatDesc &C, int beta, cudaStream_t s) {
+    const int64_t total = P * M.rows * M.cols;
+    if (total == 0) return DDQD_OK;
+    const unsigned g = grid_for(total, ADD2_THREADS);
+    constexpr int TB = ADD2_THREADS;
+    prof_begin(2, s);
+    if (algo == 1) post_add2_kernel<W, 1><<<g, TB, 0, s>>>(P, M, h1m, h1n, C, beta);
+    else post_add2_kernel<W, 2><<<g, TB, 0, s>>>(P, M, h1m, h1n, C, beta);
+    DDQD_LAUNCH_CHECK();
+    prof_end(2, (double)total * W * 8.0 * (beta ? 81.0 : 65.0), s);   // 49 reads + 16 (32) C
+    return DDQD_OK;
+}
+
+int launch_post_add2(int W, int algo, int64_t P, const MatDesc &M, int64_t h1m, int64_t h1n,
+                     const MatDesc &C, int beta, cudaStream_t s) {
+    if (W == 2) return post2_dispatch<2>(algo, P, M, h1m, h1n, C, beta, s);
+    set_error("two-level post-add: DD only");
+    return DDQD_ENOTSUP;
 }
 
 template <int W>

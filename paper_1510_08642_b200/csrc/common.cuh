@@ -58,6 +58,11 @@ int launch_pre_add(int W, int algo, int side, int64_t P, const MatDesc &X, const
                    cudaStream_t s);
 int launch_post_add(int W, int algo, int64_t P, const MatDesc &M, const MatDesc &C, int beta,
                     cudaStream_t s);
+// Two levels at once (j -> j+2; h1r x h1c / h1m x h1n = the skipped level-(j+1) extent).
+int launch_pre_add2(int W, int algo, int side, int64_t P, const MatDesc &X, int64_t h1r,
+                    int64_t h1c, const MatDesc &Y, cudaStream_t s);
+int launch_post_add2(int W, int algo, int64_t P, const MatDesc &M, int64_t h1m, int64_t h1n,
+                     const MatDesc &C, int beta, cudaStream_t s);
 int launch_elementwise(int W, int op, int64_t count, const double *x, const double *y,
                        const double *w, double *z, cudaStream_t s);
 

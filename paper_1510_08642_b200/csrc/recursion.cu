@@ -117,15 +117,42 @@ static MatDesc child(const Plan &p, char *ws, const std::vector<size_t> &off, in
 
 static MatDesc shift(MatDesc d, int64_t p0) { d.p += p0 * d.bs; return d; }
 
+// Two-level fusion (launch_pre_add2 / launch_post_add2) replaces the level j -> j+1 -> j+2
+// additions when level j+1 runs breadth-first over this chunk's 7*pc children (its operands
+// and products are then only ever needed inside the fused passes). Pairs are taken from the
+// leaves upward ((d - j) even), where the skipped level is largest. DD only: the QD kernels
+// would need 4x the registers for the 28 intermediate values, and QD additions are < 4% of
+// a QD step. DDQD_FUSE2=0 disables it.
+static bool fuse2_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("DDQD_FUSE2");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
 static int exec_level(const Plan &p, char *ws, int j, int64_t cnt, const MatDesc &A,
                       const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s) {
     if (j == p.d) return launch_leaf_gemm(p.W, p.m[j], p.l[j], p.n[j], cnt, A, B, C, beta, p.mv, s);
-    const MatDesc cA = child(p, ws, p.offA, j + 1, p.m[j + 1], p.l[j + 1]);
-    const MatDesc cB = child(p, ws, p.offB, j + 1, p.l[j + 1], p.n[j + 1]);
-    const MatDesc cM = child(p, ws, p.offM, j + 1, p.m[j + 1], p.n[j + 1]);
+    const bool two = fuse2_enabled() && p.W == 2 && j + 2 <= p.d && ((p.d - j) % 2 == 0);
     for (int64_t p0 = 0; p0 < cnt; p0 += p.chunk[j]) {
         const int64_t pc = std::min<int64_t>(p.chunk[j], cnt - p0);
         int rc;
+        if (two && p.chunk[j + 1] >= 7 * pc) {
+            const int k = j + 2;
+            const MatDesc gA = child(p, ws, p.offA, k, p.m[k], p.l[k]);
+            const MatDesc gB = child(p, ws, p.offB, k, p.l[k], p.n[k]);
+            const MatDesc gM = child(p, ws, p.offM, k, p.m[k], p.n[k]);
+            if ((rc = launch_pre_add2(p.W, p.algo, 0, pc, shift(A, p0), p.m[j + 1], p.l[j + 1], gA, s))) return rc;
+            if ((rc = launch_pre_add2(p.W, p.algo, 1, pc, shift(B, p0), p.l[j + 1], p.n[j + 1], gB, s))) return rc;
+            if ((rc = exec_level(p, ws, k, 49 * pc, gA, gB, gM, 0, s))) return rc;
+            if ((rc = launch_post_add2(p.W, p.algo, pc, gM, p.m[j + 1], p.n[j + 1], shift(C, p0), beta, s))) return rc;
+            continue;
+        }
+        const MatDesc cA = child(p, ws, p.offA, j + 1, p.m[j + 1], p.l[j + 1]);
+        const MatDesc cB = child(p, ws, p.offB, j + 1, p.l[j + 1], p.n[j + 1]);
+        const MatDesc cM = child(p, ws, p.offM, j + 1, p.m[j + 1], p.n[j + 1]);
         if ((rc = launch_pre_add(p.W, p.algo, 0, pc, shift(A, p0), cA, s))) return rc;
         if ((rc = launch_pre_add(p.W, p.algo, 1, pc, shift(B, p0), cB, s))) return rc;
         if ((rc = exec_level(p, ws, j + 1, 7 * pc, cA, cB, cM, 0, s))) return rc;

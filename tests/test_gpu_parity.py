@@ -208,7 +208,7 @@ def test_host_pointer_path_matches_device(orc):
     assert same(hC.numpy(), orc.gemm(A, B, "winograd", 64))
 
 
-@pytest.mark.parametrize("algo", ["block", "strassen"])
+@pytest.mark.parametrize("algo", ["block", "strassen", "winograd"])
 def test_gemm_ex_strided_beta1(orc, algo):
     """C := C - A B on strided sub-blocks (the LU Schur update form)."""
     N = 200
@@ -473,9 +473,11 @@ def test_launch_count_and_profile():
     ddqd.profile_start()
     ddqd.dd_gemm(A, A, "strassen", 64)
     prof = ddqd.profile_stop()
-    assert ddqd.launch_count() - n0 == 7   # BFS: 2 pre-adds per level x 2 + 1 batched leaf + 2 post-adds
+    # depth 2, breadth-first: the two levels of additions run fused (one pre-add per side,
+    # one post-add) around ONE batched leaf launch of the 49 products
+    assert ddqd.launch_count() - n0 == 4
     assert prof["leaf"][1] == 1 and prof["leaf"][2] == 49 * 64 ** 3
-    assert prof["pre"][1] == 4 and prof["post"][1] == 2
+    assert prof["pre"][1] == 2 and prof["post"][1] == 1
 
 
 @pytest.mark.parametrize("W", [2, 4])
@@ -513,3 +515,35 @@ def test_qd_host_pointer_path(orc):
     B = gen.qd_matrix(77, 85, 61, 1)
     hC = ddqd.qd_gemm(torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory(), "strassen", 16)
     assert same(hC.numpy(), orc.gemm(A, B, "strassen", threshold=16))
+
+
+@pytest.mark.parametrize("algo", ["strassen", "winograd"])
+def test_two_level_fused_additions_same_bits(orc, algo, tmp_path):
+    """The two-level fused pre/post-additions (recursion.cu, DD) against the one-level
+    kernels (DDQD_FUSE2=0 in a fresh process) and the oracle: odd shapes at depth 2..5 so
+    the skipped level and the grandchildren are padded, DFS-chunked and BFS schedules."""
+    import subprocess, sys, textwrap
+    cases = [(37, 29, 33, 4), (65, 66, 67, 16), (101, 45, 77, 10), (515, 517, 513, 32), (9, 130, 11, 2)]
+    outs = {}
+    for fuse in ("1", "0"):
+        code = textwrap.dedent(f"""
+            import numpy as np, torch, sys
+            sys.path.insert(0, {ROOT!r})
+            import ddqd_inputs as gen, paper_1510_08642_b200 as ddqd
+            res = []
+            for (m, l, n, T) in {cases!r}:
+                A = gen.dd_matrix(m, l, 7 * m + T, 0); B = gen.dd_matrix(l, n, 7 * m + T, 1)
+                C = ddqd.dd_gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), {algo!r}, T)
+                res.append(C.cpu().numpy())
+            np.savez(sys.argv[1], *res)
+        """)
+        path = str(tmp_path / f"fuse2_{algo}_{fuse}.npz")
+        env = dict(os.environ, DDQD_FUSE2=fuse)
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=env)
+        z = np.load(path)
+        outs[fuse] = [z["arr_%d" % i] for i in range(len(cases))]
+    for i, (m, l, n, T) in enumerate(cases):
+        A = gen.dd_matrix(m, l, 7 * m + T, 0); B = gen.dd_matrix(l, n, 7 * m + T, 1)
+        ref = orc.gemm(A, B, algo, threshold=T)
+        assert same(outs["1"][i], ref), (m, l, n, T)
+        assert same(outs["0"][i], ref), (m, l, n, T)
