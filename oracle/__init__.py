@@ -97,8 +97,11 @@ def two_prod(a, b):
     return _eft("or_two_prod", a, b)
 
 
-_OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "madd": 4, "madd_fused": 5}
+_OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "madd": 4, "madd_fused": 5,
+        "add_acc": 6, "sub_acc": 7, "madd_acc": 8}
 MADD_FUSED = 0x100
+ADD_ACCURATE = 0x200
+_VARIANT = {"canonical": 0, "fused": MADD_FUSED, "accurate": ADD_ACCURATE}
 
 
 def dd_op(op: str, x, y, w=None):
@@ -135,14 +138,15 @@ def dd_abs_gt(x, y) -> bool:
 # ---- GEMM --------------------------------------------------------------------
 def gemm(A, B, algo="block", threshold=32, bs=0, nthreads=0, madd="canonical"):
     """C := A B for planar [W, m, l] x [W, l, n] arrays (numerics.md s.4); madd='fused'
-    selects the fused DD multiply-add variant (numerics.md s.2)."""
+    selects the fused DD multiply-add variant (numerics.md s.2), madd='accurate' the
+    accurate-add variant (every DD/QD addition accurate, numerics.md s.2-3)."""
     A, B = _f64(A), _f64(B)
     W, m, l = A.shape
     W2, l2, n = B.shape
     if W != W2 or l != l2:
         raise ValueError("dimension mismatch")
     C = np.empty((W, m, n))
-    a = (ALGOS[algo] if isinstance(algo, str) else algo) | (MADD_FUSED if madd == "fused" else 0)
+    a = (ALGOS[algo] if isinstance(algo, str) else algo) | _VARIANT[madd]
     rc = lib().or_gemm(W, a, threshold, bs,
                        m, l, n, _p(A), _p(B), _p(C), nthreads)
     if rc:
@@ -167,7 +171,7 @@ def lu(A, panel=256, algo="strassen", threshold=128, nthreads=0, pivot=True, mad
     LU = _f64(A).copy()
     W, n = LU.shape[0], LU.shape[1]
     ipiv = np.zeros(n, dtype=np.int64)
-    a = ALGOS[algo] | (MADD_FUSED if madd == "fused" else 0)
+    a = ALGOS[algo] | _VARIANT[madd]
     info = lib().or_lu(W, 1 if pivot else 0, n, _p(LU), _pi(ipiv), panel, a, threshold, nthreads)
     if info < 0:
         raise ValueError("or_lu: invalid arguments")

@@ -68,6 +68,22 @@ static dd_t dd_neg(dd_t x) { dd_t r = { -x.hi, -x.lo }; return r; }
 
 static dd_t dd_sub(dd_t x, dd_t y) { return dd_add(x, dd_neg(y)); }
 
+/* numerics.md s.2 accurate ("IEEE-style") add (variant DDQD_ADD_ACCURATE, SURVEY.md
+ * s.8(f) row f3): both word pairs summed error-free, two renormalisations. 20 adds. */
+static dd_t dd_add_acc(dd_t x, dd_t y) {
+    double s1, s2, t1, t2;
+    dd_t r;
+    two_sum(x.hi, y.hi, &s1, &s2);
+    two_sum(x.lo, y.lo, &t1, &t2);
+    s2 = s2 + t1;
+    fast_two_sum(s1, s2, &s1, &s2);
+    s2 = s2 + t2;
+    fast_two_sum(s1, s2, &r.hi, &r.lo);
+    return r;
+}
+
+static dd_t dd_sub_acc(dd_t x, dd_t y) { return dd_add_acc(x, dd_neg(y)); }
+
 static dd_t dd_mul(dd_t x, dd_t y) {
     double p, e, t;
     dd_t r;
@@ -93,9 +109,19 @@ static dd_t dd_madd_fused(dd_t c, dd_t a, dd_t b) {
     return r;
 }
 
-static int g_madd_fused = 0;   /* set per call by or_gemm / or_lu from the algo flag 0x100 */
+/* arithmetic variant of a GEMM / LU call, set per call by or_gemm / or_lu from the algo
+ * flags: 0 canonical, 1 fused DD madd (0x100), 2 accurate adds everywhere (0x200) */
+static int g_variant = 0;
 
-static dd_t dd_madd_v(dd_t c, dd_t a, dd_t b) { return g_madd_fused ? dd_madd_fused(c, a, b) : dd_madd(c, a, b); }
+static dd_t dd_madd_acc(dd_t c, dd_t a, dd_t b) { return dd_add_acc(c, dd_mul(a, b)); }
+
+static dd_t dd_madd_v(dd_t c, dd_t a, dd_t b) {
+    if (g_variant == 1) return dd_madd_fused(c, a, b);
+    if (g_variant == 2) return dd_madd_acc(c, a, b);
+    return dd_madd(c, a, b);
+}
+static dd_t dd_add_v(dd_t x, dd_t y) { return g_variant == 2 ? dd_add_acc(x, y) : dd_add(x, y); }
+static dd_t dd_sub_v(dd_t x, dd_t y) { return g_variant == 2 ? dd_sub_acc(x, y) : dd_sub(x, y); }
 
 static dd_t dd_div(dd_t x, dd_t y) {
     dd_t q1d, r, out;
@@ -221,6 +247,48 @@ static qd_t qd_mul(qd_t a, qd_t b) {
 
 static qd_t qd_madd(qd_t c, qd_t a, qd_t b) { return qd_add(c, qd_mul(a, b)); }
 
+/* numerics.md s.3 ThreeAccum: adds t into the two-word accumulator (u, v); returns the
+ * word that has become complete (or 0 when none has) */
+static double three_accum(double *u, double *v, double t) {
+    double s, e0, e1;
+    two_sum(*v, t, &s, &e1);
+    two_sum(*u, s, &s, &e0);
+    if (e0 != 0.0 && e1 != 0.0) { *u = e0; *v = e1; return s; }
+    if (e1 == 0.0) { *u = s; *v = e0; return 0.0; }
+    *u = s; *v = e1;
+    return 0.0;
+}
+
+/* numerics.md s.3 accurate ("IEEE-style") QD add (variant DDQD_ADD_ACCURATE): the eight
+ * words merged by decreasing magnitude, accumulated word by word, then renormalised. */
+static qd_t qd_add_acc(qd_t a, qd_t b) {
+    double m[8], x[4] = { 0.0, 0.0, 0.0, 0.0 }, u, v;
+    int i = 0, j = 0, k = 0, q;
+    for (q = 0; q < 8; q++) {
+        if (j >= 4 || (i < 4 && fabs(a.w[i]) > fabs(b.w[j]))) m[q] = a.w[i++];
+        else m[q] = b.w[j++];
+    }
+    fast_two_sum(m[0], m[1], &u, &v);
+    q = 2;
+    while (k < 4) {
+        if (q == 8) {
+            x[k] = u;
+            if (k < 3) x[k + 1] = v;
+            break;
+        }
+        double s = three_accum(&u, &v, m[q++]);
+        if (s != 0.0) x[k++] = s;
+    }
+    for (; q < 8; q++) x[3] = x[3] + m[q];
+    return qd_renorm(x[0], x[1], x[2], x[3], 0.0);
+}
+
+static qd_t qd_sub_acc(qd_t a, qd_t b) { return qd_add_acc(a, qd_neg(b)); }
+static qd_t qd_madd_acc(qd_t c, qd_t a, qd_t b) { return qd_add_acc(c, qd_mul(a, b)); }
+static qd_t qd_madd_v(qd_t c, qd_t a, qd_t b) { return g_variant == 2 ? qd_madd_acc(c, a, b) : qd_madd(c, a, b); }
+static qd_t qd_add_v(qd_t x, qd_t y) { return g_variant == 2 ? qd_add_acc(x, y) : qd_add(x, y); }
+static qd_t qd_sub_v(qd_t x, qd_t y) { return g_variant == 2 ? qd_sub_acc(x, y) : qd_sub(x, y); }
+
 /* ------------------------------------------------------------------------- */
 /* Scalar entry points for the pins (arrays, planar [W][n])                   */
 /* ------------------------------------------------------------------------- */
@@ -234,7 +302,8 @@ void or_two_prod(int64_t n, const double *a, const double *b, double *p, double 
     for (int64_t i = 0; i < n; i++) two_prod(a[i], b[i], &p[i], &e[i]);
 }
 
-/* op: 0 add, 1 sub, 2 mul, 3 div (DD only), 4 madd z = x + y*w */
+/* op: 0 add, 1 sub, 2 mul, 3 div (DD only), 4 madd z = x + y*w, 5 fused madd (DD only),
+ * 6 accurate add, 7 accurate sub, 8 accurate madd (z = x + y*w with the accurate add) */
 void or_dd_op(int op, int64_t n, const double *x, const double *y, const double *w, double *z) {
     for (int64_t i = 0; i < n; i++) {
         dd_t a = { x[i], x[n + i] }, b = { y[i], y[n + i] }, r;
@@ -244,6 +313,9 @@ void or_dd_op(int op, int64_t n, const double *x, const double *y, const double 
         case 2: r = dd_mul(a, b); break;
         case 3: r = dd_div(a, b); break;
         case 5: { dd_t c = { w[i], w[n + i] }; r = dd_madd_fused(a, b, c); break; }
+        case 6: r = dd_add_acc(a, b); break;
+        case 7: r = dd_sub_acc(a, b); break;
+        case 8: { dd_t c = { w[i], w[n + i] }; r = dd_madd_acc(a, b, c); break; }
         default: { dd_t c = { w[i], w[n + i] }; r = dd_madd(a, b, c); }
         }
         z[i] = r.hi; z[n + i] = r.lo;
@@ -258,10 +330,12 @@ void or_qd_op(int op, int64_t n, const double *x, const double *y, const double 
         case 0: r = qd_add(a, b); break;
         case 1: r = qd_sub(a, b); break;
         case 2: r = qd_mul(a, b); break;
+        case 6: r = qd_add_acc(a, b); break;
+        case 7: r = qd_sub_acc(a, b); break;
         default: {
             qd_t c;
             for (int k = 0; k < 4; k++) c.w[k] = w[k * n + i];
-            r = qd_madd(a, b, c);
+            r = op == 8 ? qd_madd_acc(a, b, c) : qd_madd(a, b, c);
         }
         }
         for (int k = 0; k < 4; k++) z[k * n + i] = r.w[k];
@@ -328,12 +402,12 @@ static mat_t mat_addsub(const mat_t *x, const mat_t *y, int sub) {
             if (x->W == 2) {
                 dd_t a = { get_w(x, 0, i, j), get_w(x, 1, i, j) };
                 dd_t b = { get_w(y, 0, i, j), get_w(y, 1, i, j) };
-                dd_t r = sub ? dd_sub(a, b) : dd_add(a, b);
+                dd_t r = sub ? dd_sub_v(a, b) : dd_add_v(a, b);
                 set_w(&z, 0, i, j, r.hi); set_w(&z, 1, i, j, r.lo);
             } else {
                 qd_t a, b, r;
                 for (int w = 0; w < 4; w++) { a.w[w] = get_w(x, w, i, j); b.w[w] = get_w(y, w, i, j); }
-                r = sub ? qd_sub(a, b) : qd_add(a, b);
+                r = sub ? qd_sub_v(a, b) : qd_add_v(a, b);
                 for (int w = 0; w < 4; w++) set_w(&z, w, i, j, r.w[w]);
             }
         }
@@ -367,7 +441,7 @@ static void gemm_simple(const mat_t *A, const mat_t *B, mat_t *C) {
                 for (int64_t j = 0; j < n; j++) {
                     qd_t b, c;
                     for (int w = 0; w < 4; w++) { c.w[w] = acc[w * n + j]; b.w[w] = get_w(B, w, k, j); }
-                    c = qd_madd(c, a, b);
+                    c = qd_madd_v(c, a, b);
                     for (int w = 0; w < 4; w++) acc[w * n + j] = c.w[w];
                 }
             }
@@ -405,7 +479,7 @@ static void gemm_block(const mat_t *A, const mat_t *B, mat_t *C, int64_t bs) {
                                 for (int w = 0; w < 4; w++) {
                                     a.w[w] = get_w(A, w, i, k); b.w[w] = get_w(B, w, k, j); c.w[w] = get_w(C, w, i, j);
                                 }
-                                c = qd_madd(c, a, b);
+                                c = qd_madd_v(c, a, b);
                                 for (int w = 0; w < 4; w++) set_w(C, w, i, j, c.w[w]);
                             }
                         }
@@ -499,10 +573,11 @@ static void gemm_any(int algo, int64_t T, const mat_t *A, const mat_t *B, mat_t 
  * bs > 0 selects the explicitly tiled Block(bs) loop nest (for the Block == Simple pin). */
 int or_gemm(int W, int algo, int64_t T, int64_t bs, int64_t m, int64_t l, int64_t n,
             const double *A, const double *B, double *C, int nthreads) {
-    g_madd_fused = (algo & 0x100) ? 1 : 0;
+    if ((algo & 0x100) && (algo & 0x200)) return -1;
+    g_variant = (algo & 0x100) ? 1 : (algo & 0x200) ? 2 : 0;
     algo &= 0xff;
     if ((W != 2 && W != 4) || algo < 0 || algo > 2 || m < 0 || l < 0 || n < 0) return -1;
-    if (g_madd_fused && W != 2) return -1;
+    if (g_variant == 1 && W != 2) return -1;
     if (algo != 0 && T < 1) return -1;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -586,9 +661,12 @@ static void st_sc(int W, double *A, int64_t n, int64_t i, int64_t j, sc_t v) {
 int or_lu(int W, int pivot, int64_t n, double *A, int64_t *ipiv, int64_t K, int algo, int64_t T,
           int nthreads) {
     int info = 0;
-    g_madd_fused = (algo & 0x100) ? 1 : 0;
+    /* the accurate-add variant is a GEMM variant; the LU's own panel, TRSM and solve
+     * arithmetic is the canonical one, so an accurate LU is not defined (rejected) */
+    if (algo & 0x200) return -1;
+    g_variant = (algo & 0x100) ? 1 : 0;
     algo &= 0xff;
-    if ((W != 2 && W != 4) || n < 0 || K < 1 || (g_madd_fused && W != 2)) return -1;
+    if ((W != 2 && W != 4) || n < 0 || K < 1 || (g_variant == 1 && W != 2)) return -1;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
 #endif

@@ -266,3 +266,47 @@ def test_fused_madd_gemm_vs_exact(orc, algo):
     Ai = _int_mat(2, 17, 9, rng)
     Bi = _int_mat(2, 9, 13, rng)
     assert np.array_equal(orc.gemm(Ai, Bi, algo, 2, madd="fused")[0], Ai[0] @ Bi[0])
+
+
+@pytest.mark.parametrize("W", [2, 4])
+@pytest.mark.parametrize("algo", ALGOS)
+def test_accurate_add_gemm_vs_exact(orc, W, algo):
+    """Accurate-add variant (row f3; every addition of the madd and of the Strassen/Winograd
+    combinations is the accurate add): within 18^d 2^-96 l |A||B| (QD: 2^-200) of the exact
+    product; Block == Simple bitwise; threshold >= dims is Block; integer inputs exact; it
+    changes bits relative to the canonical arithmetic."""
+    cases = [(13, 11, 15, 3), (16, 16, 16, 2), (7, 9, 5, 1)]
+    base = 96 if W == 2 else 200
+    for (m, l, n, T) in cases:
+        A = gen.matrix(W, m, l, m + 9, 0)
+        B = gen.matrix(W, l, n, m + 9, 1)
+        C = orc.gemm(A, B, algo, threshold=T, madd="accurate")
+        E = exact_product(A, B)
+        d = 0 if algo == "block" else rec_depth(m, l, n, T)
+        nA = max(abs(frac(A[:, i, k])) for i in range(m) for k in range(l))
+        nB = max(abs(frac(B[:, k, j])) for k in range(l) for j in range(n))
+        bound = Fraction(18) ** d * Fraction(1, 2 ** base) * l * nA * nB
+        for i in range(m):
+            for j in range(n):
+                assert abs(frac(C[:, i, j]) - E[i][j]) <= bound
+    A = gen.matrix(W, 40, 40, 5, 0)
+    assert not np.array_equal(orc.gemm(A, A, algo, 8, madd="accurate"), orc.gemm(A, A, algo, 8))
+    if algo == "block":
+        for bs in (1, 3, 16):
+            assert np.array_equal(orc.gemm(A, A, "block", bs=bs, madd="accurate"), orc.gemm(A, A, "block", madd="accurate"))
+    else:
+        assert np.array_equal(orc.gemm(A, A, algo, 40, madd="accurate"), orc.gemm(A, A, "block", madd="accurate"))
+    rng = np.random.default_rng(4)
+    Ai = _int_mat(W, 17, 9, rng)
+    Bi = _int_mat(W, 9, 13, rng)
+    assert np.array_equal(orc.gemm(Ai, Bi, algo, 2, madd="accurate")[0], Ai[0] @ Bi[0])
+
+
+def test_accurate_variant_rejections(orc):
+    """The accurate-add variant is a GEMM variant: the LU (whose panel/TRSM/solve arithmetic
+    is canonical) rejects it; fused + accurate together are rejected."""
+    A = gen.dd_matrix(8, 8, 1, 0)
+    with pytest.raises(ValueError):
+        orc.lu(A, panel=4, madd="accurate")
+    with pytest.raises(ValueError):
+        orc.gemm(A, A, orc.BLOCK | orc.MADD_FUSED | orc.ADD_ACCURATE)
