@@ -49,6 +49,15 @@ enum { DDQD_BLOCK = 0, DDQD_STRASSEN = 1, DDQD_WINOGRAD = 2 };
  * variant, not to the canonical one. QD with this flag returns DDQD_ENOTSUP. */
 enum { DDQD_MADD_FUSED = 0x100 };
 
+/* Flag OR-ed into `algo` (DD and QD): every addition of the GEMM -- the multiply-add's and
+ * every Strassen/Winograd pre/post addition -- is the accurate ("IEEE-style") add of
+ * docs/numerics.md s.2-3 (DD 20 FP64 instructions instead of 11; QD the merge-and-accumulate
+ * addition), which meets a relative error bound even when leading words cancel (SPEC's
+ * add contract S:74). Bit-identical to the oracle's accurate
+ * variant. Combined with DDQD_MADD_FUSED -> DDQD_EINVAL; the LU entry points return
+ * DDQD_ENOTSUP (their panel/TRSM/solve arithmetic is the canonical one). */
+enum { DDQD_ADD_ACCURATE = 0x200 };
+
 /* Precisions: number of float64 words per element. */
 enum { DDQD_DD = 2, DDQD_QD = 4 };
 
@@ -106,6 +115,7 @@ int ddqd_gemm_ex(const ddqd_gemm_desc *desc);
  *                  order of docs/numerics.md s.4; missing quadrant rows/cols read as zero.
  *   ddqd_post_add: 7P products M -> P parents C (cropped to C's rows x cols); beta = 1
  *                  subtracts from C instead of storing.
+ * algo = DDQD_STRASSEN or DDQD_WINOGRAD, optionally | DDQD_ADD_ACCURATE (accurate adds).
  * Device pointers only; asynchronous on the thread's stream. */
 typedef struct {
     double *p;
@@ -144,7 +154,8 @@ int ddqd_lu_solve(int prec, int pivot, int64_t n, double *A, const double *b, do
 
 /* Elementwise arithmetic layer, for parity tests of the device DD/QD ops (device
  * pointers, planar [W][count]): op 0 add, 1 sub, 2 mul, 3 div, 4 madd z = x + y*w,
- * 5 fused madd (DD only, DDQD_MADD_FUSED's operation). */
+ * 5 fused madd (DD only, DDQD_MADD_FUSED's operation), 6 accurate add, 7 accurate sub,
+ * 8 accurate madd z = x + y*w (DDQD_ADD_ACCURATE's operations, DD and QD). */
 int ddqd_elementwise(int prec, int op, int64_t count, const double *x, const double *y,
                      const double *w, double *z);
 

@@ -23,6 +23,8 @@ _SO = os.path.join(_HERE, "libddqd.so")
 
 BLOCK, STRASSEN, WINOGRAD = 0, 1, 2
 MADD_FUSED = 0x100   # DDQD_MADD_FUSED: fused DD multiply-add in the leaf (docs/numerics.md s.2)
+ADD_ACCURATE = 0x200   # DDQD_ADD_ACCURATE: every GEMM addition accurate (docs/numerics.md s.2-3)
+_VARIANTS = {"canonical": 0, "fused": MADD_FUSED, "accurate": ADD_ACCURATE}
 _ALGOS = {"block": BLOCK, "strassen": STRASSEN, "winograd": WINOGRAD}
 _CODES = {-1: "EINVAL", -2: "EALIAS", -3: "ENOMEM", -4: "ECUDA", -5: "ENOTSUP"}
 
@@ -106,11 +108,12 @@ def _set_stream(t):
 
 
 def _algo(a, madd="canonical") -> int:
-    """'block' | 'strassen' | 'winograd' (or the int); madd='fused' ORs in DDQD_MADD_FUSED."""
+    """'block' | 'strassen' | 'winograd' (or the int); madd='fused' ORs in DDQD_MADD_FUSED,
+    madd='accurate' DDQD_ADD_ACCURATE."""
     v = _ALGOS[a] if isinstance(a, str) else int(a)
-    if madd not in ("canonical", "fused"):
-        raise ValueError("madd must be 'canonical' or 'fused'")
-    return v | (MADD_FUSED if madd == "fused" else 0)
+    if madd not in _VARIANTS:
+        raise ValueError("madd must be 'canonical', 'fused' or 'accurate'")
+    return v | _VARIANTS[madd]
 
 
 def _check_mat(x, W, name):
@@ -176,22 +179,27 @@ def batch_mat(t):
     return Mat(t.data_ptr(), r, c, c, r * c, W * r * c)
 
 
-def pre_add(algo, side, X, Y):
+def _add_algo(algo, madd):
+    # the additions follow the accurate variant; the fused variant only changes the leaf madd
+    return _algo(algo) | (ADD_ACCURATE if madd == "accurate" else 0)
+
+
+def pre_add(algo, side, X, Y, madd="canonical"):
     """One level's fused pre-additions: X [P,W,r,c] -> Y [7P,W,ceil(r/2),ceil(c/2)]."""
     P = 1 if X.dim() == 3 else X.shape[0]
     W = X.shape[-3]
     _set_stream(X)
     x, y = batch_mat(X), batch_mat(Y)
-    _check(lib.ddqd_pre_add(W, _algo(algo), side, P, ctypes.byref(x), ctypes.byref(y)), "pre_add")
+    _check(lib.ddqd_pre_add(W, _add_algo(algo, madd), side, P, ctypes.byref(x), ctypes.byref(y)), "pre_add")
 
 
-def post_add(algo, M, C, beta=0):
+def post_add(algo, M, C, beta=0, madd="canonical"):
     """One level's fused post-additions: M [7P,W,h,h'] -> C [P,W,r,c]."""
     P = 1 if C.dim() == 3 else C.shape[0]
     W = C.shape[-3]
     _set_stream(C)
     mm, cc = batch_mat(M), batch_mat(C)
-    _check(lib.ddqd_post_add(W, _algo(algo), P, ctypes.byref(mm), ctypes.byref(cc), beta), "post_add")
+    _check(lib.ddqd_post_add(W, _add_algo(algo, madd), P, ctypes.byref(mm), ctypes.byref(cc), beta), "post_add")
 
 
 def gemm_batched(A, B, C, algo, threshold, beta=0, madd="canonical"):
@@ -241,7 +249,8 @@ def qd_lu_solve(A, b, panel=256, algo="strassen", threshold=128, overwrite=False
     return lu_solve(A, b, panel, algo, threshold, True, overwrite)
 
 
-_OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "madd": 4, "madd_fused": 5}
+_OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "madd": 4, "madd_fused": 5,
+        "add_acc": 6, "sub_acc": 7, "madd_acc": 8}
 
 
 def elementwise(op, x, y, w=None):

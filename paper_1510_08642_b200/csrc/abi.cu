@@ -140,7 +140,11 @@ static int where(const void *p) {
 
 static int check_gemm_args(int64_t m, int64_t l, int64_t n, int algo, int64_t T) {
     if (m < 0 || l < 0 || n < 0) { set_error("negative dimension"); return DDQD_EINVAL; }
-    if (algo & ~(0xff | DDQD_MADD_FUSED)) { set_error("unknown algo flag"); return DDQD_EINVAL; }
+    if (algo & ~(0xff | DDQD_MADD_FUSED | DDQD_ADD_ACCURATE)) { set_error("unknown algo flag"); return DDQD_EINVAL; }
+    if ((algo & DDQD_MADD_FUSED) && (algo & DDQD_ADD_ACCURATE)) {
+        set_error("DDQD_MADD_FUSED and DDQD_ADD_ACCURATE are exclusive");
+        return DDQD_EINVAL;
+    }
     algo &= 0xff;
     if (algo < 0 || algo > 2) { set_error("algo must be DDQD_BLOCK, DDQD_STRASSEN or DDQD_WINOGRAD"); return DDQD_EINVAL; }
     if (algo != 0 && T < 1) { set_error("threshold must be >= 1"); return DDQD_EINVAL; }
@@ -228,6 +232,7 @@ int ddqd_lu_solve(int prec, int pivot, int64_t n, double *A, const double *b, do
     int rc = check_gemm_args(n, panel, n, algo, threshold);
     if (rc) return rc;
     if ((algo & DDQD_MADD_FUSED) && prec != 2) { set_error("the fused madd variant is DD only"); return DDQD_ENOTSUP; }
+    if (algo & DDQD_ADD_ACCURATE) { set_error("the accurate-add variant is a GEMM variant (LU: canonical)"); return DDQD_ENOTSUP; }
     if (n == 0) return DDQD_OK;
     if (!A || !b || !x || !ipiv) { set_error("null pointer"); return DDQD_EINVAL; }
     if (where(A) || where(b) || where(x) || where(ipiv)) { set_error("LU takes device pointers only"); return DDQD_ENOTSUP; }
@@ -251,7 +256,8 @@ static MatDesc to_desc(const ddqd_mat *x) { return MatDesc{x->p, x->rows, x->col
 
 int ddqd_pre_add(int prec, int algo, int side, int64_t P, const ddqd_mat *X, const ddqd_mat *Y) {
     t_err.clear();
-    if ((prec != 2 && prec != 4) || (algo != 1 && algo != 2) || (side != 0 && side != 1) || P < 0 || !X || !Y) {
+    const int a = algo & ~DDQD_ADD_ACCURATE;   // the accurate-add variant may be OR-ed in
+    if ((prec != 2 && prec != 4) || (a != 1 && a != 2) || (side != 0 && side != 1) || P < 0 || !X || !Y) {
         set_error("bad pre_add arguments");
         return DDQD_EINVAL;
     }
@@ -264,7 +270,8 @@ int ddqd_pre_add(int prec, int algo, int side, int64_t P, const ddqd_mat *X, con
 
 int ddqd_post_add(int prec, int algo, int64_t P, const ddqd_mat *M, const ddqd_mat *C, int beta) {
     t_err.clear();
-    if ((prec != 2 && prec != 4) || (algo != 1 && algo != 2) || P < 0 || !M || !C || (beta != 0 && beta != 1)) {
+    const int a = algo & ~DDQD_ADD_ACCURATE;
+    if ((prec != 2 && prec != 4) || (a != 1 && a != 2) || P < 0 || !M || !C || (beta != 0 && beta != 1)) {
         set_error("bad post_add arguments");
         return DDQD_EINVAL;
     }
@@ -278,7 +285,7 @@ int ddqd_post_add(int prec, int algo, int64_t P, const ddqd_mat *M, const ddqd_m
 int ddqd_elementwise(int prec, int op, int64_t count, const double *x, const double *y, const double *w,
                      double *z) {
     t_err.clear();
-    if ((prec != 2 && prec != 4) || op < 0 || op > 5 || (op == 5 && prec != 2) || count < 0) {
+    if ((prec != 2 && prec != 4) || op < 0 || op > 8 || (op == 5 && prec != 2) || count < 0) {
         set_error("bad elementwise arguments");
         return DDQD_EINVAL;
     }

@@ -23,11 +23,10 @@ __device__ __forceinline__ typename elem<W>::T ld_or_zero(const double *base, in
 
 // One level of pre-additions on the four quadrant values of a position: the 7 operands of
 // side 0 (A) or 1 (B); algo 1 = Strassen, 2 = Winograd (numerics.md s.4, S:239 / S:248).
-template <int W, int ALGO, int SIDE>
-__device__ __forceinline__ void pre_ops(const typename elem<W>::T &x11, const typename elem<W>::T &x12,
-                                        const typename elem<W>::T &x21, const typename elem<W>::T &x22,
-                                        typename elem<W>::T o[7]) {
-    using E = elem<W>;
+template <class E, int ALGO, int SIDE>
+__device__ __forceinline__ void pre_ops(const typename E::T &x11, const typename E::T &x12,
+                                        const typename E::T &x21, const typename E::T &x22,
+                                        typename E::T o[7]) {
     using T = typename E::T;
     if constexpr (ALGO == 1 && SIDE == 0) {        // Strassen, A side
         o[0] = E::add(x11, x22);                    // P1: A11+A22
@@ -61,11 +60,10 @@ __device__ __forceinline__ void pre_ops(const typename elem<W>::T &x11, const ty
 }
 
 // One level of post-additions: 7 products -> the 4 quadrant values of a position.
-template <int W, int ALGO>
-__device__ __forceinline__ void post_ops(const typename elem<W>::T p[7], typename elem<W>::T &c11,
-                                         typename elem<W>::T &c12, typename elem<W>::T &c21,
-                                         typename elem<W>::T &c22) {
-    using E = elem<W>;
+template <class E, int ALGO>
+__device__ __forceinline__ void post_ops(const typename E::T p[7], typename E::T &c11,
+                                         typename E::T &c12, typename E::T &c21,
+                                         typename E::T &c22) {
     using T = typename E::T;
     if constexpr (ALGO == 1) {
         c11 = E::add(E::sub(E::add(p[0], p[3]), p[4]), p[6]);   // ((P1+P4)-P5)+P7
@@ -84,9 +82,9 @@ __device__ __forceinline__ void post_ops(const typename elem<W>::T p[7], typenam
 }
 
 // side 0 = A operands, side 1 = B operands; algo 1 = Strassen, 2 = Winograd
-template <int W, int ALGO, int SIDE>
+template <int W, int ALGO, int SIDE, int V>
 __global__ void __launch_bounds__(256) pre_add_kernel(int64_t P, MatDesc X, MatDesc Y) {
-    using E = elem<W>;
+    using E = arith<W, V>;
     using T = typename E::T;
     const int64_t hr = Y.rows, hc = Y.cols;
     const int64_t per = hr * hc;
@@ -101,7 +99,7 @@ __global__ void __launch_bounds__(256) pre_add_kernel(int64_t P, MatDesc X, MatD
         const T x21 = ld_or_zero<W>(xb + (i + hr) * X.ld + j, X.ps, r2);
         const T x22 = ld_or_zero<W>(xb + (i + hr) * X.ld + (j + hc), X.ps, r2 && c2);
         T o[7];
-        pre_ops<W, ALGO, SIDE>(x11, x12, x21, x22, o);
+        pre_ops<E, ALGO, SIDE>(x11, x12, x21, x22, o);
 #pragma unroll
         for (int c = 0; c < 7; c++) E::store(Y.p + (7 * b + c) * Y.bs + i * Y.ld + j, Y.ps, o[c]);
     }
@@ -125,10 +123,10 @@ __global__ void __launch_bounds__(256) pre_add_kernel(int64_t P, MatDesc X, MatD
 // the level-(j+1) padding, as the one-level kernel's zero-filled loads would read them --
 // and then the 7 grandchildren of each. Same operations in the same order as two launches
 // of pre_add_kernel, so bit-identical; the level-(j+1) operands never touch HBM.
-template <int W, int ALGO, int SIDE>
+template <int W, int ALGO, int SIDE, int V>
 __global__ void __launch_bounds__(ADD2_THREADS, ADD2_MINB) pre_add2_kernel(int64_t P, MatDesc X, int64_t h1r,
                                                        int64_t h1c, MatDesc Y) {
-    using E = elem<W>;
+    using E = arith<W, V>;
     using T = typename E::T;
     const int64_t hr = Y.rows, hc = Y.cols;
     const int64_t per = hr * hc;
@@ -147,7 +145,7 @@ __global__ void __launch_bounds__(ADD2_THREADS, ADD2_MINB) pre_add2_kernel(int64
                 const T x12 = ld_or_zero<W>(xb + r * X.ld + (c + h1c), X.ps, c2);
                 const T x21 = ld_or_zero<W>(xb + (r + h1r) * X.ld + c, X.ps, r2);
                 const T x22 = ld_or_zero<W>(xb + (r + h1r) * X.ld + (c + h1c), X.ps, r2 && c2);
-                pre_ops<W, ALGO, SIDE>(x11, x12, x21, x22, y[sp]);
+                pre_ops<E, ALGO, SIDE>(x11, x12, x21, x22, y[sp]);
             } else {
 #pragma unroll
                 for (int k = 0; k < 7; k++) y[sp][k] = E::zero();
@@ -156,7 +154,7 @@ __global__ void __launch_bounds__(ADD2_THREADS, ADD2_MINB) pre_add2_kernel(int64
 #pragma unroll
         for (int c1 = 0; c1 < 7; c1++) {
             T o[7];
-            pre_ops<W, ALGO, SIDE>(y[0][c1], y[1][c1], y[2][c1], y[3][c1], o);
+            pre_ops<E, ALGO, SIDE>(y[0][c1], y[1][c1], y[2][c1], y[3][c1], o);
 #pragma unroll
             for (int c2 = 0; c2 < 7; c2++)
                 E::store(Y.p + (49 * b + 7 * c1 + c2) * Y.bs + i * Y.ld + j, Y.ps, o[c2]);
@@ -164,9 +162,9 @@ __global__ void __launch_bounds__(ADD2_THREADS, ADD2_MINB) pre_add2_kernel(int64
     }
 }
 
-template <int W, int ALGO>
+template <int W, int ALGO, int V>
 __global__ void __launch_bounds__(256) post_add_kernel(int64_t P, MatDesc M, MatDesc C, int beta) {
-    using E = elem<W>;
+    using E = arith<W, V>;
     using T = typename E::T;
     const int64_t hm = M.rows, hn = M.cols;
     const int64_t per = hm * hn;
@@ -178,7 +176,7 @@ __global__ void __launch_bounds__(256) post_add_kernel(int64_t P, MatDesc M, Mat
 #pragma unroll
         for (int c = 0; c < 7; c++) p[c] = E::load(M.p + (7 * b + c) * M.bs + i * M.ld + j, M.ps);
         T c11, c12, c21, c22;
-        post_ops<W, ALGO>(p, c11, c12, c21, c22);
+        post_ops<E, ALGO>(p, c11, c12, c21, c22);
         double *cb = C.p + b * C.bs;
         const bool r2 = i + hm < C.rows, cc2 = j + hn < C.cols;
         auto put = [&](int64_t r, int64_t c, const T &v) {
@@ -200,10 +198,10 @@ __global__ void __launch_bounds__(256) post_add_kernel(int64_t P, MatDesc M, Mat
 // inside the level-(j+1) extent h1m x h1n (the one-level kernel crops the rest away), the
 // 7 children into C's 4 quadrants. Bit-identical to two launches of post_add_kernel; the
 // level-(j+1) products never touch HBM.
-template <int W, int ALGO>
+template <int W, int ALGO, int V>
 __global__ void __launch_bounds__(ADD2_THREADS, ADD2_MINB) post_add2_kernel(int64_t P, MatDesc M, int64_t h1m,
                                                         int64_t h1n, MatDesc C, int beta) {
-    using E = elem<W>;
+    using E = arith<W, V>;
     using T = typename E::T;
     const int64_t hm = M.rows, hn = M.cols;
     const int64_t per = hm * hn;
@@ -218,7 +216,7 @@ __global__ void __launch_bounds__(ADD2_THREADS, ADD2_MINB) post_add2_kernel(int6
 #pragma unroll
             for (int c2 = 0; c2 < 7; c2++)
                 p[c2] = E::load(M.p + (49 * b + 7 * c1 + c2) * M.bs + i * M.ld + j, M.ps);
-            post_ops<W, ALGO>(p, y[0][c1], y[1][c1], y[2][c1], y[3][c1]);
+            post_ops<E, ALGO>(p, y[0][c1], y[1][c1], y[2][c1], y[3][c1]);
         }
         double *cb = C.p + b * C.bs;
         auto put = [&](int64_t r, int64_t c, const T &v) {
@@ -231,7 +229,7 @@ __global__ void __launch_bounds__(ADD2_THREADS, ADD2_MINB) post_add2_kernel(int6
             const int64_t r = i + (sp >> 1) * hm, c = j + (sp & 1) * hn;
             if (r < h1m && c < h1n) {
                 T c11, c12, c21, c22;
-                post_ops<W, ALGO>(y[sp], c11, c12, c21, c22);
+                post_ops<E, ALGO>(y[sp], c11, c12, c21, c22);
                 const bool r2 = r + h1m < C.rows, cc2 = c + h1n < C.cols;
                 if (r < C.rows && c < C.cols) put(r, c, c11);
                 if (r < C.rows && cc2) put(r, c + h1n, c12);
@@ -250,16 +248,18 @@ static unsigned grid_for(int64_t total, int threads = 256) {
     return (unsigned)blocks;
 }
 
-template <int W>
+// Dispatch. `algo` is 1 (Strassen) or 2 (Winograd), optionally | DDQD_ADD_ACCURATE (every
+// addition the accurate one, numerics.md s.2-3).
+template <int W, int V>
 static int pre_dispatch(int algo, int side, int64_t P, const MatDesc &X, const MatDesc &Y, cudaStream_t s) {
     const int64_t total = P * Y.rows * Y.cols;
     if (total == 0) return DDQD_OK;
     const unsigned g = grid_for(total);
     prof_begin(1, s);
-    if (algo == 1 && side == 0) pre_add_kernel<W, 1, 0><<<g, 256, 0, s>>>(P, X, Y);
-    else if (algo == 1) pre_add_kernel<W, 1, 1><<<g, 256, 0, s>>>(P, X, Y);
-    else if (side == 0) pre_add_kernel<W, 2, 0><<<g, 256, 0, s>>>(P, X, Y);
-    else pre_add_kernel<W, 2, 1><<<g, 256, 0, s>>>(P, X, Y);
+    if (algo == 1 && side == 0) pre_add_kernel<W, 1, 0, V><<<g, 256, 0, s>>>(P, X, Y);
+    else if (algo == 1) pre_add_kernel<W, 1, 1, V><<<g, 256, 0, s>>>(P, X, Y);
+    else if (side == 0) pre_add_kernel<W, 2, 0, V><<<g, 256, 0, s>>>(P, X, Y);
+    else pre_add_kernel<W, 2, 1, V><<<g, 256, 0, s>>>(P, X, Y);
     DDQD_LAUNCH_CHECK();
     prof_end(1, (double)total * W * 8.0 * 11.0, s);   // 4 quadrant reads + 7 operand writes
     return DDQD_OK;
@@ -267,11 +267,13 @@ static int pre_dispatch(int algo, int side, int64_t P, const MatDesc &X, const M
 
 int launch_pre_add(int W, int algo, int side, int64_t P, const MatDesc &X, const MatDesc &Y,
                    cudaStream_t s) {
-    if (W == 2) return pre_dispatch<2>(algo, side, P, X, Y, s);
-    return pre_dispatch<4>(algo, side, P, X, Y, s);
+    const bool acc = (algo & DDQD_ADD_ACCURATE) != 0;
+    algo &= 0xff;
+    if (W == 2) return acc ? pre_dispatch<2, 2>(algo, side, P, X, Y, s) : pre_dispatch<2, 0>(algo, side, P, X, Y, s);
+    return acc ? pre_dispatch<4, 2>(algo, side, P, X, Y, s) : pre_dispatch<4, 0>(algo, side, P, X, Y, s);
 }
 
-template <int W>
+template <int W, int V>
 static int pre2_dispatch(int algo, int side, int64_t P, const MatDesc &X, int64_t h1r, int64_t h1c,
                          const MatDesc &Y, cudaStream_t s) {
     const int64_t total = P * Y.rows * Y.cols;
@@ -279,10 +281,10 @@ static int pre2_dispatch(int algo, int side, int64_t P, const MatDesc &X, int64_
     const unsigned g = grid_for(total, ADD2_THREADS);
     constexpr int TB = ADD2_THREADS;
     prof_begin(1, s);
-    if (algo == 1 && side == 0) pre_add2_kernel<W, 1, 0><<<g, TB, 0, s>>>(P, X, h1r, h1c, Y);
-    else if (algo == 1) pre_add2_kernel<W, 1, 1><<<g, TB, 0, s>>>(P, X, h1r, h1c, Y);
-    else if (side == 0) pre_add2_kernel<W, 2, 0><<<g, TB, 0, s>>>(P, X, h1r, h1c, Y);
-    else pre_add2_kernel<W, 2, 1><<<g, TB, 0, s>>>(P, X, h1r, h1c, Y);
+    if (algo == 1 && side == 0) pre_add2_kernel<W, 1, 0, V><<<g, TB, 0, s>>>(P, X, h1r, h1c, Y);
+    else if (algo == 1) pre_add2_kernel<W, 1, 1, V><<<g, TB, 0, s>>>(P, X, h1r, h1c, Y);
+    else if (side == 0) pre_add2_kernel<W, 2, 0, V><<<g, TB, 0, s>>>(P, X, h1r, h1c, Y);
+    else pre_add2_kernel<W, 2, 1, V><<<g, TB, 0, s>>>(P, X, h1r, h1c, Y);
     DDQD_LAUNCH_CHECK();
     prof_end(1, (double)total * W * 8.0 * 65.0, s);   // 16 level-j reads + 49 level-(j+2) writes
     return DDQD_OK;
@@ -290,12 +292,15 @@ static int pre2_dispatch(int algo, int side, int64_t P, const MatDesc &X, int64_
 
 int launch_pre_add2(int W, int algo, int side, int64_t P, const MatDesc &X, int64_t h1r,
                     int64_t h1c, const MatDesc &Y, cudaStream_t s) {
-    if (W == 2) return pre2_dispatch<2>(algo, side, P, X, h1r, h1c, Y, s);
-    set_error("two-level pre-add: DD only");   // QD: 28 live QD values would spill
+    const bool acc = (algo & DDQD_ADD_ACCURATE) != 0;
+    algo &= 0xff;
+    if (W == 2 && !acc) return pre2_dispatch<2, 0>(algo, side, P, X, h1r, h1c, Y, s);
+    // QD: 28 live QD values would spill; the accurate variant keeps the one-level kernels
+    set_error("two-level pre-add: canonical DD only");
     return DDQD_ENOTSUP;
 }
 
-template <int W>
+template <int W, int V>
 static int post2_dispatch(int algo, int64_t P, const MatDesc &M, int64_t h1m, int64_t h1n,
                           const MatDesc &C, int beta, cudaStream_t s) {
     const int64_t total = P * M.rows * M.cols;
@@ -303,8 +308,8 @@ static int post2_dispatch(int algo, int64_t P, const MatDesc &M, int64_t h1m, in
     const unsigned g = grid_for(total, ADD2_THREADS);
     constexpr int TB = ADD2_THREADS;
     prof_begin(2, s);
-    if (algo == 1) post_add2_kernel<W, 1><<<g, TB, 0, s>>>(P, M, h1m, h1n, C, beta);
-    else post_add2_kernel<W, 2><<<g, TB, 0, s>>>(P, M, h1m, h1n, C, beta);
+    if (algo == 1) post_add2_kernel<W, 1, V><<<g, TB, 0, s>>>(P, M, h1m, h1n, C, beta);
+    else post_add2_kernel<W, 2, V><<<g, TB, 0, s>>>(P, M, h1m, h1n, C, beta);
     DDQD_LAUNCH_CHECK();
     prof_end(2, (double)total * W * 8.0 * (beta ? 81.0 : 65.0), s);   // 49 reads + 16 (32) C
     return DDQD_OK;
@@ -312,19 +317,21 @@ static int post2_dispatch(int algo, int64_t P, const MatDesc &M, int64_t h1m, in
 
 int launch_post_add2(int W, int algo, int64_t P, const MatDesc &M, int64_t h1m, int64_t h1n,
                      const MatDesc &C, int beta, cudaStream_t s) {
-    if (W == 2) return post2_dispatch<2>(algo, P, M, h1m, h1n, C, beta, s);
-    set_error("two-level post-add: DD only");
+    const bool acc = (algo & DDQD_ADD_ACCURATE) != 0;
+    algo &= 0xff;
+    if (W == 2 && !acc) return post2_dispatch<2, 0>(algo, P, M, h1m, h1n, C, beta, s);
+    set_error("two-level post-add: canonical DD only");
     return DDQD_ENOTSUP;
 }
 
-template <int W>
+template <int W, int V>
 static int post_dispatch(int algo, int64_t P, const MatDesc &M, const MatDesc &C, int beta, cudaStream_t s) {
     const int64_t total = P * M.rows * M.cols;
     if (total == 0) return DDQD_OK;
     const unsigned g = grid_for(total);
     prof_begin(2, s);
-    if (algo == 1) post_add_kernel<W, 1><<<g, 256, 0, s>>>(P, M, C, beta);
-    else post_add_kernel<W, 2><<<g, 256, 0, s>>>(P, M, C, beta);
+    if (algo == 1) post_add_kernel<W, 1, V><<<g, 256, 0, s>>>(P, M, C, beta);
+    else post_add_kernel<W, 2, V><<<g, 256, 0, s>>>(P, M, C, beta);
     DDQD_LAUNCH_CHECK();
     prof_end(2, (double)total * W * 8.0 * (beta ? 15.0 : 11.0), s);   // 7 product reads + 4 (8) C
     return DDQD_OK;
@@ -332,8 +339,10 @@ static int post_dispatch(int algo, int64_t P, const MatDesc &M, const MatDesc &C
 
 int launch_post_add(int W, int algo, int64_t P, const MatDesc &M, const MatDesc &C, int beta,
                     cudaStream_t s) {
-    if (W == 2) return post_dispatch<2>(algo, P, M, C, beta, s);
-    return post_dispatch<4>(algo, P, M, C, beta, s);
+    const bool acc = (algo & DDQD_ADD_ACCURATE) != 0;
+    algo &= 0xff;
+    if (W == 2) return acc ? post_dispatch<2, 2>(algo, P, M, C, beta, s) : post_dispatch<2, 0>(algo, P, M, C, beta, s);
+    return acc ? post_dispatch<4, 2>(algo, P, M, C, beta, s) : post_dispatch<4, 0>(algo, P, M, C, beta, s);
 }
 
 // ---- elementwise arithmetic layer (parity tests of ddqd_arith.cuh) ---------------------
@@ -350,6 +359,9 @@ __global__ void elementwise_kernel(int op, int64_t count, const double *x, const
         else if (op == 1) r = E::sub(a, b);
         else if (op == 4) r = E::madd(a, b, E::load(w + i, count));
         else if (op == 5) r = E::madd_fused(a, b, E::load(w + i, count));
+        else if (op == 6) r = E::add_acc(a, b);
+        else if (op == 7) r = E::sub_acc(a, b);
+        else if (op == 8) r = E::madd_acc(a, b, E::load(w + i, count));
         else if constexpr (W == 2) {
             r = (op == 2) ? dd_mul(a, b) : dd_div(a, b);
         } else {

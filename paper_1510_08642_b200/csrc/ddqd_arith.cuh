@@ -65,6 +65,21 @@ __device__ __forceinline__ dd dd_madd_fused(dd c, dd a, dd b) {
     fast_two_sum(s, t, r.hi, r.lo);
     return r;
 }
+// Accurate ("IEEE-style") add (numerics.md s.2, variant DDQD_ADD_ACCURATE, SURVEY.md s.8(f)
+// row f3): both word pairs error-free, two renormalisations; 20 DADD.
+__device__ __forceinline__ dd dd_add_acc(dd x, dd y) {
+    double s1, s2, t1, t2;
+    two_sum(x.hi, y.hi, s1, s2);
+    two_sum(x.lo, y.lo, t1, t2);
+    s2 = __dadd_rn(s2, t1);
+    fast_two_sum(s1, s2, s1, s2);
+    s2 = __dadd_rn(s2, t2);
+    dd r;
+    fast_two_sum(s1, s2, r.hi, r.lo);
+    return r;
+}
+__device__ __forceinline__ dd dd_sub_acc(dd x, dd y) { return dd_add_acc(x, dd_neg(y)); }
+__device__ __forceinline__ dd dd_madd_acc(dd c, dd a, dd b) { return dd_add_acc(c, dd_mul(a, b)); }
 __device__ __forceinline__ dd dd_div(dd x, dd y) {
     double q1 = __ddiv_rn(x.hi, y.hi);
     dd r = dd_sub(x, dd_mul(y, dd{q1, 0.0}));
@@ -191,6 +206,73 @@ __device__ __forceinline__ qd qd_madd(const qd &c, const qd &a, const qd &b) {
     return qd_add(c, qd_mul(a, b));
 }
 
+// |x| > |y| for finite doubles on the integer pipe (sign bit cleared, unsigned compare)
+__device__ __forceinline__ bool abs_gt_bits(double x, double y) {
+    unsigned long long ux, uy;
+    asm("mov.b64 %0, %1;" : "=l"(ux) : "d"(x));
+    asm("mov.b64 %0, %1;" : "=l"(uy) : "d"(y));
+    return (ux << 1) > (uy << 1);
+}
+__device__ __forceinline__ double word_at(const qd &a, int i) {   // 0 past the last word
+    return i == 0 ? a.w[0] : i == 1 ? a.w[1] : i == 2 ? a.w[2] : i == 3 ? a.w[3] : 0.0;
+}
+// ThreeAccum (numerics.md s.3): t into the two-word accumulator (u, v); returns the completed
+// word, or 0 when none completed
+__device__ __forceinline__ double three_accum(double &u, double &v, double t) {
+    double s, e0, e1;
+    two_sum(v, t, s, e1);
+    two_sum(u, s, s, e0);
+    if (nz(e0) && nz(e1)) { u = e0; v = e1; return s; }
+    if (!nz(e1)) { u = s; v = e0; return 0.0; }
+    u = s; v = e1;
+    return 0.0;
+}
+// Accurate QD add (numerics.md s.3, variant DDQD_ADD_ACCURATE): the eight words merged by
+// decreasing magnitude, accumulated with ThreeAccum, leftovers folded into the last word,
+// renormalised. Written branch-light with static register indices (fully unrolled).
+__device__ __forceinline__ qd qd_add_acc(const qd &a, const qd &b) {
+    double m[8];
+    int i = 0, j = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        const double ai = word_at(a, i), bj = word_at(b, j);
+        const bool ta = j >= 4 || (i < 4 && abs_gt_bits(ai, bj));
+        m[q] = ta ? ai : bj;
+        i += ta ? 1 : 0;
+        j += ta ? 0 : 1;
+    }
+    double u, v;
+    fast_two_sum(m[0], m[1], u, v);
+    double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
+    int k = 0, qend = 8;
+#pragma unroll
+    for (int q = 2; q < 8; q++) {
+        if (k < 4) {
+            const double s = three_accum(u, v, m[q]);
+            if (nz(s)) {
+                if (k == 0) x0 = s; else if (k == 1) x1 = s; else if (k == 2) x2 = s; else x3 = s;
+                k++;
+                if (k == 4) qend = q + 1;
+            }
+        }
+    }
+    if (k < 4) {
+        if (k == 0) { x0 = u; x1 = v; }
+        else if (k == 1) { x1 = u; x2 = v; }
+        else if (k == 2) { x2 = u; x3 = v; }
+        else x3 = u;
+    } else {
+#pragma unroll
+        for (int q = 2; q < 8; q++)
+            if (q >= qend) x3 = __dadd_rn(x3, m[q]);
+    }
+    return qd_renorm(x0, x1, x2, x3, 0.0);
+}
+__device__ __forceinline__ qd qd_sub_acc(const qd &a, const qd &b) { return qd_add_acc(a, qd_neg(b)); }
+__device__ __forceinline__ qd qd_madd_acc(const qd &c, const qd &a, const qd &b) {
+    return qd_add_acc(c, qd_mul(a, b));
+}
+
 // qd_div (numerics.md s.3): long division with three correction steps, then renorm.
 __device__ __forceinline__ qd qd_div(const qd &a, const qd &b) {
     qd r = a, t;
@@ -223,6 +305,9 @@ template <> struct elem<2> {
     static __device__ __forceinline__ T sub(T x, T y) { return dd_sub(x, y); }
     static __device__ __forceinline__ T madd(T c, T a, T b) { return dd_madd(c, a, b); }
     static __device__ __forceinline__ T madd_fused(T c, T a, T b) { return dd_madd_fused(c, a, b); }
+    static __device__ __forceinline__ T add_acc(T x, T y) { return dd_add_acc(x, y); }
+    static __device__ __forceinline__ T sub_acc(T x, T y) { return dd_sub_acc(x, y); }
+    static __device__ __forceinline__ T madd_acc(T c, T a, T b) { return dd_madd_acc(c, a, b); }
     static __device__ __forceinline__ T load(const double *p, int64_t ps) { return dd{p[0], p[ps]}; }
     static __device__ __forceinline__ void store(double *p, int64_t ps, T v) { p[0] = v.hi; p[ps] = v.lo; }
     static __device__ __forceinline__ double word(const T &v, int w) { return w == 0 ? v.hi : v.lo; }
@@ -239,6 +324,9 @@ template <> struct elem<4> {
     static __device__ __forceinline__ T sub(const T &x, const T &y) { return qd_sub(x, y); }
     static __device__ __forceinline__ T madd(const T &c, const T &a, const T &b) { return qd_madd(c, a, b); }
     static __device__ __forceinline__ T madd_fused(const T &c, const T &a, const T &b) { return qd_madd(c, a, b); }
+    static __device__ __forceinline__ T add_acc(const T &x, const T &y) { return qd_add_acc(x, y); }
+    static __device__ __forceinline__ T sub_acc(const T &x, const T &y) { return qd_sub_acc(x, y); }
+    static __device__ __forceinline__ T madd_acc(const T &c, const T &a, const T &b) { return qd_madd_acc(c, a, b); }
     static __device__ __forceinline__ T load(const double *p, int64_t ps) {
         qd r; r.w[0] = p[0]; r.w[1] = p[ps]; r.w[2] = p[2 * ps]; r.w[3] = p[3 * ps]; return r;
     }
@@ -251,6 +339,19 @@ template <> struct elem<4> {
     static __device__ __forceinline__ T mul(const T &x, const T &y) { return qd_mul(x, y); }
     static __device__ __forceinline__ T div(const T &x, const T &y) { return qd_div(x, y); }
     static __device__ __forceinline__ bool abs_gt(const T &x, const T &y) { return qd_abs_gt(x, y); }
+};
+
+// Arithmetic variant of a GEMM (the algo flags): V = 0 canonical, 1 fused DD madd
+// (DDQD_MADD_FUSED), 2 accurate adds everywhere (DDQD_ADD_ACCURATE). Kernels take
+// E = arith<W, V> and call E::add / E::sub / E::madd.
+template <int W, int V> struct arith : elem<W> {
+    using B = elem<W>;
+    using T = typename B::T;
+    static __device__ __forceinline__ T add(const T &x, const T &y) { return V == 2 ? B::add_acc(x, y) : B::add(x, y); }
+    static __device__ __forceinline__ T sub(const T &x, const T &y) { return V == 2 ? B::sub_acc(x, y) : B::sub(x, y); }
+    static __device__ __forceinline__ T madd(const T &c, const T &a, const T &b) {
+        return V == 1 ? B::madd_fused(c, a, b) : V == 2 ? B::madd_acc(c, a, b) : B::madd(c, a, b);
+    }
 };
 
 }  // namespace ddqd

@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(LeafCfg<W, BM, BN, BK, TM, TN, STAGES>::NT, MI
 leaf_gemm_kernel(int64_t m, int64_t l, int64_t n, MatDesc A, MatDesc B, MatDesc C, int beta,
                  int64_t batch0) {
     using Cfg = LeafCfg<W, BM, BN, BK, TM, TN, STAGES>;
-    using E = elem<W>;
+    using E = arith<W, MV>;   // MV: 0 canonical, 1 fused DD madd, 2 accurate adds
     using T = typename E::T;
     constexpr int NT = Cfg::NT;
     extern __shared__ __align__(16) double smem[];
@@ -150,7 +150,7 @@ leaf_gemm_kernel(int64_t m, int64_t l, int64_t n, MatDesc A, MatDesc B, MatDesc 
 #pragma unroll
                         for (int w = 0; w < W; w++) bb.w[w] = bv[w][j];
                     }
-                    acc[i][j] = MV ? E::madd_fused(acc[i][j], a, bb) : E::madd(acc[i][j], a, bb);
+                    acc[i][j] = E::madd(acc[i][j], a, bb);
                 }
             }
         }
@@ -232,19 +232,26 @@ static bool tma_enabled() {
 int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
                      const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s) {
     if (m == 0 || n == 0 || batch == 0) return DDQD_OK;
-    if (W == 2 && tma_enabled() && leaf_cfg_override() < 0) {
+    if (W == 2 && mv != 2 && tma_enabled() && leaf_cfg_override() < 0) {
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
         if (big_tiles >= 2 * 148 && m > 32 && n > 32) {
             int rc = DDQD_OK;
             if (try_leaf_tma(m, l, n, batch, A, B, C, beta, mv, s, &rc)) return rc;
         }
     }
-    if (mv) {   // fused DD madd (numerics.md s.2, row f3)
+    if (mv == 1) {   // fused DD madd (numerics.md s.2, row f3)
         if (W != 2) { set_error("the fused madd variant is DD only"); return DDQD_ENOTSUP; }
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
         if (big_tiles >= 2 * 148 && m > 32 && n > 32)
             return launch_cfg<2, 64, 64, 8, 4, 4, 4, 2, 1>(m, l, n, batch, A, B, C, beta, s);
         return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2, 1>(m, l, n, batch, A, B, C, beta, s);
+    }
+    if (mv == 2) {   // accurate adds (numerics.md s.2-3, row f3)
+        if (W == 4) return launch_cfg<4, 32, 32, 16, 2, 2, 3, 2, 2>(m, l, n, batch, A, B, C, beta, s);
+        const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
+        if (big_tiles >= 2 * 148 && m > 32 && n > 32)
+            return launch_cfg<2, 64, 64, 8, 4, 4, 4, 2, 2>(m, l, n, batch, A, B, C, beta, s);
+        return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2, 2>(m, l, n, batch, A, B, C, beta, s);
     }
     switch (leaf_cfg_override()) {
     case 0: return launch_cfg<2, 64, 64, 16, 4, 4, 3, 2>(m, l, n, batch, A, B, C, beta, s);

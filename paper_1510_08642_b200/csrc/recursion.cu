@@ -135,7 +135,8 @@ static bool fuse2_enabled() {
 static int exec_level(const Plan &p, char *ws, int j, int64_t cnt, const MatDesc &A,
                       const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s) {
     if (j == p.d) return launch_leaf_gemm(p.W, p.m[j], p.l[j], p.n[j], cnt, A, B, C, beta, p.mv, s);
-    const bool two = fuse2_enabled() && p.W == 2 && j + 2 <= p.d && ((p.d - j) % 2 == 0);
+    const bool two = fuse2_enabled() && p.W == 2 && p.mv != 2 && j + 2 <= p.d && ((p.d - j) % 2 == 0);
+    const int add_algo = p.algo | (p.mv == 2 ? DDQD_ADD_ACCURATE : 0);   // the additions' variant
     for (int64_t p0 = 0; p0 < cnt; p0 += p.chunk[j]) {
         const int64_t pc = std::min<int64_t>(p.chunk[j], cnt - p0);
         int rc;
@@ -153,10 +154,10 @@ static int exec_level(const Plan &p, char *ws, int j, int64_t cnt, const MatDesc
         const MatDesc cA = child(p, ws, p.offA, j + 1, p.m[j + 1], p.l[j + 1]);
         const MatDesc cB = child(p, ws, p.offB, j + 1, p.l[j + 1], p.n[j + 1]);
         const MatDesc cM = child(p, ws, p.offM, j + 1, p.m[j + 1], p.n[j + 1]);
-        if ((rc = launch_pre_add(p.W, p.algo, 0, pc, shift(A, p0), cA, s))) return rc;
-        if ((rc = launch_pre_add(p.W, p.algo, 1, pc, shift(B, p0), cB, s))) return rc;
+        if ((rc = launch_pre_add(p.W, add_algo, 0, pc, shift(A, p0), cA, s))) return rc;
+        if ((rc = launch_pre_add(p.W, add_algo, 1, pc, shift(B, p0), cB, s))) return rc;
         if ((rc = exec_level(p, ws, j + 1, 7 * pc, cA, cB, cM, 0, s))) return rc;
-        if ((rc = launch_post_add(p.W, p.algo, pc, cM, shift(C, p0), beta, s))) return rc;
+        if ((rc = launch_post_add(p.W, add_algo, pc, cM, shift(C, p0), beta, s))) return rc;
     }
     return DDQD_OK;
 }
@@ -164,7 +165,7 @@ static int exec_level(const Plan &p, char *ws, int j, int64_t cnt, const MatDesc
 int run_gemm(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n, int64_t batch,
              const MatDesc &A, const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s) {
     if (m == 0 || n == 0 || batch == 0) return DDQD_OK;
-    const int mv = (algo & DDQD_MADD_FUSED) ? 1 : 0;
+    const int mv = (algo & DDQD_MADD_FUSED) ? 1 : (algo & DDQD_ADD_ACCURATE) ? 2 : 0;
     algo &= 0xff;
     Plan p;
     int rc = make_plan(p, W, algo, T, m, l, n, batch, workspace_limit());

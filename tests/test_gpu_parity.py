@@ -547,3 +547,57 @@ def test_two_level_fused_additions_same_bits(orc, algo, tmp_path):
         ref = orc.gemm(A, B, algo, threshold=T)
         assert same(outs["1"][i], ref), (m, l, n, T)
         assert same(outs["0"][i], ref), (m, l, n, T)
+
+
+# ---- accurate-add variant (row f3, DDQD_ADD_ACCURATE) ----------------------------------------
+def _qd_samples(orc, n, seed, cancel=True):
+    rng = np.random.default_rng(seed)
+    raw = [rng.uniform(-1, 1, n) * np.exp2(rng.integers(-20, 20, n))]
+    for _ in range(3):
+        raw.append(raw[-1] * 2.0 ** -53 * rng.uniform(-1, 1, n))
+    raw.append(np.zeros(n))
+    return orc.qd_renorm(np.stack(raw))
+
+
+def test_accurate_add_elementwise_bitwise(orc):
+    """Device accurate DD/QD add, sub and madd (numerics.md s.2-3) vs the oracle, bitwise,
+    including exact and leading-word cancellation (the merge / ThreeAccum branches)."""
+    x, y, w = _dd_samples(100000, 41), _dd_samples(100000, 42), _dd_samples(100000, 43)
+    y[:, :20000] = -x[:, :20000]
+    y[1, 10000:20000] = _dd_samples(10000, 44)[1]
+    y[:, 10000:20000] = orc.dd_op("add", y[:, 10000:20000], np.zeros((2, 10000)))
+    for op in ("add_acc", "sub_acc", "madd_acc"):
+        got = np_(ddqd.elementwise(op, cu(x), cu(y), cu(w)))
+        assert same(got, orc.dd_op(op, x, y, w)), op
+    qx, qy, qw = (_qd_samples(orc, 40000, s) for s in (45, 46, 47))
+    qy[:, :8000] = -qx[:, :8000]
+    qy[1:, 4000:8000] = _qd_samples(orc, 4000, 48)[1:]
+    qy[:, 4000:8000] = orc.qd_renorm(np.vstack([qy[:, 4000:8000], np.zeros((1, 4000))]))
+    qy[:, 8000:9000] = 0.0
+    for op in ("add_acc", "sub_acc", "madd_acc"):
+        got = np_(ddqd.elementwise(op, cu(qx), cu(qy), cu(qw)))
+        assert same(got, orc.qd_op(op, qx, qy, qw)), op
+
+
+@pytest.mark.parametrize("W", [2, 4])
+@pytest.mark.parametrize("algo", ["block", "strassen", "winograd"])
+def test_accurate_add_gemm_bitwise(orc, W, algo):
+    """GEMM with every addition accurate: bit-exact vs the oracle's accurate variant on odd
+    shapes at several depths (DD up to 1024^3 at depth 3)."""
+    cases = [(37, 29, 33, 4), (65, 66, 67, 16), (301, 257, 299, 64)]
+    if W == 2:
+        cases.append((1024, 1024, 1024, 128))
+    for (m, l, n, T) in cases:
+        A = gen.matrix(W, m, l, 51 + m, 0)
+        B = gen.matrix(W, l, n, 51 + m, 1)
+        got = np_(ddqd.gemm(cu(A), cu(B), algo, T, madd="accurate"))
+        assert same(got, orc.gemm(A, B, algo, threshold=T, madd="accurate")), (m, l, n, T)
+
+
+def test_accurate_add_rejections():
+    A = cu(gen.dd_matrix(16, 16, 1, 0))
+    b = torch.zeros(2, 16, dtype=torch.float64, device=DEV)
+    with pytest.raises(ddqd.DDQDError):
+        ddqd.lu_solve(A.clone(), b, panel=8, algo="strassen", threshold=4, madd="accurate")
+    with pytest.raises(ValueError):   # DDQD_EINVAL: the two variants are exclusive
+        ddqd.gemm(A, A, ddqd.MADD_FUSED | ddqd.ADD_ACCURATE | 1, 4)
