@@ -152,6 +152,21 @@ int qd_lu_solve(int64_t n, double *A, const double *b, double *x, int64_t *ipiv,
 int ddqd_lu_solve(int prec, int pivot, int64_t n, double *A, const double *b, double *x,
                   int64_t *ipiv, int64_t panel, int algo, int64_t threshold);
 
+/* The LU's steps as separate calls, for a caller that runs the Schur update itself (the
+ * multi-GPU LU of paper_1510_08642_b200/mgpu.py distributes it).
+ *   ddqd_lu_panel: steps 1-2 of docs/numerics.md s.5 for the panel of columns [p, p+kb) of the
+ *     planar row-major [prec][n][n] matrix A (rows p..n-1): pivot search (pivot = 1) or the
+ *     pivot-free rule (pivot = 0), interchanges over all n columns (ipiv[k] for k in the panel),
+ *     reciprocal and scaling, the panel's rank-1 updates, then U12 := L11^{-1} A12 by forward
+ *     substitution. The caller then forms A22 := A22 - L21 U12 (e.g. ddqd_gemm_ex with beta = 1).
+ *     Returns 0, k+1 for the first exactly zero pivot in this panel (LAPACK-style, the rest of
+ *     that column's step skipped), or a negative DDQD_E* code. Synchronises.
+ *   ddqd_lu_trsv: the solve of Eq. (2) with the factors (y := P b, unit-lower forward,
+ *     upper backward with dd_div / qd_div); b, x: [prec][n]; b untouched. Asynchronous.
+ * Device pointers only; 0 <= p, 1 <= kb, p + kb <= n (kb <= 1024 when p + kb < n). */
+int ddqd_lu_panel(int prec, int pivot, int64_t n, double *A, int64_t *ipiv, int64_t p, int64_t kb);
+int ddqd_lu_trsv(int prec, int64_t n, const double *LU, const int64_t *ipiv, const double *b, double *x);
+
 /* Elementwise arithmetic layer, for parity tests of the device DD/QD ops (device
  * pointers, planar [W][count]): op 0 add, 1 sub, 2 mul, 3 div, 4 madd z = x + y*w,
  * 5 fused madd (DD only, DDQD_MADD_FUSED's operation), 6 accurate add, 7 accurate sub,

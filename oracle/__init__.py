@@ -54,6 +54,7 @@ def lib():
         L.or_gemm.argtypes = [ctypes.c_int, ctypes.c_int, i64, i64, i64, i64, i64, P, P, P, ctypes.c_int]
         L.or_lu.argtypes = [ctypes.c_int, ctypes.c_int, i64, P, PI, i64, ctypes.c_int, i64, ctypes.c_int]
         L.or_lu_solve.argtypes = [ctypes.c_int, i64, P, PI, P, P]
+        L.or_lu_panel.argtypes = [ctypes.c_int, ctypes.c_int, i64, P, PI, i64, i64]
         L.or_qd_div.argtypes = [i64, P, P, P]
         L.or_counter_madds.restype = i64
         L.or_counter_block_adds.restype = i64
@@ -176,6 +177,13 @@ def lu(A, panel=256, algo="strassen", threshold=128, nthreads=0, pivot=True, mad
     if info < 0:
         raise ValueError("or_lu: invalid arguments")
     return LU, ipiv, info
+
+
+def lu_panel(A, ipiv, p, kb, pivot=True):
+    """Steps 1-2 of numerics.md s.5 for the panel of columns [p, p+kb), in place on the
+    contiguous [W,n,n] array A and int64 ipiv[n]. Returns this panel's info (0 or k+1)."""
+    assert A.dtype == np.float64 and A.flags.c_contiguous and ipiv.dtype == np.int64
+    return lib().or_lu_panel(A.shape[0], 1 if pivot else 0, A.shape[1], _p(A), _pi(ipiv), p, kb)
 
 
 def lu_solve(LU, ipiv, b):

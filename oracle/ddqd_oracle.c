@@ -653,6 +653,50 @@ static void st_sc(int W, double *A, int64_t n, int64_t i, int64_t j, sc_t v) {
 }
 
 /* ------------------------------------------------------------------------- */
+/* Steps 1-2 for the panel of columns [p, p+kb) (numerics.md s.5): column-by-column
+ * factorisation with full-row interchanges, then U12 by forward substitution. Returns the
+ * first k+1 whose pivot is exactly zero within this panel, else 0. */
+int or_lu_panel(int W, int pivot, int64_t n, double *A, int64_t *ipiv, int64_t p, int64_t kb) {
+    int info = 0;
+    for (int64_t k = p; k < p + kb; k++) {
+        int64_t r = k;
+        if (pivot) {
+            sc_t best = ld_sc(W, A, n, k, k);
+            for (int64_t i = k + 1; i < n; i++) {
+                sc_t v = ld_sc(W, A, n, i, k);
+                if (sc_abs_gt(W, v, best)) { best = v; r = i; }
+            }
+        }
+        ipiv[k] = r;
+        if (r != k)
+            for (int64_t j = 0; j < n; j++) {
+                sc_t t = ld_sc(W, A, n, k, j);
+                st_sc(W, A, n, k, j, ld_sc(W, A, n, r, j));
+                st_sc(W, A, n, r, j, t);
+            }
+        sc_t piv = ld_sc(W, A, n, k, k);
+        if (piv.w[0] == 0.0) { if (!info) info = (int)(k + 1); continue; }
+        sc_t rinv = sc_div(W, sc_one(), piv);
+#pragma omp parallel for schedule(static)
+        for (int64_t i = k + 1; i < n; i++) {
+            sc_t lik = sc_mul(W, ld_sc(W, A, n, i, k), rinv);
+            st_sc(W, A, n, i, k, lik);
+            for (int64_t j = k + 1; j < p + kb; j++)
+                st_sc(W, A, n, i, j, sc_sub(W, ld_sc(W, A, n, i, j), sc_mul(W, lik, ld_sc(W, A, n, k, j))));
+        }
+    }
+    /* step 2: U12 := L11^{-1} A12 (unit lower, forward substitution in row order) */
+    for (int64_t i = p; i < p + kb; i++)
+#pragma omp parallel for schedule(static)
+        for (int64_t r = i + 1; r < p + kb; r++) {
+            sc_t lri = ld_sc(W, A, n, r, i);
+            for (int64_t j = p + kb; j < n; j++)
+                st_sc(W, A, n, r, j, sc_sub(W, ld_sc(W, A, n, r, j), sc_mul(W, lri, ld_sc(W, A, n, i, j))));
+        }
+    return info;
+}
+
+/* ------------------------------------------------------------------------- */
 /* numerics.md s.5: blocked right-looking LU (P:121-133 steps 1-3); partial  */
 /* pivoting per BJ:11 (pivot = 1) or the paper's pivot-free LU (pivot = 0,   */
 /* P:121). A is n x n planar [W][n][n], overwritten by L\U; ipiv[k] = pivot  */
@@ -672,44 +716,11 @@ int or_lu(int W, int pivot, int64_t n, double *A, int64_t *ipiv, int64_t K, int 
 #endif
     for (int64_t p = 0; p < n; p += K) {
         int64_t kb = (n - p < K) ? n - p : K;
-        /* step 1: panel factorisation, column by column */
-        for (int64_t k = p; k < p + kb; k++) {
-            int64_t r = k;
-            if (pivot) {
-                sc_t best = ld_sc(W, A, n, k, k);
-                for (int64_t i = k + 1; i < n; i++) {
-                    sc_t v = ld_sc(W, A, n, i, k);
-                    if (sc_abs_gt(W, v, best)) { best = v; r = i; }
-                }
-            }
-            ipiv[k] = r;
-            if (r != k)
-                for (int64_t j = 0; j < n; j++) {
-                    sc_t t = ld_sc(W, A, n, k, j);
-                    st_sc(W, A, n, k, j, ld_sc(W, A, n, r, j));
-                    st_sc(W, A, n, r, j, t);
-                }
-            sc_t piv = ld_sc(W, A, n, k, k);
-            if (piv.w[0] == 0.0) { if (!info) info = (int)(k + 1); continue; }
-            sc_t rinv = sc_div(W, sc_one(), piv);
-#pragma omp parallel for schedule(static)
-            for (int64_t i = k + 1; i < n; i++) {
-                sc_t lik = sc_mul(W, ld_sc(W, A, n, i, k), rinv);
-                st_sc(W, A, n, i, k, lik);
-                for (int64_t j = k + 1; j < p + kb; j++)
-                    st_sc(W, A, n, i, j, sc_sub(W, ld_sc(W, A, n, i, j), sc_mul(W, lik, ld_sc(W, A, n, k, j))));
-            }
-        }
+        /* steps 1-2 */
+        int pinfo = or_lu_panel(W, pivot, n, A, ipiv, p, kb);
+        if (!info) info = pinfo;
         int64_t n2 = n - p - kb;
         if (n2 <= 0) continue;
-        /* step 2: U12 := L11^{-1} A12 (unit lower, forward substitution in row order) */
-        for (int64_t i = p; i < p + kb; i++)
-#pragma omp parallel for schedule(static)
-            for (int64_t r = i + 1; r < p + kb; r++) {
-                sc_t lri = ld_sc(W, A, n, r, i);
-                for (int64_t j = p + kb; j < n; j++)
-                    st_sc(W, A, n, r, j, sc_sub(W, ld_sc(W, A, n, r, j), sc_mul(W, lri, ld_sc(W, A, n, i, j))));
-            }
         /* step 3: A22 := A22 - L21 U12, T := gemm(L21, U12) first (the underlined term) */
         mat_t L21 = mat_alloc(W, n2, kb), U12 = mat_alloc(W, kb, n2), Tm = mat_alloc(W, n2, n2);
         for (int w = 0; w < W; w++) {

@@ -63,6 +63,8 @@ def _load():
     L.qd_lu_solve.argtypes = [i64, vp, vp, vp, vp, i64, i32, i64]
     L.ddqd_lu_solve.argtypes = [i32, i32, i64, vp, vp, vp, vp, i64, i32, i64]
     L.ddqd_elementwise.argtypes = [i32, i32, i64, vp, vp, vp, vp]
+    L.ddqd_lu_panel.argtypes = [i32, i32, i64, vp, vp, i64, i64]
+    L.ddqd_lu_trsv.argtypes = [i32, i64, vp, vp, vp, vp]
     L.ddqd_set_stream.argtypes = [vp]
     L.ddqd_workspace_bytes.argtypes = [i32, i64, i64, i64, i32, i64]
     L.ddqd_workspace_bytes.restype = ctypes.c_size_t
@@ -79,7 +81,8 @@ def _load():
 
 lib = _load()
 
-EXPORTED = ["dd_gemm", "qd_gemm", "ddqd_gemm_ex", "dd_lu_solve", "qd_lu_solve", "ddqd_lu_solve", "ddqd_elementwise", "ddqd_set_stream",
+EXPORTED = ["dd_gemm", "qd_gemm", "ddqd_gemm_ex", "dd_lu_solve", "qd_lu_solve", "ddqd_lu_solve",
+            "ddqd_lu_panel", "ddqd_lu_trsv", "ddqd_elementwise", "ddqd_set_stream",
             "ddqd_workspace_bytes", "ddqd_set_workspace", "ddqd_set_workspace_limit",
             "ddqd_launch_count", "ddqd_release", "ddqd_last_error", "ddqd_version",
             "ddqd_profile_start", "ddqd_profile_stop", "ddqd_fp64_peak", "ddqd_pre_add", "ddqd_post_add"]
@@ -171,12 +174,14 @@ def gemm_ex(prec, algo, threshold, m, l, n, batch, A, lda, psA, bsA, B, ldb, psB
 
 
 def batch_mat(t):
-    """Mat descriptor of a contiguous [batch, W, rows, cols] (or [W, rows, cols]) CUDA tensor."""
-    if t.dim() == 3:
-        W, r, c = t.shape
-        return Mat(t.data_ptr(), r, c, c, r * c, W * r * c)
-    B, W, r, c = t.shape
-    return Mat(t.data_ptr(), r, c, c, r * c, W * r * c)
+    """Mat descriptor of a [batch, W, rows, cols] (or [W, rows, cols]) CUDA tensor whose rows are
+    unit-stride (strided views such as the LU's trailing block are allowed)."""
+    if t.stride(-1) != 1:
+        raise ValueError("rows must be unit-stride")
+    r, c = t.shape[-2], t.shape[-1]
+    ld, ps = t.stride(-2), t.stride(-3)
+    bs = t.stride(0) if t.dim() == 4 else ps * t.shape[0]
+    return Mat(t.data_ptr(), r, c, ld, ps, bs)
 
 
 def _add_algo(algo, madd):
@@ -233,6 +238,24 @@ def lu_solve(A, b, panel=256, algo="strassen", threshold=128, pivot=True, overwr
     info = _check(lib.ddqd_lu_solve(W, 1 if pivot else 0, n, LU.data_ptr(), b.data_ptr(), x.data_ptr(),
                                     ipiv.data_ptr(), panel, _algo(algo, madd), threshold), "lu_solve")
     return x, LU, ipiv, info
+
+
+def lu_panel(LU, ipiv, p, kb, pivot=True):
+    """Steps 1-2 of the LU for the panel [p, p+kb) of the [W,n,n] CUDA tensor LU, in place
+    (ddqd_lu_panel); ipiv: int64 [n] CUDA tensor. Returns this panel's info (0 or k+1)."""
+    W, n = LU.shape[0], LU.shape[1]
+    _set_stream(LU)
+    return _check(lib.ddqd_lu_panel(W, 1 if pivot else 0, n, LU.data_ptr(), ipiv.data_ptr(), p, kb), "lu_panel")
+
+
+def lu_trsv(LU, ipiv, b):
+    """x with LU x = P b from the factors (ddqd_lu_trsv); returns x [W,n]."""
+    torch = _torch()
+    x = torch.empty_like(b)
+    _set_stream(LU)
+    _check(lib.ddqd_lu_trsv(LU.shape[0], LU.shape[1], LU.data_ptr(), ipiv.data_ptr(), b.data_ptr(),
+                            x.data_ptr()), "lu_trsv")
+    return x
 
 
 def dd_lu_solve(A, b, panel=256, algo="strassen", threshold=128, overwrite=False):

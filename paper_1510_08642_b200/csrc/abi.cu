@@ -118,6 +118,10 @@ size_t workspace_limit() {
     return g_limit;
 }
 
+int lu_panel_impl(int W, int pivot, int64_t n, double *A, int64_t *ipiv, int64_t p, int64_t kb, cudaStream_t s,
+                  int *info_out);
+int lu_trsv_impl(int W, int64_t n, const double *A, const int64_t *ipiv, const double *b, double *x,
+                 cudaStream_t s);
 int lu_solve_impl(int W, int pivot, int64_t n, double *A, const double *b, double *x, int64_t *ipiv,
                   int64_t K, int algo, int64_t T, cudaStream_t s, int *info_out);
 
@@ -240,6 +244,29 @@ int ddqd_lu_solve(int prec, int pivot, int64_t n, double *A, const double *b, do
     rc = lu_solve_impl(prec, pivot, n, A, b, x, ipiv, panel, algo, threshold, t_stream, &info);
     if (rc) return rc;
     return info;
+}
+
+int ddqd_lu_panel(int prec, int pivot, int64_t n, double *A, int64_t *ipiv, int64_t p, int64_t kb) {
+    t_err.clear();
+    if (prec != 2 && prec != 4) { set_error("prec must be DDQD_DD or DDQD_QD"); return DDQD_EINVAL; }
+    if (pivot != 0 && pivot != 1) { set_error("pivot must be 0 or 1"); return DDQD_EINVAL; }
+    if (n < 0 || p < 0 || kb < 1 || p + kb > n) { set_error("need 0 <= p, 1 <= kb, p + kb <= n"); return DDQD_EINVAL; }
+    if (!A || !ipiv) { set_error("null pointer"); return DDQD_EINVAL; }
+    if (where(A) || where(ipiv)) { set_error("LU takes device pointers only"); return DDQD_ENOTSUP; }
+    int info = 0;
+    const int rc = lu_panel_impl(prec, pivot, n, A, ipiv, p, kb, t_stream, &info);
+    if (rc) return rc;
+    return info;
+}
+
+int ddqd_lu_trsv(int prec, int64_t n, const double *LU, const int64_t *ipiv, const double *b, double *x) {
+    t_err.clear();
+    if (prec != 2 && prec != 4) { set_error("prec must be DDQD_DD or DDQD_QD"); return DDQD_EINVAL; }
+    if (n < 0) { set_error("n must be >= 0"); return DDQD_EINVAL; }
+    if (n == 0) return DDQD_OK;
+    if (!LU || !ipiv || !b || !x) { set_error("null pointer"); return DDQD_EINVAL; }
+    if (where(LU) || where(ipiv) || where(b) || where(x)) { set_error("LU takes device pointers only"); return DDQD_ENOTSUP; }
+    return lu_trsv_impl(prec, n, LU, ipiv, b, x, t_stream);
 }
 
 int dd_lu_solve(int64_t n, double *A, const double *b, double *x, int64_t *ipiv, int64_t panel, int algo,

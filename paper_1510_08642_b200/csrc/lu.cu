@@ -619,64 +619,49 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
     return 1;
 }
 
+// Steps 1-2 of numerics.md s.5 for the panel [p, p+kb): factorisation (cooperative kernel or
+// the per-column pair), interchanges of the other columns, U12 := L11^{-1} A12.
 template <int W>
-static int lu_solve_w(int64_t n, int pivot, double *A, const double *b, double *x, int64_t *ipiv, int64_t K,
-                      int algo, int64_t T, cudaStream_t s, int *info_out) {
-    *info_out = 0;
-    if (n == 0) return DDQD_OK;
-    int st = DDQD_OK;
-    // aux: LuAux | y [W n] | cooperative-panel scratch (2 buffers)
-    const size_t ybytes = (sizeof(double) * W * (size_t)n + 255) & ~size_t(255);
-    const size_t scr_bytes = sizeof(double) * 2 * ((size_t)160 * (W + 1 + W * (size_t)K) + W * (size_t)K);
-    const size_t aux_bytes = 256 + ybytes + scr_bytes;
-    char *aux_mem = static_cast<char *>(aux_get(aux_bytes, &st));
-    if (st) return st;
-    LuAux *aux = reinterpret_cast<LuAux *>(aux_mem);
-    double *y = reinterpret_cast<double *>(aux_mem + 256);
-    double *scr = reinterpret_cast<double *>(aux_mem + 256 + ybytes);
-    DDQD_CUDA_CHECK(cudaMemsetAsync(aux, 0, sizeof(LuAux), s));
-
-    for (int64_t p = 0; p < n; p += K) {
-        const int64_t kb = std::min(K, n - p);
-        prof_begin(3, s);
-        int crc = DDQD_OK;
-        const bool coop = use_coop_panel() && try_panel_coop<W>(A, n, p, kb, pivot, ipiv, aux, scr, scr_bytes, s, &crc);
-        if (crc) return crc;
-        for (int64_t k = p; !coop && k < p + kb; k++) {
-            lu_pivot_kernel<W><<<1, 1024, 0, s>>>(A, n, k, pivot, ipiv, aux);
-            DDQD_LAUNCH_CHECK();
-            const int64_t nc = p + kb - (k + 1), nr = n - (k + 1);
-            if (nc > 0 && nr > 0) {
-                dim3 blk(32, 8);
-                dim3 grd((unsigned)((nc + 31) / 32), (unsigned)((nr + 7) / 8));
-                lu_rank1_kernel<W><<<grd, blk, 0, s>>>(A, n, k, p + kb, aux);
-                DDQD_LAUNCH_CHECK();
-            }
-        }
-        prof_end(3, (double)kb * (double)(n - p) * (double)kb / 2.0, s);   // panel madds (approx.)
-        const int64_t n2 = n - p - kb;
-        if (n2 <= 0) continue;
-        // one CTA per SM when possible: cw = ceil(n2 / 148), capped by shared memory
-        const int64_t cw_smem = std::max<int64_t>(1, (int64_t)(200 * 1024) / (8 * W * kb));
-        int cw = (int)std::max<int64_t>(1, std::min<int64_t>(cw_smem, (n2 + 147) / 148));
-        const size_t smem = sizeof(double) * W * (size_t)kb * cw;
-        if (smem > 48 * 1024)
-            DDQD_CUDA_CHECK(cudaFuncSetAttribute(lu_trsm_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem));
-        prof_begin(4, s);
-        if (kb > 1024) { set_error("panel > 1024 not supported by the TRSM kernel"); return DDQD_ENOTSUP; }
-        const int tthreads = (int)(((kb + 31) / 32) * 32);
-        lu_trsm_kernel<W><<<(unsigned)((n2 + cw - 1) / cw), tthreads, smem, s>>>(A, n, p, kb, p + kb, cw);
+static int lu_panel_w(int64_t n, int pivot, double *A, int64_t *ipiv, int64_t p, int64_t kb, LuAux *aux,
+                      double *scr, size_t scr_bytes, cudaStream_t s) {
+    prof_begin(3, s);
+    int crc = DDQD_OK;
+    const bool coop = use_coop_panel() && try_panel_coop<W>(A, n, p, kb, pivot, ipiv, aux, scr, scr_bytes, s, &crc);
+    if (crc) return crc;
+    for (int64_t k = p; !coop && k < p + kb; k++) {
+        lu_pivot_kernel<W><<<1, 1024, 0, s>>>(A, n, k, pivot, ipiv, aux);
         DDQD_LAUNCH_CHECK();
-        prof_end(4, (double)kb * (double)kb / 2.0 * (double)n2, s);
-        MatDesc L21{A + (p + kb) * n + p, n2, kb, n, n * n, 0};
-        MatDesc U12{A + p * n + (p + kb), kb, n2, n, n * n, 0};
-        MatDesc A22{A + (p + kb) * n + (p + kb), n2, n2, n, n * n, 0};
-        const int rc = run_gemm(W, algo, T, n2, kb, n2, 1, L21, U12, A22, 1, s);
-        if (rc) return rc;
+        const int64_t nc = p + kb - (k + 1), nr = n - (k + 1);
+        if (nc > 0 && nr > 0) {
+            dim3 blk(32, 8);
+            dim3 grd((unsigned)((nc + 31) / 32), (unsigned)((nr + 7) / 8));
+            lu_rank1_kernel<W><<<grd, blk, 0, s>>>(A, n, k, p + kb, aux);
+            DDQD_LAUNCH_CHECK();
+        }
     }
+    prof_end(3, (double)kb * (double)(n - p) * (double)kb / 2.0, s);   // panel madds (approx.)
+    const int64_t n2 = n - p - kb;
+    if (n2 <= 0) return DDQD_OK;
+    // one CTA per SM when possible: cw = ceil(n2 / 148), capped by shared memory
+    const int64_t cw_smem = std::max<int64_t>(1, (int64_t)(200 * 1024) / (8 * W * kb));
+    int cw = (int)std::max<int64_t>(1, std::min<int64_t>(cw_smem, (n2 + 147) / 148));
+    const size_t smem = sizeof(double) * W * (size_t)kb * cw;
+    if (smem > 48 * 1024)
+        DDQD_CUDA_CHECK(cudaFuncSetAttribute(lu_trsm_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+    if (kb > 1024) { set_error("panel > 1024 not supported by the TRSM kernel"); return DDQD_ENOTSUP; }
+    prof_begin(4, s);
+    const int tthreads = (int)(((kb + 31) / 32) * 32);
+    lu_trsm_kernel<W><<<(unsigned)((n2 + cw - 1) / cw), tthreads, smem, s>>>(A, n, p, kb, p + kb, cw);
+    DDQD_LAUNCH_CHECK();
+    prof_end(4, (double)kb * (double)kb / 2.0 * (double)n2, s);
+    return DDQD_OK;
+}
 
-    // solve: y = P b; L y' = y (j ascending); U x = y' (j descending)
+// Eq. (2) with the factors: y := P b, forward (unit L), backward (numerics.md s.5).
+template <int W>
+static int lu_trsv_w(int64_t n, const double *A, const int64_t *ipiv, const double *b, double *x, double *y,
+                     cudaStream_t s) {
     const int use_smem = ((int64_t)W * n * (int64_t)sizeof(double) <= 200 * 1024) ? 1 : 0;
     const size_t psmem = use_smem ? (size_t)W * n * sizeof(double) : 0;
     if (psmem > 48 * 1024)
@@ -707,11 +692,81 @@ static int lu_solve_w(int64_t n, int pivot, double *A, const double *b, double *
         }
     }
     prof_end(5, (double)n * (double)n, s);
+    return DDQD_OK;
+}
+
+// aux layout: LuAux | y [W n] | cooperative-panel scratch (2 buffers)
+struct LuMem {
+    LuAux *aux;
+    double *y, *scr;
+    size_t scr_bytes;
+};
+static int lu_mem(int W, int64_t n, int64_t K, LuMem *m) {
+    int st = DDQD_OK;
+    const size_t ybytes = (sizeof(double) * W * (size_t)n + 255) & ~size_t(255);
+    m->scr_bytes = sizeof(double) * 2 * ((size_t)160 * (W + 1 + W * (size_t)K) + W * (size_t)K);
+    char *mem = static_cast<char *>(aux_get(256 + ybytes + m->scr_bytes, &st));
+    if (st) return st;
+    m->aux = reinterpret_cast<LuAux *>(mem);
+    m->y = reinterpret_cast<double *>(mem + 256);
+    m->scr = reinterpret_cast<double *>(mem + 256 + ybytes);
+    return DDQD_OK;
+}
+
+template <int W>
+static int lu_solve_w(int64_t n, int pivot, double *A, const double *b, double *x, int64_t *ipiv, int64_t K,
+                      int algo, int64_t T, cudaStream_t s, int *info_out) {
+    *info_out = 0;
+    if (n == 0) return DDQD_OK;
+    LuMem mem;
+    int rc = lu_mem(W, n, K, &mem);
+    if (rc) return rc;
+    DDQD_CUDA_CHECK(cudaMemsetAsync(mem.aux, 0, sizeof(LuAux), s));
+    for (int64_t p = 0; p < n; p += K) {
+        const int64_t kb = std::min(K, n - p);
+        if ((rc = lu_panel_w<W>(n, pivot, A, ipiv, p, kb, mem.aux, mem.scr, mem.scr_bytes, s))) return rc;
+        const int64_t n2 = n - p - kb;
+        if (n2 <= 0) continue;
+        MatDesc L21{A + (p + kb) * n + p, n2, kb, n, n * n, 0};
+        MatDesc U12{A + p * n + (p + kb), kb, n2, n, n * n, 0};
+        MatDesc A22{A + (p + kb) * n + (p + kb), n2, n2, n, n * n, 0};
+        if ((rc = run_gemm(W, algo, T, n2, kb, n2, 1, L21, U12, A22, 1, s))) return rc;
+    }
+    if ((rc = lu_trsv_w<W>(n, A, ipiv, b, x, mem.y, s))) return rc;
     int info_h = 0;
-    DDQD_CUDA_CHECK(cudaMemcpyAsync(&info_h, &aux->info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    DDQD_CUDA_CHECK(cudaMemcpyAsync(&info_h, &mem.aux->info, sizeof(int), cudaMemcpyDeviceToHost, s));
     DDQD_CUDA_CHECK(cudaStreamSynchronize(s));
     *info_out = info_h;
     return DDQD_OK;
+}
+
+// One panel step on its own (the multi-GPU LU drives the Schur update itself): returns this
+// panel's info (first k+1 with an exactly zero pivot, else 0); synchronises.
+int lu_panel_impl(int W, int pivot, int64_t n, double *A, int64_t *ipiv, int64_t p, int64_t kb, cudaStream_t s,
+                  int *info_out) {
+    *info_out = 0;
+    LuMem mem;
+    int rc = lu_mem(W, n, kb, &mem);
+    if (rc) return rc;
+    DDQD_CUDA_CHECK(cudaMemsetAsync(mem.aux, 0, sizeof(LuAux), s));
+    rc = W == 2 ? lu_panel_w<2>(n, pivot, A, ipiv, p, kb, mem.aux, mem.scr, mem.scr_bytes, s)
+                : lu_panel_w<4>(n, pivot, A, ipiv, p, kb, mem.aux, mem.scr, mem.scr_bytes, s);
+    if (rc) return rc;
+    int info_h = 0;
+    DDQD_CUDA_CHECK(cudaMemcpyAsync(&info_h, &mem.aux->info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    DDQD_CUDA_CHECK(cudaStreamSynchronize(s));
+    *info_out = info_h;
+    return DDQD_OK;
+}
+
+// The solve with given factors (asynchronous on s).
+int lu_trsv_impl(int W, int64_t n, const double *A, const int64_t *ipiv, const double *b, double *x,
+                 cudaStream_t s) {
+    if (n == 0) return DDQD_OK;
+    LuMem mem;
+    int rc = lu_mem(W, n, 1, &mem);
+    if (rc) return rc;
+    return W == 2 ? lu_trsv_w<2>(n, A, ipiv, b, x, mem.y, s) : lu_trsv_w<4>(n, A, ipiv, b, x, mem.y, s);
 }
 
 int lu_solve_impl(int W, int pivot, int64_t n, double *A, const double *b, double *x, int64_t *ipiv, int64_t K,

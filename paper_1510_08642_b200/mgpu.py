@@ -18,7 +18,14 @@ One process per GPU (torchrun), torch.distributed over NCCL for the plumbing:
     A row slab and all of B, and the slabs are gathered to rank 0.
 
 Both schedules are numerically identical to the single-GPU call (same tree, same order),
-so results are bit-identical to the oracle for any world size.
+so results are bit-identical to the oracle for any world size. With beta = 1 the result is
+subtracted from C (C := C - A B), the form of the LU's Schur update.
+
+DistributedLU: the blocked LU with its trailing update
+A22 := A22 - L21 U12 run by DistributedGemm over all ranks; rank 0 keeps the matrix
+and does the sequential panel steps (4096 dependent pivot steps at c4 do not shard) and the
+solve. Every panel's update is the same recursion tree as on one GPU, so the factors and the
+solution are bit-identical to the single-GPU LU (and the oracle) for any world size.
 
 The compute steps go through a `backend` (default: the CUDA library); tests substitute a
 CPU backend built from the oracle to check this host logic with gloo on CPU.
@@ -69,18 +76,28 @@ class CudaBackend:
         import torch
         return torch.empty(shape, dtype=torch.float64, device=like.device)
 
+    def empty_i64(self, n, like):
+        import torch
+        return torch.empty(n, dtype=torch.int64, device=like.device)
+
     def pre_add(self, algo, side, X, Y):
         self.ddqd.pre_add(algo, side, X, Y)
 
-    def post_add(self, algo, M, C):
-        self.ddqd.post_add(algo, M, C, 0)
+    def post_add(self, algo, M, C, beta=0):
+        self.ddqd.post_add(algo, M, C, beta)
+
+    def lu_panel(self, A, ipiv, p, kb, pivot):
+        return self.ddqd.lu_panel(A, ipiv, p, kb, pivot)
+
+    def lu_trsv(self, A, ipiv, b):
+        return self.ddqd.lu_trsv(A, ipiv, b)
 
     def gemm_batched(self, A, B, C, algo, T):
         if A.shape[0]:
             self.ddqd.gemm_batched(A, B, C, algo, T)
 
-    def gemm_rows(self, A, B, r0, r1, out, algo, T):
-        """out[:, :r1-r0, :] := A[:, r0:r1, :] B via strided views (no copies)."""
+    def gemm_rows(self, A, B, r0, r1, out, algo, T, beta=0):
+        """out[:, :r1-r0, :] := (out -) A[:, r0:r1, :] B via strided views (no copies)."""
         W, m, l = A.shape
         n = B.shape[2]
         per = out.shape[1]
@@ -88,14 +105,15 @@ class CudaBackend:
         self.ddqd.gemm_ex(W, algo, T, r1 - r0, l, n, 1,
                           A.data_ptr() + 8 * r0 * l, l, m * l, 0,
                           B.data_ptr(), n, l * n, 0,
-                          out.data_ptr(), n, per * n, 0, 0)
+                          out.data_ptr(), n, per * n, 0, beta)
 
 
 class DistributedGemm:
-    """C := A B across the process group `dist` (rank 0 holds the operands and the result)."""
+    """C := A B (beta = 0) or C := C - A B (beta = 1) across the process group `dist` (rank 0
+    holds the operands and C; C may be a strided view with unit-stride rows)."""
 
-    def __init__(self, W, algo, T, m, l, n, dist, device=None, k=None, backend=None, chunk=None):
-        self.W, self.algo, self.T = W, algo, T
+    def __init__(self, W, algo, T, m, l, n, dist, device=None, k=None, backend=None, chunk=None, beta=0):
+        self.W, self.algo, self.T, self.beta = W, algo, T, beta
         self.m, self.l, self.n = m, l, n
         self.dist = dist
         self.rank = dist.get_rank()
@@ -135,6 +153,8 @@ class DistributedGemm:
             bufs["local"] = bk.empty((W, self.per, self.n), like)
             if self.rank == 0:
                 bufs["gather"] = [bk.empty((W, self.per, self.n), like) for _ in range(self.world)]
+                if self.beta:
+                    bufs["scatter"] = [bk.empty((W, self.per, self.n), like) for _ in range(self.world)]
         self._bufs = bufs
         return bufs
 
@@ -186,7 +206,7 @@ class DistributedGemm:
                 q.wait()
             for j in range(self.k - 1, -1, -1):
                 target = C if j == 0 else bufs["M"][j - 1]
-                bk.post_add(self.algo, bufs["M"][j], target)
+                bk.post_add(self.algo, bufs["M"][j], target, self.beta if j == 0 else 0)
         else:
             local = bufs["local"]
             sends = []
@@ -202,10 +222,55 @@ class DistributedGemm:
     def _row_slabs(self, A, B, C, bufs):
         r0, r1 = self.slices[self.rank]
         local = bufs["local"]
+        if self.beta:
+            # C := C - A B: each rank receives its C row slab and updates it in place
+            if self.rank == 0:
+                for r, (a, b) in enumerate(self.slices):
+                    bufs["scatter"][r][:, : b - a, :].copy_(C[:, a:b, :])
+            self.dist.scatter(local, bufs.get("scatter") if self.rank == 0 else None, src=0)
         if r1 > r0:
-            self.backend.gemm_rows(A, B, r0, r1, local, self.algo, self.T)
+            self.backend.gemm_rows(A, B, r0, r1, local, self.algo, self.T, self.beta)
         self.dist.gather(local, bufs.get("gather") if self.rank == 0 else None, dst=0)
         if self.rank == 0:
             for r, (a, b) in enumerate(self.slices):
                 C[:, a:b, :].copy_(bufs["gather"][r][:, : b - a, :])
         return C
+
+
+class DistributedLU:
+    """Blocked right-looking DD/QD LU + solve (numerics.md s.5) whose Schur updates run on all
+    ranks (row f4). Rank 0 holds A ([W,n,n], overwritten with the factors) and b ([W,n]); the
+    call returns (x, ipiv, info) on rank 0 and (None, None, None) elsewhere."""
+
+    def __init__(self, W, n, K, algo, T, dist, pivot=True, backend=None, k=None):
+        self.W, self.n, self.K, self.algo, self.T = W, n, K, algo, T
+        self.dist, self.pivot, self.k = dist, pivot, k
+        self.rank = dist.get_rank()
+        self.backend = backend or CudaBackend()
+
+    def __call__(self, A, b):
+        W, n, K, bk = self.W, self.n, self.K, self.backend
+        root = self.rank == 0
+        ipiv = bk.empty_i64(n, A) if root else None
+        info = 0
+        for p in range(0, n, K):
+            kb = min(K, n - p)
+            if root:
+                pi = bk.lu_panel(A, ipiv, p, kb, self.pivot)
+                info = info or pi
+            n2 = n - p - kb
+            if n2 <= 0:
+                continue
+            if root:
+                L21 = A[:, p + kb:, p:p + kb].contiguous()
+                U12 = A[:, p:p + kb, p + kb:].contiguous()
+                C = A[:, p + kb:, p + kb:]
+            else:
+                L21 = bk.empty((W, n2, kb), A)
+                U12 = bk.empty((W, kb, n2), A)
+                C = None
+            DistributedGemm(W, self.algo, self.T, n2, kb, n2, self.dist, k=self.k, backend=bk,
+                            beta=1)(L21, U12, C)
+        if not root:
+            return None, None, None
+        return bk.lu_trsv(A, ipiv, b), ipiv, info

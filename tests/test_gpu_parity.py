@@ -601,3 +601,55 @@ def test_accurate_add_rejections():
         ddqd.lu_solve(A.clone(), b, panel=8, algo="strassen", threshold=4, madd="accurate")
     with pytest.raises(ValueError):   # DDQD_EINVAL: the two variants are exclusive
         ddqd.gemm(A, A, ddqd.MADD_FUSED | ddqd.ADD_ACCURATE | 1, 4)
+
+
+# ---- LU steps as separate calls + the distributed LU (row f4) --------------------------------
+@pytest.mark.parametrize("W", [2, 4])
+def test_lu_panel_and_trsv_entry_points(orc, W):
+    """ddqd_lu_panel per panel + the caller's Schur update (ddqd_gemm_ex, beta = 1) +
+    ddqd_lu_trsv reproduce the one-call LU and the oracle bitwise (ragged last panel)."""
+    n, K, T = 150, 32, 8
+    A0 = gen.lu_matrix(n, 12) if W == 2 else gen.matrix(4, n, n, 12, 0)
+    ones = np.zeros((W, n, 1)); ones[0] = 1.0
+    b = orc.gemm(A0, ones, "block")[:, :, 0].copy()
+    xr, LUr, pr, ir = orc.solve(A0, b, panel=K, algo="winograd", threshold=T)
+    A = cu(A0)
+    ipiv = torch.empty(n, dtype=torch.int64, device=DEV)
+    info = 0
+    for p in range(0, n, K):
+        kb = min(K, n - p)
+        info = info or ddqd.lu_panel(A, ipiv, p, kb)
+        n2 = n - p - kb
+        if n2 > 0:
+            base = A.data_ptr()
+            ddqd.gemm_ex(W, "winograd", T, n2, kb, n2, 1,
+                         base + 8 * ((p + kb) * n + p), n, n * n, 0,
+                         base + 8 * (p * n + p + kb), n, n * n, 0,
+                         base + 8 * ((p + kb) * n + p + kb), n, n * n, 0, beta=1)
+    x = ddqd.lu_trsv(A, ipiv, cu(b))
+    assert info == ir
+    assert same(np_(A), LUr) and np.array_equal(np_(ipiv), pr) and same(np_(x), xr)
+
+
+@pytest.mark.parametrize("algo", ["strassen", "block"])
+def test_distributed_lu_cuda_backend_world1(orc, algo):
+    """DistributedLU through the library (ddqd_lu_panel, DistributedGemm with beta = 1 on the
+    strided trailing block, ddqd_lu_trsv) on one GPU over NCCL: bitwise the single-GPU LU."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1510_08642_b200.mgpu import DistributedLU
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    try:
+        n, K, T = 300, 64, 16
+        A0 = gen.lu_matrix(n, 13)
+        b = _b_ones(orc, A0).copy()
+        A = cu(A0)
+        x, ipiv, info = DistributedLU(2, n, K, algo, T, dist)(A, cu(b))
+        xr, LUr, pr, ir = orc.solve(A0, b, panel=K, algo=algo, threshold=T)
+        assert info == ir and same(np_(A), LUr) and same(np_(x), xr)
+        assert np.array_equal(np_(ipiv), pr)
+    finally:
+        dist.destroy_process_group()

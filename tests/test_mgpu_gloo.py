@@ -37,6 +37,15 @@ class OracleBackend:
     def empty(self, shape, like):
         return torch.empty(shape, dtype=torch.float64)
 
+    def empty_i64(self, n, like):
+        return torch.empty(n, dtype=torch.int64)
+
+    def lu_panel(self, A, ipiv, p, kb, pivot):
+        return self.o.lu_panel(A.numpy(), ipiv.numpy(), p, kb, pivot)
+
+    def lu_trsv(self, A, ipiv, b):
+        return torch.from_numpy(self.o.lu_solve(A.numpy(), ipiv.numpy(), b.numpy()))
+
     def _ew(self, name, x, y):
         W = self.W
         shp = x.shape
@@ -68,7 +77,7 @@ class OracleBackend:
             for c in range(7):
                 Y[7 * b + c] = torch.from_numpy(np.ascontiguousarray(o[c]))
 
-    def post_add(self, algo, M, C):
+    def post_add(self, algo, M, C, beta=0):
         add = lambda a, b: self._ew("add", a, b)   # noqa: E731
         sub = lambda a, b: self._ew("sub", a, b)   # noqa: E731
         Cv = C if C.dim() == 4 else C.unsqueeze(0)
@@ -84,15 +93,20 @@ class OracleBackend:
             full = np.zeros((self.W, 2 * hm, 2 * hn))
             full[:, :hm, :hn] = c11; full[:, :hm, hn:] = c12; full[:, hm:, :hn] = c21; full[:, hm:, hn:] = c22
             r, c = Cv.shape[-2], Cv.shape[-1]
-            Cv[b] = torch.from_numpy(np.ascontiguousarray(full[:, :r, :c]))
+            t = np.ascontiguousarray(full[:, :r, :c])
+            if beta:
+                t = sub(np.ascontiguousarray(Cv[b].numpy()), t)
+            Cv[b] = torch.from_numpy(t)
 
     def gemm_batched(self, A, B, C, algo, T):
         for b in range(A.shape[0]):
             C[b] = torch.from_numpy(self.o.gemm(A[b].numpy(), B[b].numpy(), algo, threshold=T))
 
-    def gemm_rows(self, A, B, r0, r1, out, algo, T):
-        out[:, : r1 - r0, :] = torch.from_numpy(
-            self.o.gemm(np.ascontiguousarray(A[:, r0:r1, :].numpy()), B.numpy(), algo, threshold=T))
+    def gemm_rows(self, A, B, r0, r1, out, algo, T, beta=0):
+        t = self.o.gemm(np.ascontiguousarray(A[:, r0:r1, :].numpy()), B.numpy(), algo, threshold=T)
+        if beta:
+            t = self._ew("sub", np.ascontiguousarray(out[:, : r1 - r0, :].numpy()), t)
+        out[:, : r1 - r0, :] = torch.from_numpy(t)
 
 
 def _worker(rank, world, port, cfg, q, chunk=None):
@@ -156,3 +170,73 @@ def test_balancer():
     assert balanced_slices(49, 8)[0] == (0, 7) and balanced_slices(49, 8)[-1] == (43, 49)
     assert choose_depth(5, 8) == 3 and choose_depth(5, 4) == 2 and choose_depth(5, 2) == 2
     assert choose_depth(5, 7) == 1 and choose_depth(0, 8) == 0
+
+
+
+# ---- distributed LU (row f4) ------------------------------------------------------------------
+def _lu_worker(rank, world, port, cfg, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_1510_08642_b200.mgpu import DistributedLU
+        W, n, K, algo, T, pivot, seed = cfg
+        if rank == 0:
+            A0 = _lu_input(W, n, seed)
+            A = torch.from_numpy(A0.copy())
+            b = torch.from_numpy(oracle.gemm(A0, _ones(W, n), "block")[:, :, 0].copy())
+        else:
+            A = torch.zeros((W, n, n), dtype=torch.float64)
+            b = None
+        x, ipiv, info = DistributedLU(W, n, K, algo, T, dist, pivot=pivot, backend=OracleBackend(W))(A, b)
+        if rank == 0:
+            q.put((x.numpy().copy(), A.numpy().copy(), ipiv.numpy().copy(), info))
+    finally:
+        dist.destroy_process_group()
+
+
+def _ones(W, n):
+    o = np.zeros((W, n, 1))
+    o[0] = 1.0
+    return o
+
+
+def _lu_input(W, n, seed):
+    if W == 2:
+        return gen.lu_matrix(n, seed)
+    return gen.matrix(4, n, n, seed, 0)   # QD, non-dominant: exercises the interchanges
+
+
+def _run_lu(cfg, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lu_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+@pytest.mark.parametrize("cfg,world", [
+    ((2, 70, 16, "strassen", 8, True, 5), 2),    # Strassen updates (depth 1-2), ragged last panel
+    ((2, 61, 20, "winograd", 4, True, 6), 3),    # three ranks, deeper Winograd updates
+    ((2, 50, 12, "block", 8, True, 7), 2),       # Block update: C row slabs with beta = 1
+    ((4, 40, 16, "winograd", 4, True, 8), 2),    # QD, pivoting with interchanges
+    ((2, 45, 16, "strassen", 4, False, 9), 2),   # the paper's pivot-free LU
+])
+def test_distributed_lu_matches_single_process(orc, cfg, world):
+    """DistributedLU (row f4): the trailing updates run over the ranks; factors, pivots, info
+    and the solution are bitwise those of the single-process oracle LU."""
+    W, n, K, algo, T, pivot, seed = cfg
+    x, LU, ipiv, info = _run_lu(cfg, world)
+    A0 = _lu_input(W, n, seed)
+    b = orc.gemm(A0, _ones(W, n), "block")[:, :, 0].copy()
+    xr, LUr, pr, ir = orc.solve(A0, b, panel=K, algo=algo, threshold=T, pivot=pivot)
+    assert info == ir
+    assert np.array_equal(ipiv, pr)
+    assert np.array_equal(LU.view(np.int64), LUr.view(np.int64))
+    assert np.array_equal(x.view(np.int64), xr.view(np.int64))
