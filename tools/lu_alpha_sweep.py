@@ -7,7 +7,10 @@ alpha = 1..10, n_min = 32, trailing update by Winograd(n_min) (P:
 DD and QD. Reports the time (CUDA events, median of 3) and the maximum relative error of
 x (components with x_i = 0 are normalised by ||x||_inf), next to the paper's
 8-thread times: DD 4.3 s at alpha = 2 (row-wise 13.0 s), QD 23.4 s at alpha = 5
-(row-wise 56 s). Also runs the pivoted variant at the best alpha for comparison.
+(row-wise 56 s). Also runs the pivoted variant at the best alpha for comparison, and the
+row-wise parallel (unblocked) LU the paper compares against: one panel K = n, i.e.
+every column's pivot/scale/rank-1 update over all rows in parallel with no GEMM (DESIGN.md
+reading R20).
 
     python tools/lu_alpha_sweep.py [--n 1024] [--out profiles/r01/lu_alpha_sweep.md]
 """
@@ -52,9 +55,9 @@ def main():
         xt = torch.zeros((W, n, 1), dtype=torch.float64, device="cuda")
         xt[0, :, 0] = torch.arange(n, dtype=torch.float64)
         b = ddqd.gemm(A0, xt, "block")[:, :, 0].contiguous()
-        runs = [(alpha, False) for alpha in range(1, 11)] + [(2 if W == 2 else 5, True)]
+        runs = [(alpha, False) for alpha in range(1, 11)] + [(2 if W == 2 else 5, True), ("row-wise", False)]
         for alpha, pivot in runs:
-            K = alpha * nmin
+            K = n if alpha == "row-wise" else alpha * nmin
             ts = []
             for rep in range(4):
                 A = A0.clone()
