@@ -64,10 +64,10 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variant", action="store_true",
-                    help="skip the extra fused-madd measurement reported under 'variants'")
-    ap.add_argument("--madd", default="canonical", choices=["canonical", "fused"],
-                    help="DD multiply-add: the paper's QD-library sequence (20 FP64 ops) or the "
-                         "fused variant of numerics.md s.2 (15 ops; row f3)")
+                    help="skip the extra fused / accurate measurements reported under 'variants'")
+    ap.add_argument("--madd", default="canonical", choices=["canonical", "fused", "accurate"],
+                    help="arithmetic: the paper's QD-library sequences (DD madd 20 FP64 ops), the "
+                         "fused multiply-add or the accurate adds of numerics.md s.2-3 (row f3)")
     return ap.parse_args()
 
 
@@ -421,23 +421,28 @@ def main():
     classical = ops * m * l * n / (ms_per_step * 1e-3) / peak   # BJ:5's literal formula (may be > 1)
 
     variants = None
-    if W == 2 and args.madd == "canonical" and world == 1 and not args.no_variant:
-        # the fused DD multiply-add of numerics.md s.2 (SURVEY s.8(f) row f3) on the same inputs:
-        # a different (documented) rounding, reported beside the paper-faithful headline
-        def fstep():
-            ddqd.gemm(A, B, algo, T, out=C, madd="fused")
-        fstep()
-        torch.cuda.synchronize()
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record()
-        for _ in range(args.steps):
-            fstep()
-        f1.record()
-        torch.cuda.synchronize()
-        fms = f0.elapsed_time(f1)
-        variants = {"madd_fused": {"value": flops_per_step * args.steps / (fms * 1e-3) / 1e9, "unit": "GFLOP/s",
-                                   "ms_per_step": fms / args.steps, "fp64_ops_per_madd": 15,
-                                   "note": "DDQD_MADD_FUSED: bit-exact vs the oracle's fused variant, not the canonical"}}
+    if args.madd == "canonical" and world == 1 and not args.no_variant:
+        # the arithmetic variants of SURVEY s.8(f) row f3 on the same inputs: different
+        # (documented, oracle-mirrored) roundings, reported beside the paper-faithful headline
+        variants = {}
+        notes = {"fused": ("DDQD_MADD_FUSED", {2: 15, 4: None}),
+                 "accurate": ("DDQD_ADD_ACCURATE", {2: 29, 4: None})}
+        for v, (flag, opc) in notes.items():
+            def vstep():
+                ddqd.gemm(A, B, algo, T, out=C, madd=v)
+            vstep()
+            torch.cuda.synchronize()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record()
+            for _ in range(args.steps):
+                vstep()
+            f1.record()
+            torch.cuda.synchronize()
+            fms = f0.elapsed_time(f1)
+            variants["madd_" + v] = {
+                "value": flops_per_step * args.steps / (fms * 1e-3) / 1e9, "unit": "GFLOP/s",
+                "ms_per_step": fms / args.steps, "fp64_ops_per_madd": opc[W],
+                "note": flag + ": bit-exact vs the oracle's " + v + " variant, not the canonical"}
 
     e2e = None
     if not args.no_e2e and world == 1:

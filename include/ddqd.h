@@ -43,10 +43,11 @@ extern "C" {
 /* Algorithms. */
 enum { DDQD_BLOCK = 0, DDQD_STRASSEN = 1, DDQD_WINOGRAD = 2 };
 
-/* Flag OR-ed into `algo` (DD only): the leaf uses the fused DD multiply-add of
- * docs/numerics.md s.2 (15 FP64 instructions instead of the QD-library dd_add(c, dd_mul(a,b))
- * = 20). Results are then bit-identical to the oracle's fused
- * variant, not to the canonical one. QD with this flag returns DDQD_ENOTSUP. */
+/* Flag OR-ed into `algo`: the leaf uses the fused multiply-add of docs/numerics.md s.2-3
+ * (DD: 15 FP64 instructions instead of the QD-library dd_add(c, dd_mul(a,b)) = 20; QD: the
+ * product's expansion enters qd_add's network unrenormalised, one renormalisation fewer;
+ * SURVEY.md s.8(f) row f3). Results are then bit-identical to the oracle's fused variant,
+ * not (in general) to the canonical one. */
 enum { DDQD_MADD_FUSED = 0x100 };
 
 /* Flag OR-ed into `algo` (DD and QD): every addition of the GEMM -- the multiply-add's and
@@ -169,7 +170,7 @@ int ddqd_lu_trsv(int prec, int64_t n, const double *LU, const int64_t *ipiv, con
 
 /* Elementwise arithmetic layer, for parity tests of the device DD/QD ops (device
  * pointers, planar [W][count]): op 0 add, 1 sub, 2 mul, 3 div, 4 madd z = x + y*w,
- * 5 fused madd (DD only, DDQD_MADD_FUSED's operation), 6 accurate add, 7 accurate sub,
+ * 5 fused madd (DDQD_MADD_FUSED's operation), 6 accurate add, 7 accurate sub,
  * 8 accurate madd z = x + y*w (DDQD_ADD_ACCURATE's operations, DD and QD). */
 int ddqd_elementwise(int prec, int op, int64_t count, const double *x, const double *y,
                      const double *w, double *z);

@@ -247,6 +247,47 @@ static qd_t qd_mul(qd_t a, qd_t b) {
 
 static qd_t qd_madd(qd_t c, qd_t a, qd_t b) { return qd_add(c, qd_mul(a, b)); }
 
+/* numerics.md s.3 fused QD multiply-add (variant DDQD_MADD_FUSED):
+ * the product's five-term expansion (p0, p1, s0, s1, s2) of qd_mul is added to c by the
+ * qd_add network without renormalising it first (s2 joins the final tail). */
+static qd_t qd_madd_fused(qd_t c, qd_t a, qd_t b) {
+    double p0, p1, p2, p3, p4, p5, q0, q1, q2, q3, q4, q5;
+    double s0, s1, s2, t0, t1, tail;
+    double u0, u1, u2, u3, v0, v1, v2, v3;
+    two_prod(a.w[0], b.w[0], &p0, &q0);
+    two_prod(a.w[0], b.w[1], &p1, &q1);
+    two_prod(a.w[1], b.w[0], &p2, &q2);
+    two_prod(a.w[0], b.w[2], &p3, &q3);
+    two_prod(a.w[1], b.w[1], &p4, &q4);
+    two_prod(a.w[2], b.w[0], &p5, &q5);
+    three_sum(&p1, &p2, &q0);
+    three_sum(&p2, &q1, &q2);
+    three_sum(&p3, &p4, &p5);
+    two_sum(p2, p3, &s0, &t0);
+    two_sum(q1, p4, &s1, &t1);
+    s2 = q2 + p5;
+    two_sum(s1, t0, &s1, &t0);
+    s2 = s2 + (t0 + t1);
+    tail = a.w[0] * b.w[3];
+    tail = tail + a.w[1] * b.w[2];
+    tail = tail + a.w[2] * b.w[1];
+    tail = tail + a.w[3] * b.w[0];
+    tail = tail + q0;
+    tail = tail + q3;
+    tail = tail + q4;
+    tail = tail + q5;
+    s1 = s1 + tail;
+    two_sum(c.w[0], p0, &u0, &v0);
+    two_sum(c.w[1], p1, &u1, &v1);
+    two_sum(c.w[2], s0, &u2, &v2);
+    two_sum(c.w[3], s1, &u3, &v3);
+    two_sum(u1, v0, &u1, &v0);
+    three_sum(&u2, &v0, &v1);
+    three_sum2(&u3, &v0, &v2);
+    v0 = ((v0 + v1) + v3) + s2;
+    return qd_renorm(u0, u1, u2, u3, v0);
+}
+
 /* numerics.md s.3 ThreeAccum: adds t into the two-word accumulator (u, v); returns the
  * word that has become complete (or 0 when none has) */
 static double three_accum(double *u, double *v, double t) {
@@ -285,7 +326,11 @@ static qd_t qd_add_acc(qd_t a, qd_t b) {
 
 static qd_t qd_sub_acc(qd_t a, qd_t b) { return qd_add_acc(a, qd_neg(b)); }
 static qd_t qd_madd_acc(qd_t c, qd_t a, qd_t b) { return qd_add_acc(c, qd_mul(a, b)); }
-static qd_t qd_madd_v(qd_t c, qd_t a, qd_t b) { return g_variant == 2 ? qd_madd_acc(c, a, b) : qd_madd(c, a, b); }
+static qd_t qd_madd_v(qd_t c, qd_t a, qd_t b) {
+    if (g_variant == 1) return qd_madd_fused(c, a, b);
+    if (g_variant == 2) return qd_madd_acc(c, a, b);
+    return qd_madd(c, a, b);
+}
 static qd_t qd_add_v(qd_t x, qd_t y) { return g_variant == 2 ? qd_add_acc(x, y) : qd_add(x, y); }
 static qd_t qd_sub_v(qd_t x, qd_t y) { return g_variant == 2 ? qd_sub_acc(x, y) : qd_sub(x, y); }
 
@@ -335,7 +380,7 @@ void or_qd_op(int op, int64_t n, const double *x, const double *y, const double 
         default: {
             qd_t c;
             for (int k = 0; k < 4; k++) c.w[k] = w[k * n + i];
-            r = op == 8 ? qd_madd_acc(a, b, c) : qd_madd(a, b, c);
+            r = op == 8 ? qd_madd_acc(a, b, c) : op == 5 ? qd_madd_fused(a, b, c) : qd_madd(a, b, c);
         }
         }
         for (int k = 0; k < 4; k++) z[k * n + i] = r.w[k];
@@ -577,7 +622,6 @@ int or_gemm(int W, int algo, int64_t T, int64_t bs, int64_t m, int64_t l, int64_
     g_variant = (algo & 0x100) ? 1 : (algo & 0x200) ? 2 : 0;
     algo &= 0xff;
     if ((W != 2 && W != 4) || algo < 0 || algo > 2 || m < 0 || l < 0 || n < 0) return -1;
-    if (g_variant == 1 && W != 2) return -1;
     if (algo != 0 && T < 1) return -1;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -710,7 +754,7 @@ int or_lu(int W, int pivot, int64_t n, double *A, int64_t *ipiv, int64_t K, int 
     if (algo & 0x200) return -1;
     g_variant = (algo & 0x100) ? 1 : 0;
     algo &= 0xff;
-    if ((W != 2 && W != 4) || n < 0 || K < 1 || (g_variant == 1 && W != 2)) return -1;
+    if ((W != 2 && W != 4) || n < 0 || K < 1) return -1;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
 #endif

@@ -162,7 +162,6 @@ static int gemm_entry(int W, int64_t m, int64_t l, int64_t n, const double *A, c
     t_err.clear();
     int rc = check_gemm_args(m, l, n, algo, T);
     if (rc) return rc;
-    if ((algo & DDQD_MADD_FUSED) && W != 2) { set_error("the fused madd variant is DD only"); return DDQD_ENOTSUP; }
     const size_t bA = sizeof(double) * W * (size_t)m * l, bB = sizeof(double) * W * (size_t)l * n,
                  bC = sizeof(double) * W * (size_t)m * n;
     if (overlaps(A, bA, C, bC) || overlaps(B, bB, C, bC)) { set_error("C overlaps A or B"); return DDQD_EALIAS; }
@@ -216,7 +215,6 @@ int ddqd_gemm_ex(const ddqd_gemm_desc *d) {
     if (d->prec != 2 && d->prec != 4) { set_error("prec must be DDQD_DD or DDQD_QD"); return DDQD_EINVAL; }
     int rc = check_gemm_args(d->m, d->l, d->n, d->algo, d->threshold);
     if (rc) return rc;
-    if ((d->algo & DDQD_MADD_FUSED) && d->prec != 2) { set_error("the fused madd variant is DD only"); return DDQD_ENOTSUP; }
     if (d->batch < 0 || (d->beta != 0 && d->beta != 1)) { set_error("bad batch or beta"); return DDQD_EINVAL; }
     if (d->lda < d->l || d->ldb < d->n || d->ldc < d->n) { set_error("leading dimension too small"); return DDQD_EINVAL; }
     if (d->m == 0 || d->n == 0 || d->batch == 0) return DDQD_OK;
@@ -235,7 +233,6 @@ int ddqd_lu_solve(int prec, int pivot, int64_t n, double *A, const double *b, do
     if (n < 0 || panel < 1) { set_error("n must be >= 0 and panel >= 1"); return DDQD_EINVAL; }
     int rc = check_gemm_args(n, panel, n, algo, threshold);
     if (rc) return rc;
-    if ((algo & DDQD_MADD_FUSED) && prec != 2) { set_error("the fused madd variant is DD only"); return DDQD_ENOTSUP; }
     if (algo & DDQD_ADD_ACCURATE) { set_error("the accurate-add variant is a GEMM variant (LU: canonical)"); return DDQD_ENOTSUP; }
     if (n == 0) return DDQD_OK;
     if (!A || !b || !x || !ipiv) { set_error("null pointer"); return DDQD_EINVAL; }
@@ -312,7 +309,7 @@ int ddqd_post_add(int prec, int algo, int64_t P, const ddqd_mat *M, const ddqd_m
 int ddqd_elementwise(int prec, int op, int64_t count, const double *x, const double *y, const double *w,
                      double *z) {
     t_err.clear();
-    if ((prec != 2 && prec != 4) || op < 0 || op > 8 || (op == 5 && prec != 2) || count < 0) {
+    if ((prec != 2 && prec != 4) || op < 0 || op > 8 || count < 0) {
         set_error("bad elementwise arguments");
         return DDQD_EINVAL;
     }

@@ -273,6 +273,46 @@ __device__ __forceinline__ qd qd_madd_acc(const qd &c, const qd &a, const qd &b)
     return qd_add_acc(c, qd_mul(a, b));
 }
 
+// Fused QD multiply-add (numerics.md s.3, variant DDQD_MADD_FUSED): qd_mul's five-term
+// product expansion is added to c by the qd_add network without renormalising it first.
+__device__ __forceinline__ qd qd_madd_fused(const qd &c, const qd &a, const qd &b) {
+    double p0, p1, p2, p3, p4, p5, q0, q1, q2, q3, q4, q5;
+    two_prod(a.w[0], b.w[0], p0, q0);
+    two_prod(a.w[0], b.w[1], p1, q1);
+    two_prod(a.w[1], b.w[0], p2, q2);
+    two_prod(a.w[0], b.w[2], p3, q3);
+    two_prod(a.w[1], b.w[1], p4, q4);
+    two_prod(a.w[2], b.w[0], p5, q5);
+    three_sum(p1, p2, q0);
+    three_sum(p2, q1, q2);
+    three_sum(p3, p4, p5);
+    double s0, s1, s2, t0, t1;
+    two_sum(p2, p3, s0, t0);
+    two_sum(q1, p4, s1, t1);
+    s2 = __dadd_rn(q2, p5);
+    two_sum(s1, t0, s1, t0);
+    s2 = __dadd_rn(s2, __dadd_rn(t0, t1));
+    double tail = __dmul_rn(a.w[0], b.w[3]);
+    tail = __dadd_rn(tail, __dmul_rn(a.w[1], b.w[2]));
+    tail = __dadd_rn(tail, __dmul_rn(a.w[2], b.w[1]));
+    tail = __dadd_rn(tail, __dmul_rn(a.w[3], b.w[0]));
+    tail = __dadd_rn(tail, q0);
+    tail = __dadd_rn(tail, q3);
+    tail = __dadd_rn(tail, q4);
+    tail = __dadd_rn(tail, q5);
+    s1 = __dadd_rn(s1, tail);
+    double u0, u1, u2, u3, v0, v1, v2, v3;
+    two_sum(c.w[0], p0, u0, v0);
+    two_sum(c.w[1], p1, u1, v1);
+    two_sum(c.w[2], s0, u2, v2);
+    two_sum(c.w[3], s1, u3, v3);
+    two_sum(u1, v0, u1, v0);
+    three_sum(u2, v0, v1);
+    three_sum2(u3, v0, v2);
+    v0 = __dadd_rn(__dadd_rn(__dadd_rn(v0, v1), v3), s2);
+    return qd_renorm(u0, u1, u2, u3, v0);
+}
+
 // qd_div (numerics.md s.3): long division with three correction steps, then renorm.
 __device__ __forceinline__ qd qd_div(const qd &a, const qd &b) {
     qd r = a, t;
@@ -323,7 +363,7 @@ template <> struct elem<4> {
     static __device__ __forceinline__ T add(const T &x, const T &y) { return qd_add(x, y); }
     static __device__ __forceinline__ T sub(const T &x, const T &y) { return qd_sub(x, y); }
     static __device__ __forceinline__ T madd(const T &c, const T &a, const T &b) { return qd_madd(c, a, b); }
-    static __device__ __forceinline__ T madd_fused(const T &c, const T &a, const T &b) { return qd_madd(c, a, b); }
+    static __device__ __forceinline__ T madd_fused(const T &c, const T &a, const T &b) { return qd_madd_fused(c, a, b); }
     static __device__ __forceinline__ T add_acc(const T &x, const T &y) { return qd_add_acc(x, y); }
     static __device__ __forceinline__ T sub_acc(const T &x, const T &y) { return qd_sub_acc(x, y); }
     static __device__ __forceinline__ T madd_acc(const T &c, const T &a, const T &b) { return qd_madd_acc(c, a, b); }

@@ -239,8 +239,8 @@ int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, cons
             if (try_leaf_tma(m, l, n, batch, A, B, C, beta, mv, s, &rc)) return rc;
         }
     }
-    if (mv == 1) {   // fused DD madd (numerics.md s.2, row f3)
-        if (W != 2) { set_error("the fused madd variant is DD only"); return DDQD_ENOTSUP; }
+    if (mv == 1) {   // fused DD / QD madd (numerics.md s.2-3, row f3)
+        if (W == 4) return launch_cfg<4, 32, 32, 16, 2, 2, 3, 2, 1>(m, l, n, batch, A, B, C, beta, s);
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
         if (big_tiles >= 2 * 148 && m > 32 && n > 32)
             return launch_cfg<2, 64, 64, 8, 4, 4, 4, 2, 1>(m, l, n, batch, A, B, C, beta, s);

@@ -401,16 +401,22 @@ def test_fused_madd_gemm_bitwise(orc, algo):
         assert same(got, orc.gemm(A, B, algo, threshold=T, madd="fused")), (m, l, n)
 
 
-def test_fused_madd_lu_and_qd_rejected(orc):
+def test_fused_madd_lu_and_qd(orc):
+    """Fused-madd LU (DD) and the fused QD multiply-add (elementwise and GEMM), bitwise."""
     n = 160
     A = gen.lu_matrix(n, 5)
     b = _b_ones(orc, A)
     x_ref, LU_ref, _, _ = orc.solve(A, b, panel=32, algo="strassen", threshold=16, madd="fused")
     x, LU, piv, info = ddqd.lu_solve(cu(A), cu(b), panel=32, algo="strassen", threshold=16, madd="fused")
     assert info == 0 and same(np_(LU), LU_ref) and same(np_(x), x_ref)
-    Q = cu(gen.qd_matrix(8, 8, 1, 0))
-    with pytest.raises(ddqd.DDQDError):
-        ddqd.gemm(Q, Q, "block", madd="fused")
+    qx, qy, qw = (_qd_samples(orc, 50000, s) for s in (61, 62, 63))
+    qx[:, :5000] = -orc.qd_op("mul", qy[:, :5000], qw[:, :5000])
+    assert same(np_(ddqd.elementwise("madd_fused", cu(qx), cu(qy), cu(qw))), orc.qd_op("madd_fused", qx, qy, qw))
+    for algo, (m, l, n_, T) in (("block", (65, 70, 61, 8)), ("winograd", (130, 129, 131, 16)),
+                                ("strassen", (300, 257, 299, 64))):
+        Q1, Q2 = gen.qd_matrix(m, l, 3, 0), gen.qd_matrix(l, n_, 3, 1)
+        got = np_(ddqd.gemm(cu(Q1), cu(Q2), algo, T, madd="fused"))
+        assert same(got, orc.gemm(Q1, Q2, algo, threshold=T, madd="fused")), algo
 
 
 # ---- schedule / plumbing robustness ---------------------------------------------------------

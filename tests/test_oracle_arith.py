@@ -359,3 +359,31 @@ def test_qd_add_accurate_special_cases(orc):
     assert frac(orc.qd_op("add_acc", one, two)[:, 0]) == 1 + Fraction(1, 2 ** 60) + Fraction(1, 2 ** 200)
     c, a, b = (orc.qd_renorm(_rand_qd(rng, 200)) for _ in range(3))
     assert np.array_equal(orc.qd_op("madd_acc", c, a, b), orc.qd_op("add_acc", c, orc.qd_op("mul", a, b)))
+
+
+def test_qd_madd_fused_variant(orc):
+    """numerics.md s.3 fused QD madd (row f3; qd_mul's product expansion enters the qd_add
+    network unrenormalised): |err| <= 2^-205 (|c| + |ab|) against exact rationals, with
+    exact cancellation c = -ab included; calibrated worst cases on these samples are
+    2^-211.2 (|c|+|ab|-relative) and 2^-209.2 (relative, no cancellation), asserted with
+    a 2x margin so a dropped product term fails; outputs normalised."""
+    rng = np.random.default_rng(35)
+    n = 2500
+    c, a, b = (orc.qd_renorm(_rand_qd(rng, n)) for _ in range(3))
+    c[:, :500] = -orc.qd_op("mul", a[:, :500], b[:, :500])
+    z = orc.qd_op("madd_fused", c, a, b)
+    assert is_normalised(z)
+    for i in range(n):
+        C, A, B = frac(c[:, i]), frac(a[:, i]), frac(b[:, i])
+        ex = C + A * B
+        err = abs(frac(z[:, i]) - ex)
+        assert err <= Fraction(1, 2 ** 210) * (abs(C) + abs(A * B))
+        if i >= 500 and ex:
+            assert err <= Fraction(1, 2 ** 208) * abs(ex)
+    # the fused sequence is the canonical one minus the product renormalisation: on
+    # DD-valued inputs (two zero words) both agree with the exact value within the DD bound
+    da = np.vstack([a[:2], np.zeros((2, n))]); db = np.vstack([b[:2], np.zeros((2, n))])
+    zf = orc.qd_op("madd_fused", np.zeros((4, n)), da, db)
+    for i in range(0, n, 5):
+        ex = frac(da[:, i]) * frac(db[:, i])
+        assert abs(frac(zf[:, i]) - ex) <= 16 * EPS_QD * abs(ex)

@@ -310,3 +310,28 @@ def test_accurate_variant_rejections(orc):
         orc.lu(A, panel=4, madd="accurate")
     with pytest.raises(ValueError):
         orc.gemm(A, A, orc.BLOCK | orc.MADD_FUSED | orc.ADD_ACCURATE)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_fused_madd_qd_gemm_vs_exact(orc, algo):
+    """Fused QD madd variant (row f3): every algorithm within 18^d 2^-200 l |A||B| of the
+    exact product; integer inputs exact; Block == Simple."""
+    for (m, l, n, T) in [(13, 11, 15, 3), (9, 16, 7, 1)]:
+        A = gen.qd_matrix(m, l, m + 11, 0)
+        B = gen.qd_matrix(l, n, m + 11, 1)
+        C = orc.gemm(A, B, algo, threshold=T, madd="fused")
+        E = exact_product(A, B)
+        d = 0 if algo == "block" else rec_depth(m, l, n, T)
+        nA = max(abs(frac(A[:, i, k])) for i in range(m) for k in range(l))
+        nB = max(abs(frac(B[:, k, j])) for k in range(l) for j in range(n))
+        bound = Fraction(18) ** d * Fraction(1, 2 ** 200) * l * nA * nB
+        for i in range(m):
+            for j in range(n):
+                assert abs(frac(C[:, i, j]) - E[i][j]) <= bound
+    rng = np.random.default_rng(5)
+    Ai = _int_mat(4, 17, 9, rng)
+    Bi = _int_mat(4, 9, 13, rng)
+    assert np.array_equal(orc.gemm(Ai, Bi, algo, 2, madd="fused")[0], Ai[0] @ Bi[0])
+    if algo == "block":
+        A = gen.qd_matrix(20, 20, 2, 0)
+        assert np.array_equal(orc.gemm(A, A, "block", bs=3, madd="fused"), orc.gemm(A, A, "block", madd="fused"))
