@@ -27,6 +27,9 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+GEMM_METRIC = "DD/QD GEMM effective GFLOPS (2mln/s) and % FP64-pipe roofline"
+LU_METRIC = "DD LU effective GFLOPS (2n^3/3 per solve / s)"
+
 WORKLOADS = {
     "c1": dict(W=2, algo="strassen", T=128, m=1024, l=1024, n=1024, seed=2,
                name="BJ configs[1]: DD Strassen GEMM 1024^3, threshold 128 (depth 3), seed 2"),
@@ -175,11 +178,13 @@ def reference_arm(args, wl, rank, world):
     value = 2.0 * ms * ls * ns * args.steps / tot / 1e9
     cores = cpu_cores()
     line = {
-        "impl": "reference", "metric": "effective GFLOPS (2mln/s)", "value": value, "unit": "GFLOP/s",
+        "impl": "reference", "metric": GEMM_METRIC, "value": value, "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": MAD_DTYPE[wl["W"]], "data": "synthetic (seeded, BJ recipe)",
-        "config": {"workload": wl["name"], "sample": desc},
+        "vs_baseline": None, "dtype": MAD_DTYPE[wl["W"]], "data": "synthetic (seeded SplitMix64, BASELINE.json recipe)",
+        "config": {"workload": wl["name"], "m": wl["m"], "l": wl["l"], "n": wl["n"], "algo": wl["algo"],
+                   "threshold": wl["T"], "madd": "canonical", "parallelism": "oracle on the host cores",
+                   "sample": desc},
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -206,11 +211,12 @@ def reference_lu(args, wl, orc):
     value = 2.0 / 3.0 * n ** 3 * args.steps / tot / 1e9
     desc = f"oracle LU+solve, n={n} (c4 recipe, panel {wl['panel']}, {wl['algo']} T={wl['T']})"
     print(json.dumps({
-        "impl": "reference", "metric": "DD LU effective GFLOPS (2n^3/3 per solve / s)", "value": value,
+        "impl": "reference", "metric": LU_METRIC, "value": value,
         "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": MAD_DTYPE[2], "data": "synthetic (seeded, BJ recipe)",
-        "config": {"workload": wl["name"], "sample": desc},
+        "vs_baseline": None, "dtype": MAD_DTYPE[2], "data": "synthetic (seeded SplitMix64, BASELINE.json recipe)",
+        "config": {"workload": wl["name"], "n": wl["n"], "panel": wl["panel"], "algo": wl["algo"],
+                   "threshold": wl["T"], "parallelism": "oracle on the host cores", "sample": desc},
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cpu_cores(), "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
     return 0
@@ -282,7 +288,7 @@ def lu_bench(args, wl, rank, world, local):
     dominant = max(shares, key=shares.get)
     if rank == 0:
         line = {
-            "metric": "DD LU effective GFLOPS (2n^3/3 per solve / s)", "value": value, "unit": "GFLOP/s",
+            "metric": LU_METRIC, "value": value, "unit": "GFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
             "dtype": MAD_DTYPE[2], "representation": REPR[2], "data": "synthetic (seeded SplitMix64, BASELINE.json recipe)",
@@ -476,7 +482,7 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": "DD/QD GEMM effective GFLOPS (2mln/s) and % FP64-pipe roofline",
+            "metric": GEMM_METRIC,
             "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": MAD_DTYPE[W], "representation": REPR[W],
