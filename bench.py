@@ -393,7 +393,10 @@ def main():
 
     # roofline of the dominant kernel: the batched leaf GEMM (FP64-pipe bound)
     leaf_ms, leaf_n, leaf_madds = prof["leaf"]
-    ops = OPS_PER_MADD[W] if args.madd == "canonical" else 15
+    # FP64 lane-ops per madd of the selected arithmetic (the QD variants' common-path counts
+    # are not fixed numbers; they are reported against the canonical 200)
+    ops = {"canonical": OPS_PER_MADD[W], "fused": 15 if W == 2 else OPS_PER_MADD[W],
+           "accurate": 29 if W == 2 else OPS_PER_MADD[W]}[args.madd]
     leaf_avg_s = (leaf_ms / leaf_n) * 1e-3 if leaf_n else float("nan")
     leaf_ops_per_launch = ops * leaf_madds / leaf_n if leaf_n else 0.0
     achieved = leaf_ops_per_launch / leaf_avg_s / 1e12 if leaf_n else 0.0

@@ -40,6 +40,36 @@ __global__ void __launch_bounds__(256, MINB) k_madd(double *out, int iters, doub
     if (s == 12345.678) out[blockIdx.x] = s;
 }
 
+// QD: CH accumulators, operands from shared memory (4 words each)
+template <int CH, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_qmadd(double *out, int iters, double s0) {
+    __shared__ double sa[4][64], sb[4][64];
+    if (threadIdx.x < 64) {
+        for (int w = 0; w < 4; w++) {
+            sa[w][threadIdx.x] = (s0 + 0.001 * threadIdx.x) * (w ? 1e-17 * w : 1.0);
+            sb[w][threadIdx.x] = (0.5 - 0.0001 * threadIdx.x) * (w ? -3e-18 * w : 1.0);
+        }
+    }
+    __syncthreads();
+    qd acc[CH];
+#pragma unroll
+    for (int j = 0; j < CH; j++) acc[j] = qd{{0.0, 0.0, 0.0, 0.0}};
+    for (int i = 0; i < iters; i++) {
+        const int r = (i + threadIdx.x) & 63;
+        qd a[2], b[2];
+#pragma unroll
+        for (int q = 0; q < 2; q++)
+#pragma unroll
+            for (int w = 0; w < 4; w++) { a[q].w[w] = sa[w][(r + q) & 63]; b[q].w[w] = sb[w][(r + 7 * q) & 63]; }
+#pragma unroll
+        for (int j = 0; j < CH; j++) acc[j] = qd_madd(acc[j], a[j / 2 % 2], b[j % 2]);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < CH; j++) s += acc[j].w[0] + acc[j].w[3];
+    if (s == 12345.678) out[blockIdx.x] = s;
+}
+
 __global__ void __launch_bounds__(256) k_dadd(double *out, int iters, double b) {
     double x[16];
 #pragma unroll
@@ -87,5 +117,17 @@ int main() {
     run("madd CH=8  MINB=4", k_madd<8, 4>, 8, 4);
     run("madd CH=4  MINB=4", k_madd<4, 4>, 4, 4);
     run("madd CH=32 MINB=1", k_madd<32, 1>, 32, 1);
+    // QD: count 200 FP64 lane-ops per madd (the common-path count ncu confirmed in the leaf)
+    auto runq = [&](const char *name, auto kern, int ch, int ctas_per_sm) {
+        const int blocks = sms * ctas_per_sm * 4;
+        const double ms = time_ms([&] { kern<<<blocks, 256>>>(out, iters / 4, 1.0); });
+        const double rate = (double)blocks * 256 * (iters / 4) * ch * 200 / (ms * 1e-3);
+        printf("%-28s %.3f T lane-ops/s = %.3f of the DADD stream  (%s)\n", name, rate / 1e12,
+               rate / dadd_rate, cudaGetErrorString(cudaGetLastError()));
+    };
+    runq("qd madd CH=4 MINB=2", k_qmadd<4, 2>, 4, 2);
+    runq("qd madd CH=2 MINB=2", k_qmadd<2, 2>, 2, 2);
+    runq("qd madd CH=4 MINB=1", k_qmadd<4, 1>, 4, 1);
+    runq("qd madd CH=8 MINB=1", k_qmadd<8, 1>, 8, 1);
     return 0;
 }
