@@ -431,6 +431,111 @@ __global__ void __launch_bounds__(1024) lu_trsm_kernel(double *A, int64_t n, int
     }
 }
 
+// Warp-per-column U12 := L11^{-1} A12 (default for kb <= 256). Every column of U12 is an
+// independent forward substitution, so one warp owns one column: lane t holds rows
+// r = t + 32q (q < RPL) in registers; at step i the owner of row i broadcasts it with
+// shuffles and every lane updates its rows r > i -- a_ri := a_ri - l_ri * a_ii in i order,
+// the same per-element sequence as lu_trsm_kernel and the oracle, with no CTA barrier per
+// step. L11's columns stream through a double-buffered shared-memory ring (cp.async, 8-byte
+// granules written transposed so the lanes' reads are conflict-free), CH columns per stage.
+// warps (= columns) per CTA: 16 for DD; 8 for QD, whose 8 four-word rows per lane need
+// more than the 128 registers a 512-thread CTA allows
+template <int W> struct TrsmWpb { static constexpr int v = W == 2 ? 16 : 8; };
+template <int W> struct TrsmCh { static constexpr int v = W == 2 ? 16 : 8; };   // 2 x 64 KB ring
+
+__device__ __forceinline__ void lu_cp_async8(void *smem, const void *gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void lu_cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void lu_cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+template <int W, int RPL>
+__global__ void __launch_bounds__(TrsmWpb<W>::v * 32) lu_trsm_warp_kernel(double *A, int64_t n, int64_t p,
+                                                                     int kb, int64_t c0, int64_t ncols) {
+    using E = elem<W>;
+    using T = typename E::T;
+    constexpr int CH = TrsmCh<W>::v;
+    extern __shared__ double Ls[];   // [2][W][CH][kb]: word w of l_{p+r, p+i0+ii} at [b][w][ii][r]
+    const int lane = threadIdx.x & 31, wrp = threadIdx.x >> 5;
+    const int64_t col = c0 + (int64_t)blockIdx.x * TrsmWpb<W>::v + wrp;
+    const bool active = col < c0 + ncols;
+    const int SS = CH * kb, BUF = W * SS;
+    const int nst = (kb + CH - 1) / CH;
+    auto issue = [&](int st) {   // stage st = L11 columns [st*CH, st*CH + ch) into buffer st & 1
+        if (st < nst) {
+            const int i0 = st * CH, ch = kb - i0 < CH ? kb - i0 : CH;
+            double *buf = Ls + (st & 1) * BUF;
+            for (int e = threadIdx.x; e < ch * kb; e += blockDim.x) {
+                const int r = e / ch, ii = e % ch;   // consecutive threads walk a row of L11
+                const double *src = A + (p + r) * n + (p + i0 + ii);
+#pragma unroll
+                for (int w = 0; w < W; w++) lu_cp_async8(buf + w * SS + ii * kb + r, src + (int64_t)w * n * n);
+            }
+        }
+        lu_cp_commit();   // possibly empty: keeps the group count uniform
+    };
+    issue(0);
+    issue(1);
+    T v[RPL];
+#pragma unroll
+    for (int q = 0; q < RPL; q++) {
+        const int r = lane + 32 * q;
+        v[q] = (active && r < kb) ? ldA<W>(A, n, p + r, col) : E::zero();
+    }
+    // i = 32 qq + h: the owner slot qq of row i is a compile-time index (a runtime-indexed
+    // pick would put v[] in local memory)
+#pragma unroll
+    for (int qq = 0; qq < RPL; qq++) {
+        if (32 * qq >= kb) break;
+        for (int h = 0; h < 32; h += CH) {
+            const int i0 = 32 * qq + h;
+            if (i0 >= kb) break;
+            const int st = i0 / CH;
+            const int ch = kb - i0 < CH ? kb - i0 : CH;
+            lu_cp_wait1();     // stage st has landed (only st + 1 may still be in flight)
+            __syncthreads();
+            const double *buf = Ls + (st & 1) * BUF;
+            // every warp runs the steps (a warp past the last column works on zeros and stores
+            // nothing), so the shuffles are never under a divergent branch
+            for (int ii = 0; ii < ch; ii++) {
+                const int i = i0 + ii;
+                const double *lrow = buf + ii * kb;
+                T x;
+#pragma unroll
+                for (int w = 0; w < W; w++) E::set_word(x, w, __shfl_sync(0xffffffffu, E::word(v[qq], w), h + ii));
+                // rows of slots q > qq are all below row i: unmasked straight-line updates (the
+                // chains interleave); only slot qq (rows <= i keep their value) and a ragged last
+                // slot (rows >= kb) are masked
+#pragma unroll
+                for (int q = qq; q < RPL; q++) {
+                    if (32 * q >= kb) break;
+                    const bool full = 32 * q + 32 <= kb;
+                    const int r = lane + 32 * q;
+                    const int rc = full ? r : (r < kb ? r : kb - 1);
+                    T l;
+#pragma unroll
+                    for (int w = 0; w < W; w++) E::set_word(l, w, lrow[w * SS + rc]);
+                    const T nv = E::sub(v[q], E::mul(l, x));
+                    if (q == qq) {
+                        if (lane > h + ii && r < kb) v[q] = nv;
+                    } else if (full || r < kb) {
+                        v[q] = nv;
+                    }
+                }
+            }
+            __syncthreads();   // every warp is done with buffer st & 1
+            issue(st + 2);
+        }
+    }
+    if (!active) return;
+#pragma unroll
+    for (int q = 0; q < RPL; q++) {
+        const int r = lane + 32 * q;
+        if (r < kb) stA<W>(A, n, p + r, col, v[q]);
+    }
+}
+
 // ---- solves ----------------------------------------------------------------------------------
 // y := P b (ipiv swaps applied in order), in shared memory when it fits.
 __global__ void __launch_bounds__(1024) lu_perm_kernel(const double *b, double *y, const int64_t *ipiv,
@@ -619,6 +724,17 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
     return 1;
 }
 
+// DDQD_LU_TRSM=strip selects the row-parallel strip kernel (one CTA barrier per step) for
+// every panel width; default: the warp-per-column kernel when kb <= 256.
+static bool trsm_warp_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_LU_TRSM");
+        v = (e && std::string(e) == "strip") ? 0 : 1;
+    }
+    return v == 1;
+}
+
 // Steps 1-2 of numerics.md s.5 for the panel [p, p+kb): factorisation (cooperative kernel or
 // the per-column pair), interchanges of the other columns, U12 := L11^{-1} A12.
 template <int W>
@@ -651,8 +767,21 @@ static int lu_panel_w(int64_t n, int pivot, double *A, int64_t *ipiv, int64_t p,
                                              (int)smem));
     if (kb > 1024) { set_error("panel > 1024 not supported by the TRSM kernel"); return DDQD_ENOTSUP; }
     prof_begin(4, s);
-    const int tthreads = (int)(((kb + 31) / 32) * 32);
-    lu_trsm_kernel<W><<<(unsigned)((n2 + cw - 1) / cw), tthreads, smem, s>>>(A, n, p, kb, p + kb, cw);
+    if (kb <= 256 && trsm_warp_enabled()) {
+        const size_t wsmem = sizeof(double) * 2 * W * (size_t)TrsmCh<W>::v * kb;
+        static bool wattr[64] = {};   // set once per device to the largest ring (kb = 256)
+        if (!wattr[current_device()]) {
+            DDQD_CUDA_CHECK(cudaFuncSetAttribute(lu_trsm_warp_kernel<W, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)(sizeof(double) * 2 * W * TrsmCh<W>::v * 256)));
+            wattr[current_device()] = true;
+        }
+        constexpr int WPB = TrsmWpb<W>::v;
+        lu_trsm_warp_kernel<W, 8><<<(unsigned)((n2 + WPB - 1) / WPB), WPB * 32, wsmem, s>>>(
+            A, n, p, (int)kb, p + kb, n2);
+    } else {
+        const int tthreads = (int)(((kb + 31) / 32) * 32);
+        lu_trsm_kernel<W><<<(unsigned)((n2 + cw - 1) / cw), tthreads, smem, s>>>(A, n, p, kb, p + kb, cw);
+    }
     DDQD_LAUNCH_CHECK();
     prof_end(4, (double)kb * (double)kb / 2.0 * (double)n2, s);
     return DDQD_OK;
