@@ -536,6 +536,148 @@ __global__ void __launch_bounds__(TrsmWpb<W>::v * 32) lu_trsm_warp_kernel(double
     }
 }
 
+// Blocked U12 := L11^{-1} A12 (default for kb <= 256). A CTA keeps a strip of TB_CW columns
+// of U12 in shared memory and walks L11 in 32-row blocks b:
+//   (a) the 32x32 diagonal block: one warp per column, lane = row, shuffles broadcast the
+//       finished row (32 dependent steps);
+//   (b) every row below the block takes the block's 32 updates, in i order, from registers:
+//       a thread owns one column and up to TB_RPT rows, so each step is TB_RPT independent
+//       DD chains fed by one broadcast x and TB_RPT multipliers from a staged L11 chunk.
+// Element (r, c) still receives a_rc := a_rc - l_ri * u_ic for i = 0 .. r-1 ascending, the
+// oracle's forward substitution, so the result is bit-identical to lu_trsm_kernel.
+constexpr int TB_NT = 256;    // threads per CTA (8 warps: TB_CW / 8 columns each in phase (a))
+constexpr int TB_LC = 8;      // L11 columns per off-diagonal stage
+template <int W, int KB, int TB_CW>   // TB_CW columns per CTA: 16, or 8 to spread small panels
+__global__ void __launch_bounds__(TB_NT) lu_trsm_blk_kernel(double *A, int64_t n, int64_t p,
+                                                            int64_t c0, int64_t ncols) {
+    constexpr int TB_G = TB_NT / TB_CW;          // row groups in phase (b)
+    constexpr int TB_RPT = (KB - 32 + TB_G - 1) / TB_G;   // rows per thread in phase (b)
+    constexpr int kb = KB;   // compile-time panel width: every block's row count below is static,
+                             // so phase (b)'s TB_RPT chains are straight-line code
+    using E = elem<W>;
+    using T = typename E::T;
+    extern __shared__ double sm[];
+    double *Us = sm;                                  // [W][kb][TB_CW]
+    double *Ld = Us + (size_t)W * kb * TB_CW;         // [W][32][32]: Ld[w][i][r]
+    double *Lo = Ld + (size_t)W * 32 * 32;            // [W][TB_LC][224]: Lo[w][ii][r']
+    const int US = kb * TB_CW, LDS_ = 32 * 32, LOS = TB_LC * 224;
+    const int tid = threadIdx.x, lane = tid & 31, wrp = tid >> 5;
+    const int64_t col0 = c0 + (int64_t)blockIdx.x * TB_CW;
+    const int nc = (int)((c0 + ncols - col0) < TB_CW ? (c0 + ncols - col0) : TB_CW);
+
+    for (int e = tid; e < kb * TB_CW; e += TB_NT) {
+        const int r = e / TB_CW, c = e % TB_CW;
+        const T v = c < nc ? ldA<W>(A, n, p + r, col0 + c) : E::zero();
+#pragma unroll
+        for (int w = 0; w < W; w++) Us[w * US + r * TB_CW + c] = E::word(v, w);
+    }
+#pragma unroll
+    for (int b0 = 0; b0 < kb; b0 += 32) {
+        constexpr int bs = 32;   // KB is a multiple of 32
+        __syncthreads();   // Us rows of the previous block complete; Ld free
+        for (int e = tid; e < bs * bs; e += TB_NT) {
+            const int r = e / bs, i = e % bs;
+            const T l = ldA<W>(A, n, p + b0 + r, p + b0 + i);
+#pragma unroll
+            for (int w = 0; w < W; w++) Ld[w * LDS_ + i * 32 + r] = E::word(l, w);
+        }
+        __syncthreads();
+        // (a) diagonal block: warp wrp solves columns wrp (and wrp + 8), lane = row b0 + lane
+        {
+            const int ca = wrp, cb = TB_CW > 8 ? wrp + 8 : wrp;
+            T va = E::zero(), vb = E::zero();
+            if (lane < bs) {
+#pragma unroll
+                for (int w = 0; w < W; w++) {
+                    E::set_word(va, w, Us[w * US + (b0 + lane) * TB_CW + ca]);
+                    E::set_word(vb, w, Us[w * US + (b0 + lane) * TB_CW + cb]);
+                }
+            }
+            for (int i = 0; i < bs; i++) {
+                T xa, xb, l;
+#pragma unroll
+                for (int w = 0; w < W; w++) {
+                    E::set_word(xa, w, __shfl_sync(0xffffffffu, E::word(va, w), i));
+                    E::set_word(xb, w, __shfl_sync(0xffffffffu, E::word(vb, w), i));
+                    E::set_word(l, w, Ld[w * LDS_ + i * 32 + lane]);
+                }
+                const T na = E::sub(va, E::mul(l, xa));
+                const T nb = E::sub(vb, E::mul(l, xb));
+                if (lane > i && lane < bs) { va = na; vb = nb; }
+            }
+            if (lane < bs) {
+#pragma unroll
+                for (int w = 0; w < W; w++) {
+                    Us[w * US + (b0 + lane) * TB_CW + ca] = E::word(va, w);
+                    if (TB_CW > 8) Us[w * US + (b0 + lane) * TB_CW + cb] = E::word(vb, w);
+                }
+            }
+        }
+        // (b) rows below the block: thread = (column c, row group g), rows rb + g + TB_G k
+        const int rb = b0 + bs, R = kb - rb;   // compile-time after unrolling
+        if (R <= 0) continue;
+        const int c = tid % TB_CW, g = tid / TB_CW;
+        T v[TB_RPT];
+        __syncthreads();   // (a) results visible
+#pragma unroll
+        for (int k = 0; k < TB_RPT; k++) {
+            const int r = g + TB_G * k;
+            v[k] = E::zero();
+            if (r < R) {
+#pragma unroll
+                for (int w = 0; w < W; w++) E::set_word(v[k], w, Us[w * US + (rb + r) * TB_CW + c]);
+            }
+        }
+        for (int i0 = 0; i0 < bs; i0 += TB_LC) {
+            const int lc = bs - i0 < TB_LC ? bs - i0 : TB_LC;
+            __syncthreads();   // previous chunk consumed
+            for (int e = tid; e < R * lc; e += TB_NT) {
+                const int r = e / lc, ii = e % lc;
+                const T l = ldA<W>(A, n, p + rb + r, p + b0 + i0 + ii);
+#pragma unroll
+                for (int w = 0; w < W; w++) Lo[w * LOS + ii * 224 + r] = E::word(l, w);
+            }
+            __syncthreads();
+            for (int ii = 0; ii < lc; ii++) {
+                const int i = b0 + i0 + ii;
+                T x;
+#pragma unroll
+                for (int w = 0; w < W; w++) E::set_word(x, w, Us[w * US + i * TB_CW + c]);
+#pragma unroll
+                for (int k = 0; k < TB_RPT; k++) {
+                    const int r = g + TB_G * k;
+                    if (TB_G * k < R) {   // compile-time skip of whole empty row slots
+                        const int rr = r < R ? r : R - 1;
+                        T l;
+#pragma unroll
+                        for (int w = 0; w < W; w++) E::set_word(l, w, Lo[w * LOS + ii * 224 + rr]);
+                        const T nv = E::sub(v[k], E::mul(l, x));
+                        if (r < R) v[k] = nv;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < TB_RPT; k++) {
+            const int r = g + TB_G * k;
+            if (r < R) {
+#pragma unroll
+                for (int w = 0; w < W; w++) Us[w * US + (rb + r) * TB_CW + c] = E::word(v[k], w);
+            }
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < kb * TB_CW; e += TB_NT) {
+        const int r = e / TB_CW, cc = e % TB_CW;
+        if (cc < nc) {
+            T v;
+#pragma unroll
+            for (int w = 0; w < W; w++) E::set_word(v, w, Us[w * US + r * TB_CW + cc]);
+            stA<W>(A, n, p + r, col0 + cc, v);
+        }
+    }
+}
+
 // ---- solves ----------------------------------------------------------------------------------
 // y := P b (ipiv swaps applied in order), in shared memory when it fits.
 __global__ void __launch_bounds__(1024) lu_perm_kernel(const double *b, double *y, const int64_t *ipiv,
@@ -725,14 +867,15 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
 }
 
 // DDQD_LU_TRSM=strip selects the row-parallel strip kernel (one CTA barrier per step) for
-// every panel width; default: the warp-per-column kernel when kb <= 256.
-static bool trsm_warp_enabled() {
+// every panel width, =warp the warp-per-column kernel; default: the blocked kernel for
+// 256-wide panels (c4's), the warp-per-column kernel for other widths <= 256.
+static int trsm_mode() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("DDQD_LU_TRSM");
-        v = (e && std::string(e) == "strip") ? 0 : 1;
+        v = (e && std::string(e) == "strip") ? 0 : (e && std::string(e) == "warp") ? 1 : 2;
     }
-    return v == 1;
+    return v;
 }
 
 // Steps 1-2 of numerics.md s.5 for the panel [p, p+kb): factorisation (cooperative kernel or
@@ -767,7 +910,20 @@ static int lu_panel_w(int64_t n, int pivot, double *A, int64_t *ipiv, int64_t p,
                                              (int)smem));
     if (kb > 1024) { set_error("panel > 1024 not supported by the TRSM kernel"); return DDQD_ENOTSUP; }
     prof_begin(4, s);
-    if (kb <= 256 && trsm_warp_enabled()) {
+    if (kb == 256 && trsm_mode() == 2) {
+        // 16-column strips while they fill ~1.5 waves of the SMs, else 8 (twice the CTAs, each
+        // with half the chain): the per-CTA chain, not the FP64 rate, bounds small panels
+        static bool battr[2][64] = {};
+        const bool wide = (n2 + 15) / 16 >= 222;
+        const size_t bsmem = sizeof(double) * W * ((size_t)256 * (wide ? 16 : 8) + 32 * 32 + (size_t)TB_LC * 224);
+        auto kfn = wide ? lu_trsm_blk_kernel<W, 256, 16> : lu_trsm_blk_kernel<W, 256, 8>;
+        if (!battr[wide][current_device()]) {
+            DDQD_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
+            battr[wide][current_device()] = true;
+        }
+        const int cw = wide ? 16 : 8;
+        kfn<<<(unsigned)((n2 + cw - 1) / cw), TB_NT, bsmem, s>>>(A, n, p, p + kb, n2);
+    } else if (kb <= 256 && trsm_mode() >= 1) {
         const size_t wsmem = sizeof(double) * 2 * W * (size_t)TrsmCh<W>::v * kb;
         static bool wattr[64] = {};   // set once per device to the largest ring (kb = 256)
         if (!wattr[current_device()]) {
