@@ -685,16 +685,24 @@ __global__ void __launch_bounds__(1024) lu_perm_kernel(const double *b, double *
     extern __shared__ double sy[];
     double *buf = use_smem ? sy : y;
     for (int64_t i = threadIdx.x; i < (int64_t)W * n; i += blockDim.x) buf[i] = b[i];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int64_t k = 0; k < n; k++) {
-            const int64_t r = ipiv[k];
-            if (r != k)
-                for (int w = 0; w < W; w++) {
-                    const double t = buf[w * n + k];
-                    buf[w * n + k] = buf[w * n + r];
-                    buf[w * n + r] = t;
-                }
+    // the swaps are applied in order by one thread; ipiv is staged through shared memory in
+    // chunks first so that thread does not pay a global-memory round trip per entry
+    __shared__ long long piv_s[2048];
+    for (int64_t k0 = 0; k0 < n; k0 += 2048) {
+        const int kc = (int)((n - k0) < 2048 ? (n - k0) : 2048);
+        __syncthreads();
+        for (int k = threadIdx.x; k < kc; k += blockDim.x) piv_s[k] = ipiv[k0 + k];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int k = 0; k < kc; k++) {
+                const int64_t kk = k0 + k, r = piv_s[k];
+                if (r != kk)
+                    for (int w = 0; w < W; w++) {
+                        const double t = buf[w * n + kk];
+                        buf[w * n + kk] = buf[w * n + r];
+                        buf[w * n + r] = t;
+                    }
+            }
         }
     }
     __syncthreads();
@@ -785,6 +793,154 @@ __global__ void trsv_bwd_update(const double *A, int64_t n, double *y, const dou
     T v = ldv<W>(y, n, i);
     for (int t = nb - 1; t >= 0; t--) v = E::sub(v, E::mul(ldA<W>(A, n, i, J + t), lds<W>(xs, 256, t)));
     stv<W>(y, n, i, v);
+}
+
+// ---- blocked diagonal solves and coalesced updates (default when nb % 32 == 0) ---------------
+// A diagonal block [J, J+nb) is walked in 32-row sub-blocks (forward: ascending, backward:
+// descending). Warp 0 solves the sub-block's 32x32 triangle with shuffles (lane = row; forward
+// broadcasts the finished row, backward forms x_t = div(y_t, u_tt) on the owner and broadcasts
+// it); then every thread that owns a row outside the sub-block (below it going forward, above it
+// going backward) folds the sub-block's 32 products into its row in the numerics.md s.5 order,
+// with its 32 multipliers loaded up front (independent of the chain). Same per-element
+// sequence as trsv_fwd_diag / trsv_bwd_diag and the oracle.
+template <int W, bool FWD>
+__global__ void __launch_bounds__(256) trsv_diag_blk(const double *A, int64_t n, double *y, double *x,
+                                                     int64_t J, int nb) {
+    using E = elem<W>;
+    using T = typename E::T;
+    constexpr int PL = W == 2 ? 32 : 8;   // multipliers preloaded per chunk (registers)
+    __shared__ double ys[W * 256];   // the block's y (forward) / x (backward) values
+    const int tid = threadIdx.x, lane = tid & 31, wrp = tid >> 5;
+    if (tid < nb) sts<W>(ys, 256, tid, ldv<W>(y, n, J + tid));
+    const int nsb = nb / 32;
+    for (int k = 0; k < nsb; k++) {
+        const int sb = FWD ? k : nsb - 1 - k;
+        const int b0 = 32 * sb;
+        __syncthreads();   // ys of the previous sub-block complete
+        if (wrp == 0) {
+            // the sub-block triangle: lane = row b0 + lane; multipliers PL columns at a time
+            T v = lds<W>(ys, 256, b0 + lane);
+#pragma unroll
+            for (int c = 0; c < 32 / PL; c++) {
+                const int s0 = FWD ? c * PL : 32 - (c + 1) * PL;
+                T l[PL];
+#pragma unroll
+                for (int i = 0; i < PL; i++) l[i] = ldA<W>(A, n, J + b0 + lane, J + b0 + s0 + i);
+#pragma unroll
+                for (int ss = 0; ss < PL; ss++) {
+                    const int i = FWD ? ss : PL - 1 - ss;
+                    const int t = s0 + i;
+                    T xt;
+                    if (FWD) {
+#pragma unroll
+                        for (int w = 0; w < W; w++) E::set_word(xt, w, __shfl_sync(0xffffffffu, E::word(v, w), t));
+                    } else {
+                        T u;   // u_tt, from lane t's multipliers
+#pragma unroll
+                        for (int w = 0; w < W; w++) E::set_word(u, w, __shfl_sync(0xffffffffu, E::word(l[i], w), t));
+                        const T d = E::div(v, u);
+#pragma unroll
+                        for (int w = 0; w < W; w++) E::set_word(xt, w, __shfl_sync(0xffffffffu, E::word(d, w), t));
+                        if (lane == t) v = xt;   // this lane's row is finished: it now holds x_t
+                    }
+                    const T nv = E::sub(v, E::mul(l[i], xt));
+                    if (FWD ? (lane > t) : (lane < t)) v = nv;
+                }
+            }
+            sts<W>(ys, 256, b0 + lane, v);
+        }
+        __syncthreads();
+        // rows outside the sub-block take its 32 products, in order
+        const int r = tid;
+        const bool mine = FWD ? (r >= b0 + 32 && r < nb) : (r < b0);
+        if (mine) {
+            T v = lds<W>(ys, 256, r);
+#pragma unroll
+            for (int c = 0; c < 32 / PL; c++) {
+                const int s0 = FWD ? c * PL : 32 - (c + 1) * PL;
+                T l[PL];
+#pragma unroll
+                for (int i = 0; i < PL; i++) l[i] = ldA<W>(A, n, J + r, J + b0 + s0 + i);
+#pragma unroll
+                for (int ss = 0; ss < PL; ss++) {
+                    const int i = FWD ? ss : PL - 1 - ss;
+                    v = E::sub(v, E::mul(l[i], lds<W>(ys, 256, b0 + s0 + i)));
+                }
+            }
+            sts<W>(ys, 256, r, v);
+        }
+    }
+    __syncthreads();
+    if (tid < nb) stv<W>(FWD ? y : x, n, J + tid, lds<W>(ys, 256, tid));
+}
+
+// Coalesced off-diagonal update: 128 rows per CTA, the block's columns staged TU_CC at a time
+// through a double-buffered cp.async ring (row segments read contiguously, stored transposed
+// with padding), each thread folding its row in the numerics.md s.5 order (forward: j
+// ascending into y; backward: j descending, with x).
+constexpr int TU_ROWS = 128, TU_LD = TU_ROWS + 1;
+template <int W> struct TuCc { static constexpr int v = W == 2 ? 32 : 16; };   // 2 x ~66 KB ring
+template <int W, bool FWD>
+__global__ void __launch_bounds__(TU_ROWS) trsv_update_co(const double *A, int64_t n, double *y,
+                                                          const double *x, int64_t J, int nb) {
+    using E = elem<W>;
+    using T = typename E::T;
+    constexpr int TU_CC = TuCc<W>::v;
+    constexpr int LS = TU_CC * TU_LD, BUF = W * LS;
+    extern __shared__ double sm[];
+    double *vs = sm;                              // [W][256] the block's y (fwd) or x (bwd)
+    double *Lt = sm + W * 256;                    // [2][W][TU_CC][TU_LD]
+    const double *src = FWD ? y : x;
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) sts<W>(vs, 256, t, ldv<W>(src, n, J + t));
+    const int64_t r0 = (FWD ? J + nb : 0) + (int64_t)blockIdx.x * TU_ROWS;
+    const int64_t rend = FWD ? n : J;
+    const int nr = (int)((rend - r0) < TU_ROWS ? (rend - r0) : TU_ROWS);
+    const int me = threadIdx.x;
+    const int nch = (nb + TU_CC - 1) / TU_CC;
+    auto chunk_c0 = [&](int ch, int *cc_n) {
+        const int cs = ch * TU_CC;
+        *cc_n = nb - cs < TU_CC ? nb - cs : TU_CC;
+        return FWD ? cs : nb - cs - *cc_n;   // backward: chunks from the right
+    };
+    auto issue = [&](int ch) {
+        if (ch < nch) {
+            int cc_n;
+            const int c0 = chunk_c0(ch, &cc_n);
+            double *buf = Lt + (ch & 1) * BUF;
+            for (int e = threadIdx.x; e < nr * TU_CC; e += blockDim.x) {
+                const int r = e / TU_CC, cc = e % TU_CC;
+                if (cc < cc_n) {
+                    const double *g = A + (r0 + r) * n + (J + c0 + cc);
+#pragma unroll
+                    for (int w = 0; w < W; w++) lu_cp_async8(buf + w * LS + cc * TU_LD + r, g + (int64_t)w * n * n);
+                }
+            }
+        }
+        lu_cp_commit();
+    };
+    issue(0);
+    issue(1);
+    T v = me < nr ? ldv<W>(y, n, r0 + me) : E::zero();
+    __syncthreads();   // vs
+    for (int ch = 0; ch < nch; ch++) {
+        int cc_n;
+        const int c0 = chunk_c0(ch, &cc_n);
+        lu_cp_wait1();
+        __syncthreads();
+        const double *buf = Lt + (ch & 1) * BUF;
+        if (me < nr) {
+            for (int k = 0; k < cc_n; k++) {
+                const int cc = FWD ? k : cc_n - 1 - k;
+                T a;
+#pragma unroll
+                for (int w = 0; w < W; w++) E::set_word(a, w, buf[w * LS + cc * TU_LD + me]);
+                v = E::sub(v, E::mul(a, lds<W>(vs, 256, c0 + cc)));
+            }
+        }
+        __syncthreads();
+        issue(ch + 2);
+    }
+    if (me < nr) stv<W>(y, n, r0 + me, v);
 }
 
 // ---- host driver -------------------------------------------------------------------------------
@@ -943,6 +1099,17 @@ static int lu_panel_w(int64_t n, int pivot, double *A, int64_t *ipiv, int64_t p,
     return DDQD_OK;
 }
 
+// DDQD_LU_TRSV=plain keeps the one-thread-per-row diagonal kernels and uncoalesced updates
+// (the reference schedule); default: warp-level diagonal blocks + coalesced updates.
+static bool trsv_fast_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_LU_TRSV");
+        v = (e && std::string(e) == "plain") ? 0 : 1;
+    }
+    return v == 1;
+}
+
 // Eq. (2) with the factors: y := P b, forward (unit L), backward (numerics.md s.5).
 template <int W>
 static int lu_trsv_w(int64_t n, const double *A, const int64_t *ipiv, const double *b, double *x, double *y,
@@ -956,11 +1123,28 @@ static int lu_trsv_w(int64_t n, const double *A, const int64_t *ipiv, const doub
     lu_perm_kernel<<<1, 1024, psmem, s>>>(b, y, ipiv, W, n, use_smem);
     DDQD_LAUNCH_CHECK();
     const int NB = 256;
+    const bool fast = trsv_fast_enabled();
+    const size_t usm = sizeof(double) * W * (256 + 2 * (size_t)TuCc<W>::v * TU_LD);
+    static bool tattr[64] = {};
+    if (fast && !tattr[current_device()]) {
+        DDQD_CUDA_CHECK(cudaFuncSetAttribute(trsv_update_co<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
+        DDQD_CUDA_CHECK(cudaFuncSetAttribute(trsv_update_co<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
+        tattr[current_device()] = true;
+    }
     for (int64_t J = 0; J < n; J += NB) {
         const int nb = (int)std::min<int64_t>(NB, n - J);
+        const int64_t rows = n - J - nb;
+        if (fast && nb % 32 == 0) {
+            trsv_diag_blk<W, true><<<1, 256, 0, s>>>(A, n, y, nullptr, J, nb);
+            DDQD_LAUNCH_CHECK();
+            if (rows > 0) {
+                trsv_update_co<W, true><<<(unsigned)((rows + TU_ROWS - 1) / TU_ROWS), TU_ROWS, usm, s>>>(A, n, y, nullptr, J, nb);
+                DDQD_LAUNCH_CHECK();
+            }
+            continue;
+        }
         trsv_fwd_diag<W><<<1, 256, 0, s>>>(A, n, y, J, nb);
         DDQD_LAUNCH_CHECK();
-        const int64_t rows = n - J - nb;
         if (rows > 0) {
             trsv_fwd_update<W><<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(A, n, y, J, nb);
             DDQD_LAUNCH_CHECK();
@@ -969,6 +1153,15 @@ static int lu_trsv_w(int64_t n, const double *A, const int64_t *ipiv, const doub
     const int64_t last = ((n - 1) / NB) * NB;
     for (int64_t J = last; J >= 0; J -= NB) {
         const int nb = (int)std::min<int64_t>(NB, n - J);
+        if (fast && nb % 32 == 0) {
+            trsv_diag_blk<W, false><<<1, 256, 0, s>>>(A, n, y, x, J, nb);
+            DDQD_LAUNCH_CHECK();
+            if (J > 0) {
+                trsv_update_co<W, false><<<(unsigned)((J + TU_ROWS - 1) / TU_ROWS), TU_ROWS, usm, s>>>(A, n, y, x, J, nb);
+                DDQD_LAUNCH_CHECK();
+            }
+            continue;
+        }
         trsv_bwd_diag<W><<<1, 256, 0, s>>>(A, n, y, x, J, nb);
         DDQD_LAUNCH_CHECK();
         if (J > 0) {
