@@ -199,6 +199,18 @@ def test_c3_full_size_sampled(orc):
     assert np.abs(err).max() <= bound * 2.0 ** -10     # typical error is far inside the bound
 
 
+def test_c3_full_size_bitwise(orc):
+    """BJ:10 (config 3) at its full size, DD Winograd 8191 x 8193 x 8190, T = 256 (depth 5),
+    seed 4, as bench.py runs it: the whole product bit-identical to the oracle's recursion
+    (~2 minutes of the oracle on the host cores)."""
+    m, l, n, T = 8191, 8193, 8190, 256
+    A = gen.dd_matrix(m, l, 4, 0)
+    B = gen.dd_matrix(l, n, 4, 1)
+    got = np_(ddqd.dd_gemm(cu(A), cu(B), "winograd", T))
+    ref = orc.gemm(A, B, "winograd", threshold=T)
+    assert same(got, ref)
+
+
 def test_host_pointer_path_matches_device(orc):
     A = gen.dd_matrix(300, 257, 7, 0)
     B = gen.dd_matrix(257, 301, 7, 1)
@@ -307,6 +319,29 @@ def test_c4_lu_full_size_properties():
     xx = np_(x)
     err = np.abs((xx[0] - 1.0) + xx[1]).max()
     assert err <= 2.0 ** -96 * n * 3 * 18
+
+
+def test_c4_lu_full_size_bitwise(orc):
+    """BJ:11 (config 4) at its full size, n = 4096, panel 256, Strassen update (T = 128), in the
+    launch configuration bench.py times: factors, pivots and x bit-identical to the oracle's
+    (the LU cannot be sampled entry by entry, so the whole oracle LU runs on the host cores)."""
+    n = 4096
+    A = gen.lu_matrix(n, 5)
+    b = _b_ones(orc, A).copy()
+    x_ref, LU_ref, piv_ref, info_ref = orc.solve(A, b, panel=256, algo="strassen", threshold=128)
+    x, LU, piv, info = ddqd.dd_lu_solve(cu(A), cu(b), panel=256, algo="strassen", threshold=128)
+    assert info == info_ref == 0
+    assert np.array_equal(np_(piv), piv_ref)
+    assert same(np_(LU), LU_ref) and same(np_(x), x_ref)
+
+
+def test_c2_qd_winograd_full_size_bitwise(orc):
+    """BJ:9 (config 2) at its full size, QD Winograd 1024^3, T = 128, seed 3, as bench.py runs
+    it: every entry bit-identical to the oracle's recursion."""
+    A = gen.qd_matrix(1024, 1024, 3, 0)
+    B = gen.qd_matrix(1024, 1024, 3, 1)
+    got = np_(ddqd.qd_gemm(cu(A), cu(B), "winograd", 128))
+    assert same(got, orc.gemm(A, B, "winograd", threshold=128))
 
 
 # ---- multi-GPU schedule's CUDA backend, world size 1 (one GPU available) ---------------
