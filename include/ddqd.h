@@ -126,6 +126,27 @@ typedef struct {
 int ddqd_pre_add(int prec, int algo, int side, int64_t P, const ddqd_mat *X, const ddqd_mat *Y);
 int ddqd_post_add(int prec, int algo, int64_t P, const ddqd_mat *M, const ddqd_mat *C, int beta);
 
+/* The multi-GPU fused combine: one recursion level's post-additions with the
+ * 7P children given as a DEVICE array of 7P pointers (child c of parent b at children[7b + c];
+ * each a planar W-word hm x hn matrix: word w of (i, j) at child[w*ps + i*ld + j]). The
+ * pointers may be CUDA IPC mappings of other GPUs' buffers, so the gather over NVLink and the
+ * DD/QD combination run in one kernel. Only position rows [r0, r1) are formed: C quadrant rows
+ * i and i + hm of every parent (cropped to C; C = P parents as in ddqd_post_add; beta = 1
+ * subtracts). hm, hn must be ceil(C rows / 2), ceil(C cols / 2). Asynchronous. */
+int ddqd_post_add_ptrs(int prec, int algo, int64_t P, const double *const *children, int64_t hm, int64_t hn,
+                       int64_t ld, int64_t ps, int64_t r0, int64_t r1, const ddqd_mat *C, int beta);
+
+/* CUDA IPC plumbing for that combine: ddqd_ipc_alloc allocates a device buffer (cudaMalloc,
+ * so it is exportable as a whole); ddqd_ipc_handle writes its 64-byte cudaIpcMemHandle_t;
+ * another process maps it with ddqd_ipc_open (peer access enabled lazily) and unmaps it with
+ * ddqd_ipc_close; ddqd_ipc_free releases the owner's allocation. DDQD_ENOMEM / DDQD_ECUDA on
+ * failure (message in ddqd_last_error). */
+int ddqd_ipc_alloc(size_t bytes, void **ptr);
+int ddqd_ipc_free(void *ptr);
+int ddqd_ipc_handle(const void *ptr, void *handle64);
+int ddqd_ipc_open(const void *handle64, void **ptr);
+int ddqd_ipc_close(void *ptr);
+
 /*
  * dd_lu_solve -- blocked right-looking LU with partial pivoting (P:121-133 steps 1-3,
  * pivoting per BJ:11) and the solve of Eq. (2), DD only.

@@ -64,6 +64,12 @@ def _load():
     L.ddqd_lu_solve.argtypes = [i32, i32, i64, vp, vp, vp, vp, i64, i32, i64]
     L.ddqd_elementwise.argtypes = [i32, i32, i64, vp, vp, vp, vp]
     L.ddqd_lu_panel.argtypes = [i32, i32, i64, vp, vp, i64, i64]
+    L.ddqd_post_add_ptrs.argtypes = [i32, i32, i64, vp, i64, i64, i64, i64, i64, i64, ctypes.POINTER(Mat), i32]
+    L.ddqd_ipc_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]
+    L.ddqd_ipc_free.argtypes = [vp]
+    L.ddqd_ipc_handle.argtypes = [vp, ctypes.c_char_p]
+    L.ddqd_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+    L.ddqd_ipc_close.argtypes = [vp]
     L.ddqd_lu_trsv.argtypes = [i32, i64, vp, vp, vp, vp]
     L.ddqd_set_stream.argtypes = [vp]
     L.ddqd_workspace_bytes.argtypes = [i32, i64, i64, i64, i32, i64]
@@ -82,7 +88,8 @@ def _load():
 lib = _load()
 
 EXPORTED = ["dd_gemm", "qd_gemm", "ddqd_gemm_ex", "dd_lu_solve", "qd_lu_solve", "ddqd_lu_solve",
-            "ddqd_lu_panel", "ddqd_lu_trsv", "ddqd_elementwise", "ddqd_set_stream",
+            "ddqd_lu_panel", "ddqd_lu_trsv", "ddqd_post_add_ptrs", "ddqd_ipc_alloc", "ddqd_ipc_free",
+            "ddqd_ipc_handle", "ddqd_ipc_open", "ddqd_ipc_close", "ddqd_elementwise", "ddqd_set_stream",
             "ddqd_workspace_bytes", "ddqd_set_workspace", "ddqd_set_workspace_limit",
             "ddqd_launch_count", "ddqd_release", "ddqd_last_error", "ddqd_version",
             "ddqd_profile_start", "ddqd_profile_stop", "ddqd_fp64_peak", "ddqd_pre_add", "ddqd_post_add"]
@@ -205,6 +212,72 @@ def post_add(algo, M, C, beta=0, madd="canonical"):
     _set_stream(C)
     mm, cc = batch_mat(M), batch_mat(C)
     _check(lib.ddqd_post_add(W, _add_algo(algo, madd), P, ctypes.byref(mm), ctypes.byref(cc), beta), "post_add")
+
+
+def post_add_ptrs(algo, children, C, r0=0, r1=None, beta=0, madd="canonical"):
+    """One level's post-additions reading the 7P children through device pointers
+    (ddqd_post_add_ptrs): children = list of 7P CUDA tensors [W, hm, hn] (same shape and strides;
+    they may be IPC mappings of other GPUs' memory), C = [P, W, r, c] or [W, r, c]; position rows
+    [r0, r1) only."""
+    torch = _torch()
+    P = 1 if C.dim() == 3 else C.shape[0]
+    if len(children) != 7 * P:
+        raise ValueError("need 7 children per parent")
+    W, hm, hn = children[0].shape
+    ld, ps = children[0].stride(1), children[0].stride(0)
+    ptrs = torch.tensor([t.data_ptr() for t in children], dtype=torch.int64, device=C.device)
+    _set_stream(C)
+    cc = batch_mat(C)
+    rc = lib.ddqd_post_add_ptrs(W, _add_algo(algo, madd), P, ptrs.data_ptr(), hm, hn, ld, ps, r0,
+                                hm if r1 is None else r1, ctypes.byref(cc), beta)
+    _check(rc, "post_add_ptrs")
+    return ptrs   # keep alive until the kernel ran (caller synchronises)
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a raw device allocation (for torch.as_tensor)."""
+
+    def __init__(self, ptr, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def ipc_alloc(shape, device):
+    """A float64 CUDA tensor in its own cudaMalloc allocation (exportable with ipc_handle);
+    returns (tensor, raw pointer). Free with ipc_free(pointer) after the tensor is dropped."""
+    torch = _torch()
+    n = 1
+    for d in shape:
+        n *= int(d)
+    p = ctypes.c_void_p()
+    with torch.cuda.device(device):
+        _check(lib.ddqd_ipc_alloc(8 * max(n, 1), ctypes.byref(p)), "ipc_alloc")
+        t = torch.as_tensor(_CudaArray(p.value, shape), device=device)
+    return t, p.value
+
+
+def ipc_free(ptr):
+    _check(lib.ddqd_ipc_free(ctypes.c_void_p(ptr)), "ipc_free")
+
+
+def ipc_handle(ptr) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    _check(lib.ddqd_ipc_handle(ctypes.c_void_p(ptr), buf), "ipc_handle")
+    return buf.raw
+
+
+def ipc_open(handle: bytes, shape, device):
+    """Map another process's ipc_alloc buffer; returns (tensor view, raw pointer)."""
+    torch = _torch()
+    p = ctypes.c_void_p()
+    with torch.cuda.device(device):
+        _check(lib.ddqd_ipc_open(handle, ctypes.byref(p)), "ipc_open")
+        t = torch.as_tensor(_CudaArray(p.value, shape), device=device)
+    return t, p.value
+
+
+def ipc_close(ptr):
+    _check(lib.ddqd_ipc_close(ctypes.c_void_p(ptr)), "ipc_close")
 
 
 def gemm_batched(A, B, C, algo, threshold, beta=0, madd="canonical"):

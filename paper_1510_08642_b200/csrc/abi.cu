@@ -384,6 +384,61 @@ int ddqd_release(void) {
 
 const char *ddqd_last_error(void) { return t_err.c_str(); }
 
+int ddqd_post_add_ptrs(int prec, int algo, int64_t P, const double *const *children, int64_t hm, int64_t hn,
+                       int64_t ld, int64_t ps, int64_t r0, int64_t r1, const ddqd_mat *C, int beta) {
+    t_err.clear();
+    const int a = algo & ~DDQD_ADD_ACCURATE;
+    if ((prec != 2 && prec != 4) || (a != 1 && a != 2) || P < 0 || !children || !C || (beta != 0 && beta != 1) ||
+        hm < 0 || hn < 0 || ld < hn || r0 < 0 || r1 < r0 || r1 > hm) {
+        set_error("bad post_add_ptrs arguments");
+        return DDQD_EINVAL;
+    }
+    if (hm != (C->rows + 1) / 2 || hn != (C->cols + 1) / 2) {
+        set_error("post_add_ptrs: product shape must be ceil(parent/2)");
+        return DDQD_EINVAL;
+    }
+    return launch_post_add_ptrs(prec, algo, P, children, hm, hn, ld, ps, r0, r1, to_desc(C), beta, t_stream);
+}
+
+// CUDA IPC plumbing for the multi-GPU combine (buffers other processes map and read/write)
+int ddqd_ipc_alloc(size_t bytes, void **ptr) {
+    t_err.clear();
+    if (!ptr) { set_error("null pointer"); return DDQD_EINVAL; }
+    *ptr = nullptr;
+    const cudaError_t e = cudaMalloc(ptr, bytes ? bytes : 256);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        return DDQD_ENOMEM;
+    }
+    return DDQD_OK;
+}
+int ddqd_ipc_free(void *ptr) {
+    DDQD_CUDA_CHECK(cudaFree(ptr));
+    return DDQD_OK;
+}
+int ddqd_ipc_handle(const void *ptr, void *handle64) {
+    t_err.clear();
+    if (!ptr || !handle64) { set_error("null pointer"); return DDQD_EINVAL; }
+    cudaIpcMemHandle_t h;
+    DDQD_CUDA_CHECK(cudaIpcGetMemHandle(&h, const_cast<void *>(ptr)));
+    static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+    memcpy(handle64, &h, sizeof(h));
+    return DDQD_OK;
+}
+int ddqd_ipc_open(const void *handle64, void **ptr) {
+    t_err.clear();
+    if (!ptr || !handle64) { set_error("null pointer"); return DDQD_EINVAL; }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof(h));
+    DDQD_CUDA_CHECK(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return DDQD_OK;
+}
+int ddqd_ipc_close(void *ptr) {
+    DDQD_CUDA_CHECK(cudaIpcCloseMemHandle(ptr));
+    return DDQD_OK;
+}
+
 int ddqd_version(void) { return 100; }
 
 }  // extern "C"

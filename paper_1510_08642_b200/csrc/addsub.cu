@@ -345,6 +345,66 @@ int launch_post_add(int W, int algo, int64_t P, const MatDesc &M, const MatDesc 
     return acc ? post_dispatch<4, 2>(algo, P, M, C, beta, s) : post_dispatch<4, 0>(algo, P, M, C, beta, s);
 }
 
+// ---- post-addition over peer memory (the multi-GPU fused combine) --------
+// Same combination as post_add_kernel, but the 7P children are addressed through a device
+// array of pointers (each a W-plane hm x hn matrix with row stride ld and plane stride ps) --
+// on a multi-GPU node they live on other GPUs and are read over NVLink (CUDA IPC mappings), so
+// the gather and the DD/QD combine are one kernel -- and only the position rows [r0, r1) are
+// formed (each rank assembles its share of C). Parent b's C quadrant rows sit at i and i + hm.
+template <int W, int ALGO, int V>
+__global__ void __launch_bounds__(256) post_add_ptr_kernel(int64_t P, const double *const *ch, int64_t hm,
+                                                           int64_t hn, int64_t ld, int64_t ps, int64_t r0,
+                                                           int64_t r1, MatDesc C, int beta) {
+    using E = arith<W, V>;
+    using T = typename E::T;
+    const int64_t rows = r1 - r0;
+    const int64_t per = rows * hn;
+    const int64_t total = P * per;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = t / per, rem = t % per, i = r0 + rem / hn, j = rem % hn;
+        T p[7];
+#pragma unroll
+        for (int c = 0; c < 7; c++) p[c] = E::load(ch[7 * b + c] + i * ld + j, ps);
+        T c11, c12, c21, c22;
+        post_ops<E, ALGO>(p, c11, c12, c21, c22);
+        double *cb = C.p + b * C.bs;
+        const bool r2 = i + hm < C.rows, cc2 = j + hn < C.cols;
+        auto put = [&](int64_t r, int64_t c, const T &v) {
+            double *q = cb + r * C.ld + c;
+            if (beta) E::store(q, C.ps, E::sub(E::load(q, C.ps), v));
+            else E::store(q, C.ps, v);
+        };
+        if (i < C.rows && j < C.cols) put(i, j, c11);
+        if (i < C.rows && cc2) put(i, j + hn, c12);
+        if (r2 && j < C.cols) put(i + hm, j, c21);
+        if (r2 && cc2) put(i + hm, j + hn, c22);
+    }
+}
+
+int launch_post_add_ptrs(int W, int algo, int64_t P, const double *const *ch, int64_t hm, int64_t hn,
+                         int64_t ld, int64_t ps, int64_t r0, int64_t r1, const MatDesc &C, int beta,
+                         cudaStream_t s) {
+    const int64_t total = P * (r1 - r0) * hn;
+    if (total <= 0) return DDQD_OK;
+    const bool acc = (algo & DDQD_ADD_ACCURATE) != 0;
+    algo &= 0xff;
+    const unsigned g = grid_for(total);
+    prof_begin(2, s);
+#define DDQD_PP(WW, AA, VV) post_add_ptr_kernel<WW, AA, VV><<<g, 256, 0, s>>>(P, ch, hm, hn, ld, ps, r0, r1, C, beta)
+    if (W == 2) {
+        if (algo == 1) { if (acc) DDQD_PP(2, 1, 2); else DDQD_PP(2, 1, 0); }
+        else { if (acc) DDQD_PP(2, 2, 2); else DDQD_PP(2, 2, 0); }
+    } else {
+        if (algo == 1) { if (acc) DDQD_PP(4, 1, 2); else DDQD_PP(4, 1, 0); }
+        else { if (acc) DDQD_PP(4, 2, 2); else DDQD_PP(4, 2, 0); }
+    }
+#undef DDQD_PP
+    DDQD_LAUNCH_CHECK();
+    prof_end(2, (double)total * W * 8.0 * (beta ? 15.0 : 11.0), s);
+    return DDQD_OK;
+}
+
 // ---- elementwise arithmetic layer (parity tests of ddqd_arith.cuh) ---------------------
 template <int W>
 __global__ void elementwise_kernel(int op, int64_t count, const double *x, const double *y,

@@ -63,6 +63,10 @@ int launch_pre_add2(int W, int algo, int side, int64_t P, const MatDesc &X, int6
                     int64_t h1c, const MatDesc &Y, cudaStream_t s);
 int launch_post_add2(int W, int algo, int64_t P, const MatDesc &M, int64_t h1m, int64_t h1n,
                      const MatDesc &C, int beta, cudaStream_t s);
+// Post-addition with the 7P children addressed through a device pointer array (peer memory).
+int launch_post_add_ptrs(int W, int algo, int64_t P, const double *const *ch, int64_t hm, int64_t hn,
+                         int64_t ld, int64_t ps, int64_t r0, int64_t r1, const MatDesc &C, int beta,
+                         cudaStream_t s);
 int launch_elementwise(int W, int op, int64_t count, const double *x, const double *y,
                        const double *w, double *z, cudaStream_t s);
 

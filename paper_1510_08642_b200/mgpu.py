@@ -86,6 +86,26 @@ class CudaBackend:
     def post_add(self, algo, M, C, beta=0):
         self.ddqd.post_add(algo, M, C, beta)
 
+    def sync(self):
+        import torch
+        torch.cuda.synchronize()
+
+    def ipc_alloc(self, shape, like):
+        t, ptr = self.ddqd.ipc_alloc(shape, like.device)
+        return t, self.ddqd.ipc_handle(ptr), ptr
+
+    def ipc_open(self, handle, shape, like):
+        return self.ddqd.ipc_open(handle, shape, like.device)
+
+    def ipc_close(self, ptr):
+        self.ddqd.ipc_close(ptr)
+
+    def ipc_free(self, ptr):
+        self.ddqd.ipc_free(ptr)
+
+    def post_add_ptrs(self, algo, children, C, r0, r1):
+        return self.ddqd.post_add_ptrs(algo, children, C, r0, r1)
+
     def lu_panel(self, A, ipiv, p, kb, pivot):
         return self.ddqd.lu_panel(A, ipiv, p, kb, pivot)
 
@@ -112,8 +132,19 @@ class DistributedGemm:
     """C := A B (beta = 0) or C := C - A B (beta = 1) across the process group `dist` (rank 0
     holds the operands and C; C may be a strided view with unit-stride rows)."""
 
-    def __init__(self, W, algo, T, m, l, n, dist, device=None, k=None, backend=None, chunk=None, beta=0):
+    def __init__(self, W, algo, T, m, l, n, dist, device=None, k=None, backend=None, chunk=None, beta=0,
+                 combine="nccl", replicated_inputs=False):
         self.W, self.algo, self.T, self.beta = W, algo, T, beta
+        # combine = "nccl": products stream to rank 0 over NCCL point-to-point, rank 0 post-adds;
+        # "p2p": products stay resident, the post-adds read peers' buffers through CUDA IPC
+        # mappings (fused gather + combine kernels, levels split over the ranks, each rank writes
+        # its rows of C straight into rank 0's C buffer). beta = 1 needs combine = "nccl".
+        if combine not in ("nccl", "p2p"):
+            raise ValueError("combine must be 'nccl' or 'p2p'")
+        if combine == "p2p" and beta:
+            raise ValueError("the p2p combine computes C := A B (beta = 0)")
+        self.combine = combine
+        self.replicated_inputs = replicated_inputs   # every rank already holds A and B
         self.m, self.l, self.n = m, l, n
         self.dist = dist
         self.rank = dist.get_rank()
@@ -132,6 +163,12 @@ class DistributedGemm:
             self.slices = balanced_slices(m, self.world)          # C row slabs
             self.per = max(hi - lo for lo, hi in self.slices)
         self._bufs = None
+        self._p2p = None
+        if self.k > 0:
+            # p2p combine: parents of level j (1 <= j < k) split over the ranks; level 0 (C)
+            # split by position rows of the level-1 products
+            self.pslices = {j: balanced_slices(7 ** j, self.world) for j in range(1, self.k)}
+            self.rslices = balanced_slices(self.shapes[1][0], self.world)
 
     # buffers are allocated lazily on the operands' device
     def _alloc(self, like):
@@ -168,8 +205,11 @@ class DistributedGemm:
 
     def __call__(self, A, B, C):
         dist, W = self.dist, self.W
-        dist.broadcast(A, 0)
-        dist.broadcast(B, 0)
+        if not self.replicated_inputs:
+            dist.broadcast(A, 0)
+            dist.broadcast(B, 0)
+        if self.k > 0 and self.combine == "p2p":
+            return self._p2p_call(A, B, C)
         bufs = self._alloc(A)
         if self.k == 0:
             return self._row_slabs(A, B, C, bufs)
@@ -218,6 +258,128 @@ class DistributedGemm:
             for q in sends:
                 q.wait()
         return C
+
+    # ---- p2p combine ----------------------------------------------------------------------------
+    def _owner(self, level, p):
+        """(rank, offset) holding product/parent p of `level` (k: products; 1..k-1: parents)."""
+        sl = self.slices if level == self.k else self.pslices[level]
+        for r, (lo, hi) in enumerate(sl):
+            if lo <= p < hi:
+                return r, p - lo
+        raise IndexError(p)
+
+    def _p2p_setup(self, like):
+        if self._p2p is not None:
+            return self._p2p
+        W, bk, dist = self.W, self.backend, self.dist
+        local, handles, frees = {}, {}, []
+        for level in range(1, self.k + 1):
+            mj, _, nj = self.shapes[level]
+            sl = self.slices if level == self.k else self.pslices[level]
+            cnt = max(1, max(hi - lo for lo, hi in sl))
+            t, h, f = bk.ipc_alloc((cnt, W, mj, nj), like)
+            local[level], handles[level] = t, h
+            frees.append(f)
+        if self.rank == 0:
+            t, h, f = bk.ipc_alloc((W, self.m, self.n), like)
+            local["C"], handles["C"] = t, h
+            frees.append(f)
+        allh = [None] * self.world
+        dist.all_gather_object(allh, handles)
+        views, closes = {}, []
+        for level in range(1, self.k + 1):
+            mj, _, nj = self.shapes[level]
+            sl = self.slices if level == self.k else self.pslices[level]
+            for r in range(self.world):
+                if r == self.rank:
+                    views[(level, r)] = local[level]
+                else:
+                    cnt = max(1, max(hi - lo for lo, hi in sl))
+                    v, c = bk.ipc_open(allh[r][level], (cnt, W, mj, nj), like)
+                    views[(level, r)] = v
+                    closes.append(c)
+        if self.rank == 0:
+            views["C"] = local["C"]
+        else:
+            v, c = bk.ipc_open(allh[0]["C"], (W, self.m, self.n), like)
+            views["C"] = v
+            closes.append(c)
+        self._p2p = {"local": local, "views": views, "frees": frees, "closes": closes}
+        return self._p2p
+
+    def _p2p_call(self, A, B, C):
+        """Products stay where they are computed; the k levels of post-additions read them (and
+        each other's level results) over peer memory, each level split over the ranks; the last
+        level writes every rank's rows of C into rank 0's buffer."""
+        dist, bk, W, k = self.dist, self.backend, self.W, self.k
+        st = self._p2p_setup(A)
+        bufs = self._alloc_operands(A)
+        X, Y = A, B
+        for j in range(k):
+            a, b = self._ancestor_range(j)
+            if b > a:
+                Xs = X if j == 0 else X[a:b]
+                Ys = Y if j == 0 else Y[a:b]
+                bk.pre_add(self.algo, 0, Xs, bufs["A"][j][7 * a:7 * b])
+                bk.pre_add(self.algo, 1, Ys, bufs["B"][j][7 * a:7 * b])
+            X, Y = bufs["A"][j], bufs["B"][j]
+        lo, hi = self.slices[self.rank]
+        Mk = st["local"][k]
+        for c0 in range(lo, hi, self.chunk):
+            c1 = min(hi, c0 + self.chunk)
+            bk.gemm_batched(X[c0:c1], Y[c0:c1], Mk[c0 - lo:c1 - lo], self.algo, self.T)
+        keep = []
+        for j in range(k - 1, -1, -1):
+            bk.sync()
+            dist.barrier()            # level j+1 complete on every rank
+            if j > 0:
+                a, b = self.pslices[j][self.rank]
+                if b > a:
+                    children = []
+                    for q in range(a, b):
+                        for c in range(7):
+                            o, off = self._owner(j + 1, 7 * q + c)
+                            children.append(st["views"][(j + 1, o)][off])
+                    keep.append(bk.post_add_ptrs(self.algo, children, st["local"][j][:b - a], 0, None))
+            else:
+                r0, r1 = self.rslices[self.rank]
+                if r1 > r0:
+                    children = []
+                    for c in range(7):
+                        o, off = self._owner(1, c)
+                        children.append(st["views"][(1, o)][off])
+                    keep.append(bk.post_add_ptrs(self.algo, children, st["views"]["C"], r0, r1))
+        bk.sync()
+        dist.barrier()                # every rank's rows of C are in rank 0's buffer
+        if self.rank == 0:
+            C.copy_(st["local"]["C"])
+        return C
+
+    def _alloc_operands(self, like):
+        """Operand buffers of the top-k pre-additions (no product buffers: p2p keeps those)."""
+        if getattr(self, "_opbufs", None) is None:
+            W, bk = self.W, self.backend
+            ob = {"A": [], "B": []}
+            for j in range(1, self.k + 1):
+                mj, lj, nj = self.shapes[j]
+                ob["A"].append(bk.empty((7 ** j, W, mj, lj), like))
+                ob["B"].append(bk.empty((7 ** j, W, lj, nj), like))
+            self._opbufs = ob
+        return self._opbufs
+
+    def release(self):
+        """Unmap peers' buffers and free this rank's exported buffers (p2p combine)."""
+        if self._p2p is not None:
+            self.backend.sync()
+            self.dist.barrier()       # nobody reads a buffer that is about to go away
+            for c in self._p2p["closes"]:
+                self.backend.ipc_close(c)
+            self._p2p["views"].clear()
+            self._p2p["local"].clear()
+            self.dist.barrier()
+            for f in self._p2p["frees"]:
+                self.backend.ipc_free(f)
+            self._p2p = None
 
     def _row_slabs(self, A, B, C, bufs):
         r0, r1 = self.slices[self.rank]

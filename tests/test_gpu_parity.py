@@ -694,3 +694,33 @@ def test_distributed_lu_cuda_backend_world1(orc, algo):
         assert np.array_equal(np_(ipiv), pr)
     finally:
         dist.destroy_process_group()
+
+
+# ---- fused p2p combine over CUDA IPC mappings (row e) -------------------------------------------
+@pytest.mark.parametrize("cfg,world", [
+    ((2, "winograd", 32, 301, 257, 299, 1), 2),
+    ((2, "strassen", 16, 200, 203, 190, 2), 3),
+    ((4, "winograd", 16, 130, 129, 131, 2), 2),
+])
+def test_p2p_combine_cuda_ipc_bitwise(orc, cfg, world):
+    """DistributedGemm(combine='p2p') with 2-3 processes on this GPU: every process computes its
+    depth-k products into its own cudaMalloc buffer, the post-addition levels read them through
+    CUDA IPC mappings (ddqd_post_add_ptrs), split over the processes, and each writes its rows
+    of C into rank 0's buffer: bit-identical to the single-GPU recursion and the oracle."""
+    import multiprocessing as pymp
+    import socket
+    from tests import _p2p_worker
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    ctx = pymp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_p2p_worker.run, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    k, C = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+    assert k != "error", C
+    assert all(p.exitcode == 0 for p in procs)
+    W, algo, T, m, l, n, _ = cfg
+    ref = orc.gemm(gen.matrix(W, m, l, 31, 0), gen.matrix(W, l, n, 31, 1), algo, threshold=T)
+    assert k >= 1 and same(C, ref)

@@ -40,6 +40,52 @@ class OracleBackend:
     def empty_i64(self, n, like):
         return torch.empty(n, dtype=torch.int64)
 
+    # "peer memory" for the p2p combine: files in /dev/shm mapped by every process
+    _count = 0
+
+    def sync(self):
+        pass
+
+    def ipc_alloc(self, shape, like):
+        OracleBackend._count += 1
+        path = f"/dev/shm/ddqd_p2p_{os.getpid()}_{OracleBackend._count}"
+        n = int(np.prod(shape))
+        t = torch.from_file(path, shared=True, size=n, dtype=torch.float64).view(*shape)
+        return t, (path, n), path
+
+    def ipc_open(self, handle, shape, like):
+        path, n = handle
+        return torch.from_file(path, shared=True, size=n, dtype=torch.float64).view(*shape), None
+
+    def ipc_close(self, c):
+        pass
+
+    def ipc_free(self, path):
+        os.remove(path)
+
+    def post_add_ptrs(self, algo, children, C, r0, r1):
+        """Position rows [r0, r1) of the one-level post-addition, children given as tensors."""
+        add = lambda a, b: self._ew("add", a, b)   # noqa: E731
+        sub = lambda a, b: self._ew("sub", a, b)   # noqa: E731
+        Cv = C if C.dim() == 4 else C.unsqueeze(0)
+        hm, hn = children[0].shape[-2], children[0].shape[-1]
+        r1 = hm if r1 is None else r1
+        rr, cc = Cv.shape[-2], Cv.shape[-1]
+        for b in range(Cv.shape[0]):
+            p = [np.ascontiguousarray(children[7 * b + c].numpy()[:, r0:r1, :]) for c in range(7)]
+            if algo == "strassen":
+                q = [add(sub(add(p[0], p[3]), p[4]), p[6]), add(p[2], p[4]), add(p[1], p[3]),
+                     add(add(sub(p[0], p[1]), p[2]), p[5])]
+            else:
+                u2 = add(p[0], p[5]); u3 = add(u2, p[6]); u4 = add(u2, p[4])
+                q = [add(p[0], p[1]), add(u4, p[2]), sub(u3, p[3]), add(u3, p[4])]
+            for quad, (dr, dc) in enumerate(((0, 0), (0, hn), (hm, 0), (hm, hn))):
+                ra, rb = r0 + dr, min(r1 + dr, rr)
+                ca, cb = dc, min(hn + dc, cc)
+                if rb > ra and cb > ca:
+                    Cv[b, :, ra:rb, ca:cb] = torch.from_numpy(np.ascontiguousarray(q[quad][:, : rb - ra, : cb - ca]))
+        return None
+
     def lu_panel(self, A, ipiv, p, kb, pivot):
         return self.o.lu_panel(A.numpy(), ipiv.numpy(), p, kb, pivot)
 
@@ -109,7 +155,7 @@ class OracleBackend:
         out[:, : r1 - r0, :] = torch.from_numpy(t)
 
 
-def _worker(rank, world, port, cfg, q, chunk=None):
+def _worker(rank, world, port, cfg, q, chunk=None, combine="nccl"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -118,20 +164,23 @@ def _worker(rank, world, port, cfg, q, chunk=None):
         A = torch.from_numpy(gen.matrix(W, m, l, 21, 0)) if rank == 0 else torch.zeros((W, m, l), dtype=torch.float64)
         B = torch.from_numpy(gen.matrix(W, l, n, 21, 1)) if rank == 0 else torch.zeros((W, l, n), dtype=torch.float64)
         C = torch.zeros((W, m, n), dtype=torch.float64)
-        dg = DistributedGemm(W, algo, T, m, l, n, dist, k=k, backend=OracleBackend(W), chunk=chunk)
+        dg = DistributedGemm(W, algo, T, m, l, n, dist, k=k, backend=OracleBackend(W), chunk=chunk,
+                             combine=combine)
         dg(A, B, C)
         dg(A, B, C)    # buffers are reused across steps
         if rank == 0:
             q.put((dg.k, C.numpy().copy()))
+        if combine == "p2p":
+            dg.release()
     finally:
         dist.destroy_process_group()
 
 
-def _run(cfg, world=2, chunk=None):
+def _run(cfg, world=2, chunk=None, combine="nccl"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q, chunk)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q, chunk, combine)) for r in range(world)]
     for p in procs:
         p.start()
     k, C = q.get(timeout=300)
@@ -240,3 +289,20 @@ def test_distributed_lu_matches_single_process(orc, cfg, world):
     assert np.array_equal(ipiv, pr)
     assert np.array_equal(LU.view(np.int64), LUr.view(np.int64))
     assert np.array_equal(x.view(np.int64), xr.view(np.int64))
+
+
+
+@pytest.mark.parametrize("cfg,world", [
+    ((2, "winograd", 4, 37, 29, 33, 1), 2),     # one level over peer memory
+    ((2, "strassen", 3, 40, 41, 42, 2), 3),     # two levels: parents split over 3 ranks
+    ((4, "winograd", 2, 19, 23, 17, 2), 2),     # QD
+])
+def test_p2p_combine_matches_single_process(orc, cfg, world):
+    """The fused p2p combine: products stay on their ranks, every level's
+    post-additions read them through (here: file-backed) shared mappings, split over the
+    ranks, and the ranks write their rows of C into rank 0's buffer -- bit-identical to the
+    single-process recursion."""
+    W, algo, T, m, l, n, _ = cfg
+    k, C = _run(cfg, world=world, combine="p2p")
+    ref = orc.gemm(gen.matrix(W, m, l, 21, 0), gen.matrix(W, l, n, 21, 1), algo, threshold=T)
+    assert k >= 1 and np.array_equal(C.view(np.int64), ref.view(np.int64))
