@@ -121,12 +121,12 @@ class Clocks:
 
 # ---- CPU oracle sample (cpu_baseline and --impl reference) ----------------------------
 def oracle_sample(wl):
-    """Bounded sample of the workload for the oracle: the leading (m/4, l/4, n/4) block
-    (same recipe, same algorithm and threshold) for c3; the full problem for c1; the leading
-    (m/2, l/2, n/2) block for c2. Returns (A, B, shape, description)."""
+    """Bounded sample of the workload for the oracle (~10-20 s of host work for c3): the
+    leading (m/2, l/2, n/2) block (same recipe, same algorithm and threshold) for c3; the full
+    problem for c1 and c2. Returns (A, B, shape, description)."""
     import ddqd_inputs as gen
     m, l, n = wl["m"], wl["l"], wl["n"]
-    div = {"c3": 4, "c2": 2, "c1": 1}[wl["key"]]
+    div = {"c3": 2, "c2": 1, "c1": 1}[wl["key"]]
     ms, ls, ns = (m + div - 1) // div, (l + div - 1) // div, (n + div - 1) // div
     A = gen.matrix(wl["W"], ms, ls, wl["seed"], 0)
     B = gen.matrix(wl["W"], ls, ns, wl["seed"], 1)
