@@ -137,7 +137,12 @@ def dd_abs_gt(x, y) -> bool:
 
 
 # ---- GEMM --------------------------------------------------------------------
-def gemm(A, B, algo="block", threshold=32, bs=0, nthreads=0, madd="canonical"):
+def splitk_flag(s: int) -> int:
+    """DDQD_SPLITK(s) algo bits (s in 1, 2, 4, 8)."""
+    return {1: 0, 2: 0x1000, 4: 0x2000, 8: 0x3000}[s]
+
+
+def gemm(A, B, algo="block", threshold=32, bs=0, nthreads=0, madd="canonical", splitk=1):
     """C := A B for planar [W, m, l] x [W, l, n] arrays (numerics.md s.4); madd='fused'
     selects the fused DD multiply-add variant (numerics.md s.2), madd='accurate' the
     accurate-add variant (every DD/QD addition accurate, numerics.md s.2-3)."""
@@ -147,7 +152,7 @@ def gemm(A, B, algo="block", threshold=32, bs=0, nthreads=0, madd="canonical"):
     if W != W2 or l != l2:
         raise ValueError("dimension mismatch")
     C = np.empty((W, m, n))
-    a = (ALGOS[algo] if isinstance(algo, str) else algo) | _VARIANT[madd]
+    a = (ALGOS[algo] if isinstance(algo, str) else algo) | _VARIANT[madd] | splitk_flag(splitk)
     rc = lib().or_gemm(W, a, threshold, bs,
                        m, l, n, _p(A), _p(B), _p(C), nthreads)
     if rc:

@@ -497,6 +497,46 @@ static void gemm_simple(const mat_t *A, const mat_t *B, mat_t *C) {
     }
 }
 
+static mat_t view(int W, int64_t rows, int64_t cols, int64_t ld, int64_t ps, const double *p);
+static mat_t mat_alloc(int W, int64_t rows, int64_t cols);
+static void mat_free(mat_t *m);
+
+/* numerics.md s.4 split-k leaf (variant DDQD_SPLITK(s)): the k range
+ * is cut into s contiguous slices of ceil(l/s) (the last ragged, possibly empty); each slice's
+ * partial product is the Simple sum from +0 over its k ascending; the s partials are combined
+ * by the fixed pairwise tree ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)) with the (variant's) add. */
+static int g_split = 1;
+
+static void gemm_splitk(const mat_t *A, const mat_t *B, mat_t *C, int s) {
+    int64_t m = A->rows, l = A->cols, n = B->cols, L = (l + s - 1) / s;
+    int W = A->W;
+    mat_t P[8];
+    for (int q = 0; q < s; q++) {
+        int64_t k0 = q * L < l ? q * L : l, k1 = (q + 1) * L < l ? (q + 1) * L : l;
+        P[q] = mat_alloc(W, m, n);
+        mat_t a = view(W, m, k1 - k0, A->ld, A->ps, A->p + k0);
+        mat_t b = view(W, k1 - k0, n, B->ld, B->ps, B->p + k0 * B->ld);
+        gemm_simple(&a, &b, &P[q]);   /* k1 == k0: all +0 */
+    }
+    for (int stride = 1; stride < s; stride *= 2)
+        for (int q = 0; q + stride < s; q += 2 * stride) {
+            mat_t t = mat_addsub(&P[q], &P[q + stride], 0);
+            g_block_adds--;   /* the split tree is not a Strassen/Winograd block addition */
+            mat_free(&P[q]);
+            P[q] = t;
+        }
+    for (int w = 0; w < W; w++)
+        for (int64_t i = 0; i < m; i++)
+            for (int64_t j = 0; j < n; j++) set_w(C, w, i, j, get_w(&P[0], w, i, j));
+    for (int q = 0; q < s; q++) if (P[q].p) mat_free(&P[q]);
+}
+
+/* the leaf of every algorithm: Simple, or its split-k variant */
+static void gemm_leaf(const mat_t *A, const mat_t *B, mat_t *C) {
+    if (g_split > 1) gemm_splitk(A, B, C, g_split);
+    else gemm_simple(A, B, C);
+}
+
 /* Block(bs): C_ij := sum_k A_ik B_kj over bs x bs pieces, k-blocks ascending,
  * accumulating into C in place, so each element still sees k ascending from +0. */
 static void gemm_block(const mat_t *A, const mat_t *B, mat_t *C, int64_t bs) {
@@ -546,7 +586,7 @@ static void gemm_rec(int algo, int64_t T, const mat_t *A, const mat_t *B, mat_t 
     int64_t m = A->rows, l = A->cols, n = B->cols;
     int64_t mn = m < l ? m : l;
     if (n < mn) mn = n;
-    if (mn <= T) { gemm_simple(A, B, C); return; }
+    if (mn <= T) { gemm_leaf(A, B, C); return; }
     int64_t hm = (m + 1) / 2, hl = (l + 1) / 2, hn = (n + 1) / 2;
     mat_t A11 = mat_quadrant(A, 0, 0, hm, hl), A12 = mat_quadrant(A, 0, hl, hm, hl);
     mat_t A21 = mat_quadrant(A, hm, 0, hm, hl), A22 = mat_quadrant(A, hm, hl, hm, hl);
@@ -609,7 +649,7 @@ static mat_t view(int W, int64_t rows, int64_t cols, int64_t ld, int64_t ps, con
 }
 
 static void gemm_any(int algo, int64_t T, const mat_t *A, const mat_t *B, mat_t *C) {
-    if (algo == 0) gemm_simple(A, B, C);
+    if (algo == 0) gemm_leaf(A, B, C);
     else gemm_rec(algo, T, A, B, C);
 }
 
@@ -619,7 +659,9 @@ static void gemm_any(int algo, int64_t T, const mat_t *A, const mat_t *B, mat_t 
 int or_gemm(int W, int algo, int64_t T, int64_t bs, int64_t m, int64_t l, int64_t n,
             const double *A, const double *B, double *C, int nthreads) {
     if ((algo & 0x100) && (algo & 0x200)) return -1;
+    if (algo & ~0x33ff) return -1;
     g_variant = (algo & 0x100) ? 1 : (algo & 0x200) ? 2 : 0;
+    g_split = 1 << ((algo >> 12) & 3);           /* DDQD_SPLITK: 1, 2, 4 or 8 */
     algo &= 0xff;
     if ((W != 2 && W != 4) || algo < 0 || algo > 2 || m < 0 || l < 0 || n < 0) return -1;
     if (algo != 0 && T < 1) return -1;
@@ -753,6 +795,7 @@ int or_lu(int W, int pivot, int64_t n, double *A, int64_t *ipiv, int64_t K, int 
      * arithmetic is the canonical one, so an accurate LU is not defined (rejected) */
     if (algo & 0x200) return -1;
     g_variant = (algo & 0x100) ? 1 : 0;
+    g_split = 1 << ((algo >> 12) & 3);
     algo &= 0xff;
     if ((W != 2 && W != 4) || n < 0 || K < 1) return -1;
 #ifdef _OPENMP

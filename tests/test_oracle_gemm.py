@@ -335,3 +335,49 @@ def test_fused_madd_qd_gemm_vs_exact(orc, algo):
     if algo == "block":
         A = gen.qd_matrix(20, 20, 2, 0)
         assert np.array_equal(orc.gemm(A, A, "block", bs=3, madd="fused"), orc.gemm(A, A, "block", madd="fused"))
+
+
+def test_splitk_tree_order_pin(orc):
+    """Split-k (numerics.md s.4, row a4): 1x4 . 4x1 DD products p = (1, 0, 2^-60 + 2^-120,
+    -2^-60). The pairwise tree (p0+p1)+(p2+p3) keeps the 2^-120 (1 + 2^-120 is a DD value);
+    the canonical k-ascending fold loses it when 2^-60 + 2^-120 meets 1 (121 bits). So
+    s = 2, 4, 8 give exactly 1 + 2^-120 and the canonical Block exactly 1."""
+    A = np.zeros((2, 1, 4)); A[0] = 1.0
+    B = np.zeros((2, 4, 1))
+    B[0, :, 0] = [1.0, 0.0, 2.0 ** -60, -2.0 ** -60]
+    B[1, 2, 0] = 2.0 ** -120
+    assert frac(orc.gemm(A, B, "block")[:, 0, 0]) == 1
+    for s in (2, 4, 8):
+        C = orc.gemm(A, B, "block", splitk=s)
+        assert list(C[:, 0, 0]) == [1.0, 2.0 ** -120], s
+
+
+@pytest.mark.parametrize("W", [2, 4])
+@pytest.mark.parametrize("algo", ALGOS)
+def test_splitk_vs_exact(orc, W, algo):
+    """Split-k leaves within 18^d 2^-96 l |A||B| (QD 2^-200) of the exact product for s = 2,
+    4, 8 including slices that are empty (l < s); integer inputs exact; s = 1 is the canonical
+    result; the count law is unchanged."""
+    base = 96 if W == 2 else 200
+    for (m, l, n, T, s) in [(9, 13, 7, 4, 4), (6, 3, 5, 2, 8), (16, 16, 16, 3, 2), (5, 1, 4, 1, 8)]:
+        A = gen.matrix(W, m, l, m + 13, 0)
+        B = gen.matrix(W, l, n, m + 13, 1)
+        C = orc.gemm(A, B, algo, threshold=T, splitk=s)
+        E = exact_product(A, B)
+        d = 0 if algo == "block" else rec_depth(m, l, n, T)
+        nA = max(abs(frac(A[:, i, k])) for i in range(m) for k in range(l))
+        nB = max(abs(frac(B[:, k, j])) for k in range(l) for j in range(n))
+        bound = Fraction(18) ** d * Fraction(1, 2 ** base) * l * nA * nB
+        for i in range(m):
+            for j in range(n):
+                assert abs(frac(C[:, i, j]) - E[i][j]) <= bound, (m, l, n, s)
+        assert np.array_equal(orc.gemm(A, B, algo, threshold=T, splitk=1), orc.gemm(A, B, algo, threshold=T))
+    rng = np.random.default_rng(8)
+    Ai = _int_mat(W, 17, 9, rng)
+    Bi = _int_mat(W, 9, 13, rng)
+    assert np.array_equal(orc.gemm(Ai, Bi, algo, 2, splitk=4)[0], Ai[0] @ Bi[0])
+    orc.reset_counters()
+    orc.gemm(gen.matrix(W, 16, 16, 1, 0), gen.matrix(W, 16, 16, 1, 1), algo, threshold=4, splitk=4)
+    madds, _ = orc.counters()
+    d = 0 if algo == "block" else rec_depth(16, 16, 16, 4)
+    assert madds == 7 ** d * (16 // 2 ** d) ** 3
