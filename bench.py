@@ -31,6 +31,8 @@ GEMM_METRIC = "DD/QD GEMM effective GFLOPS (2mln/s) and % FP64-pipe roofline"
 LU_METRIC = "DD LU effective GFLOPS (2n^3/3 per solve / s)"
 
 WORKLOADS = {
+    "c0": dict(W=2, algo="block", T=128, m=128, l=128, n=128, seed=1,
+               name="BJ configs[0]: DD Block GEMM 128^3, seed 1 (latency-bound; split-k variants)"),
     "c1": dict(W=2, algo="strassen", T=128, m=1024, l=1024, n=1024, seed=2,
                name="BJ configs[1]: DD Strassen GEMM 1024^3, threshold 128 (depth 3), seed 2"),
     "c2": dict(W=4, algo="winograd", T=128, m=1024, l=1024, n=1024, seed=3,
@@ -126,7 +128,7 @@ def oracle_sample(wl):
     problem for c1 and c2. Returns (A, B, shape, description)."""
     import ddqd_inputs as gen
     m, l, n = wl["m"], wl["l"], wl["n"]
-    div = {"c3": 2, "c2": 1, "c1": 1}[wl["key"]]
+    div = {"c3": 2, "c2": 1, "c1": 1, "c0": 1}[wl["key"]]
     ms, ls, ns = (m + div - 1) // div, (l + div - 1) // div, (n + div - 1) // div
     A = gen.matrix(wl["W"], ms, ls, wl["seed"], 0)
     B = gen.matrix(wl["W"], ls, ns, wl["seed"], 1)
@@ -483,11 +485,14 @@ def main():
         # the arithmetic variants of SURVEY s.8(f) row f3 on the same inputs: different
         # (documented, oracle-mirrored) roundings, reported beside the paper-faithful headline
         variants = {}
-        notes = {"fused": ("DDQD_MADD_FUSED", {2: 15, 4: None}),
-                 "accurate": ("DDQD_ADD_ACCURATE", {2: 29, 4: None})}
-        for v, (flag, opc) in notes.items():
+        notes = {"fused": ("DDQD_MADD_FUSED", {2: 15, 4: None}, "fused", 1),
+                 "accurate": ("DDQD_ADD_ACCURATE", {2: 29, 4: None}, "accurate", 1)}
+        if args.workload == "c0":   # small shapes: the split-k cluster leaf (row a4)
+            for sk in (2, 4, 8):
+                notes["splitk%d" % sk] = ("DDQD_SPLITK(%d)" % sk, {2: 20, 4: 200}, "canonical", sk)
+        for v, (flag, opc, mv, sk) in notes.items():
             def vstep():
-                ddqd.gemm(A, B, algo, T, out=C, madd=v)
+                ddqd.gemm(A, B, algo, T, out=C, madd=mv, splitk=sk)
             vstep()
             torch.cuda.synchronize()
             f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -497,7 +502,7 @@ def main():
             f1.record()
             torch.cuda.synchronize()
             fms = f0.elapsed_time(f1)
-            variants["madd_" + v] = {
+            variants[("madd_" + v) if sk == 1 else v] = {
                 "value": flops_per_step * args.steps / (fms * 1e-3) / 1e9, "unit": "GFLOP/s",
                 "ms_per_step": fms / args.steps, "fp64_ops_per_madd": opc[W],
                 "note": flag + ": bit-exact vs the oracle's " + v + " variant, not the canonical"}

@@ -59,6 +59,15 @@ enum { DDQD_MADD_FUSED = 0x100 };
  * DDQD_ENOTSUP (their panel/TRSM/solve arithmetic is the canonical one). */
 enum { DDQD_ADD_ACCURATE = 0x200 };
 
+/* Split-k leaf (docs/numerics.md s.4): OR DDQD_SPLITK(s), s = 2, 4 or
+ * 8, into `algo` and every leaf product (the whole product for DDQD_BLOCK) cuts k into s
+ * contiguous slices of ceil(l/s), forms each slice's partial from +0 with k ascending, and
+ * combines the partials by the fixed pairwise tree ((p0+p1)+(p2+p3))+... . On the device one
+ * thread-block cluster of s CTAs owns a 32x32 tile and the partials meet in distributed shared
+ * memory, so small products (config 0: 128^3) fill s times more SMs. A different, documented
+ * rounding from the canonical k-ascending sum: bit-identical to the oracle's split-k. */
+#define DDQD_SPLITK(s) ((s) == 2 ? 0x1000 : (s) == 4 ? 0x2000 : (s) == 8 ? 0x3000 : 0)
+
 /* Precisions: number of float64 words per element. */
 enum { DDQD_DD = 2, DDQD_QD = 4 };
 

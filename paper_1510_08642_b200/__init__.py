@@ -117,13 +117,18 @@ def _set_stream(t):
     lib.ddqd_set_stream(ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
 
 
-def _algo(a, madd="canonical") -> int:
+_SPLITK = {1: 0, 2: 0x1000, 4: 0x2000, 8: 0x3000}   # DDQD_SPLITK(s)
+
+
+def _algo(a, madd="canonical", splitk=1) -> int:
     """'block' | 'strassen' | 'winograd' (or the int); madd='fused' ORs in DDQD_MADD_FUSED,
     madd='accurate' DDQD_ADD_ACCURATE."""
     v = _ALGOS[a] if isinstance(a, str) else int(a)
     if madd not in _VARIANTS:
         raise ValueError("madd must be 'canonical', 'fused' or 'accurate'")
-    return v | _VARIANTS[madd]
+    if splitk not in _SPLITK:
+        raise ValueError("splitk must be 1, 2, 4 or 8")
+    return v | _VARIANTS[madd] | _SPLITK[splitk]
 
 
 def _check_mat(x, W, name):
@@ -134,7 +139,7 @@ def _check_mat(x, W, name):
         raise ValueError(f"{name} must be contiguous (planar row-major)")
 
 
-def gemm(A, B, algo="block", threshold=128, out=None, madd="canonical"):
+def gemm(A, B, algo="block", threshold=128, out=None, madd="canonical", splitk=1):
     """C := A B with A [W,m,l], B [W,l,n] float64 CUDA tensors, W = 2 (DD) or 4 (QD).
     Pinned/ordinary CPU tensors for A, B and `out` use the library's host-staging path
     (copies inside the call, synchronous)."""
@@ -156,20 +161,20 @@ def gemm(A, B, algo="block", threshold=128, out=None, madd="canonical"):
         raise ValueError("out has the wrong shape")
     _set_stream(A)
     f = lib.dd_gemm if W == 2 else lib.qd_gemm
-    _check(f(m, l, n, A.data_ptr(), B.data_ptr(), out.data_ptr(), _algo(algo, madd), threshold), "gemm")
+    _check(f(m, l, n, A.data_ptr(), B.data_ptr(), out.data_ptr(), _algo(algo, madd, splitk), threshold), "gemm")
     return out
 
 
-def dd_gemm(A, B, algo="block", threshold=128, out=None, madd="canonical"):
+def dd_gemm(A, B, algo="block", threshold=128, out=None, madd="canonical", splitk=1):
     if A.shape[0] != 2:
         raise ValueError("dd_gemm takes [2, rows, cols] tensors")
-    return gemm(A, B, algo, threshold, out, madd)
+    return gemm(A, B, algo, threshold, out, madd, splitk)
 
 
-def qd_gemm(A, B, algo="block", threshold=128, out=None, madd="canonical"):
+def qd_gemm(A, B, algo="block", threshold=128, out=None, madd="canonical", splitk=1):
     if A.shape[0] != 4:
         raise ValueError("qd_gemm takes [4, rows, cols] tensors")
-    return gemm(A, B, algo, threshold, out, madd)
+    return gemm(A, B, algo, threshold, out, madd, splitk)
 
 
 def gemm_ex(prec, algo, threshold, m, l, n, batch, A, lda, psA, bsA, B, ldb, psB, bsB,

@@ -144,7 +144,7 @@ static int where(const void *p) {
 
 static int check_gemm_args(int64_t m, int64_t l, int64_t n, int algo, int64_t T) {
     if (m < 0 || l < 0 || n < 0) { set_error("negative dimension"); return DDQD_EINVAL; }
-    if (algo & ~(0xff | DDQD_MADD_FUSED | DDQD_ADD_ACCURATE)) { set_error("unknown algo flag"); return DDQD_EINVAL; }
+    if (algo & ~(0xff | DDQD_MADD_FUSED | DDQD_ADD_ACCURATE | 0x3000)) { set_error("unknown algo flag"); return DDQD_EINVAL; }
     if ((algo & DDQD_MADD_FUSED) && (algo & DDQD_ADD_ACCURATE)) {
         set_error("DDQD_MADD_FUSED and DDQD_ADD_ACCURATE are exclusive");
         return DDQD_EINVAL;

@@ -229,9 +229,16 @@ static bool tma_enabled() {
     return v == 1;
 }
 
+int launch_leaf_splitk(int W, int split, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
+                       const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s);   // leaf_splitk.cu
+
 int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
                      const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s) {
     if (m == 0 || n == 0 || batch == 0) return DDQD_OK;
+    // mv: arithmetic variant (low 4 bits) | log2(split-k) << 4
+    const int split = 1 << ((mv >> 4) & 3);
+    mv &= 0xf;
+    if (split > 1) return launch_leaf_splitk(W, split, m, l, n, batch, A, B, C, beta, mv, s);
     if (W == 2 && mv != 2 && tma_enabled() && leaf_cfg_override() < 0) {
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
         if (big_tiles >= 2 * 148 && m > 32 && n > 32) {

@@ -135,8 +135,9 @@ static bool fuse2_enabled() {
 static int exec_level(const Plan &p, char *ws, int j, int64_t cnt, const MatDesc &A,
                       const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s) {
     if (j == p.d) return launch_leaf_gemm(p.W, p.m[j], p.l[j], p.n[j], cnt, A, B, C, beta, p.mv, s);
-    const bool two = fuse2_enabled() && p.W == 2 && p.mv != 2 && j + 2 <= p.d && ((p.d - j) % 2 == 0);
-    const int add_algo = p.algo | (p.mv == 2 ? DDQD_ADD_ACCURATE : 0);   // the additions' variant
+    const int var = p.mv & 0xf;
+    const bool two = fuse2_enabled() && p.W == 2 && var != 2 && j + 2 <= p.d && ((p.d - j) % 2 == 0);
+    const int add_algo = p.algo | (var == 2 ? DDQD_ADD_ACCURATE : 0);   // the additions' variant
     for (int64_t p0 = 0; p0 < cnt; p0 += p.chunk[j]) {
         const int64_t pc = std::min<int64_t>(p.chunk[j], cnt - p0);
         int rc;
@@ -165,7 +166,8 @@ static int exec_level(const Plan &p, char *ws, int j, int64_t cnt, const MatDesc
 int run_gemm(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n, int64_t batch,
              const MatDesc &A, const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s) {
     if (m == 0 || n == 0 || batch == 0) return DDQD_OK;
-    const int mv = (algo & DDQD_MADD_FUSED) ? 1 : (algo & DDQD_ADD_ACCURATE) ? 2 : 0;
+    const int mv = ((algo & DDQD_MADD_FUSED) ? 1 : (algo & DDQD_ADD_ACCURATE) ? 2 : 0) |
+                   (((algo >> 12) & 3) << 4);   // split-k (DDQD_SPLITK) rides in bits 4-5
     algo &= 0xff;
     Plan p;
     int rc = make_plan(p, W, algo, T, m, l, n, batch, workspace_limit());

@@ -724,3 +724,45 @@ def test_p2p_combine_cuda_ipc_bitwise(orc, cfg, world):
     W, algo, T, m, l, n, _ = cfg
     ref = orc.gemm(gen.matrix(W, m, l, 31, 0), gen.matrix(W, l, n, 31, 1), algo, threshold=T)
     assert k >= 1 and same(C, ref)
+
+
+# ---- split-k leaf: clusters of CTAs reducing through distributed shared memory (row a4) ---------
+def test_splitk_tree_pin_on_device(orc):
+    """The oracle's tree-order pin (1 + 2^-120 kept only by the pairwise tree) on the device."""
+    A = np.zeros((2, 1, 4)); A[0] = 1.0
+    B = np.zeros((2, 4, 1))
+    B[0, :, 0] = [1.0, 0.0, 2.0 ** -60, -2.0 ** -60]
+    B[1, 2, 0] = 2.0 ** -120
+    for s in (2, 4, 8):
+        got = np_(ddqd.dd_gemm(cu(A), cu(B), "block", splitk=s))
+        assert list(got[:, 0, 0]) == [1.0, 2.0 ** -120]
+        assert same(got, orc.gemm(A, B, "block", splitk=s))
+
+
+@pytest.mark.parametrize("W", [2, 4])
+@pytest.mark.parametrize("s", [2, 4, 8])
+def test_splitk_bitwise(orc, W, s):
+    """Split-k leaves bit-identical to the oracle: ragged tiles, l < s (empty slices), l not a
+    multiple of s or of the 16-deep k chunk, Block and recursion leaves, the accurate variant."""
+    cases = [("block", 37, 29, 33, 1), ("block", 5, 3, 7, 1), ("block", 64, 100, 70, 1),
+             ("winograd", 67, 66, 65, 16), ("strassen", 40, 41, 42, 8)]
+    for algo, m, l, n, T in cases:
+        A = gen.matrix(W, m, l, 5 * m + s, 0)
+        B = gen.matrix(W, l, n, 5 * m + s, 1)
+        got = np_(ddqd.gemm(cu(A), cu(B), algo, T, splitk=s))
+        assert same(got, orc.gemm(A, B, algo, threshold=T, splitk=s)), (algo, m, l, n)
+    A = gen.matrix(W, 45, 50, 9, 0); B = gen.matrix(W, 50, 40, 9, 1)
+    got = np_(ddqd.gemm(cu(A), cu(B), "block", madd="accurate", splitk=s))
+    assert same(got, orc.gemm(A, B, "block", madd="accurate", splitk=s))
+
+
+def test_c0_splitk8(orc):
+    """BJ:7 (config 0) with the split-k leaf (8-CTA clusters, 128 CTAs for the 16 tiles):
+    bit-exact vs the oracle's split-k and within 2^-96 l |A||B| of the exact product."""
+    A = gen.dd_matrix(128, 128, 1, 0)
+    B = gen.dd_matrix(128, 128, 1, 1)
+    got = np_(ddqd.dd_gemm(cu(A), cu(B), "block", splitk=8))
+    assert same(got, orc.gemm(A, B, "block", splitk=8))
+    r, c = np.meshgrid(np.arange(128), np.arange(128), indexing="ij")
+    _, err = orc.exact_entries(A, B, got, r.ravel(), c.ravel())
+    assert np.abs(err).max() <= 2.0 ** -96 * 128 * np.abs(A[0]).max() * np.abs(B[0]).max()
