@@ -122,13 +122,14 @@ class Clocks:
 
 
 # ---- CPU oracle sample (cpu_baseline and --impl reference) ----------------------------
-def oracle_sample(wl):
-    """Bounded sample of the workload for the oracle (~10-20 s of host work for c3): the
-    leading (m/2, l/2, n/2) block (same recipe, same algorithm and threshold) for c3; the full
-    problem for c1 and c2. Returns (A, B, shape, description)."""
+def oracle_sample(wl, per_step=False):
+    """Bounded sample of the workload for the oracle: for the cpu_baseline (one run, ~10-20 s
+    of host work) the leading (m/2, l/2, n/2) block of c3 (same recipe, algorithm and
+    threshold) and the full c0/c1/c2 problems; per step of the reference arm (run K + W times)
+    the leading (m/4, l/4, n/4) block of c3 (~2 s). Returns (A, B, shape, description)."""
     import ddqd_inputs as gen
     m, l, n = wl["m"], wl["l"], wl["n"]
-    div = {"c3": 2, "c2": 1, "c1": 1, "c0": 1}[wl["key"]]
+    div = {"c3": 4 if per_step else 2, "c2": 1, "c1": 1, "c0": 1}[wl["key"]]
     ms, ls, ns = (m + div - 1) // div, (l + div - 1) // div, (n + div - 1) // div
     A = gen.matrix(wl["W"], ms, ls, wl["seed"], 0)
     B = gen.matrix(wl["W"], ls, ns, wl["seed"], 1)
@@ -176,7 +177,7 @@ def reference_arm(args, wl, rank, world):
     orc.build()
     if wl.get("lu"):
         return reference_lu(args, wl, orc)
-    A, B, (ms, ls, ns), desc = oracle_sample(wl)
+    A, B, (ms, ls, ns), desc = oracle_sample(wl, per_step=True)
     for _ in range(args.warmup):
         run_oracle_once(orc, wl, A, B)
     tot = sum(run_oracle_once(orc, wl, A, B) for _ in range(args.steps))
