@@ -65,6 +65,9 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--k", type=int, default=None, help="multi-GPU product depth (default: balancer)")
+    ap.add_argument("--schedule", default="products", choices=["products", "ctiles", "auto"],
+                    help="multi-GPU schedule: depth-k product distribution (bit-identical to one GPU), "
+                         "C row tiles each recursing on its slab, or whichever measures faster (BJ:5)")
     ap.add_argument("--combine", default="nccl", choices=["nccl", "p2p"],
                     help="multi-GPU combine: products to rank 0 over NCCL point-to-point (default), or "
                          "the fused post-additions reading peers' products over CUDA IPC / NVLink")
@@ -405,7 +408,11 @@ def main():
 
     if world > 1:
         from paper_1510_08642_b200 import mgpu
-        sched = mgpu.DistributedGemm(W, algo, T, m, l, n, dist, dev, k=args.k, combine=args.combine)
+        if args.schedule == "auto":
+            sched = mgpu.AutoDistributedGemm(W, algo, T, m, l, n, dist, dev, combine=args.combine)
+        else:
+            sched = mgpu.DistributedGemm(W, algo, T, m, l, n, dist, dev,
+                                         k=0 if args.schedule == "ctiles" else args.k, combine=args.combine)
 
         def step():
             sched(A, B, C)
@@ -549,8 +556,9 @@ def main():
                        "madd": args.madd,
                        "depth": d, "leaf_shape": list(shapes[-1]), "leaf_madds_per_step": leaf_madds_step,
                        "l2": "no flush: each operand (%.2f GB) exceeds the 126 MB L2" % (A.numel() * 8 / 1e9),
-                       "parallelism": f"{world} GPU" + (f"s, depth-k product distribution, {args.combine} combine"
-                                                        if world > 1 else "")},
+                       "parallelism": f"{world} GPU" + (f"s, schedule {args.schedule}"
+                                                        + (f" (chose {sched.choice})" if args.schedule == "auto" else "")
+                                                        + f", {args.combine} combine" if world > 1 else "")},
             "roofline": roofline,
             "fp64_roofline_fraction": {
                 "algorithmic_leaf": roofline["frac"],

@@ -21,6 +21,12 @@ Both schedules are numerically identical to the single-GPU call (same tree, same
 so results are bit-identical to the oracle for any world size. With beta = 1 the result is
 subtracted from C (C := C - A B), the form of the LU's Schur update.
 
+AutoDistributedGemm (BJ:5 (4) "the top-level 7 products are distributed over GPUs, or C is
+partitioned into tiles that each GPU recurses on, choosing whichever measures faster"): times
+both schedules once (max over ranks) and keeps the faster. The C-tile schedule recurses on row
+slabs of C (each slab its own Strassen/Winograd tree), so it rounds differently from the
+one-GPU call; it is bit-exact against the oracle run slab by slab.
+
 DistributedLU: the blocked LU with its trailing update
 A22 := A22 - L21 U12 run by DistributedGemm over all ranks; rank 0 keeps the matrix
 and does the sequential panel steps (4096 dependent pivot steps at c4 do not shard) and the
@@ -436,3 +442,43 @@ class DistributedLU:
         if not root:
             return None, None, None
         return bk.lu_trsv(A, ipiv, b), ipiv, info
+
+
+class AutoDistributedGemm:
+    """C := A B with whichever of the two multi-GPU schedules measures faster on this machine
+    (BJ:5 (4)): "products" (depth-k product distribution, bit-identical to one GPU) or
+    "ctiles" (C row slabs, each rank recursing on its slab). The first call runs both, timed
+    with device syncs and a barrier on either side, takes the max over ranks (so every rank
+    makes the same choice) and leaves C from the chosen schedule; later calls run only it."""
+
+    def __init__(self, W, algo, T, m, l, n, dist, device=None, backend=None, **kw):
+        self.dist = dist
+        self.backend = backend or CudaBackend()
+        self.cands = {
+            "products": DistributedGemm(W, algo, T, m, l, n, dist, device, backend=self.backend, **kw),
+            "ctiles": DistributedGemm(W, algo, T, m, l, n, dist, device, k=0, backend=self.backend, **kw),
+        }
+        self.choice = None
+        self.timings = {}
+
+    def _timed(self, name, A, B, C):
+        import time
+        self.backend.sync()
+        self.dist.barrier()
+        t0 = time.perf_counter()
+        self.cands[name](A, B, C)
+        self.backend.sync()
+        dt = time.perf_counter() - t0
+        allt = [None] * self.dist.get_world_size()
+        self.dist.all_gather_object(allt, dt)
+        return max(allt)
+
+    def __call__(self, A, B, C):
+        if self.choice is None:
+            for name in ("ctiles", "products"):
+                self.timings[name] = self._timed(name, A, B, C)
+            self.choice = min(self.timings, key=self.timings.get)
+            if self.choice != "products":          # C holds the last schedule's result
+                self.cands[self.choice](A, B, C)
+            return C
+        return self.cands[self.choice](A, B, C)

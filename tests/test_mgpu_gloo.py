@@ -306,3 +306,52 @@ def test_p2p_combine_matches_single_process(orc, cfg, world):
     k, C = _run(cfg, world=world, combine="p2p")
     ref = orc.gemm(gen.matrix(W, m, l, 21, 0), gen.matrix(W, l, n, 21, 1), algo, threshold=T)
     assert k >= 1 and np.array_equal(C.view(np.int64), ref.view(np.int64))
+
+
+
+def _auto_worker(rank, world, port, cfg, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1510_08642_b200.mgpu import AutoDistributedGemm, DistributedGemm
+        W, algo, T, m, l, n = cfg
+        A = torch.from_numpy(gen.matrix(W, m, l, 23, 0)) if rank == 0 else torch.zeros((W, m, l), dtype=torch.float64)
+        B = torch.from_numpy(gen.matrix(W, l, n, 23, 1)) if rank == 0 else torch.zeros((W, l, n), dtype=torch.float64)
+        C = torch.zeros((W, m, n), dtype=torch.float64)
+        C2 = torch.zeros((W, m, n), dtype=torch.float64)
+        DistributedGemm(W, algo, T, m, l, n, dist, k=0, backend=OracleBackend(W))(A, B, C2)   # C tiles
+        ag = AutoDistributedGemm(W, algo, T, m, l, n, dist, backend=OracleBackend(W))
+        ag(A, B, C)
+        choice1 = ag.choice
+        ag(A, B, C)
+        if rank == 0:
+            q.put((choice1, ag.choice, C.numpy().copy(), C2.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_c_tiles_and_auto_schedule(orc):
+    """BJ:5 (4): the C-tile schedule (each rank recurses on its row slab of C) is bit-exact
+    against the oracle run slab by slab; AutoDistributedGemm times both schedules, makes the
+    same choice on every rank, and returns the chosen schedule's exact result."""
+    from paper_1510_08642_b200.mgpu import balanced_slices
+    cfg = (2, "winograd", 4, 37, 29, 33)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_auto_worker, args=(r, 2, port, cfg, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    choice1, choice2, C, C2 = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    W, algo, T, m, l, n = cfg
+    A, B = gen.matrix(W, m, l, 23, 0), gen.matrix(W, l, n, 23, 1)
+    tiles = np.concatenate([orc.gemm(np.ascontiguousarray(A[:, a:b]), B, algo, threshold=T)
+                            for a, b in balanced_slices(m, 2)], axis=1)
+    assert np.array_equal(C2.view(np.int64), tiles.view(np.int64))
+    assert choice1 == choice2 and choice1 in ("products", "ctiles")
+    expect = orc.gemm(A, B, algo, threshold=T) if choice1 == "products" else tiles
+    assert np.array_equal(C.view(np.int64), expect.view(np.int64))
+    assert not np.array_equal(tiles, orc.gemm(A, B, algo, threshold=T))   # the two schedules round differently
