@@ -766,3 +766,28 @@ def test_c0_splitk8(orc):
     r, c = np.meshgrid(np.arange(128), np.arange(128), indexing="ij")
     _, err = orc.exact_entries(A, B, got, r.ravel(), c.ravel())
     assert np.abs(err).max() <= 2.0 ** -96 * 128 * np.abs(A[0]).max() * np.abs(B[0]).max()
+
+
+def test_two_lane_schedule_same_bits(orc, tmp_path):
+    """DDQD_LANES=2 (the last depth-first level's chunks alternate between two streams with
+    separate workspace): bit-identical to the oracle, under a workspace limit that forces
+    depth-first levels."""
+    import subprocess, sys, textwrap
+    code = textwrap.dedent(f"""
+        import numpy as np, torch, sys
+        sys.path.insert(0, {ROOT!r})
+        import ddqd_inputs as gen, paper_1510_08642_b200 as ddqd
+        A = gen.dd_matrix(515, 517, 43, 0); B = gen.dd_matrix(517, 513, 43, 1)
+        ddqd.set_workspace_limit(60 << 20)   # depth-first top 2 levels (37 MB), second lane fits (51 MB)
+        C = ddqd.dd_gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), "winograd", 32)
+        Q = gen.qd_matrix(260, 250, 5, 0); R = gen.qd_matrix(250, 270, 5, 1)
+        D = ddqd.qd_gemm(torch.from_numpy(Q).cuda(), torch.from_numpy(R).cuda(), "strassen", 16)
+        np.savez(sys.argv[1], C.cpu().numpy(), D.cpu().numpy())
+    """)
+    path = str(tmp_path / "lanes.npz")
+    subprocess.run([sys.executable, "-c", code, path], check=True, env=dict(os.environ, DDQD_LANES="2"))
+    z = np.load(path)
+    A = gen.dd_matrix(515, 517, 43, 0); B = gen.dd_matrix(517, 513, 43, 1)
+    assert same(z["arr_0"], orc.gemm(A, B, "winograd", threshold=32))
+    Q = gen.qd_matrix(260, 250, 5, 0); R = gen.qd_matrix(250, 270, 5, 1)
+    assert same(z["arr_1"], orc.gemm(Q, R, "strassen", threshold=16))
