@@ -19,6 +19,11 @@
 
 namespace ddqd {
 
+#ifndef LEAF_TMA_KK_UNROLL
+#define LEAF_TMA_KK_UNROLL 1
+#endif
+constexpr int kLeafTmaKkUnroll = LEAF_TMA_KK_UNROLL;   // k-step unroll of the inner loop (tuning)
+
 namespace tma {
 constexpr int BM = 64, BN = 64, BK = 8, TM = 4, TN = 4, S = 4, W = 2;
 constexpr int NT = (BM / TM) * (BN / TN);          // 256
@@ -117,6 +122,7 @@ leaf_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const double *bs = Bs + st * B_STAGE;   // [W][BK][BN]
         const int krem = (int)(l - (int64_t)kt * BK);
         const int kmax = krem < BK ? krem : BK;   // uniform: no madds past l
+#pragma unroll kLeafTmaKkUnroll
         for (int kk = 0; kk < kmax; kk++) {
             double av[W][TM], bv[W][TN];
 #pragma unroll
