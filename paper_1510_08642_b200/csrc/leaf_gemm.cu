@@ -32,7 +32,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // k-step unroll of the inner loop: 4 lets the compiler issue the next steps' shared-memory
 // fragment loads under the current step's FP64 chains. Measured (c3 cp.async leaf / c2 QD):
 // 1: 0.9162 / 0.8795, 2: 0.9194, 4: 0.9218 / 0.8799, 8: 0.9233 / 0.7997 of the FP64 peak.
-// (The TMA leaf keeps 1: unrolling it measured slower on c1, 0.836 -> 0.815.)
+// (The TMA leaf takes 2: see leaf_tma.cu.)
 #ifndef LEAF_KK_UNROLL
 #define LEAF_KK_UNROLL 4
 #endif

@@ -19,10 +19,13 @@
 
 namespace ddqd {
 
+// k-step unroll of the inner loop. Measured (c1 / c4 leaf fraction of the FP64 peak):
+// 1: 0.833 / 0.873, 2: 0.837 / 0.878, 4: 0.815 / -, 8: 0.768 / -; the cp.async leaf with its
+// unroll of 4 measures 0.841 / 0.880 on the same shapes.
 #ifndef LEAF_TMA_KK_UNROLL
-#define LEAF_TMA_KK_UNROLL 1
+#define LEAF_TMA_KK_UNROLL 2
 #endif
-constexpr int kLeafTmaKkUnroll = LEAF_TMA_KK_UNROLL;   // k-step unroll of the inner loop (tuning)
+constexpr int kLeafTmaKkUnroll = LEAF_TMA_KK_UNROLL;
 
 namespace tma {
 constexpr int BM = 64, BN = 64, BK = 8, TM = 4, TN = 4, S = 4, W = 2;
