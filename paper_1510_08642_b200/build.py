@@ -39,19 +39,40 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every .cu to an object in parallel (no cross-file device code), then link."""
     if not force and not needs_build():
         return SO
+    from concurrent.futures import ThreadPoolExecutor
     extra = os.environ.get("DDQD_NVCC_EXTRA", "").split()   # tuning experiments only
-    cmd = [NVCC, *NVCC_FLAGS, *extra, "-o", SO, *sources()]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [NVCC, *flags, *extra, "-c", "-o", obj, src]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        return obj, " ".join(cmd) + "\n" + r.stdout + r.stderr, r.returncode
+
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, sources()))
+    objs = [o for o, _, _ in results]
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", SO, *objs]
+    logtxt = "".join(t for _, t, _ in results)
+    failed = [t for _, t, rc in results if rc != 0]
+    if not failed:
+        r = subprocess.run(link, capture_output=True, text=True)
+        logtxt += " ".join(link) + "\n" + r.stdout + r.stderr
+        if r.returncode != 0:
+            failed.append(r.stdout + r.stderr)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
+        f.write(logtxt)
+    if failed:
+        sys.stderr.write("".join(failed))
         raise RuntimeError("nvcc failed building libddqd.so (see %s)" % log)
     if verbose:
-        sys.stderr.write(r.stderr)
+        sys.stderr.write(logtxt)
     return SO
 
 
