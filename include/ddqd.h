@@ -78,7 +78,7 @@ enum {
     DDQD_EALIAS = -2,  /* C overlaps A or B                                              */
     DDQD_ENOMEM = -3,  /* workspace / staging allocation failed                          */
     DDQD_ECUDA = -4,   /* a CUDA runtime error (message in ddqd_last_error)              */
-    DDQD_ENOTSUP = -5  /* not supported (e.g. QD LU, host pointers to *_ex)              */
+    DDQD_ENOTSUP = -5  /* not supported (host pointers to *_ex / LU, accurate-add LU)    */
 };
 
 /*
@@ -86,7 +86,8 @@ enum {
  *   m, l, n   : A is m x l, B is l x n, C is m x n (>= 0).
  *   A, B, C   : planar contiguous [W][rows][cols] (W = 2 for dd_gemm, 4 for qd_gemm).
  *   algo      : DDQD_BLOCK, DDQD_STRASSEN or DDQD_WINOGRAD (the 7-product
- *               recursions whose leaves are Block).
+ *               recursions whose leaves are Block), optionally OR-ed with DDQD_MADD_FUSED or
+ *               DDQD_ADD_ACCURATE, and with DDQD_SPLITK(s) (arithmetic variants above).
  *   threshold : n_min of P:52 -- a (sub)problem recurses while min(m,l,n) > threshold
  *               (>= 1; ignored for DDQD_BLOCK). Odd halves are zero padded virtually.
  * Results are bit-identical to the oracle under docs/numerics.md (k ascending per leaf
