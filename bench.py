@@ -27,6 +27,20 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# the paper's own CPU numbers closest to each workload (context only)
+PAPER_CONTEXT = {
+    "c1": {"value": 0.693, "unit": "GFLOP/s", "seconds": 3.1, "what": "DD Strassen(32), n = 1024, 8 threads",
+           "cpu": "Intel Xeon E5-2620 v2 2.1 GHz, qd 2.3.15", "source": "PAPER.md:74-76 (Table 1)"},
+    "c2": {"value": 0.125, "unit": "GFLOP/s", "seconds": 17.2, "what": "QD Winograd(32), n = 1024, 8 threads",
+           "cpu": "Intel Xeon E5-2620 v2 2.1 GHz, qd 2.3.15", "source": "PAPER.md:103-105 (Table 2)"},
+    "c3": {"value": 0.693, "unit": "GFLOP/s", "seconds": None,
+           "what": "no paper run at this size; its best DD rate: Strassen/Winograd(32), n = 1024, 8 threads",
+           "cpu": "Intel Xeon E5-2620 v2 2.1 GHz, qd 2.3.15", "source": "PAPER.md:74-76 (Table 1)"},
+    "c4": {"value": 2.0 / 3.0 * 1024 ** 3 / 4.3 / 1e9, "unit": "GFLOP/s", "seconds": 4.3,
+           "what": "DD pivot-free LU, n = 1024 (inferred), Winograd(32) update, alpha = 2, 8 threads",
+           "cpu": "Intel Xeon E5-2620 v2 2.1 GHz, qd 2.3.15", "source": "PAPER.md:164"},
+}
+
 GEMM_METRIC = "DD/QD GEMM effective GFLOPS (2mln/s) and % FP64-pipe roofline"
 LU_METRIC = "DD LU effective GFLOPS (2n^3/3 per solve / s)"
 
@@ -358,6 +372,7 @@ def lu_bench(args, wl, rank, world, local):
             "time_shares": shares,
             "max_abs_err_x_minus_1": err,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+            "paper_context": PAPER_CONTEXT["c4"],
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -567,6 +582,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "variants": variants,
+            "paper_context": PAPER_CONTEXT.get(args.workload),
             "gpu_launches": int(launches),
             "clocks": clk,
         }
