@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -78,6 +79,12 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--custom", default=None, metavar="M,L,N",
+                    help="a custom GEMM workload instead of a BASELINE config (with --prec/--algo/--threshold/--seed)")
+    ap.add_argument("--prec", default="dd", choices=["dd", "qd"])
+    ap.add_argument("--algo", default="winograd", choices=["block", "strassen", "winograd"])
+    ap.add_argument("--threshold", type=int, default=128)
+    ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--k", type=int, default=None, help="multi-GPU product depth (default: balancer)")
     ap.add_argument("--schedule", default="products", choices=["products", "ctiles", "auto"],
                     help="multi-GPU schedule: depth-k product distribution (bit-identical to one GPU), "
@@ -146,7 +153,11 @@ def oracle_sample(wl, per_step=False):
     the leading (m/4, l/4, n/4) block of c3 (~2 s). Returns (A, B, shape, description)."""
     import ddqd_inputs as gen
     m, l, n = wl["m"], wl["l"], wl["n"]
-    div = {"c3": 4 if per_step else 2, "c2": 1, "c1": 1, "c0": 1}[wl["key"]]
+    if wl["key"] == "custom":   # keep the sample near 1024^3 (DD) / 512^3 (QD) multiply-adds
+        target = (1024 if wl["W"] == 2 else 512) ** 3
+        div = max(1, int(math.ceil((m * l * n / target) ** (1.0 / 3.0))))
+    else:
+        div = {"c3": 4 if per_step else 2, "c2": 1, "c1": 1, "c0": 1}[wl["key"]]
     ms, ls, ns = (m + div - 1) // div, (l + div - 1) // div, (n + div - 1) // div
     A = gen.matrix(wl["W"], ms, ls, wl["seed"], 0)
     B = gen.matrix(wl["W"], ls, ns, wl["seed"], 1)
@@ -386,7 +397,15 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    wl = dict(WORKLOADS[args.workload])
+    if args.custom:
+        m_, l_, n_ = (int(v) for v in args.custom.split(","))
+        W_ = 2 if args.prec == "dd" else 4
+        args.workload = "custom"
+        wl = dict(W=W_, algo=args.algo, T=args.threshold, m=m_, l=l_, n=n_, seed=args.seed,
+                  name=f"custom: {args.prec.upper()} {args.algo} GEMM {m_}x{l_}x{n_}, threshold {args.threshold}, "
+                       f"seed {args.seed}")
+    else:
+        wl = dict(WORKLOADS[args.workload])
     wl["key"] = args.workload
     if args.impl == "reference":
         return reference_arm(args, wl, rank, world)

@@ -11,7 +11,13 @@
 #include "../../include/ddqd.h"
 #include "common.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace ddqd {
+
+NvtxRange::NvtxRange(const char *name) { nvtxRangePushA(name); }
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
+
 
 static thread_local std::string t_err;
 static thread_local cudaStream_t t_stream = nullptr;
@@ -159,6 +165,7 @@ static int check_gemm_args(int64_t m, int64_t l, int64_t n, int algo, int64_t T)
 
 static int gemm_entry(int W, int64_t m, int64_t l, int64_t n, const double *A, const double *B,
                        double *C, int algo, int64_t T) {
+    NvtxRange nv(W == 2 ? "dd_gemm" : "qd_gemm");
     t_err.clear();
     int rc = check_gemm_args(m, l, n, algo, T);
     if (rc) return rc;
@@ -210,6 +217,7 @@ int qd_gemm(int64_t m, int64_t l, int64_t n, const double *A, const double *B, d
 }
 
 int ddqd_gemm_ex(const ddqd_gemm_desc *d) {
+    NvtxRange nv("ddqd_gemm_ex");
     t_err.clear();
     if (!d) { set_error("null descriptor"); return DDQD_EINVAL; }
     if (d->prec != 2 && d->prec != 4) { set_error("prec must be DDQD_DD or DDQD_QD"); return DDQD_EINVAL; }
@@ -227,6 +235,7 @@ int ddqd_gemm_ex(const ddqd_gemm_desc *d) {
 
 int ddqd_lu_solve(int prec, int pivot, int64_t n, double *A, const double *b, double *x, int64_t *ipiv,
                   int64_t panel, int algo, int64_t threshold) {
+    NvtxRange nv("ddqd_lu_solve");
     t_err.clear();
     if (prec != 2 && prec != 4) { set_error("prec must be DDQD_DD or DDQD_QD"); return DDQD_EINVAL; }
     if (pivot != 0 && pivot != 1) { set_error("pivot must be 0 or 1"); return DDQD_EINVAL; }

@@ -23,6 +23,13 @@ cudaStream_t cur_stream();
 void count_launch(int64_t n = 1);
 int current_device();   // cudaGetDevice, masked to [0, 64) for per-device caches
 
+// NVTX ranges (header-only NVTX3; free when no profiler is attached): the recursion levels,
+// the LU phases and the ABI entry points show up by name in Nsight Systems / Compute.
+struct NvtxRange {
+    explicit NvtxRange(const char *name);
+    ~NvtxRange();
+};
+
 // Live per-class kernel timing for bench.py (CUDA events on the launching stream), active
 // only between ddqd_profile_start/stop. Classes: 0 leaf GEMM (work = madds), 1 pre-add
 // (work = algorithmic bytes), 2 post-add (bytes), 3 LU kernels.

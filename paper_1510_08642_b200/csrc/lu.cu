@@ -1039,6 +1039,7 @@ static int trsm_mode() {
 template <int W>
 static int lu_panel_w(int64_t n, int pivot, double *A, int64_t *ipiv, int64_t p, int64_t kb, LuAux *aux,
                       double *scr, size_t scr_bytes, cudaStream_t s) {
+    NvtxRange nv("LU panel + TRSM");
     prof_begin(3, s);
     int crc = DDQD_OK;
     const bool coop = use_coop_panel() && try_panel_coop<W>(A, n, p, kb, pivot, ipiv, aux, scr, scr_bytes, s, &crc);
@@ -1114,6 +1115,7 @@ static bool trsv_fast_enabled() {
 template <int W>
 static int lu_trsv_w(int64_t n, const double *A, const int64_t *ipiv, const double *b, double *x, double *y,
                      cudaStream_t s) {
+    NvtxRange nv("LU solves");
     const int use_smem = ((int64_t)W * n * (int64_t)sizeof(double) <= 200 * 1024) ? 1 : 0;
     const size_t psmem = use_smem ? (size_t)W * n * sizeof(double) : 0;
     if (psmem > 48 * 1024)

@@ -207,9 +207,16 @@ static int exec_chunk(const Plan &p, char *ws, int j, int64_t p0, int64_t pc, co
     return launch_post_add(p.W, add_algo, pc, cM, shift(C, p0), beta, s);
 }
 
+static const char *kLevelNames[] = {"level 0", "level 1", "level 2", "level 3", "level 4", "level 5",
+                                     "level 6", "level 7", "level 8+"};
+
 static int exec_level(const Plan &p, char *ws, int j, int64_t cnt, const MatDesc &A,
                       const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s, int lane) {
-    if (j == p.d) return launch_leaf_gemm(p.W, p.m[j], p.l[j], p.n[j], cnt, A, B, C, beta, p.mv, s);
+    if (j == p.d) {
+        NvtxRange nv("leaf GEMM");
+        return launch_leaf_gemm(p.W, p.m[j], p.l[j], p.n[j], cnt, A, B, C, beta, p.mv, s);
+    }
+    NvtxRange nv(kLevelNames[j < 8 ? j : 8]);
     const int64_t nch = (cnt + p.chunk[j] - 1) / p.chunk[j];
     int rc;
     if (p.lanes == 2 && j == p.s - 1 && nch >= 2) {
