@@ -32,6 +32,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // k-step unroll of the inner loop: 4 lets the compiler issue the next steps' shared-memory
 // fragment loads under the current step's FP64 chains. Measured (c3 cp.async leaf / c2 QD):
 // 1: 0.9162 / 0.8795, 2: 0.9194, 4: 0.9218 / 0.8799, 8: 0.9233 / 0.7997 of the FP64 peak.
+// QD keeps 1: on ragged leaves (2000x1500x1800 Winograd(256): 500x375x450 leaves, whose edge
+// tiles mix real and zero-padded lanes that take different renormalisation branches) the
+// unrolled QD loop measured 0.633 vs 0.751 of the peak.
 // (The TMA leaf takes 2: see leaf_tma.cu.)
 #ifndef LEAF_KK_UNROLL
 #define LEAF_KK_UNROLL 4
@@ -63,6 +66,7 @@ leaf_gemm_kernel(int64_t m, int64_t l, int64_t n, MatDesc A, MatDesc B, MatDesc 
                  int64_t batch0) {
     using Cfg = LeafCfg<W, BM, BN, BK, TM, TN, STAGES>;
     using E = arith<W, MV>;   // MV: 0 canonical, 1 fused DD madd, 2 accurate adds
+    constexpr int kUnroll = W == 2 ? kLeafKkUnroll : 1;   // QD: see kLeafKkUnroll
     using T = typename E::T;
     constexpr int NT = Cfg::NT;
     extern __shared__ __align__(16) double smem[];
@@ -126,7 +130,7 @@ leaf_gemm_kernel(int64_t m, int64_t l, int64_t n, MatDesc A, MatDesc B, MatDesc 
         const double *bs = Bs + st * Cfg::B_STAGE;
         const int64_t krem = l - kt * BK;
         const int kmax = krem < BK ? (int)krem : BK;   // uniform: no madds past l
-#pragma unroll kLeafKkUnroll
+#pragma unroll kUnroll
         for (int kk = 0; kk < kmax; kk++) {
             double av[W][TM], bv[W][TN];
 #pragma unroll
