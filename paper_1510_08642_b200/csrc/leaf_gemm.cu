@@ -88,6 +88,16 @@ leaf_gemm_kernel(int64_t m, int64_t l, int64_t n, MatDesc A, MatDesc B, MatDesc 
         for (int j = 0; j < TN; j++) acc[i][j] = E::zero();
 
     const int64_t KT = (l + BK - 1) / BK;
+    // QD: micro-tile entries outside C (zero-padded rows/columns of edge tiles) are skipped.
+    // Their lanes would otherwise take the zero branches of the renormalisation while their
+    // neighbours take the data branches, and the warp would run both; skipping leaves one path.
+    // (Never stored either way, so the results are unchanged; DD has no data branches.)
+    bool live[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; i++)
+#pragma unroll
+        for (int j = 0; j < TN; j++)
+            live[i][j] = W == 2 || (row0 + micro_idx<BM, TM>(ty, i) < m && col0 + micro_idx<BN, TN>(tx, j) < n);
 
     auto load_stage = [&](int stage, int64_t kt) {
         const int64_t k0 = kt * BK;
@@ -164,7 +174,7 @@ leaf_gemm_kernel(int64_t m, int64_t l, int64_t n, MatDesc A, MatDesc B, MatDesc 
 #pragma unroll
                         for (int w = 0; w < W; w++) bb.w[w] = bv[w][j];
                     }
-                    acc[i][j] = E::madd(acc[i][j], a, bb);
+                    if (W == 2 || live[i][j]) acc[i][j] = E::madd(acc[i][j], a, bb);
                 }
             }
         }
