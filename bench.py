@@ -520,6 +520,17 @@ def main():
             roofline["traffic"] = tr
             roofline["traffic_source"] = src
     leaf_madds_step = (7 ** d) * shapes[-1][0] * shapes[-1][1] * shapes[-1][2]
+    # whole-step algorithmic roofline: the leaf's FP64 work at the FP64 peak plus the additions'
+    # algorithmic bytes at the HBM peak, over the measured step time
+    hbm_peak, hbm_src = 6550.7e9, "MEASURED_PEAKS.json (driver copy benchmark)"
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm_peak = float(json.load(f)["hbm_gbs"]) * 1e9
+    except Exception:
+        hbm_src = "the driver's last measured copy bandwidth (file absent)"
+    add_bytes_step = (prof["pre"][2] + prof["post"][2]) / args.steps
+    step_alg = ((ops * leaf_madds_step / peak + add_bytes_step / hbm_peak) / (ms_per_step * 1e-3)
+                if world == 1 else None)   # per-rank profiles do not add up to the whole job
     classical = ops * m * l * n / (ms_per_step * 1e-3) / peak   # BJ:5's literal formula (may be > 1)
 
     variants = None
@@ -596,8 +607,11 @@ def main():
             "roofline": roofline,
             "fp64_roofline_fraction": {
                 "algorithmic_leaf": roofline["frac"],
+                "algorithmic_step": step_alg,
                 "classical_normalised": classical,
-                "note": "classical = ops_per_madd*m*l*n/(P64*t) (BJ:5 literal; > 1 possible for Strassen/Winograd)"},
+                "note": "algorithmic_step = (ops_per_madd*leaf_madds/P64 + addition_bytes/HBM_peak) / t_step "
+                        "(SURVEY.md s.8(d); HBM peak %.0f GB/s from %s); classical = ops_per_madd*m*l*n/(P64*t) "
+                        "(BJ:5 literal; > 1 possible for Strassen/Winograd)" % (hbm_peak / 1e9, hbm_src)},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "variants": variants,
