@@ -135,17 +135,24 @@ __global__ void __launch_bounds__(ADD2_THREADS, ADD2_MINB) pre_add2_kernel(int64
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = t / per, rem = t % per, i = rem / hc, j = rem % hc;
         const double *xb = X.p + b * X.bs;
-        T y[4][7];
+        // all 16 loads first (predicated, zero-filled), so they are in flight together
+        T x[4][4];
+        bool live[4];
 #pragma unroll
         for (int sp = 0; sp < 4; sp++) {
             const int64_t r = i + (sp >> 1) * hr, c = j + (sp & 1) * hc;
-            if (r < h1r && c < h1c) {
-                const bool r2 = r + h1r < X.rows, c2 = c + h1c < X.cols;
-                const T x11 = E::load(xb + r * X.ld + c, X.ps);
-                const T x12 = ld_or_zero<W>(xb + r * X.ld + (c + h1c), X.ps, c2);
-                const T x21 = ld_or_zero<W>(xb + (r + h1r) * X.ld + c, X.ps, r2);
-                const T x22 = ld_or_zero<W>(xb + (r + h1r) * X.ld + (c + h1c), X.ps, r2 && c2);
-                pre_ops<E, ALGO, SIDE>(x11, x12, x21, x22, y[sp]);
+            live[sp] = r < h1r && c < h1c;
+            const bool r2 = r + h1r < X.rows, c2 = c + h1c < X.cols;
+            x[sp][0] = ld_or_zero<W>(xb + r * X.ld + c, X.ps, live[sp]);
+            x[sp][1] = ld_or_zero<W>(xb + r * X.ld + (c + h1c), X.ps, live[sp] && c2);
+            x[sp][2] = ld_or_zero<W>(xb + (r + h1r) * X.ld + c, X.ps, live[sp] && r2);
+            x[sp][3] = ld_or_zero<W>(xb + (r + h1r) * X.ld + (c + h1c), X.ps, live[sp] && r2 && c2);
+        }
+        T y[4][7];
+#pragma unroll
+        for (int sp = 0; sp < 4; sp++) {
+            if (live[sp]) {
+                pre_ops<E, ALGO, SIDE>(x[sp][0], x[sp][1], x[sp][2], x[sp][3], y[sp]);
             } else {
 #pragma unroll
                 for (int k = 0; k < 7; k++) y[sp][k] = E::zero();
