@@ -10,7 +10,11 @@
 // size = whole batch (breadth-first) below a split level s and 1 parent (depth-first)
 // above it; s is the smallest level whose breadth-first workspace fits the limit. The
 // chunking changes only the launch grouping, never the arithmetic: results are bitwise
-// those of the oracle's recursion.
+// those of the oracle's recursion. Where level j+1 is breadth-first, the additions of two
+// levels run as one pass (pre_add2 / post_add2, DD). Optionally (DDQD_LANES=2) the chunks of
+// the last depth-first level alternate between two streams with separate workspace.
+// Arithmetic variants ride in Plan::mv: bits 0-3 the madd/add variant, bits 4-5 log2 of the
+// split-k factor of the leaves.
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
