@@ -1,0 +1,33 @@
+"""bench.py's reference arm (the oracle timed on the host cores) runs without a GPU: it must
+print one JSON line with the same metric/config keys as our arm (CPU only)."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(*args):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                       cwd=ROOT, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_gemm_line():
+    d = _run("--impl", "reference", "--workload", "c1", "--steps", "1", "--warmup", "0")
+    assert d["impl"] == "reference"
+    assert d["metric"] == "DD/QD GEMM effective GFLOPS (2mln/s) and % FP64-pipe roofline"
+    assert d["unit"] == "GFLOP/s" and d["higher_is_better"] is True and d["value"] > 0
+    assert d["config"]["m"] == d["config"]["l"] == d["config"]["n"] == 1024
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+def test_reference_arm_custom_workload():
+    d = _run("--impl", "reference", "--custom", "100,90,80", "--prec", "qd", "--algo", "strassen",
+             "--threshold", "16", "--steps", "1", "--warmup", "0")
+    assert d["config"]["algo"] == "strassen" and d["value"] > 0
