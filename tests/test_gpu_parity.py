@@ -121,6 +121,30 @@ def test_errors():
         ddqd.dd_gemm(A, A, out=A)                  # aliasing -> EALIAS
 
 
+def test_abi_errors_of_the_newer_entry_points():
+    """Argument errors of the LU step, peer-memory combine and IPC entry points come back as
+    status codes (no crash, no exception across the ABI), with a message."""
+    import ctypes
+    L = ddqd.lib
+    A = cu(gen.dd_matrix(8, 8, 1, 0))
+    ipiv = torch.empty(8, dtype=torch.int64, device=DEV)
+    assert L.ddqd_lu_panel(2, 1, 8, A.data_ptr(), ipiv.data_ptr(), 4, 8) == -1    # p + kb > n
+    assert L.ddqd_lu_panel(3, 1, 8, A.data_ptr(), ipiv.data_ptr(), 0, 4) == -1    # bad precision
+    assert L.ddqd_lu_panel(2, 1, 8, None, ipiv.data_ptr(), 0, 4) == -1             # null pointer
+    assert L.ddqd_last_error()
+    assert L.ddqd_lu_trsv(2, 8, None, None, None, None) == -1
+    M = ddqd.Mat(A.data_ptr(), 8, 8, 8, 64, 128)
+    assert L.ddqd_post_add_ptrs(2, 1, 1, None, 4, 4, 4, 16, 0, 4, ctypes.byref(M), 0) == -1   # no pointer table
+    assert L.ddqd_post_add_ptrs(2, 3, 1, A.data_ptr(), 4, 4, 4, 16, 0, 4, ctypes.byref(M), 0) == -1  # bad algo
+    assert L.ddqd_post_add_ptrs(2, 1, 1, A.data_ptr(), 3, 4, 4, 16, 0, 3, ctypes.byref(M), 0) == -1  # hm != ceil(8/2)
+    assert L.ddqd_ipc_handle(None, None) == -1
+    assert L.ddqd_ipc_open(None, None) == -1
+    with pytest.raises(ValueError):
+        ddqd.dd_gemm(A, A, "block", splitk=3)           # split-k must be 1, 2, 4 or 8
+    with pytest.raises(ValueError):
+        ddqd.gemm(A, A, 0x4000 | 0, 8)                   # unknown algo flag -> EINVAL
+
+
 # ---- recursion --------------------------------------------------------------------
 @pytest.mark.parametrize("algo", ["strassen", "winograd"])
 @pytest.mark.parametrize("W", [2, 4])
