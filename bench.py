@@ -294,11 +294,13 @@ def lu_bench(args, wl, rank, world, local):
         assert info == 0, info
         return e0.elapsed_time(e1)
 
-    for _ in range(args.warmup):
-        step()
     peak = max(ddqd.fp64_peak("dadd")[0], ddqd.fp64_peak("dfma")[0])
+    # the sampler starts before the warm-up: its 0.5 s start-up idles the GPU, which must not
+    # sit right before the timed region (the clocks would ramp inside it)
     clocks = Clocks(local)
     clocks.start()
+    for _ in range(args.warmup):
+        step()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -454,12 +456,11 @@ def main():
         def step():
             ddqd.gemm(A, B, algo, T, out=C, madd=args.madd)
 
+    clocks = Clocks(local)      # before the warm-up (see the LU path)
+    clocks.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-
-    clocks = Clocks(local)
-    clocks.start()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()

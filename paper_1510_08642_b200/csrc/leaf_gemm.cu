@@ -256,6 +256,21 @@ static bool tma_enabled() {
 int launch_leaf_splitk(int W, int split, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
                        const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s);   // leaf_splitk.cu
 
+// DDQD_LEAF_TAIL=0 disables the tail split below (A/B measurements)
+static bool tail_split_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_LEAF_TAIL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+static MatDesc shift_batch(MatDesc d, int64_t b0) { d.p += b0 * d.bs; return d; }
+
+static int launch_leaf_one(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
+                           const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s);
+
 int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
                      const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s) {
     if (m == 0 || n == 0 || batch == 0) return DDQD_OK;
@@ -263,6 +278,37 @@ int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, cons
     const int split = 1 << ((mv >> 4) & 3);
     mv &= 0xf;
     if (split > 1) return launch_leaf_splitk(W, split, m, l, n, batch, A, B, C, beta, mv, s);
+    // Tail split (DD): a batch of 64x64-tile leaves whose last wave would leave most of the
+    // GPU idle runs its whole waves with 64x64 tiles and the remaining leaves with 32x32 tiles
+    // (4x the CTAs for the same work) -- same per-element order, so the same bits.
+    // E.g. c1: 343 leaves x 4 tiles = 1372 CTAs = 4.64 waves of 296 (1.071 -> 1.047 ms).
+    // Only for batches of >= 32 leaves: on the 7-leaf Strassen updates of the c4 LU the
+    // model below also predicts a gain, but the measured step was not faster (58.25 vs 58.5 ms).
+    if (W == 2 && tail_split_enabled() && leaf_cfg_override() < 0 && m > 32 && n > 32 && batch >= 32) {
+        const int64_t t = ((m + 63) / 64) * ((n + 63) / 64), slots = 2 * 148;
+        const int64_t total = t * batch, waves = total / slots, rem = total % slots;
+        if (waves >= 2 && rem > 0 && rem * 4 < slots * 3) {   // last wave under 75% full
+            const int64_t b1 = waves * slots / t;              // leaves filling the whole waves
+            // cost model in big-tile wave times: a 32x32 tile is 1/4 of the work at ~0.8 of
+            // the efficiency, 4 fit per SM; split only when it saves >= 5%
+            const int64_t small = (batch - b1) * t * 4, slots_small = 4 * 148;
+            const double t_split = (double)((b1 * t + slots - 1) / slots) +
+                                   0.3125 * (double)((small + slots_small - 1) / slots_small);
+            if (b1 > 0 && b1 < batch && t_split < 0.95 * (double)(waves + 1)) {
+                int rc = launch_leaf_one(W, m, l, n, b1, A, B, C, beta, mv, s);
+                if (rc) return rc;
+                const MatDesc A2 = shift_batch(A, b1), B2 = shift_batch(B, b1), C2 = shift_batch(C, b1);
+                if (mv == 1) return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2, 1>(m, l, n, batch - b1, A2, B2, C2, beta, s);
+                if (mv == 2) return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2, 2>(m, l, n, batch - b1, A2, B2, C2, beta, s);
+                return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2>(m, l, n, batch - b1, A2, B2, C2, beta, s);
+            }
+        }
+    }
+    return launch_leaf_one(W, m, l, n, batch, A, B, C, beta, mv, s);
+}
+
+static int launch_leaf_one(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
+                           const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s) {
     if (W == 2 && mv != 2 && tma_enabled() && leaf_cfg_override() < 0) {
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
         if (big_tiles >= 2 * 148 && m > 32 && n > 32) {

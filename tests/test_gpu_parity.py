@@ -815,3 +815,16 @@ def test_two_lane_schedule_same_bits(orc, tmp_path):
     assert same(z["arr_0"], orc.gemm(A, B, "winograd", threshold=32))
     Q = gen.qd_matrix(260, 250, 5, 0); R = gen.qd_matrix(250, 270, 5, 1)
     assert same(z["arr_1"], orc.gemm(Q, R, "strassen", threshold=16))
+
+
+@pytest.mark.parametrize("algo,madd", [("strassen", "canonical"), ("winograd", "canonical"),
+                                       ("strassen", "fused"), ("winograd", "accurate")])
+def test_leaf_tail_split_bitwise(orc, algo, madd):
+    """The DD leaf tail split (whole waves on 64x64 tiles, the remaining leaves on 32x32
+    tiles): 557^3 with T = 64 gives 343 ragged 70x70 leaves = 1372 CTAs, 4.6 waves -- the
+    c1 situation with ragged tiles; bit-identical to the oracle for every madd variant."""
+    m, l, n = 557, 556, 558
+    A = gen.dd_matrix(m, l, 31, 0)
+    B = gen.dd_matrix(l, n, 31, 1)
+    got = np_(ddqd.dd_gemm(cu(A), cu(B), algo, 64, madd=madd))
+    assert same(got, orc.gemm(A, B, algo, threshold=64, madd=madd))
