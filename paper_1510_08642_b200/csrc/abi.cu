@@ -163,6 +163,66 @@ static int check_gemm_args(int64_t m, int64_t l, int64_t n, int algo, int64_t T)
     return DDQD_OK;
 }
 
+size_t streamed_top_bytes(int W, int64_t m, int64_t l, int64_t n);   // recursion.cu
+int run_gemm_streamed(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n, const MatDesc &A,
+                      const MatDesc &B, const MatDesc &C, char *tws, cudaEvent_t rest_ready,
+                      cudaStream_t s, int (*on_quad)(int q, void *ctx), void *ctx);
+
+// DDQD_HOST_STREAM=0 disables the overlapped host path (A/B measurements)
+static bool host_stream_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_HOST_STREAM");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// copy stream + events of the overlapped host path, per host thread and device
+struct CopyRes {
+    cudaStream_t cs = nullptr;
+    cudaEvent_t start = nullptr, first = nullptr, rest = nullptr, quad = nullptr;
+};
+
+// device-to-host copy of one finished C quadrant on the copy stream (run_gemm_streamed's hook)
+struct QuadCopy {
+    CopyRes *cr;
+    cudaStream_t s;
+    int W;
+    int64_t m, n;
+    const double *dC;
+    double *hC;
+};
+static int copy_quad(int q, void *ctx) {
+    const QuadCopy &c = *static_cast<QuadCopy *>(ctx);
+    const int64_t hm = (c.m + 1) / 2, hn = (c.n + 1) / 2;
+    const int64_t r0 = q >= 2 ? hm : 0, nr = q >= 2 ? c.m - hm : hm;
+    const int64_t c0 = (q & 1) ? hn : 0, nc = (q & 1) ? c.n - hn : hn;
+    if (nr == 0 || nc == 0) return DDQD_OK;
+    DDQD_CUDA_CHECK(cudaEventRecord(c.cr->quad, c.s));
+    DDQD_CUDA_CHECK(cudaStreamWaitEvent(c.cr->cs, c.cr->quad, 0));
+    const size_t d8 = sizeof(double);
+    for (int w = 0; w < c.W; w++) {
+        const int64_t off = w * c.m * c.n + r0 * c.n + c0;
+        DDQD_CUDA_CHECK(cudaMemcpy2DAsync(c.hC + off, c.n * d8, c.dC + off, c.n * d8, nc * d8, nr,
+                                          cudaMemcpyDeviceToHost, c.cr->cs));
+    }
+    return DDQD_OK;
+}
+static int copy_res(CopyRes **out) {
+    static thread_local CopyRes res[64];
+    CopyRes &r = res[current_device()];
+    if (!r.cs) {
+        DDQD_CUDA_CHECK(cudaStreamCreateWithFlags(&r.cs, cudaStreamNonBlocking));
+        DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.start, cudaEventDisableTiming));
+        DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.first, cudaEventDisableTiming));
+        DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.rest, cudaEventDisableTiming));
+        DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.quad, cudaEventDisableTiming));
+    }
+    *out = &r;
+    return DDQD_OK;
+}
+
 static int gemm_entry(int W, int64_t m, int64_t l, int64_t n, const double *A, const double *B,
                        double *C, int algo, int64_t T) {
     NvtxRange nv(W == 2 ? "dd_gemm" : "qd_gemm");
@@ -184,17 +244,68 @@ static int gemm_entry(int W, int64_t m, int64_t l, int64_t n, const double *A, c
     }
     if (!(wa == 1 && wb == 1 && wc == 1)) { set_error("A, B, C must be all device or all host pointers"); return DDQD_EINVAL; }
     // host path: stage through library-owned device memory, copy back, synchronise
+    const bool streamed = (algo & 0xff) == DDQD_WINOGRAD && std::min(std::min(m, l), n) > T &&
+                          host_stream_enabled();
+    const size_t oB = (bA + 255) & ~size_t(255), oC = oB + ((bB + 255) & ~size_t(255)),
+                 oT = oC + ((bC + 255) & ~size_t(255));
     int st = DDQD_OK;
-    char *dev = static_cast<char *>(buf_get(g_stage, bA + bB + bC + 512, &st, "staging buffers"));
+    char *dev = static_cast<char *>(buf_get(g_stage, oT + (streamed ? streamed_top_bytes(W, m, l, n) : 0) + 256,
+                                            &st, "staging buffers"));
     if (st) return st;
     double *dA = reinterpret_cast<double *>(dev);
-    double *dB = reinterpret_cast<double *>(dev + ((bA + 255) & ~size_t(255)));
-    double *dC = reinterpret_cast<double *>(dev + ((bA + 255) & ~size_t(255)) + ((bB + 255) & ~size_t(255)));
-    if (bA) DDQD_CUDA_CHECK(cudaMemcpyAsync(dA, A, bA, cudaMemcpyHostToDevice, s));
-    if (bB) DDQD_CUDA_CHECK(cudaMemcpyAsync(dB, B, bB, cudaMemcpyHostToDevice, s));
+    double *dB = reinterpret_cast<double *>(dev + oB);
+    double *dC = reinterpret_cast<double *>(dev + oC);
     MatDesc mA{dA, m, l, l, m * l, 0}, mB{dB, l, n, n, l * n, 0}, mC{dC, m, n, n, m * n, 0};
-    rc = run_gemm(W, algo, T, m, l, n, 1, mA, mB, mC, 0, s);
-    if (rc) return rc;
+    if (streamed) {
+        // Winograd: A11 and B11 first on the copy stream; M1 = A11 B11 runs while the rest of
+        // A and B is copied (run_gemm_streamed); bitwise the same result as the plain path
+        CopyRes *cr;
+        if ((rc = copy_res(&cr))) return rc;
+        const int64_t hm = (m + 1) / 2, hl = (l + 1) / 2, hn = (n + 1) / 2;
+        const size_t d8 = sizeof(double);
+        cudaStream_t cs = cr->cs;
+        DDQD_CUDA_CHECK(cudaEventRecord(cr->start, s));
+        DDQD_CUDA_CHECK(cudaStreamWaitEvent(cs, cr->start, 0));
+        for (int w = 0; w < W; w++) {
+            DDQD_CUDA_CHECK(cudaMemcpy2DAsync(dA + w * m * l, l * d8, A + w * m * l, l * d8, hl * d8, hm,
+                                              cudaMemcpyHostToDevice, cs));
+            DDQD_CUDA_CHECK(cudaMemcpy2DAsync(dB + w * l * n, n * d8, B + w * l * n, n * d8, hn * d8, hl,
+                                              cudaMemcpyHostToDevice, cs));
+        }
+        DDQD_CUDA_CHECK(cudaEventRecord(cr->first, cs));
+        for (int w = 0; w < W; w++) {
+            DDQD_CUDA_CHECK(cudaMemcpy2DAsync(dA + w * m * l + hl, l * d8, A + w * m * l + hl, l * d8,
+                                              (l - hl) * d8, hm, cudaMemcpyHostToDevice, cs));
+            DDQD_CUDA_CHECK(cudaMemcpyAsync(dA + w * m * l + hm * l, A + w * m * l + hm * l, (m - hm) * l * d8,
+                                            cudaMemcpyHostToDevice, cs));
+            DDQD_CUDA_CHECK(cudaMemcpy2DAsync(dB + w * l * n + hn, n * d8, B + w * l * n + hn, n * d8,
+                                              (n - hn) * d8, hl, cudaMemcpyHostToDevice, cs));
+            DDQD_CUDA_CHECK(cudaMemcpyAsync(dB + w * l * n + hl * n, B + w * l * n + hl * n, (l - hl) * n * d8,
+                                            cudaMemcpyHostToDevice, cs));
+        }
+        DDQD_CUDA_CHECK(cudaEventRecord(cr->rest, cs));
+        DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, cr->first, 0));
+        // C quadrant by quadrant (each copied back while the next products run) when a quadrant
+        // is >= 32 MB; measured on c2 (8 MB quadrants) the split products cost more than the
+        // overlapped copy gains (10.5 vs 10.2 ms), on c3 (268 MB) it saves 14 ms per call
+        const bool quads = (size_t)W * hm * hn * d8 >= (size_t(32) << 20);
+        QuadCopy qc{cr, s, W, m, n, dC, C};
+        rc = run_gemm_streamed(W, algo, T, m, l, n, mA, mB, mC, dev + oT, cr->rest, s,
+                               quads ? copy_quad : nullptr, &qc);
+        // the copy stream must not outlive the call into the caller's buffers
+        cudaError_t e = cudaStreamSynchronize(cs);
+        if (rc) return rc;
+        if (e != cudaSuccess) { set_error(std::string("copy stream: ") + cudaGetErrorString(e)); return DDQD_ECUDA; }
+        if (quads) {
+            DDQD_CUDA_CHECK(cudaStreamSynchronize(s));
+            return DDQD_OK;
+        }
+    } else {
+        if (bA) DDQD_CUDA_CHECK(cudaMemcpyAsync(dA, A, bA, cudaMemcpyHostToDevice, s));
+        if (bB) DDQD_CUDA_CHECK(cudaMemcpyAsync(dB, B, bB, cudaMemcpyHostToDevice, s));
+        rc = run_gemm(W, algo, T, m, l, n, 1, mA, mB, mC, 0, s);
+        if (rc) return rc;
+    }
     DDQD_CUDA_CHECK(cudaMemcpyAsync(C, dC, bC, cudaMemcpyDeviceToHost, s));
     DDQD_CUDA_CHECK(cudaStreamSynchronize(s));
     return DDQD_OK;

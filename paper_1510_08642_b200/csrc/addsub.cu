@@ -169,7 +169,10 @@ __global__ void __launch_bounds__(ADD2_THREADS, ADD2_MINB) pre_add2_kernel(int64
     }
 }
 
-template <int W, int ALGO, int V>
+// Q >= 0 forms only C quadrant Q (0 = C11, 1 = C12, 2 = C21, 3 = C22; the other values and the
+// products they alone read are dead code): the host-streamed top level writes C quadrant by
+// quadrant so each one's device-to-host copy overlaps the remaining products.
+template <int W, int ALGO, int V, int Q = -1>
 __global__ void __launch_bounds__(256) post_add_kernel(int64_t P, MatDesc M, MatDesc C, int beta) {
     using E = arith<W, V>;
     using T = typename E::T;
@@ -191,10 +194,10 @@ __global__ void __launch_bounds__(256) post_add_kernel(int64_t P, MatDesc M, Mat
             if (beta) E::store(q, C.ps, E::sub(E::load(q, C.ps), v));
             else E::store(q, C.ps, v);
         };
-        if (i < C.rows && j < C.cols) put(i, j, c11);
-        if (i < C.rows && cc2) put(i, j + hn, c12);
-        if (r2 && j < C.cols) put(i + hm, j, c21);
-        if (r2 && cc2) put(i + hm, j + hn, c22);
+        if ((Q < 0 || Q == 0) && i < C.rows && j < C.cols) put(i, j, c11);
+        if ((Q < 0 || Q == 1) && i < C.rows && cc2) put(i, j + hn, c12);
+        if ((Q < 0 || Q == 2) && r2 && j < C.cols) put(i + hm, j, c21);
+        if ((Q < 0 || Q == 3) && r2 && cc2) put(i + hm, j + hn, c22);
     }
 }
 
@@ -350,6 +353,38 @@ int launch_post_add(int W, int algo, int64_t P, const MatDesc &M, const MatDesc 
     algo &= 0xff;
     if (W == 2) return acc ? post_dispatch<2, 2>(algo, P, M, C, beta, s) : post_dispatch<2, 0>(algo, P, M, C, beta, s);
     return acc ? post_dispatch<4, 2>(algo, P, M, C, beta, s) : post_dispatch<4, 0>(algo, P, M, C, beta, s);
+}
+
+template <int W, int V>
+static int post_quad_dispatch(int algo, int q, const MatDesc &M, const MatDesc &C, cudaStream_t s) {
+    const int64_t total = M.rows * M.cols;
+    if (total == 0) return DDQD_OK;
+    const unsigned g = grid_for(total);
+    static const double reads[2][4] = {{4, 2, 2, 4}, {2, 4, 4, 4}};   // products read: Strassen, Winograd
+    prof_begin(2, s);
+    if (algo == 1) {
+        if (q == 0) post_add_kernel<W, 1, V, 0><<<g, 256, 0, s>>>(1, M, C, 0);
+        else if (q == 1) post_add_kernel<W, 1, V, 1><<<g, 256, 0, s>>>(1, M, C, 0);
+        else if (q == 2) post_add_kernel<W, 1, V, 2><<<g, 256, 0, s>>>(1, M, C, 0);
+        else post_add_kernel<W, 1, V, 3><<<g, 256, 0, s>>>(1, M, C, 0);
+    } else {
+        if (q == 0) post_add_kernel<W, 2, V, 0><<<g, 256, 0, s>>>(1, M, C, 0);
+        else if (q == 1) post_add_kernel<W, 2, V, 1><<<g, 256, 0, s>>>(1, M, C, 0);
+        else if (q == 2) post_add_kernel<W, 2, V, 2><<<g, 256, 0, s>>>(1, M, C, 0);
+        else post_add_kernel<W, 2, V, 3><<<g, 256, 0, s>>>(1, M, C, 0);
+    }
+    DDQD_LAUNCH_CHECK();
+    prof_end(2, (double)total * W * 8.0 * (reads[algo == 2][q] + 1.0), s);
+    return DDQD_OK;
+}
+
+// one C quadrant of a single parent's post-addition (the host-streamed top level)
+int launch_post_quad(int W, int algo, int q, const MatDesc &M, const MatDesc &C, cudaStream_t s) {
+    const bool acc = (algo & DDQD_ADD_ACCURATE) != 0;
+    algo &= 0xff;
+    if (q < 0 || q > 3 || (algo != 1 && algo != 2)) { set_error("launch_post_quad: bad quadrant/algo"); return DDQD_EINVAL; }
+    if (W == 2) return acc ? post_quad_dispatch<2, 2>(algo, q, M, C, s) : post_quad_dispatch<2, 0>(algo, q, M, C, s);
+    return acc ? post_quad_dispatch<4, 2>(algo, q, M, C, s) : post_quad_dispatch<4, 0>(algo, q, M, C, s);
 }
 
 // ---- post-addition over peer memory (the multi-GPU fused combine) --------

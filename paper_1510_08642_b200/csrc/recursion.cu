@@ -264,3 +264,72 @@ int run_gemm(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n, int64_
 }
 
 }  // namespace ddqd
+
+namespace ddqd {
+
+// ---- host-streamed top level (the host-pointer entry, Winograd) -----------------------------
+// Winograd's first product M1 = A11 B11 reads only the leading quadrants, so the host
+// path copies A11 and B11 first and runs M1 while the copy engine brings in the rest of A and
+// B; then the top level's pre-additions and the other products in an order that completes C
+// quadrant by quadrant -- C11 = U1 after M2; C22 = U7 after M6, M7, M5; C12 = U5 after M3;
+// C21 = U6 after M4 -- each quadrant formed by its own post-addition pass (the same chain of
+// DD/QD operations per element) and handed to on_quad, which starts its device-to-host copy
+// while the next products run (for a small C -- on_quad null -- M2..M7 run as one batch and
+// one post-addition forms C: there the batch's fuller waves are worth more than the overlapped
+// copy). Each product is the same recursion as in run_gemm (the
+// planner's chunking never changes the arithmetic), so the result is bitwise that of the
+// device-pointer call.
+static void top_shapes(int64_t m, int64_t l, int64_t n, int64_t *hm, int64_t *hl, int64_t *hn) {
+    *hm = (m + 1) / 2; *hl = (l + 1) / 2; *hn = (n + 1) / 2;
+}
+
+size_t streamed_top_bytes(int W, int64_t m, int64_t l, int64_t n) {
+    int64_t hm, hl, hn;
+    top_shapes(m, l, n, &hm, &hl, &hn);
+    const size_t w = (size_t)7 * W * sizeof(double);
+    return align256(w * hm * ws_ld(hl)) + align256(w * hl * ws_ld(hn)) + align256(w * hm * ws_ld(hn));
+}
+
+int run_gemm_streamed(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n, const MatDesc &A,
+                      const MatDesc &B, const MatDesc &C, char *tws, cudaEvent_t rest_ready,
+                      cudaStream_t s, int (*on_quad)(int q, void *ctx), void *ctx) {
+    int64_t hm, hl, hn;
+    top_shapes(m, l, n, &hm, &hl, &hn);
+    const size_t w = (size_t)7 * W * sizeof(double);
+    auto kid = [&](char *base, int64_t r, int64_t c) {
+        MatDesc d;
+        d.p = reinterpret_cast<double *>(base);
+        d.rows = r; d.cols = c; d.ld = ws_ld(c); d.ps = r * d.ld; d.bs = (int64_t)W * d.ps;
+        return d;
+    };
+    const MatDesc cA = kid(tws, hm, hl);
+    const MatDesc cB = kid(tws + align256(w * hm * ws_ld(hl)), hl, hn);
+    const MatDesc cM = kid(tws + align256(w * hm * ws_ld(hl)) + align256(w * hl * ws_ld(hn)), hm, hn);
+    const int add_algo = (algo & 0xff) | (algo & DDQD_ADD_ACCURATE);
+    int rc;
+    {
+        NvtxRange nv("M1 = A11 B11 (overlaps the H2D copy)");
+        MatDesc a11 = A, b11 = B;
+        a11.rows = hm; a11.cols = hl; b11.rows = hl; b11.cols = hn;
+        if ((rc = run_gemm(W, algo, T, hm, hl, hn, 1, a11, b11, cM, 0, s))) return rc;
+    }
+    DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, rest_ready, 0));
+    NvtxRange nv("level 0 (streamed)");
+    if ((rc = launch_pre_add(W, add_algo, 0, 1, A, cA, s))) return rc;
+    if ((rc = launch_pre_add(W, add_algo, 1, 1, B, cB, s))) return rc;
+    if (!on_quad) {   // small C: M2..M7 as one batch (better filled waves), one post-addition
+        if ((rc = run_gemm(W, algo, T, hm, hl, hn, 6, shift(cA, 1), shift(cB, 1), shift(cM, 1), 0, s))) return rc;
+        return launch_post_add(W, add_algo, 1, cM, C, 0, s);
+    }
+    // (first product index, count) of each step, then the quadrant it completes
+    static const int steps[4][3] = {{1, 1, 0}, {4, 3, 3}, {2, 1, 1}, {3, 1, 2}};
+    for (const auto &st : steps) {
+        if ((rc = run_gemm(W, algo, T, hm, hl, hn, st[1], shift(cA, st[0]), shift(cB, st[0]),
+                           shift(cM, st[0]), 0, s))) return rc;
+        if ((rc = launch_post_quad(W, add_algo, st[2], cM, C, s))) return rc;
+        if (on_quad && (rc = on_quad(st[2], ctx))) return rc;
+    }
+    return DDQD_OK;
+}
+
+}  // namespace ddqd

@@ -828,3 +828,40 @@ def test_leaf_tail_split_bitwise(orc, algo, madd):
     B = gen.dd_matrix(l, n, 31, 1)
     got = np_(ddqd.dd_gemm(cu(A), cu(B), algo, 64, madd=madd))
     assert same(got, orc.gemm(A, B, algo, threshold=64, madd=madd))
+
+
+@pytest.mark.parametrize("W", [2, 4])
+def test_host_streamed_winograd_bitwise(orc, W):
+    """The overlapped host path (Winograd: A11, B11 copied first and M1 = A11 B11 computed
+    while the rest of A and B is copied; then the top level's pre-adds, M2..M7 as a batch,
+    the post-adds): bitwise the device-pointer call and the oracle -- odd and even
+    dimensions (ragged quadrants), depth 1 to 3, pinned and pageable host memory, the
+    arithmetic variants."""
+    gemm = ddqd.dd_gemm if W == 2 else ddqd.qd_gemm
+    cases = [(129, 130, 131, 64, "canonical", True), (200, 201, 199, 32, "canonical", False),
+             (97, 64, 65, 16, "accurate", True), (66, 67, 68, 32, "fused", True)]
+    for m, l, n, T, madd, pin in cases:
+        A = gen.matrix(W, m, l, m + T, 0)
+        B = gen.matrix(W, l, n, m + T, 1)
+        hA, hB = torch.from_numpy(A), torch.from_numpy(B)
+        if pin:
+            hA, hB = hA.pin_memory(), hB.pin_memory()
+        hC = gemm(hA, hB, "winograd", T, madd=madd).numpy()
+        assert same(hC, np_(gemm(cu(A), cu(B), "winograd", T, madd=madd))), (m, l, n, madd)
+        assert same(hC, orc.gemm(A, B, "winograd", threshold=T, madd=madd)), (m, l, n, madd)
+
+
+@pytest.mark.parametrize("madd", ["canonical", "accurate"])
+def test_host_streamed_winograd_quadrant_copies(madd):
+    """The quadrant-by-quadrant host path (C quadrants >= 32 MB: each formed by its own
+    post-addition pass and copied back while the next products run): bitwise the
+    device-pointer call, ragged quadrants (odd m and n), pinned and pageable C."""
+    m, l, n, T = 2901, 130, 2899, 64
+    A = gen.dd_matrix(m, l, 77, 0)
+    B = gen.dd_matrix(l, n, 77, 1)
+    dev = np_(ddqd.dd_gemm(cu(A), cu(B), "winograd", T, madd=madd))
+    for pin in (True, False):
+        hA, hB = torch.from_numpy(A), torch.from_numpy(B)
+        if pin:
+            hA, hB = hA.pin_memory(), hB.pin_memory()
+        assert same(ddqd.dd_gemm(hA, hB, "winograd", T, madd=madd).numpy(), dev), pin
