@@ -13,7 +13,11 @@
  * tensors). The simple GEMM entry points also accept HOST pointers for A, B and C
  * together (detected with cudaPointerGetAttributes): the library then stages them
  * through its own device buffers, copies the result back and synchronises the stream
- * before returning (the end-to-end path bench.py times as "e2e").
+ * before returning (the end-to-end path bench.py times as "e2e"). For Winograd the
+ * copies overlap the products (A11, B11 first; M1 = A11 B11 runs while the rest
+ * arrives; large C is copied back quadrant by quadrant from a library copy stream);
+ * the result is bitwise that of the device-pointer call. Pinned host memory is needed
+ * for the overlap; pageable memory works, with the copies serialised.
  *
  * Ownership: the caller owns every buffer passed in; the library never frees caller
  * memory. The library owns a per-device workspace (grown on demand, freed by
