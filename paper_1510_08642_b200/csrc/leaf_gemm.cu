@@ -307,8 +307,25 @@ int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, cons
     return launch_leaf_one(W, m, l, n, batch, A, B, C, beta, mv, s);
 }
 
+int launch_leaf_small(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
+                      const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s);   // leaf_small.cu
+
+// DDQD_LEAF_SMALL=0 disables the small-output leaf (A/B measurements)
+static bool small_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_LEAF_SMALL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 static int launch_leaf_one(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
                            const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s) {
+    // few outputs (the 32x32 grid would leave SMs without a CTA): latency-bound, one element
+    // per thread (leaf_small.cu)
+    if (small_enabled() && leaf_cfg_override() < 0 && ((m + 31) / 32) * ((n + 31) / 32) * batch < 148)
+        return launch_leaf_small(W, m, l, n, batch, A, B, C, beta, mv, s);
     if (W == 2 && mv != 2 && tma_enabled() && leaf_cfg_override() < 0) {
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
         if (big_tiles >= 2 * 148 && m > 32 && n > 32) {

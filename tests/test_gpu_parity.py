@@ -865,3 +865,28 @@ def test_host_streamed_winograd_quadrant_copies(madd):
         if pin:
             hA, hB = hA.pin_memory(), hB.pin_memory()
         assert same(ddqd.dd_gemm(hA, hB, "winograd", T, madd=madd).numpy(), dev), pin
+
+
+@pytest.mark.parametrize("algo,T", [("block", 128), ("winograd", 32)])
+def test_cuda_graph_capture(orc, algo, T):
+    """Library calls captured into a CUDA graph (the workspace warmed by one eager call first)
+    replay to the oracle's bits -- the c0 bench's graph variant relies on this."""
+    A = gen.dd_matrix(128, 128, 1, 0)
+    B = gen.dd_matrix(128, 128, 1, 1)
+    dA, dB = cu(A), cu(B)
+    C = torch.empty((2, 128, 128), dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        ddqd.dd_gemm(dA, dB, algo, T, out=C)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    C.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ddqd.dd_gemm(dA, dB, algo, T, out=C)
+    torch.cuda.synchronize()
+    assert not C.abs().sum().item()   # capture does not execute
+    g.replay()
+    torch.cuda.synchronize()
+    assert same(np_(C), orc.gemm(A, B, algo, threshold=T))
