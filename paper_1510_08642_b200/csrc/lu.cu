@@ -804,7 +804,7 @@ __global__ void trsv_bwd_update(const double *A, int64_t n, double *y, const dou
 // with its 32 multipliers loaded up front (independent of the chain). Same per-element
 // sequence as trsv_fwd_diag / trsv_bwd_diag and the oracle.
 template <int W, bool FWD>
-__global__ void __launch_bounds__(256) trsv_diag_blk(const double *A, int64_t n, double *y, double *x,
+__global__ void __launch_bounds__(288) trsv_diag_blk(const double *A, int64_t n, double *y, double *x,
                                                      int64_t J, int nb) {
     using E = elem<W>;
     using T = typename E::T;
@@ -813,6 +813,68 @@ __global__ void __launch_bounds__(256) trsv_diag_blk(const double *A, int64_t n,
     const int tid = threadIdx.x, lane = tid & 31, wrp = tid >> 5;
     if (tid < nb) sts<W>(ys, 256, tid, ldv<W>(y, n, J + tid));
     const int nsb = nb / 32;
+    if constexpr (PL == 32) {
+        // DD (launched with 288 threads): threads 0..255 own the block's rows, warp 8 solves the
+        // 32x32 triangles. Every multiplier is loaded one phase AHEAD -- a row's 32 of sub-block
+        // k while warp 8 solves triangle k, warp 8's next triangle's 32 while the rows fold --
+        // so the uncoalesced row-segment loads (one row per lane) are never waited for on the
+        // chain. Same operations in the same order as the generic path below.
+        const bool solver = wrp == 8;
+        T l[32];
+        auto mine = [&](int b0) { return !solver && (FWD ? (tid >= b0 + 32 && tid < nb) : (tid < b0)); };
+        auto tri_load = [&](int sb) {
+#pragma unroll
+            for (int i = 0; i < 32; i++) l[i] = ldA<W>(A, n, J + 32 * sb + lane, J + 32 * sb + i);
+        };
+        if (solver) tri_load(FWD ? 0 : nsb - 1);
+        for (int k = 0; k < nsb; k++) {
+            const int sb = FWD ? k : nsb - 1 - k;
+            const int b0 = 32 * sb;
+            if (mine(b0)) {
+#pragma unroll
+                for (int i = 0; i < 32; i++) l[i] = ldA<W>(A, n, J + tid, J + b0 + i);
+            }
+            __syncthreads();   // ys of the previous sub-block complete
+            if (solver) {
+                T v = lds<W>(ys, 256, b0 + lane);
+#pragma unroll
+                for (int ss = 0; ss < 32; ss++) {
+                    const int t = FWD ? ss : 31 - ss;
+                    T xt;
+                    if (FWD) {
+#pragma unroll
+                        for (int w = 0; w < W; w++) E::set_word(xt, w, __shfl_sync(0xffffffffu, E::word(v, w), t));
+                    } else {
+                        T u;
+#pragma unroll
+                        for (int w = 0; w < W; w++) E::set_word(u, w, __shfl_sync(0xffffffffu, E::word(l[t], w), t));
+                        const T d = E::div(v, u);
+#pragma unroll
+                        for (int w = 0; w < W; w++) E::set_word(xt, w, __shfl_sync(0xffffffffu, E::word(d, w), t));
+                        if (lane == t) v = xt;
+                    }
+                    const T nv = E::sub(v, E::mul(l[t], xt));
+                    if (FWD ? (lane > t) : (lane < t)) v = nv;
+                }
+                sts<W>(ys, 256, b0 + lane, v);
+            }
+            __syncthreads();
+            if (solver) {
+                if (k + 1 < nsb) tri_load(FWD ? sb + 1 : sb - 1);
+            } else if (mine(b0)) {
+                T v = lds<W>(ys, 256, tid);
+#pragma unroll
+                for (int ss = 0; ss < 32; ss++) {
+                    const int i = FWD ? ss : 31 - ss;
+                    v = E::sub(v, E::mul(l[i], lds<W>(ys, 256, b0 + i)));
+                }
+                sts<W>(ys, 256, tid, v);
+            }
+        }
+        __syncthreads();
+        if (tid < nb) stv<W>(FWD ? y : x, n, J + tid, lds<W>(ys, 256, tid));
+        return;
+    }
     for (int k = 0; k < nsb; k++) {
         const int sb = FWD ? k : nsb - 1 - k;
         const int b0 = 32 * sb;
@@ -1137,7 +1199,7 @@ static int lu_trsv_w(int64_t n, const double *A, const int64_t *ipiv, const doub
         const int nb = (int)std::min<int64_t>(NB, n - J);
         const int64_t rows = n - J - nb;
         if (fast && nb % 32 == 0) {
-            trsv_diag_blk<W, true><<<1, 256, 0, s>>>(A, n, y, nullptr, J, nb);
+            trsv_diag_blk<W, true><<<1, W == 2 ? 288 : 256, 0, s>>>(A, n, y, nullptr, J, nb);
             DDQD_LAUNCH_CHECK();
             if (rows > 0) {
                 trsv_update_co<W, true><<<(unsigned)((rows + TU_ROWS - 1) / TU_ROWS), TU_ROWS, usm, s>>>(A, n, y, nullptr, J, nb);
@@ -1156,7 +1218,7 @@ static int lu_trsv_w(int64_t n, const double *A, const int64_t *ipiv, const doub
     for (int64_t J = last; J >= 0; J -= NB) {
         const int nb = (int)std::min<int64_t>(NB, n - J);
         if (fast && nb % 32 == 0) {
-            trsv_diag_blk<W, false><<<1, 256, 0, s>>>(A, n, y, x, J, nb);
+            trsv_diag_blk<W, false><<<1, W == 2 ? 288 : 256, 0, s>>>(A, n, y, x, J, nb);
             DDQD_LAUNCH_CHECK();
             if (J > 0) {
                 trsv_update_co<W, false><<<(unsigned)((J + TU_ROWS - 1) / TU_ROWS), TU_ROWS, usm, s>>>(A, n, y, x, J, nb);
