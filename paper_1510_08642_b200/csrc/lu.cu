@@ -991,12 +991,25 @@ __global__ void __launch_bounds__(TU_ROWS) trsv_update_co(const double *A, int64
         __syncthreads();
         const double *buf = Lt + (ch & 1) * BUF;
         if (me < nr) {
-            for (int k = 0; k < cc_n; k++) {
-                const int cc = FWD ? k : cc_n - 1 - k;
+            auto prod = [&](int cc) {
                 T a;
 #pragma unroll
                 for (int w = 0; w < W; w++) E::set_word(a, w, buf[w * LS + cc * TU_LD + me]);
-                v = E::sub(v, E::mul(a, lds<W>(vs, 256, c0 + cc)));
+                return E::mul(a, lds<W>(vs, 256, c0 + cc));
+            };
+            if (cc_n == TU_CC) {
+                // whole chunk: the products (independent of v) 8 at a time ahead of the subs, so
+                // only the subtraction chain is serial (same operations, same order)
+#pragma unroll
+                for (int k0 = 0; k0 < TU_CC; k0 += 8) {
+                    T pr[8];
+#pragma unroll
+                    for (int u = 0; u < 8; u++) pr[u] = prod(FWD ? k0 + u : TU_CC - 1 - (k0 + u));
+#pragma unroll
+                    for (int u = 0; u < 8; u++) v = E::sub(v, pr[u]);
+                }
+            } else {
+                for (int k = 0; k < cc_n; k++) v = E::sub(v, prod(FWD ? k : cc_n - 1 - k));
             }
         }
         __syncthreads();
