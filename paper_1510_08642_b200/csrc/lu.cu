@@ -375,20 +375,32 @@ __global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n
 }
 
 // Apply the panel's interchanges (in order) to the columns outside the panel.
-__global__ void lu_laswp_kernel(double *A, int W, int64_t n, int64_t p, int64_t kb, const int64_t *ipiv) {
+__global__ void __launch_bounds__(256) lu_laswp_kernel(double *A, int W, int64_t n, int64_t p, int64_t kb,
+                                                       const int64_t *ipiv) {
+    // the panel's pivots staged in shared memory (256 at a time): the per-column loop then
+    // reads them without a global round trip per entry (the interchanges themselves stay in
+    // order, one column-plane per thread)
+    __shared__ long long ps[256];
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t ncols = n - kb;
-    if (t >= (int64_t)W * ncols) return;
-    const int plane = (int)(t / ncols);
-    int64_t j = t % ncols;
+    const bool act = t < (int64_t)W * ncols;
+    const int plane = act ? (int)(t / ncols) : 0;
+    int64_t j = act ? t % ncols : 0;
     if (j >= p) j += kb;
     double *Ap = A + (int64_t)plane * n * n;
-    for (int64_t kk = 0; kk < kb; kk++) {
-        const int64_t k = p + kk, r = ipiv[k];
-        if (r != k) {
-            const double a = Ap[k * n + j];
-            Ap[k * n + j] = Ap[r * n + j];
-            Ap[r * n + j] = a;
+    for (int64_t c0 = 0; c0 < kb; c0 += 256) {
+        const int cn = (int)((kb - c0) < 256 ? (kb - c0) : 256);
+        __syncthreads();
+        for (int i = threadIdx.x; i < cn; i += blockDim.x) ps[i] = ipiv[p + c0 + i];
+        __syncthreads();
+        if (!act) continue;
+        for (int i = 0; i < cn; i++) {
+            const int64_t k = p + c0 + i, r = ps[i];
+            if (r != k) {
+                const double a = Ap[k * n + j];
+                Ap[k * n + j] = Ap[r * n + j];
+                Ap[r * n + j] = a;
+            }
         }
     }
 }
@@ -693,15 +705,24 @@ __global__ void __launch_bounds__(1024) lu_perm_kernel(const double *b, double *
         __syncthreads();
         for (int k = threadIdx.x; k < kc; k += blockDim.x) piv_s[k] = ipiv[k0 + k];
         __syncthreads();
-        if (threadIdx.x == 0) {
-            for (int k = 0; k < kc; k++) {
-                const int64_t kk = k0 + k, r = piv_s[k];
-                if (r != kk)
-                    for (int w = 0; w < W; w++) {
-                        const double t = buf[w * n + kk];
-                        buf[w * n + kk] = buf[w * n + r];
-                        buf[w * n + r] = t;
+        if (threadIdx.x < 32) {
+            // warp 0 reads 32 pivots at a time and visits only the actual interchanges, in
+            // order; lane w < W swaps plane w (the planes are independent, and each plane's
+            // swaps stay in one thread, so their order is kept)
+            const int lane = threadIdx.x;
+            for (int k = 0; k < kc; k += 32) {
+                const int64_t r_l = k + lane < kc ? piv_s[k + lane] : k0 + k + lane;
+                unsigned mask = __ballot_sync(0xffffffffu, r_l != k0 + k + lane);
+                while (mask) {
+                    const int j = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    const int64_t kk = k0 + k + j, r = __shfl_sync(0xffffffffu, r_l, j);
+                    if (lane < W) {
+                        const double t = buf[lane * n + kk];
+                        buf[lane * n + kk] = buf[lane * n + r];
+                        buf[lane * n + r] = t;
                     }
+                }
             }
         }
     }
