@@ -322,9 +322,12 @@ static bool small_enabled() {
 
 static int launch_leaf_one(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
                            const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s) {
-    // few outputs (the 32x32 grid would leave SMs without a CTA): latency-bound, one element
-    // per thread (leaf_small.cu)
-    if (small_enabled() && leaf_cfg_override() < 0 && ((m + 31) / 32) * ((n + 31) / 32) * batch < 148)
+    // few outputs (the 32x32 grid would leave SMs without a CTA, and one element per thread
+    // gives <= 2 CTAs of 128 per SM): latency-bound, one element per thread (leaf_small.cu).
+    // With more outputs its 4 shared loads per madd make it slower than the 2x2 micro-tiles
+    // (c4's last Strassen update, 7 x 128^3: 30.7 us small vs ~21 us 32x32).
+    if (small_enabled() && leaf_cfg_override() < 0 && ((m + 31) / 32) * ((n + 31) / 32) * batch < 148 &&
+        m * n * batch <= 148 * 256)
         return launch_leaf_small(W, m, l, n, batch, A, B, C, beta, mv, s);
     if (W == 2 && mv != 2 && tma_enabled() && leaf_cfg_override() < 0) {
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
