@@ -23,6 +23,16 @@
 
 namespace ddqd {
 
+#ifndef LU_CREP
+#define LU_CREP 16
+#endif
+// replicas of the panel's per-column candidate arrays: all CTAs read all candidates right after
+// the grid barrier, and one copy puts every reader on the same few L2 lines. c4 (2 runs each):
+// 1 replica 56.87 / 56.88 ms, 4: 56.57 / 56.91, 8: 56.20 / 56.78, 16: 56.22 / 56.22.
+// (Every warp merging all candidates itself instead of one pass per CTA made the hot spot 8x
+// worse: 82.5 ms.)
+constexpr int kLuCrep = LU_CREP;
+
 void *aux_get(size_t bytes, int *status);   // abi.cu (separate from the GEMM workspace)
 
 template <int W>
@@ -204,7 +214,7 @@ __global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n
     const int64_t left = n - r0;
     const int nrows = left <= 0 ? 0 : (int)(left < rows_per ? left : rows_per);
     // scratch per buffer parity: cand value [W][G], cand idx [G], cand rows [G][W][kb], krow [W][kb]
-    const size_t per_buf = (size_t)G * (W + 1) + (size_t)G * W * kb + (size_t)W * kb;
+    const size_t per_buf = (size_t)G * (W + 1) * kLuCrep + (size_t)G * W * kb + (size_t)W * kb;
 
     for (int e = tid; e < nrows * kb; e += blockDim.x) {
         const int li = e / kb, j = e % kb;
@@ -226,9 +236,16 @@ __global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n
         const int64_t k = p + kk;
         mark(7);
         double *buf = scr + (size_t)(kk & 1) * per_buf;
-        double *cand_v = buf;                                            // [W][G]
-        long long *cand_i = reinterpret_cast<long long *>(buf + (size_t)W * G);
-        double *cand_rows = buf + (size_t)(W + 1) * G;                   // [G][W][kb]
+        // kLuCrep replicas of the candidate arrays ([W][G] values, [G] rows each); CTA b reads
+        // replica b % kLuCrep, so the 148 readers of a column spread over kLuCrep x the lines
+        double *cand_v = buf + (size_t)(blockIdx.x % kLuCrep) * G * (W + 1);
+        long long *cand_i = reinterpret_cast<long long *>(cand_v + (size_t)W * G);
+        auto put_cand = [&](int q, const T &v, long long i) {
+            double *cv = buf + (size_t)q * G * (W + 1);
+            for (int w = 0; w < W; w++) cv[(size_t)w * G + blockIdx.x] = E::word(v, w);
+            reinterpret_cast<long long *>(cv + (size_t)W * G)[blockIdx.x] = i;
+        };
+        double *cand_rows = buf + (size_t)(W + 1) * G * kLuCrep;         // [G][W][kb]
         double *krow = cand_rows + (size_t)G * W * kb;                   // [W][kb]
 
         // 1. local candidate of column kk over owned rows >= k (row k only without pivoting);
@@ -243,11 +260,8 @@ __global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n
                     if (gi >= k && (pivot || gi == k)) { best = lds<W>(S, SS, tid * kb + kk); bi = gi; }
                 }
                 warp_argmax<W>(best, bi);
-                if (tid == 0) {
-                    for (int w = 0; w < W; w++) cand_v[(size_t)w * G + blockIdx.x] = E::word(best, w);
-                    cand_i[blockIdx.x] = bi;
-                    ri[0] = bi;
-                }
+                if (tid < kLuCrep) put_cand(tid, best, bi);
+                if (tid == 0) ri[0] = bi;
             }
             __syncthreads();
             lbi = ri[0];
@@ -262,10 +276,7 @@ __global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n
             }
             block_argmax<W>(best, bi, rv, ri);
             lbi = ri[0];
-            if (tid == 0) {
-                for (int w = 0; w < W; w++) cand_v[(size_t)w * G + blockIdx.x] = rv[w * 32];
-                cand_i[blockIdx.x] = lbi;
-            }
+            if (tid < kLuCrep) put_cand(tid, lds<W>(rv, 32, 0), lbi);
         }
         if (lbi >= 0) {
             const int li = (int)(lbi - r0);
@@ -1075,7 +1086,7 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
     G = (int)((R + rows_per - 1) / rows_per);
     const size_t smem = sizeof(double) * W * ((size_t)rows_per * kb + (size_t)kb + (size_t)rows_per);
     if (smem > 200 * 1024) return 0;
-    const size_t per_buf = (size_t)G * (W + 1) + (size_t)G * W * kb + (size_t)W * kb;
+    const size_t per_buf = (size_t)G * (W + 1) * kLuCrep + (size_t)G * W * kb + (size_t)W * kb;
     if (2 * per_buf * sizeof(double) > scr_bytes) return 0;
     static size_t attr_dev[64];
     size_t &attr = attr_dev[dv];
@@ -1280,7 +1291,7 @@ struct LuMem {
 static int lu_mem(int W, int64_t n, int64_t K, LuMem *m) {
     int st = DDQD_OK;
     const size_t ybytes = (sizeof(double) * W * (size_t)n + 255) & ~size_t(255);
-    m->scr_bytes = sizeof(double) * 2 * ((size_t)160 * (W + 1 + W * (size_t)K) + W * (size_t)K);
+    m->scr_bytes = sizeof(double) * 2 * ((size_t)160 * ((W + 1) * kLuCrep + W * (size_t)K) + W * (size_t)K);
     char *mem = static_cast<char *>(aux_get(256 + ybytes + m->scr_bytes, &st));
     if (st) return st;
     m->aux = reinterpret_cast<LuAux *>(mem);
