@@ -16,18 +16,10 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "cp_async.cuh"
 #include "ddqd_arith.cuh"
 
 namespace ddqd {
-
-__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, bool pred) {
-    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    int sz = pred ? 8 : 0;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // k-step unroll of the inner loop: 4 lets the compiler issue the next steps' shared-memory
 // fragment loads under the current step's FP64 chains. Measured (c3 cp.async leaf / c2 QD):

@@ -11,6 +11,7 @@
 // runs 128 CTAs -- ~28 chains per SM sub-partition, under the latency bound. Same per-element
 // operation order as leaf_gemm_kernel (acc from +0, k ascending, E::madd), so the same bits.
 #include "common.cuh"
+#include "cp_async.cuh"
 #include "ddqd_arith.cuh"
 
 namespace ddqd {
@@ -20,15 +21,6 @@ namespace {
 constexpr int kSmBM = 8, kSmBN = 16, kSmStages = 3, kSmNT = kSmBM * kSmBN;
 // k depth per stage: 32 (DD) / 16 (QD) keeps the 3-stage ring at 36 KB of static shared memory
 template <int W> struct SmBK { static constexpr int v = W == 2 ? 32 : 16; };
-
-__device__ __forceinline__ void sm_cp_async8(void *smem, const void *gmem, bool pred) {
-    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    int sz = pred ? 8 : 0;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void sm_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void sm_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 template <int W, int MV>
 __global__ void __launch_bounds__(kSmNT) leaf_small_kernel(int64_t m, int64_t l, int64_t n, MatDesc A,
@@ -56,14 +48,14 @@ __global__ void __launch_bounds__(kSmNT) leaf_small_kernel(int64_t m, int64_t l,
             const int w = e / (kSmBM * kSmBK), rem = e % (kSmBM * kSmBK), r = rem / kSmBK, kk = rem % kSmBK;
             const int64_t ri = row0 + r, gk = k0 + kk;
             const bool ok = ri < m && gk < l;
-            sm_cp_async8(as + e, ok ? Ab + w * A.ps + ri * A.ld + gk : Ab, ok);
+            cp_async8(as + e, ok ? Ab + w * A.ps + ri * A.ld + gk : Ab, ok);
         }
 #pragma unroll
         for (int e = tid; e < BST; e += kSmNT) {
             const int w = e / (kSmBK * kSmBN), rem = e % (kSmBK * kSmBN), kk = rem / kSmBN, c = rem % kSmBN;
             const int64_t gk = k0 + kk, cj = col0 + c;
             const bool ok = gk < l && cj < n;
-            sm_cp_async8(bs + e, ok ? Bb + w * B.ps + gk * B.ld + cj : Bb, ok);
+            cp_async8(bs + e, ok ? Bb + w * B.ps + gk * B.ld + cj : Bb, ok);
         }
     };
 
@@ -72,15 +64,15 @@ __global__ void __launch_bounds__(kSmNT) leaf_small_kernel(int64_t m, int64_t l,
 #pragma unroll
     for (int st = 0; st < kSmStages - 1; st++) {
         if (st < KT) load_stage(st, st);
-        sm_commit();
+        cp_async_commit();
     }
     for (int64_t kt = 0; kt < KT; kt++) {
-        sm_wait<kSmStages - 2>();
+        cp_async_wait<kSmStages - 2>();
         __syncthreads();
         {
             const int64_t nk = kt + kSmStages - 1;
             if (nk < KT) load_stage((int)(nk % kSmStages), nk);
-            sm_commit();
+            cp_async_commit();
         }
         const int st = (int)(kt % kSmStages);
         const double *as = As + st * AST + ty * kSmBK;
@@ -121,7 +113,7 @@ __global__ void __launch_bounds__(kSmNT) leaf_small_kernel(int64_t m, int64_t l,
             for (; kk < kmax; kk++) acc = E::madd(acc, lda(kk), ldb(kk));
         }
     }
-    sm_wait<0>();
+    cp_async_wait<0>();
     if (!live) return;
     double *cp = C.p + b * C.bs + gi * C.ld + gj;
     if (beta) E::store(cp, C.ps, E::sub(E::load(cp, C.ps), acc));

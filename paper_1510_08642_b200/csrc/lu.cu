@@ -19,6 +19,7 @@
 #include <string>
 
 #include "common.cuh"
+#include "cp_async.cuh"
 #include "ddqd_arith.cuh"
 
 namespace ddqd {
@@ -466,12 +467,6 @@ __global__ void __launch_bounds__(1024) lu_trsm_kernel(double *A, int64_t n, int
 template <int W> struct TrsmWpb { static constexpr int v = W == 2 ? 16 : 8; };
 template <int W> struct TrsmCh { static constexpr int v = W == 2 ? 16 : 8; };   // 2 x 64 KB ring
 
-__device__ __forceinline__ void lu_cp_async8(void *smem, const void *gmem) {
-    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void lu_cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void lu_cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
 template <int W, int RPL>
 __global__ void __launch_bounds__(TrsmWpb<W>::v * 32) lu_trsm_warp_kernel(double *A, int64_t n, int64_t p,
@@ -493,10 +488,10 @@ __global__ void __launch_bounds__(TrsmWpb<W>::v * 32) lu_trsm_warp_kernel(double
                 const int r = e / ch, ii = e % ch;   // consecutive threads walk a row of L11
                 const double *src = A + (p + r) * n + (p + i0 + ii);
 #pragma unroll
-                for (int w = 0; w < W; w++) lu_cp_async8(buf + w * SS + ii * kb + r, src + (int64_t)w * n * n);
+                for (int w = 0; w < W; w++) cp_async8(buf + w * SS + ii * kb + r, src + (int64_t)w * n * n);
             }
         }
-        lu_cp_commit();   // possibly empty: keeps the group count uniform
+        cp_async_commit();   // possibly empty: keeps the group count uniform
     };
     issue(0);
     issue(1);
@@ -516,7 +511,7 @@ __global__ void __launch_bounds__(TrsmWpb<W>::v * 32) lu_trsm_warp_kernel(double
             if (i0 >= kb) break;
             const int st = i0 / CH;
             const int ch = kb - i0 < CH ? kb - i0 : CH;
-            lu_cp_wait1();     // stage st has landed (only st + 1 may still be in flight)
+            cp_async_wait<1>();     // stage st has landed (only st + 1 may still be in flight)
             __syncthreads();
             const double *buf = Ls + (st & 1) * BUF;
             // every warp runs the steps (a warp past the last column works on zeros and stores
@@ -1006,11 +1001,11 @@ __global__ void __launch_bounds__(TU_ROWS) trsv_update_co(const double *A, int64
                 if (cc < cc_n) {
                     const double *g = A + (r0 + r) * n + (J + c0 + cc);
 #pragma unroll
-                    for (int w = 0; w < W; w++) lu_cp_async8(buf + w * LS + cc * TU_LD + r, g + (int64_t)w * n * n);
+                    for (int w = 0; w < W; w++) cp_async8(buf + w * LS + cc * TU_LD + r, g + (int64_t)w * n * n);
                 }
             }
         }
-        lu_cp_commit();
+        cp_async_commit();
     };
     issue(0);
     issue(1);
@@ -1019,7 +1014,7 @@ __global__ void __launch_bounds__(TU_ROWS) trsv_update_co(const double *A, int64
     for (int ch = 0; ch < nch; ch++) {
         int cc_n;
         const int c0 = chunk_c0(ch, &cc_n);
-        lu_cp_wait1();
+        cp_async_wait<1>();
         __syncthreads();
         const double *buf = Lt + (ch & 1) * BUF;
         if (me < nr) {
