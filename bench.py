@@ -322,6 +322,23 @@ def lu_bench(args, wl, rank, world, local):
     achieved = 20.0 * leaf_madds / (leaf_ms * 1e-3) / 1e12 if leaf_ms else 0.0
     shares = {k: v[0] / ms for k, v in prof.items()}
     dominant = max(shares, key=shares.get)
+    roof_leaf = {"bound": "alu", "achieved": achieved, "peak": peak / 1e12, "unit": "TFLOP/s",
+                 "frac": achieved / (peak / 1e12) if peak else None,
+                 "kernel": "leaf_gemm_kernel / leaf_tma_kernel (Schur update, Strassen d = 1)",
+                 "share_of_step": shares["leaf"], "traffic": None}
+    # the dominant kernel: the panel factorisation (FP64 work = its rank-1 updates, R K^2 / 2 DD
+    # madds per panel of R rows, 20 FP64 lane-ops each) -- far below the pipe: it is bound by
+    # the latency of its 4096 dependent pivot steps, not by an execution unit
+    pan_ms, pan_n, pan_madds = prof["lu_panel"]
+    pan_ach = 20.0 * pan_madds / (pan_ms * 1e-3) / 1e12 if pan_ms else 0.0
+    roof_pan = {"bound": "alu", "achieved": pan_ach, "peak": peak / 1e12, "unit": "TFLOP/s",
+                "frac": pan_ach / (peak / 1e12) if peak else None,
+                "kernel": "lu_panel_coop_kernel (+ lu_laswp_kernel)", "launches": int(pan_n),
+                "share_of_step": shares["lu_panel"], "traffic": None,
+                "latency_bound": "one grid barrier + candidate exchange per column, ~14k cycles per "
+                                 "pivot step x 4096 steps (DESIGN.md s.7, profiles/r01/lu_panel_phase_probe_*)",
+                "work_def": "rank-1 panel updates R*K^2/2 DD madds x 20 FP64 lane-ops"}
+    roof_dom = roof_pan if shares["lu_panel"] >= shares["leaf"] else roof_leaf
 
     e2e = None
     if not args.no_e2e and world == 1:
@@ -377,11 +394,8 @@ def lu_bench(args, wl, rank, world, local):
             "config": {"workload": wl["name"], "n": n, "panel": K, "algo": algo, "threshold": T,
                        "parallelism": f"{world} GPU replica(s)",
                        "l2": "A (268 MB) exceeds L2; fresh copy of A before each step, outside the events"},
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak / 1e12, "unit": "TFLOP/s",
-                         "frac": achieved / (peak / 1e12) if peak else None,
-                         "kernel": "leaf_gemm_kernel (Schur update)", "traffic": None,
-                         "note": "LU time is dominated by '%s' (share %.2f); panel steps are latency-bound"
-                                 % (dominant, shares[dominant])},
+            "roofline": roof_dom,
+            "roofline_schur_leaf": roof_leaf,
             "time_shares": shares,
             "max_abs_err_x_minus_1": err,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
