@@ -113,8 +113,10 @@ def _set_stream(t):
     """Make the library use torch's current stream (of t's device; of the current device for
     host tensors, whose staging copies then run on that stream)."""
     torch = _torch()
-    dev = t.device if t.is_cuda else torch.device("cuda", torch.cuda.current_device())
-    lib.ddqd_set_stream(ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+    idx = t.device.index if t.is_cuda else torch.cuda.current_device()
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)   # no Stream object per call
+    ptr = raw(idx) if raw is not None else torch.cuda.current_stream(idx).cuda_stream
+    lib.ddqd_set_stream(ctypes.c_void_p(ptr))
 
 
 _SPLITK = {1: 0, 2: 0x1000, 4: 0x2000, 8: 0x3000}   # DDQD_SPLITK(s)
