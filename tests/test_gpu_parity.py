@@ -890,3 +890,27 @@ def test_cuda_graph_capture(orc, algo, T):
     g.replay()
     torch.cuda.synchronize()
     assert same(np_(C), orc.gemm(A, B, algo, threshold=T))
+
+
+def test_randomized_shapes_all_paths(orc):
+    """Seeded random sweep over shapes (1..300, ragged), thresholds, algorithms, DD/QD and the
+    arithmetic variants, device and host pointers: every result bit-identical to the oracle.
+    Exercises the leaf selection (small-output / 32x32 / 64x64 / TMA / tail split), the
+    recursion's padding and the overlapped host path together."""
+    rng = np.random.default_rng(20261019)
+    for case in range(80):
+        W = int(rng.choice([2, 2, 2, 4]))
+        m, l, n = (int(x) for x in rng.integers(1, 301, 3))
+        algo = str(rng.choice(["block", "strassen", "winograd"]))
+        T = int(rng.choice([8, 16, 32, 64, 128]))
+        madd = str(rng.choice(["canonical", "canonical", "fused", "accurate"]))
+        host = bool(rng.integers(0, 4) == 0)
+        A = gen.matrix(W, m, l, 1000 + case, 0)
+        B = gen.matrix(W, l, n, 1000 + case, 1)
+        gemm = ddqd.dd_gemm if W == 2 else ddqd.qd_gemm
+        if host:
+            got = gemm(torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory(), algo, T,
+                       madd=madd).numpy()
+        else:
+            got = np_(gemm(cu(A), cu(B), algo, T, madd=madd))
+        assert same(got, orc.gemm(A, B, algo, threshold=T, madd=madd)), (case, W, m, l, n, algo, T, madd, host)
