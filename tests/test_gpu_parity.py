@@ -914,3 +914,27 @@ def test_randomized_shapes_all_paths(orc):
         else:
             got = np_(gemm(cu(A), cu(B), algo, T, madd=madd))
         assert same(got, orc.gemm(A, B, algo, threshold=T, madd=madd)), (case, W, m, l, n, algo, T, madd, host)
+
+
+def test_randomized_lu_sweep(orc):
+    """Seeded random LU solves (n 1..400, panel widths incl. ragged last panels, every update
+    algorithm, DD/QD, pivoting on non-dominant matrices or the paper's pivot-free mode on
+    dominant ones): factors, pivots and solution bit-identical to the oracle."""
+    rng = np.random.default_rng(4096)
+    for case in range(16):
+        W = int(rng.choice([2, 2, 4]))
+        n = int(rng.integers(1, 401))
+        K = int(rng.choice([16, 32, 48, 64, 100, 128, 256]))
+        algo = str(rng.choice(["block", "strassen", "winograd"]))
+        T = int(rng.choice([8, 16, 32, 64]))
+        pivot = bool(rng.integers(0, 3) > 0)
+        A = gen.matrix(W, n, n, 500 + case, 0)
+        if not pivot:   # the pivot-free LU needs non-zero leading minors: make A dominant
+            A[0][np.arange(n), np.arange(n)] += n
+        b = gen.matrix(W, 1, n, 500 + case, 1)[:, 0, :].copy()
+        ref = orc.solve(A, b, panel=K, algo=algo, threshold=T, pivot=pivot)
+        got = ddqd.lu_solve(cu(A), cu(b), panel=K, algo=algo, threshold=T, pivot=pivot)
+        tag = (case, W, n, K, algo, T, pivot)
+        assert got[3] == ref[3] == 0, tag
+        assert np.array_equal(np_(got[2]), ref[2]), tag
+        assert same(np_(got[1]), ref[1]) and same(np_(got[0]), ref[0]), tag
