@@ -58,6 +58,24 @@ int current_device() {
     return d & 63;
 }
 
+// SM count of the current device (148 on a B200), cached per device: grid sizing and the leaf
+// configuration choices count waves in units of it
+int sm_count() {
+    static int cache[64];
+    const int d = current_device();
+    if (!cache[d]) {
+        int v = 0;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+            cudaGetLastError();
+            v = 148;
+        }
+        cache[d] = v;
+    }
+    return cache[d];
+}
+
 // Library-owned per-device buffers. Growth frees the old buffer (cudaFree synchronises the
 // device, so no in-flight kernel can still be using it).
 struct DevBuf {

@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(ADD2_THREADS, ADD2_MINB) post_add2_kernel(int6
 
 static unsigned grid_for(int64_t total, int threads = 256) {
     int64_t blocks = (total + threads - 1) / threads;
-    const int64_t cap = 148 * 16 * 256 / threads;   // grid-stride beyond 16 CTAs (of 256) per SM
+    const int64_t cap = (int64_t)sm_count() * 16 * 256 / threads;   // grid-stride beyond 16 CTAs (of 256) per SM
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     return (unsigned)blocks;

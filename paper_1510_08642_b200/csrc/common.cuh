@@ -22,6 +22,7 @@ void set_error(const std::string &msg);
 cudaStream_t cur_stream();
 void count_launch(int64_t n = 1);
 int current_device();   // cudaGetDevice, masked to [0, 64) for per-device caches
+int sm_count();         // multiprocessors of the current device (cached)
 
 // NVTX ranges (header-only NVTX3; free when no profiler is attached): the recursion levels,
 // the LU phases and the ABI entry points show up by name in Nsight Systems / Compute.

@@ -277,13 +277,13 @@ int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, cons
     // Only for batches of >= 32 leaves: on the 7-leaf Strassen updates of the c4 LU the
     // model below also predicts a gain, but the measured step was not faster (58.25 vs 58.5 ms).
     if (W == 2 && tail_split_enabled() && leaf_cfg_override() < 0 && m > 32 && n > 32 && batch >= 32) {
-        const int64_t t = ((m + 63) / 64) * ((n + 63) / 64), slots = 2 * 148;
+        const int64_t t = ((m + 63) / 64) * ((n + 63) / 64), slots = 2 * (int64_t)sm_count();
         const int64_t total = t * batch, waves = total / slots, rem = total % slots;
         if (waves >= 2 && rem > 0 && rem * 4 < slots * 3) {   // last wave under 75% full
             const int64_t b1 = waves * slots / t;              // leaves filling the whole waves
             // cost model in big-tile wave times: a 32x32 tile is 1/4 of the work at ~0.8 of
             // the efficiency, 4 fit per SM; split only when it saves >= 5%
-            const int64_t small = (batch - b1) * t * 4, slots_small = 4 * 148;
+            const int64_t small = (batch - b1) * t * 4, slots_small = 4 * (int64_t)sm_count();
             const double t_split = (double)((b1 * t + slots - 1) / slots) +
                                    0.3125 * (double)((small + slots_small - 1) / slots_small);
             if (b1 > 0 && b1 < batch && t_split < 0.95 * (double)(waves + 1)) {
@@ -318,12 +318,12 @@ static int launch_leaf_one(int W, int64_t m, int64_t l, int64_t n, int64_t batch
     // gives <= 2 CTAs of 128 per SM): latency-bound, one element per thread (leaf_small.cu).
     // With more outputs its 4 shared loads per madd make it slower than the 2x2 micro-tiles
     // (c4's last Strassen update, 7 x 128^3: 30.7 us small vs ~21 us 32x32).
-    if (small_enabled() && leaf_cfg_override() < 0 && ((m + 31) / 32) * ((n + 31) / 32) * batch < 148 &&
-        m * n * batch <= 148 * 256)
+    if (small_enabled() && leaf_cfg_override() < 0 && ((m + 31) / 32) * ((n + 31) / 32) * batch < sm_count() &&
+        m * n * batch <= (int64_t)sm_count() * 256)
         return launch_leaf_small(W, m, l, n, batch, A, B, C, beta, mv, s);
     if (W == 2 && mv != 2 && tma_enabled() && leaf_cfg_override() < 0) {
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
-        if (big_tiles >= 2 * 148 && m > 32 && n > 32) {
+        if (big_tiles >= 2 * sm_count() && m > 32 && n > 32) {
             int rc = DDQD_OK;
             if (try_leaf_tma(m, l, n, batch, A, B, C, beta, mv, s, &rc)) return rc;
         }
@@ -331,14 +331,14 @@ static int launch_leaf_one(int W, int64_t m, int64_t l, int64_t n, int64_t batch
     if (mv == 1) {   // fused DD / QD madd (numerics.md s.2-3, row f3)
         if (W == 4) return launch_cfg<4, 32, 32, 16, 2, 2, 3, 2, 1>(m, l, n, batch, A, B, C, beta, s);
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
-        if (big_tiles >= 2 * 148 && m > 32 && n > 32)
+        if (big_tiles >= 2 * sm_count() && m > 32 && n > 32)
             return launch_cfg<2, 64, 64, 8, 4, 4, 4, 2, 1>(m, l, n, batch, A, B, C, beta, s);
         return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2, 1>(m, l, n, batch, A, B, C, beta, s);
     }
     if (mv == 2) {   // accurate adds (numerics.md s.2-3, row f3)
         if (W == 4) return launch_cfg<4, 32, 32, 16, 2, 2, 3, 2, 2>(m, l, n, batch, A, B, C, beta, s);
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
-        if (big_tiles >= 2 * 148 && m > 32 && n > 32)
+        if (big_tiles >= 2 * sm_count() && m > 32 && n > 32)
             return launch_cfg<2, 64, 64, 8, 4, 4, 4, 2, 2>(m, l, n, batch, A, B, C, beta, s);
         return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2, 2>(m, l, n, batch, A, B, C, beta, s);
     }
@@ -359,7 +359,7 @@ static int launch_leaf_one(int W, int64_t m, int64_t l, int64_t n, int64_t batch
     if (W == 2) {
         // 64x64 tiles when the grid fills the GPU and the leaf is not smaller than a tile
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
-        if (big_tiles >= 2 * 148 && m > 32 && n > 32)   // tools/tune_leaf.py: BK = 8 x 4 stages is the fastest DD tile
+        if (big_tiles >= 2 * sm_count() && m > 32 && n > 32)   // tools/tune_leaf.py: BK = 8 x 4 stages is the fastest DD tile
             return launch_cfg<2, 64, 64, 8, 4, 4, 4, 2>(m, l, n, batch, A, B, C, beta, s);
         return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2>(m, l, n, batch, A, B, C, beta, s);
     }

@@ -1160,9 +1160,9 @@ static int lu_panel_w(int64_t n, int pivot, double *A, int64_t *ipiv, int64_t p,
     prof_end(3, (double)kb * (double)(n - p) * (double)kb / 2.0, s);   // panel madds (approx.)
     const int64_t n2 = n - p - kb;
     if (n2 <= 0) return DDQD_OK;
-    // one CTA per SM when possible: cw = ceil(n2 / 148), capped by shared memory
+    // one CTA per SM when possible: cw = ceil(n2 / #SMs), capped by shared memory
     const int64_t cw_smem = std::max<int64_t>(1, (int64_t)(200 * 1024) / (8 * W * kb));
-    int cw = (int)std::max<int64_t>(1, std::min<int64_t>(cw_smem, (n2 + 147) / 148));
+    int cw = (int)std::max<int64_t>(1, std::min<int64_t>(cw_smem, (n2 + sm_count() - 1) / sm_count()));
     const size_t smem = sizeof(double) * W * (size_t)kb * cw;
     if (smem > 48 * 1024)
         DDQD_CUDA_CHECK(cudaFuncSetAttribute(lu_trsm_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1173,7 +1173,7 @@ static int lu_panel_w(int64_t n, int pivot, double *A, int64_t *ipiv, int64_t p,
         // 16-column strips while they fill ~1.5 waves of the SMs, else 8 (twice the CTAs, each
         // with half the chain): the per-CTA chain, not the FP64 rate, bounds small panels
         static bool battr[2][64] = {};
-        const bool wide = (n2 + 15) / 16 >= 222;
+        const bool wide = (n2 + 15) / 16 >= 3 * sm_count() / 2;
         const size_t bsmem = sizeof(double) * W * ((size_t)256 * (wide ? 16 : 8) + 32 * 32 + (size_t)TB_LC * 224);
         auto kfn = wide ? lu_trsm_blk_kernel<W, 256, 16> : lu_trsm_blk_kernel<W, 256, 8>;
         if (!battr[wide][current_device()]) {
