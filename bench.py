@@ -202,6 +202,26 @@ def ncu_leaf_traffic(workload):
     return tot, f"{os.path.relpath(files[-1], ROOT)} (grid {grid})"
 
 
+def ncu_panel_traffic():
+    """DRAM bytes (read + write) of one LU panel launch from the committed `ncu --set full`
+    capture (profiles/rNN/ncu_lu_raw.csv; first captured panel)."""
+    import csv
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_lu_raw.csv")))
+    if not files:
+        return None, None
+    rows = list(csv.reader(open(files[-1])))
+    hdr, units = rows[0], rows[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for vals in rows[2:]:
+        if "lu_panel_coop_kernel" not in vals[hdr.index("Kernel Name")]:
+            continue
+        tot = sum(float(vals[hdr.index(k)].replace(",", "")) * scale.get(units[hdr.index(k)], 1)
+                  for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        return tot, f"{os.path.relpath(files[-1], ROOT)} (grid {vals[hdr.index('launch__grid_size')]})"
+    return None, None
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -348,7 +368,14 @@ def lu_bench(args, wl, rank, world, local):
                 "share_of_step": shares["lu_panel"], "traffic": None,
                 "latency_bound": "one grid barrier + candidate exchange per column, ~14k cycles per "
                                  "pivot step x 4096 steps (DESIGN.md s.7, profiles/r01/lu_panel_phase_probe_*)",
-                "work_def": "rank-1 panel updates R*K^2/2 DD madds x 20 FP64 lane-ops"}
+                "work_def": "rank-1 panel updates R*K^2/2 DD madds x 20 FP64 lane-ops",
+                "algorithmic_bytes_per_launch": 16.0 * K * (n - K * (n // K - 1) / 2.0) * 2,
+                "traffic_note": "one panel launch reads its slab once (R x K DD) and writes it back "
+                                "(the write stays in the 126 MB L2 within the launch)"}
+    tr, src = ncu_panel_traffic()
+    if tr is not None:
+        roof_pan["traffic"] = tr
+        roof_pan["traffic_source"] = src
     roof_dom = roof_pan if shares["lu_panel"] >= shares["leaf"] else roof_leaf
 
     e2e = None
