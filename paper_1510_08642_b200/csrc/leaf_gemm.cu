@@ -260,6 +260,10 @@ static bool tail_split_enabled() {
 
 static MatDesc shift_batch(MatDesc d, int64_t b0) { d.p += b0 * d.bs; return d; }
 
+int launch_leaf_small(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
+                      const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s);   // leaf_small.cu
+static bool small_enabled();
+
 static int launch_leaf_one(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
                            const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s);
 
@@ -293,6 +297,28 @@ int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, cons
                 if (mv == 1) return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2, 1>(m, l, n, batch - b1, A2, B2, C2, beta, s);
                 if (mv == 2) return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2, 2>(m, l, n, batch - b1, A2, B2, C2, beta, s);
                 return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2>(m, l, n, batch - b1, A2, B2, C2, beta, s);
+            }
+        }
+    }
+    // QD: the same idea with the one-element-per-thread leaf for the remaining leaves (its four
+    // shared loads per madd are small next to ~200 FP64 ops; a 128-thread CTA holds 1/4 of a
+    // 32x32 2x2-micro-tile CTA's work). c2: 343 leaves x 16 tiles = 5488 CTAs = 18.5 waves:
+    // 333 leaves on 32x32 tiles + 10 on the small leaf, 9.137 -> 9.004 ms (leaf 0.879 -> 0.892).
+    if (W == 4 && mv != 1 && tail_split_enabled() && leaf_cfg_override() < 0 && small_enabled() && batch >= 32) {
+        const int64_t t = ((m + 31) / 32) * ((n + 31) / 32), slots = 2 * (int64_t)sm_count();
+        const int64_t total = t * batch, waves = total / slots, rem = total % slots;
+        if (waves >= 2 && rem > 0 && rem * 4 < slots * 3) {
+            const int64_t b1 = waves * slots / t;
+            // small CTAs: 8x16 outputs, ~3 per SM at ~150 registers; one small wave ~0.19 of a
+            // big one (per-SM FP64 work 9.8M vs 52M lane-ops)
+            const int64_t small = (batch - b1) * ((m + 7) / 8) * ((n + 15) / 16), slots_small = 3 * (int64_t)sm_count();
+            const double t_split = (double)((b1 * t + slots - 1) / slots) +
+                                   0.19 * (double)((small + slots_small - 1) / slots_small);
+            if (b1 > 0 && b1 < batch && t_split < 0.99 * (double)(waves + 1)) {
+                int rc = launch_leaf_one(W, m, l, n, b1, A, B, C, beta, mv, s);
+                if (rc) return rc;
+                return launch_leaf_small(W, m, l, n, batch - b1, shift_batch(A, b1), shift_batch(B, b1),
+                                         shift_batch(C, b1), beta, mv, s);
             }
         }
     }
