@@ -31,3 +31,24 @@ def test_reference_arm_custom_workload():
     d = _run("--impl", "reference", "--custom", "100,90,80", "--prec", "qd", "--algo", "strassen",
              "--threshold", "16", "--steps", "1", "--warmup", "0")
     assert d["config"]["algo"] == "strassen" and d["value"] > 0
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("wl", ["c0", "c4"])
+def test_our_arm_contract_keys(wl):
+    """Our arm's JSON line carries the contract keys (GPU): roofline with achieved/peak/frac,
+    e2e with the copied bytes, clocks, gpu_launches > 0, cpu_baseline from the oracle."""
+    d = _run("--workload", wl, "--steps", "2", "--warmup", "1")
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+              "gpu_launches", "clocks"):
+        assert k in d, k
+    r = d["roofline"]
+    assert r["bound"] in ("hbm", "tensor", "alu") and r["peak"] > 0 and 0 < r["frac"] <= 1.0
+    assert abs(r["achieved"] / r["peak"] - r["frac"]) < 1e-9
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
