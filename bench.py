@@ -77,9 +77,9 @@ def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None,
-                    help="timed steps (default per workload: c0 200, c1 50, c2 10, c3/c4 5)")
+                    help="timed steps (default per workload: c0 200, c1 50, c2 20, c3/c4 5)")
     ap.add_argument("--warmup", type=int, default=None,
-                    help="untimed warm-up steps (default per workload: c0 20, c1 5, else 3)")
+                    help="untimed warm-up steps (default per workload: c0 20, c1/c2 5, else 3)")
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--custom", default=None, metavar="M,L,N",
                     help="a custom GEMM workload instead of a BASELINE config (with --prec/--algo/--threshold/--seed)")
@@ -105,8 +105,8 @@ def parse_args():
     args = ap.parse_args()
     # microsecond-scale steps need more of them for a stable number (and enough warm-up to
     # bring the clocks back up after the sampler's start-up idle)
-    dsteps = {"c0": 200, "c1": 50, "c2": 10}.get(args.workload, 5) if args.custom is None else 5
-    dwarm = {"c0": 20, "c1": 5}.get(args.workload, 3) if args.custom is None else 3
+    dsteps = {"c0": 200, "c1": 50, "c2": 20}.get(args.workload, 5) if args.custom is None else 5
+    dwarm = {"c0": 20, "c1": 5, "c2": 5}.get(args.workload, 3) if args.custom is None else 3
     if args.steps is None:
         args.steps = dsteps
     if args.warmup is None:
