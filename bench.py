@@ -190,7 +190,7 @@ def ncu_leaf_traffic(workload):
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_full_leaf_{workload}_raw.csv")))
     if not files:
-        return None, None
+        return None, None, None, ""
     rows = list(csv.reader(open(files[-1])))
     hdr, units, vals = rows[0], rows[1], rows[2]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
@@ -199,7 +199,19 @@ def ncu_leaf_traffic(workload):
         i = hdr.index(name)
         tot += float(vals[i].replace(",", "")) * scale.get(units[i], 1)
     grid = vals[hdr.index("launch__grid_size")] if "launch__grid_size" in hdr else None
-    return tot, f"{os.path.relpath(files[-1], ROOT)} (grid {grid})"
+    name = vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else ""
+    return tot, f"{os.path.relpath(files[-1], ROOT)} (grid {grid})", int(grid) if grid else None, name
+
+
+def leaf_tile(name):
+    """Output tile (rows, cols) of one CTA of a captured leaf kernel, from its name."""
+    import re
+    if "leaf_small_kernel" in name:
+        return 8, 16
+    if "leaf_tma_kernel" in name:
+        return 64, 64
+    mt = re.search(r"leaf_gemm_kernel<\s*\d+\s*,\s*(\d+)\s*,\s*(\d+)", name)
+    return (int(mt.group(1)), int(mt.group(2))) if mt else None
 
 
 def ncu_panel_traffic():
@@ -582,10 +594,18 @@ def main():
         lm, ll, ln = shapes[-1]
         per_launch_leaves = leaf_madds / leaf_n / (lm * ll * ln)
         roofline["algorithmic_bytes_per_launch"] = per_launch_leaves * W * 8.0 * (lm * ll + ll * ln + lm * ln)
-        tr, src = ncu_leaf_traffic(args.workload)
+        tr, src, grid, kname = ncu_leaf_traffic(args.workload)
         if tr is not None:
             roofline["traffic"] = tr
             roofline["traffic_source"] = src
+            tile = leaf_tile(kname)
+            if tile and grid:
+                # the captured launch's own algorithmic bytes (a tail-split step has launches of
+                # different sizes, so the per-step average above is not its denominator)
+                leaves = grid / (((lm + tile[0] - 1) // tile[0]) * ((ln + tile[1] - 1) // tile[1]))
+                cap_alg = leaves * W * 8.0 * (lm * ll + ll * ln + lm * ln)
+                roofline["traffic_captured_launch_algorithmic_bytes"] = cap_alg
+                roofline["traffic_over_algorithmic"] = tr / cap_alg
     leaf_madds_step = (7 ** d) * shapes[-1][0] * shapes[-1][1] * shapes[-1][2]
     # whole-step algorithmic roofline: the leaf's FP64 work at the FP64 peak plus the additions'
     # algorithmic bytes at the HBM peak, over the measured step time
