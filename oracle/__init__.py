@@ -51,6 +51,7 @@ def lib():
         L.or_qd_op.argtypes = [ctypes.c_int, i64, P, P, P, P]
         L.or_qd_renorm.argtypes = [i64, P, P]
         L.or_dd_abs_gt.argtypes = [P, P]
+        L.or_qd_abs_gt.argtypes = [P, P]
         L.or_gemm.argtypes = [ctypes.c_int, ctypes.c_int, i64, i64, i64, i64, i64, P, P, P, ctypes.c_int]
         L.or_lu.argtypes = [ctypes.c_int, ctypes.c_int, i64, P, PI, i64, ctypes.c_int, i64, ctypes.c_int]
         L.or_lu_solve.argtypes = [ctypes.c_int, i64, P, PI, P, P]
@@ -134,6 +135,12 @@ def qd_renorm(c):
 
 def dd_abs_gt(x, y) -> bool:
     return bool(lib().or_dd_abs_gt(_p(_f64(x)), _p(_f64(y))))
+
+
+def qd_abs_gt(x, y) -> bool:
+    """|x| > |y| in the QD magnitude order (numerics.md s.3: sign folded on the leading
+    word, then the four words compared lexicographically) -- the LU's pivot order."""
+    return bool(lib().or_qd_abs_gt(_p(_f64(x)), _p(_f64(y))))
 
 
 # ---- GEMM --------------------------------------------------------------------

@@ -14,10 +14,12 @@
  *
  * Citation key: P:n = PAPER.md line n, S:n = SPEC.md line n, BJ:n = BASELINE.json line n.
  *
- * Parity status: DD ops, Simple/Block, Strassen, Winograd and LU are pinned by
- * tests/test_oracle_*.py (exact rationals, closed forms, special cases, invariants).
- * The exact QD op *sequences* are parity unpinned (only accuracy and invariants pin
- * them: no reference implementation of Hida-Li-Bailey exists in this container).
+ * Parity status: every function here is pinned by tests/test_oracle_*.py (exact
+ * rationals, closed forms, special cases, invariants, brute force on tiny inputs), and
+ * tools/oracle_mutation_check.py shows that plausible mistakes in the EFTs, DD/QD ops,
+ * the pivot orders and the solve's permutation each fail a pin. Which QD algorithm is
+ * used (Hida-Li-Bailey "sloppy", reading R1) is a reading of P:58, not
+ * something the paper's text fixes.
  */
 #include <math.h>
 #include <stdint.h>
@@ -695,6 +697,12 @@ static int qd_abs_gt(qd_t x, qd_t y) {
     for (int i = 0; i < 4; i++)
         if (ax.w[i] != ay.w[i]) return ax.w[i] > ay.w[i];
     return 0;
+}
+
+int or_qd_abs_gt(const double *x, const double *y) {
+    qd_t a, b;
+    for (int k = 0; k < 4; k++) { a.w[k] = x[k]; b.w[k] = y[k]; }
+    return qd_abs_gt(a, b);
 }
 
 void or_qd_div(int64_t n, const double *x, const double *y, double *z) {

@@ -435,6 +435,26 @@ def test_lu_qd_and_pivot_free_bitwise(orc, W, pivot):
     assert same(np_(LU), LU_ref) and same(np_(x), x_ref)
 
 
+@pytest.mark.parametrize("W", [2, 4])
+def test_lu_pivot_ties_below_leading_word_bitwise(orc, W):
+    """Pivot candidates whose leading words are equal up to sign, so the sign fold and the
+    lower words decide the pivot (the oracle's order is pinned against exact elimination,
+    tests/test_oracle_lu.py); the device picks the same rows and produces the same bits."""
+    n = 160
+    rng = np.random.default_rng(5 + W)
+    A = gen.matrix(W, n, n, 29, 0) * rng.choice([-1.0, 1.0], (1, n, n))
+    for k in range(0, n, 7):                      # copy the leading word(s) down each 7th column
+        rows = rng.choice(np.arange(k, n), size=min(12, n - k), replace=False)
+        A[:W // 2, rows, k] = A[:W // 2, rows[:1], k] * rng.choice([-1.0, 1.0], rows.size)
+    b = gen.matrix(W, 1, n, 29, 1)[:, 0, :].copy()
+    x_ref, LU_ref, piv_ref, info_ref = orc.solve(A, b, panel=32, algo="strassen", threshold=16)
+    x, LU, piv, info = ddqd.lu_solve(cu(A), cu(b), panel=32, algo="strassen", threshold=16)
+    assert info == info_ref
+    assert np.any(piv_ref != np.arange(n))
+    assert np.array_equal(np_(piv), piv_ref)
+    assert same(np_(LU), LU_ref) and same(np_(x), x_ref)
+
+
 def test_qd_lu_c4_recipe_512_bitwise(orc):
     n = 512
     A = _qd_lu_matrix(n, 5)

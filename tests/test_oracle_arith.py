@@ -202,6 +202,28 @@ def test_qd_mul_add_error_bounds(orc):
         assert abs(frac(d[:, i]) - (X - Y)) <= Fraction(1, 2 ** 205) * (abs(X) + abs(Y))
 
 
+def test_qd_add_exact_when_three_leading_words_cancel(orc):
+    """x + y with y = (-x0, -x1, -x2, z3): the exact sum x3 + z3 is a two-word expansion, and
+    the sloppy qd_add (numerics.md s.3) returns it exactly -- every TwoSum above the last
+    word is exact on zeros, the last word's TwoSum error reaches the renormalisation intact.
+    A dropped or mis-signed error term of the fourth-word TwoSum is an O(2^-53) relative error
+    here (the error bounds alone cannot see it: it sits at 2^-212 of |x|)."""
+    rng = np.random.default_rng(12)
+    n = 3000
+    x = gen.qd_matrix(1, n, 14, 0).reshape(4, n)
+    z3 = x[3] * rng.uniform(-0.9, 0.9, n)
+    y = np.stack([-x[0], -x[1], -x[2], z3])
+    assert is_normalised(y)
+    for op, yy, sgn in (("add", y, 1), ("sub", -y, -1)):
+        r = orc.qd_op(op, x, yy)
+        inexact = 0
+        for i in range(n):
+            want = Fraction(float(x[3, i])) + Fraction(float(z3[i]))
+            inexact += float(x[3, i]) + float(z3[i]) != want
+            assert frac(r[:, i]) == want, (op, i)
+        assert inexact > n // 4        # the fourth-word TwoSum has an error term in most cases
+
+
 def test_qd_on_dd_values_agrees_with_dd(orc):
     rng = np.random.default_rng(8)
     a, b = rand_dd(rng, 1000), rand_dd(rng, 1000)

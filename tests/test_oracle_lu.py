@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import ddqd_inputs as gen
-from tests.util import EPS_DD, frac
+from tests.util import EPS_DD, frac, frac_mat
 
 
 def _b_of_ones(orc, A):
@@ -202,3 +202,134 @@ def test_pivot_free_mode(orc):
     assert info == 0 and np.array_equal(piv, np.arange(30))
     assert np.abs(LU[0][np.tril(np.ones((30, 30), bool), -1)]).max() > 1.0
     assert _residual_ok(orc, A, LU, piv, factor=1e6)[0]
+
+
+# ---- pivot order with signs and y := P b on systems that do interchange --
+def _round_expansion(F, W):
+    """A W-word expansion of the rational F (each word the correctly rounded remainder)."""
+    out = []
+    for _ in range(W):
+        w = float(F)
+        out.append(w)
+        F -= Fraction(w)
+    return out
+
+
+def _signed_qd(rng, n):
+    """Random normalised QD values with mixed signs (leading words negative for ~half)."""
+    A = gen.qd_matrix(1, n, int(rng.integers(1, 1 << 30)), 0).reshape(4, n)
+    return A * rng.choice([-1.0, 1.0], n)
+
+
+def test_qd_abs_order_unit_table(orc):
+    """numerics.md s.3 QD magnitude order: the sign is folded on the leading word, then all four
+    words are compared lexicographically. Each row would fail a plausible mistake: no sign
+    fold (rows 1-2), a per-word fabs instead of a fold (rows 3-4), comparing only the leading
+    word(s) (rows 5-6), '>=' instead of '>' (row 7)."""
+    q = lambda *w: list(w) + [0.0] * (4 - len(w))
+    t = 2.0 ** -60
+    table = [
+        (q(-0.75), q(0.5), True),                                   # negative but larger
+        (q(0.5), q(-0.75), False),
+        (q(0.75, -2.0 ** -55), q(0.75, t), False),                 # |.| = 0.75 - 2^-55 < 0.75 + 2^-60
+        (q(-0.75, 2.0 ** -55), q(0.75, t), False),                 # folded: (0.75, -2^-55)
+        (q(-0.75, -t, -2.0 ** -115), q(0.75, t, 2.0 ** -116), True),   # third word decides
+        (q(0.75, t, 2.0 ** -115, -2.0 ** -170), q(-0.75, -t, -2.0 ** -115, -2.0 ** -171), False),
+        (q(-0.75, -t, 2.0 ** -115, 2.0 ** -170), q(0.75, t, -2.0 ** -115, -2.0 ** -170), False),
+    ]
+    for x, y, want in table:
+        assert orc.qd_abs_gt(x, y) == want, (x, y)
+        assert abs(frac(x)) > abs(frac(y)) if want else abs(frac(x)) <= abs(frac(y))
+    # random mixed-sign pairs sharing 1, 2 or 3 leading words: the order is |Fraction| order
+    rng = np.random.default_rng(31)
+    X = _signed_qd(rng, 600)
+    Y = _signed_qd(rng, 600)
+    for i in range(600):
+        share = i % 4                       # 0: independent; 1..3: copy the leading words
+        if share:
+            s = np.sign(X[0, i]) * np.sign(Y[0, i])
+            Y[:share, i] = X[:share, i] * s
+        x, y = X[:, i], Y[:, i]
+        assert orc.qd_abs_gt(x, y) == (abs(frac(x)) > abs(frac(y))), (x, y)
+
+
+def _exact_pivots(A):
+    """Partial pivoting in exact rationals (ties -> lowest row): the pivot sequence of the
+    textbook elimination on the represented values of A [W, n, n]."""
+    M = frac_mat(A)
+    n = len(M)
+    piv = []
+    for k in range(n):
+        r = max(range(k, n), key=lambda i: (abs(M[i][k]), -i))
+        piv.append(r)
+        M[k], M[r] = M[r], M[k]
+        for i in range(k + 1, n):
+            f = M[i][k] / M[k][k]
+            for j in range(k, n):
+                M[i][j] -= f * M[k][j]
+    return piv
+
+
+@pytest.mark.parametrize("W", [2, 4])
+def test_pivot_sequence_matches_exact_elimination(orc, W):
+    """Mixed-sign random matrices (about half the entries negative, and the QD ones sharing
+    leading words across a column so lower words and signs decide): every pivot the oracle
+    picks equals the exact-rational partial-pivoting choice (brute force, n = 12). The
+    DD/QD elimination perturbs the reduced columns only at 2^-100 relative, far below the
+    gaps between candidates of a random matrix."""
+    n = 12
+    rng = np.random.default_rng(7 + W)
+    A = (gen.dd_matrix(n, n, 21, 0) if W == 2 else gen.qd_matrix(n, n, 21, 0))
+    A = A * rng.choice([-1.0, 1.0], (1, n, n))
+    if W == 4:   # column 0: equal leading words up to sign, the pivot decided below them
+        A[:2, 1:6, 0] = A[:2, 0:1, 0] * rng.choice([-1.0, 1.0], 5)
+    LU, ipiv, info = orc.lu(A, panel=4, algo="block")
+    assert info == 0
+    want = _exact_pivots(A)
+    assert list(ipiv) == want
+    assert any(r != k for k, r in enumerate(want))
+    assert any(A[0, r, k] < 0 for k, r in enumerate(want))      # some pivots are negative
+
+
+def test_column0_pivot_negative_entry(orc):
+    """ipiv[0] = argmax |a_i0| where the largest magnitude is a negative entry."""
+    for W in (2, 4):
+        n = 6
+        A = np.zeros((W, n, n))
+        A[0] = np.eye(n)
+        A[0, :, 0] = [0.25, 0.5, -0.875, 0.75, -0.125, 0.5]
+        A[0, 0, 1] = 1.0
+        LU, ipiv, info = orc.lu(A, panel=2, algo="block")
+        assert ipiv[0] == 2 and info == 0
+
+
+@pytest.mark.parametrize("W,algo,T", [(2, "strassen", 4), (2, "winograd", 3), (4, "winograd", 4),
+                                      (4, "block", 16)])
+def test_solve_nondominant_system_exact_rhs(orc, W, algo, T):
+    """P:144 setting on a system that interchanges rows: x = [0..n-1], b := A x formed
+    exactly (Fractions, rounded to a W-word expansion); the solve (y := P b with the swaps in
+    ipiv order, then the two substitutions) returns x within 100 n kappa eps ||x||. Applying
+    the swaps in reverse (or not at all) gives O(1) errors."""
+    n = 24
+    rng = np.random.default_rng(100 + W + T)
+    A = (gen.dd_matrix(n, n, 40 + T, 0) if W == 2 else gen.qd_matrix(n, n, 40 + T, 0))
+    A = A * rng.choice([-1.0, 1.0], (1, n, n))
+    Fa = frac_mat(A)
+    b = np.zeros((W, n))
+    for i in range(n):
+        b[:, i] = _round_expansion(sum((Fa[i][j] * j for j in range(n)), Fraction(0)), W)
+    x, LU, ipiv, info = orc.solve(A, b, panel=8, algo=algo, threshold=T)
+    assert info == 0
+    swaps = [(k, int(r)) for k, r in enumerate(ipiv) if r != k]
+    assert len(swaps) >= 3
+    # the order of the swaps matters on this system (a reversed application differs)
+    y_fwd, y_rev = list(range(n)), list(range(n))
+    for k, r in swaps:
+        y_fwd[k], y_fwd[r] = y_fwd[r], y_fwd[k]
+    for k, r in reversed(swaps):
+        y_rev[k], y_rev[r] = y_rev[r], y_rev[k]
+    assert y_fwd != y_rev
+    kappa = np.linalg.cond(A[0], np.inf)
+    eps = 2.0 ** -104 if W == 2 else 2.0 ** -209
+    err = max(abs(float(frac(x[:, i]) - i)) for i in range(n))
+    assert err <= 100 * n * kappa * eps * (n - 1), (err, kappa)
