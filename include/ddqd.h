@@ -72,6 +72,15 @@ enum { DDQD_ADD_ACCURATE = 0x200 };
  * rounding from the canonical k-ascending sum: bit-identical to the oracle's split-k. */
 #define DDQD_SPLITK(s) ((s) == 2 ? 0x1000 : (s) == 4 ? 0x2000 : (s) == 8 ? 0x3000 : 0)
 
+/* Forced recursion depth (reading R21): OR DDQD_DEPTH(d), 0 <= d <= 254, into `algo`
+ * (Strassen / Winograd) and the recursion halves (m, l, n) with ceil exactly d times instead of
+ * applying the threshold stop rule (`threshold` is then ignored). Used by the multi-GPU band
+ * schedule: a row band of A and a column band of B, each the union of one contiguous band of
+ * the depth-d leaves' rows (columns) mapped up through the d levels, multiplied with the depth
+ * of the whole problem, gives exactly (bitwise) those rows and columns of the whole product --
+ * the same recursion tree restricted to the band. Bit-identical to the oracle's forced depth. */
+#define DDQD_DEPTH(d) ((int)(((d) + 1) & 0xff) << 16)
+
 /* Precisions: number of float64 words per element. */
 enum { DDQD_DD = 2, DDQD_QD = 4 };
 
@@ -149,6 +158,17 @@ int ddqd_post_add(int prec, int algo, int64_t P, const ddqd_mat *M, const ddqd_m
  * subtracts). hm, hn must be ceil(C rows / 2), ceil(C cols / 2). Asynchronous. */
 int ddqd_post_add_ptrs(int prec, int algo, int64_t P, const double *const *children, int64_t hm, int64_t hn,
                        int64_t ld, int64_t ps, int64_t r0, int64_t r1, const ddqd_mat *C, int beta);
+
+/* Band packing for the multi-GPU band schedule (paper_1510_08642_b200/mgpu.py): a gather /
+ * scatter of a rows x cols sub-matrix given by index maps.
+ *   dir 0 (pack)  : compact[w][i][j] := full[w][rmap[i]][cmap[j]]
+ *   dir 1 (unpack): full[w][rmap[i]][cmap[j]] := compact[w][i][j]
+ * rmap: DEVICE int64[rows], cmap: DEVICE int64[cols] (NULL = identity); indices must lie inside
+ * full's rows / cols (not checked on the device: the maps come from the caller's own band
+ * plan); full and compact are single matrices (bs ignored) with their own ld / ps. Pure data
+ * movement (no arithmetic), asynchronous on the thread's stream; DDQD_EINVAL on bad shapes. */
+int ddqd_band_copy(int prec, int dir, int64_t rows, int64_t cols, const int64_t *rmap, const int64_t *cmap,
+                   const ddqd_mat *full, const ddqd_mat *compact);
 
 /* CUDA IPC plumbing for that combine: ddqd_ipc_alloc allocates a device buffer (cudaMalloc,
  * so it is exportable as a whole); ddqd_ipc_handle writes its 64-byte cudaIpcMemHandle_t;

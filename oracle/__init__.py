@@ -149,17 +149,23 @@ def splitk_flag(s: int) -> int:
     return {1: 0, 2: 0x1000, 4: 0x2000, 8: 0x3000}[s]
 
 
-def gemm(A, B, algo="block", threshold=32, bs=0, nthreads=0, madd="canonical", splitk=1):
+def depth_flag(d) -> int:
+    """DDQD_DEPTH(d) algo bits: recurse exactly d levels (reading R21)."""
+    return 0 if d is None else (int(d) + 1) << 16
+
+
+def gemm(A, B, algo="block", threshold=32, bs=0, nthreads=0, madd="canonical", splitk=1, depth=None):
     """C := A B for planar [W, m, l] x [W, l, n] arrays (numerics.md s.4); madd='fused'
     selects the fused DD multiply-add variant (numerics.md s.2), madd='accurate' the
-    accurate-add variant (every DD/QD addition accurate, numerics.md s.2-3)."""
+    accurate-add variant (every DD/QD addition accurate, numerics.md s.2-3); depth = d forces
+    exactly d recursion levels instead of the threshold stop rule (reading R21)."""
     A, B = _f64(A), _f64(B)
     W, m, l = A.shape
     W2, l2, n = B.shape
     if W != W2 or l != l2:
         raise ValueError("dimension mismatch")
     C = np.empty((W, m, n))
-    a = (ALGOS[algo] if isinstance(algo, str) else algo) | _VARIANT[madd] | splitk_flag(splitk)
+    a = (ALGOS[algo] if isinstance(algo, str) else algo) | _VARIANT[madd] | splitk_flag(splitk) | depth_flag(depth)
     rc = lib().or_gemm(W, a, threshold, bs,
                        m, l, n, _p(A), _p(B), _p(C), nthreads)
     if rc:

@@ -582,13 +582,18 @@ static void mat_place(mat_t *dst, const mat_t *src, int64_t r0, int64_t c0) {
                 set_w(dst, w, r0 + i, c0 + j, get_w(src, w, i, j));
 }
 
+/* Forced recursion depth (DDQD_DEPTH(d), reading R21): recurse exactly d levels
+ * instead of applying the stop rule -- the recursion tree of a larger problem restricted to
+ * a row/column band of it (the multi-GPU band schedule). -1 = the P:52 stop rule. */
+static int g_fdepth = -1;
+
 /* Strassen / Winograd with stop rule min(m,l,n) <= T and
  * explicit zero padding to (ceil(m/2), ceil(l/2), ceil(n/2)) per level. */
-static void gemm_rec(int algo, int64_t T, const mat_t *A, const mat_t *B, mat_t *C) {
+static void gemm_rec(int algo, int64_t T, int dep, const mat_t *A, const mat_t *B, mat_t *C) {
     int64_t m = A->rows, l = A->cols, n = B->cols;
     int64_t mn = m < l ? m : l;
     if (n < mn) mn = n;
-    if (mn <= T) { gemm_leaf(A, B, C); return; }
+    if (g_fdepth >= 0 ? dep >= g_fdepth : mn <= T) { gemm_leaf(A, B, C); return; }
     int64_t hm = (m + 1) / 2, hl = (l + 1) / 2, hn = (n + 1) / 2;
     mat_t A11 = mat_quadrant(A, 0, 0, hm, hl), A12 = mat_quadrant(A, 0, hl, hm, hl);
     mat_t A21 = mat_quadrant(A, hm, 0, hm, hl), A22 = mat_quadrant(A, hm, hl, hm, hl);
@@ -600,13 +605,13 @@ static void gemm_rec(int algo, int64_t T, const mat_t *A, const mat_t *B, mat_t 
     if (algo == 1) {
         /* Strassen: P1..P7 */
         mat_t X, Y, t1, t2;
-        X = mat_add(&A11, &A22); Y = mat_add(&B11, &B22); gemm_rec(algo, T, &X, &Y, &P[0]); mat_free(&X); mat_free(&Y);
-        X = mat_add(&A21, &A22); gemm_rec(algo, T, &X, &B11, &P[1]); mat_free(&X);
-        Y = mat_sub(&B12, &B22); gemm_rec(algo, T, &A11, &Y, &P[2]); mat_free(&Y);
-        Y = mat_sub(&B21, &B11); gemm_rec(algo, T, &A22, &Y, &P[3]); mat_free(&Y);
-        X = mat_add(&A11, &A12); gemm_rec(algo, T, &X, &B22, &P[4]); mat_free(&X);
-        X = mat_sub(&A21, &A11); Y = mat_add(&B11, &B12); gemm_rec(algo, T, &X, &Y, &P[5]); mat_free(&X); mat_free(&Y);
-        X = mat_sub(&A12, &A22); Y = mat_add(&B21, &B22); gemm_rec(algo, T, &X, &Y, &P[6]); mat_free(&X); mat_free(&Y);
+        X = mat_add(&A11, &A22); Y = mat_add(&B11, &B22); gemm_rec(algo, T, dep + 1, &X, &Y, &P[0]); mat_free(&X); mat_free(&Y);
+        X = mat_add(&A21, &A22); gemm_rec(algo, T, dep + 1, &X, &B11, &P[1]); mat_free(&X);
+        Y = mat_sub(&B12, &B22); gemm_rec(algo, T, dep + 1, &A11, &Y, &P[2]); mat_free(&Y);
+        Y = mat_sub(&B21, &B11); gemm_rec(algo, T, dep + 1, &A22, &Y, &P[3]); mat_free(&Y);
+        X = mat_add(&A11, &A12); gemm_rec(algo, T, dep + 1, &X, &B22, &P[4]); mat_free(&X);
+        X = mat_sub(&A21, &A11); Y = mat_add(&B11, &B12); gemm_rec(algo, T, dep + 1, &X, &Y, &P[5]); mat_free(&X); mat_free(&Y);
+        X = mat_sub(&A12, &A22); Y = mat_add(&B21, &B22); gemm_rec(algo, T, dep + 1, &X, &Y, &P[6]); mat_free(&X); mat_free(&Y);
         /* C11 = ((P1+P4)-P5)+P7, C12 = P3+P5, C21 = P2+P4, C22 = ((P1-P2)+P3)+P6 */
         t1 = mat_add(&P[0], &P[3]); t2 = mat_sub(&t1, &P[4]); C11 = mat_add(&t2, &P[6]); mat_free(&t1); mat_free(&t2);
         C12 = mat_add(&P[2], &P[4]);
@@ -616,13 +621,13 @@ static void gemm_rec(int algo, int64_t T, const mat_t *A, const mat_t *B, mat_t 
         /* Winograd: S1..S4, T1..T4, M1..M7, U1..U7 */
         mat_t S1 = mat_add(&A21, &A22), S2 = mat_sub(&S1, &A11), S3 = mat_sub(&A11, &A21), S4 = mat_sub(&A12, &S2);
         mat_t T1 = mat_sub(&B12, &B11), T2 = mat_sub(&B22, &T1), T3 = mat_sub(&B22, &B12), T4 = mat_sub(&T2, &B21);
-        gemm_rec(algo, T, &A11, &B11, &P[0]);
-        gemm_rec(algo, T, &A12, &B21, &P[1]);
-        gemm_rec(algo, T, &S4, &B22, &P[2]);
-        gemm_rec(algo, T, &A22, &T4, &P[3]);
-        gemm_rec(algo, T, &S1, &T1, &P[4]);
-        gemm_rec(algo, T, &S2, &T2, &P[5]);
-        gemm_rec(algo, T, &S3, &T3, &P[6]);
+        gemm_rec(algo, T, dep + 1, &A11, &B11, &P[0]);
+        gemm_rec(algo, T, dep + 1, &A12, &B21, &P[1]);
+        gemm_rec(algo, T, dep + 1, &S4, &B22, &P[2]);
+        gemm_rec(algo, T, dep + 1, &A22, &T4, &P[3]);
+        gemm_rec(algo, T, dep + 1, &S1, &T1, &P[4]);
+        gemm_rec(algo, T, dep + 1, &S2, &T2, &P[5]);
+        gemm_rec(algo, T, dep + 1, &S3, &T3, &P[6]);
         mat_free(&S1); mat_free(&S2); mat_free(&S3); mat_free(&S4);
         mat_free(&T1); mat_free(&T2); mat_free(&T3); mat_free(&T4);
         mat_t U2 = mat_add(&P[0], &P[5]);
@@ -652,7 +657,7 @@ static mat_t view(int W, int64_t rows, int64_t cols, int64_t ld, int64_t ps, con
 
 static void gemm_any(int algo, int64_t T, const mat_t *A, const mat_t *B, mat_t *C) {
     if (algo == 0) gemm_leaf(A, B, C);
-    else gemm_rec(algo, T, A, B, C);
+    else gemm_rec(algo, T, 0, A, B, C);
 }
 
 /* C := A B, planar contiguous [W][m][l] x [W][l][n] -> [W][m][n].
@@ -661,8 +666,9 @@ static void gemm_any(int algo, int64_t T, const mat_t *A, const mat_t *B, mat_t 
 int or_gemm(int W, int algo, int64_t T, int64_t bs, int64_t m, int64_t l, int64_t n,
             const double *A, const double *B, double *C, int nthreads) {
     if ((algo & 0x100) && (algo & 0x200)) return -1;
-    if (algo & ~0x33ff) return -1;
+    if (algo & ~0xff33ff) return -1;
     g_variant = (algo & 0x100) ? 1 : (algo & 0x200) ? 2 : 0;
+    g_fdepth = ((algo >> 16) & 0xff) - 1;        /* DDQD_DEPTH(d): d + 1 in bits 16-23 */
     g_split = 1 << ((algo >> 12) & 3);           /* DDQD_SPLITK: 1, 2, 4 or 8 */
     algo &= 0xff;
     if ((W != 2 && W != 4) || algo < 0 || algo > 2 || m < 0 || l < 0 || n < 0) return -1;
@@ -803,6 +809,7 @@ int or_lu(int W, int pivot, int64_t n, double *A, int64_t *ipiv, int64_t K, int 
      * arithmetic is the canonical one, so an accurate LU is not defined (rejected) */
     if (algo & 0x200) return -1;
     g_variant = (algo & 0x100) ? 1 : 0;
+    g_fdepth = -1;                               /* the LU's updates use the P:52 stop rule */
     g_split = 1 << ((algo >> 12) & 3);
     algo &= 0xff;
     if ((W != 2 && W != 4) || n < 0 || K < 1) return -1;

@@ -64,6 +64,7 @@ def _load():
     L.ddqd_lu_solve.argtypes = [i32, i32, i64, vp, vp, vp, vp, i64, i32, i64]
     L.ddqd_elementwise.argtypes = [i32, i32, i64, vp, vp, vp, vp]
     L.ddqd_lu_panel.argtypes = [i32, i32, i64, vp, vp, i64, i64]
+    L.ddqd_band_copy.argtypes = [i32, i32, i64, i64, vp, vp, ctypes.POINTER(Mat), ctypes.POINTER(Mat)]
     L.ddqd_post_add_ptrs.argtypes = [i32, i32, i64, vp, i64, i64, i64, i64, i64, i64, ctypes.POINTER(Mat), i32]
     L.ddqd_ipc_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]
     L.ddqd_ipc_free.argtypes = [vp]
@@ -92,7 +93,8 @@ EXPORTED = ["dd_gemm", "qd_gemm", "ddqd_gemm_ex", "dd_lu_solve", "qd_lu_solve", 
             "ddqd_ipc_handle", "ddqd_ipc_open", "ddqd_ipc_close", "ddqd_elementwise", "ddqd_set_stream",
             "ddqd_workspace_bytes", "ddqd_set_workspace", "ddqd_set_workspace_limit",
             "ddqd_launch_count", "ddqd_release", "ddqd_last_error", "ddqd_version",
-            "ddqd_profile_start", "ddqd_profile_stop", "ddqd_fp64_peak", "ddqd_pre_add", "ddqd_post_add"]
+            "ddqd_profile_start", "ddqd_profile_stop", "ddqd_fp64_peak", "ddqd_pre_add", "ddqd_post_add",
+            "ddqd_band_copy"]
 
 
 def _check(rc: int, what: str) -> int:
@@ -120,6 +122,15 @@ def _set_stream(t):
 
 
 _SPLITK = {1: 0, 2: 0x1000, 4: 0x2000, 8: 0x3000}   # DDQD_SPLITK(s)
+
+
+def depth_flag(d) -> int:
+    """DDQD_DEPTH(d): recurse exactly d levels (the band schedule's compact problems)."""
+    if d is None:
+        return 0
+    if not 0 <= int(d) <= 254:
+        raise ValueError("depth must be in 0..254")
+    return (int(d) + 1) << 16
 
 
 def _algo(a, madd="canonical", splitk=1) -> int:
@@ -180,9 +191,10 @@ def qd_gemm(A, B, algo="block", threshold=128, out=None, madd="canonical", split
 
 
 def gemm_ex(prec, algo, threshold, m, l, n, batch, A, lda, psA, bsA, B, ldb, psB, bsB,
-            C, ldc, psC, bsC, beta=0, madd="canonical"):
-    """Strided/batched form (ddqd_gemm_ex); A, B, C are device addresses (ints)."""
-    d = GemmDesc(prec, _algo(algo, madd), threshold, m, l, n, batch, A, lda, psA, bsA, B, ldb, psB, bsB,
+            C, ldc, psC, bsC, beta=0, madd="canonical", depth=None):
+    """Strided/batched form (ddqd_gemm_ex); A, B, C are device addresses (ints); depth = d ORs in
+    DDQD_DEPTH(d) (exactly d recursion levels, threshold unused)."""
+    d = GemmDesc(prec, _algo(algo, madd) | depth_flag(depth), threshold, m, l, n, batch, A, lda, psA, bsA, B, ldb, psB, bsB,
                  C, ldc, psC, bsC, beta)
     return _check(lib.ddqd_gemm_ex(ctypes.byref(d)), "gemm_ex")
 
@@ -287,7 +299,7 @@ def ipc_close(ptr):
     _check(lib.ddqd_ipc_close(ctypes.c_void_p(ptr)), "ipc_close")
 
 
-def gemm_batched(A, B, C, algo, threshold, beta=0, madd="canonical"):
+def gemm_batched(A, B, C, algo, threshold, beta=0, madd="canonical", depth=None):
     """C[b] := A[b] B[b] for contiguous [batch, W, .., ..] CUDA tensors (one library schedule)."""
     batch, W, m, l = A.shape
     n = B.shape[3]
@@ -295,7 +307,25 @@ def gemm_batched(A, B, C, algo, threshold, beta=0, madd="canonical"):
     return gemm_ex(W, algo, threshold, m, l, n, batch,
                    A.data_ptr(), l, m * l, W * m * l,
                    B.data_ptr(), n, l * n, W * l * n,
-                   C.data_ptr(), n, m * n, W * m * n, beta, madd)
+                   C.data_ptr(), n, m * n, W * m * n, beta, madd, depth)
+
+
+def band_copy(direction, full, compact, rmap=None, cmap=None):
+    """ddqd_band_copy: direction 'pack' (compact := full[rmap][:, cmap]) or 'unpack'
+    (full[rmap][:, cmap] := compact) for [W, r, c] CUDA tensors with unit-stride rows; rmap /
+    cmap: int64 CUDA tensors (None = identity). The compact extent is compact's shape."""
+    W, rows, cols = compact.shape
+    if full.shape[0] != W:
+        raise ValueError("word counts differ")
+    dirv = {"pack": 0, "unpack": 1}[direction]
+    for mp, k in ((rmap, rows), (cmap, cols)):
+        if mp is not None and (mp.dtype != _torch().int64 or mp.numel() != k or not mp.is_contiguous()):
+            raise ValueError("maps must be contiguous int64 of the compact extent")
+    _set_stream(compact)
+    f, c = batch_mat(full), batch_mat(compact)
+    _check(lib.ddqd_band_copy(W, dirv, rows, cols, rmap.data_ptr() if rmap is not None else None,
+                              cmap.data_ptr() if cmap is not None else None, ctypes.byref(f), ctypes.byref(c)),
+           "band_copy")
 
 
 def lu_solve(A, b, panel=256, algo="strassen", threshold=128, pivot=True, overwrite=False,

@@ -168,14 +168,15 @@ static int where(const void *p) {
 
 static int check_gemm_args(int64_t m, int64_t l, int64_t n, int algo, int64_t T) {
     if (m < 0 || l < 0 || n < 0) { set_error("negative dimension"); return DDQD_EINVAL; }
-    if (algo & ~(0xff | DDQD_MADD_FUSED | DDQD_ADD_ACCURATE | 0x3000)) { set_error("unknown algo flag"); return DDQD_EINVAL; }
+    if (algo & ~(0xff | DDQD_MADD_FUSED | DDQD_ADD_ACCURATE | 0x3000 | 0xff0000)) { set_error("unknown algo flag"); return DDQD_EINVAL; }
+    const bool depth_forced = (algo & 0xff0000) != 0;   // DDQD_DEPTH(d): the threshold is unused
     if ((algo & DDQD_MADD_FUSED) && (algo & DDQD_ADD_ACCURATE)) {
         set_error("DDQD_MADD_FUSED and DDQD_ADD_ACCURATE are exclusive");
         return DDQD_EINVAL;
     }
     algo &= 0xff;
     if (algo < 0 || algo > 2) { set_error("algo must be DDQD_BLOCK, DDQD_STRASSEN or DDQD_WINOGRAD"); return DDQD_EINVAL; }
-    if (algo != 0 && T < 1) { set_error("threshold must be >= 1"); return DDQD_EINVAL; }
+    if (algo != 0 && T < 1 && !depth_forced) { set_error("threshold must be >= 1"); return DDQD_EINVAL; }
     const double elems = (double)m * (double)l + (double)l * (double)n + (double)m * (double)n;
     if (elems * 4.0 > 9.0e18) { set_error("size overflow"); return DDQD_EINVAL; }
     return DDQD_OK;
@@ -262,8 +263,8 @@ static int gemm_entry(int W, int64_t m, int64_t l, int64_t n, const double *A, c
     }
     if (!(wa == 1 && wb == 1 && wc == 1)) { set_error("A, B, C must be all device or all host pointers"); return DDQD_EINVAL; }
     // host path: stage through library-owned device memory, copy back, synchronise
-    const bool streamed = (algo & 0xff) == DDQD_WINOGRAD && std::min(std::min(m, l), n) > T &&
-                          host_stream_enabled();
+    const bool streamed = (algo & 0xff) == DDQD_WINOGRAD && !(algo & 0xff0000) &&
+                          std::min(std::min(m, l), n) > T && host_stream_enabled();
     const size_t oB = (bA + 255) & ~size_t(255), oC = oB + ((bB + 255) & ~size_t(255)),
                  oT = oC + ((bC + 255) & ~size_t(255));
     int st = DDQD_OK;
@@ -536,6 +537,23 @@ int ddqd_post_add_ptrs(int prec, int algo, int64_t P, const double *const *child
         return DDQD_EINVAL;
     }
     return launch_post_add_ptrs(prec, algo, P, children, hm, hn, ld, ps, r0, r1, to_desc(C), beta, t_stream);
+}
+
+int ddqd_band_copy(int prec, int dir, int64_t rows, int64_t cols, const int64_t *rmap, const int64_t *cmap,
+                   const ddqd_mat *full, const ddqd_mat *compact) {
+    t_err.clear();
+    if ((prec != 2 && prec != 4) || (dir != 0 && dir != 1) || rows < 0 || cols < 0 || !full || !compact ||
+        !full->p || !compact->p) {
+        set_error("bad band_copy arguments");
+        return DDQD_EINVAL;
+    }
+    if (compact->rows < rows || compact->cols < cols || compact->ld < cols || full->ld < full->cols ||
+        (!rmap && rows > full->rows) || (!cmap && cols > full->cols)) {
+        set_error("band_copy: shapes do not fit");
+        return DDQD_EINVAL;
+    }
+    if (rows == 0 || cols == 0) return DDQD_OK;
+    return launch_band_copy(prec, dir, rows, cols, rmap, cmap, to_desc(full), to_desc(compact), t_stream);
 }
 
 // CUDA IPC plumbing for the multi-GPU combine (buffers other processes map and read/write)

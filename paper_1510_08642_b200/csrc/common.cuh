@@ -77,6 +77,9 @@ int launch_post_quad(int W, int algo, int q, const MatDesc &M, const MatDesc &C,
 int launch_post_add_ptrs(int W, int algo, int64_t P, const double *const *ch, int64_t hm, int64_t hn,
                          int64_t ld, int64_t ps, int64_t r0, int64_t r1, const MatDesc &C, int beta,
                          cudaStream_t s);
+// Band pack (dir 0) / unpack (dir 1) through row / column index maps (band.cu).
+int launch_band_copy(int W, int dir, int64_t rows, int64_t cols, const int64_t *rmap, const int64_t *cmap,
+                     const MatDesc &full, const MatDesc &compact, cudaStream_t s);
 int launch_elementwise(int W, int op, int64_t count, const double *x, const double *y,
                        const double *w, double *z, cudaStream_t s);
 

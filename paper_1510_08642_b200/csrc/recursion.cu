@@ -28,6 +28,7 @@ size_t workspace_limit();                          // abi.cu
 
 struct Plan {
     int W = 2, algo = 0, d = 0, s = 0, mv = 0;
+    int fd = -1;                        // DDQD_DEPTH(fd): recurse exactly fd levels (T unused)
     int64_t T = 1;
     std::vector<int64_t> m, l, n;       // level shapes, 0..d
     std::vector<int64_t> chunk;         // parents per chunk at level j (j < d)
@@ -58,7 +59,7 @@ static void plan_shapes(Plan &p, int64_t m, int64_t l, int64_t n) {
     p.m = {m}; p.l = {l}; p.n = {n};
     if (p.algo == 0) { p.d = 0; return; }
     int d = 0;
-    while (std::min(std::min(m, l), n) > p.T) {
+    while (p.fd >= 0 ? d < p.fd : std::min(std::min(m, l), n) > p.T) {
         m = (m + 1) / 2; l = (l + 1) / 2; n = (n + 1) / 2;
         p.m.push_back(m); p.l.push_back(l); p.n.push_back(n);
         d++;
@@ -113,8 +114,13 @@ static int lanes_wanted() {
     return v;
 }
 
+// DDQD_DEPTH(d) rides in algo bits 16-23 as d + 1 (0 = the threshold stop rule)
+static int forced_depth(int algo) { return ((algo >> 16) & 0xff) - 1; }
+
 static int make_plan(Plan &p, int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n,
                      int64_t batch, size_t limit) {
+    p.fd = forced_depth(algo);
+    algo &= 0xff;
     p.W = W; p.algo = algo; p.T = T;
     plan_shapes(p, m, l, n);
     if (p.d == 0) { p.bytes = 0; p.s = 0; return DDQD_OK; }
@@ -131,7 +137,7 @@ static int make_plan(Plan &p, int W, int algo, int64_t T, int64_t m, int64_t l, 
 
 size_t gemm_workspace_bytes(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n,
                             int64_t batch, size_t limit, int *dfs_levels) {
-    algo &= 0xff;
+    algo &= 0xff00ff;
     Plan p;
     make_plan(p, W, algo, T, m, l, n, batch, limit);
     if (dfs_levels) *dfs_levels = p.s;
@@ -251,7 +257,7 @@ int run_gemm(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n, int64_
     if (m == 0 || n == 0 || batch == 0) return DDQD_OK;
     const int mv = ((algo & DDQD_MADD_FUSED) ? 1 : (algo & DDQD_ADD_ACCURATE) ? 2 : 0) |
                    (((algo >> 12) & 3) << 4);   // split-k (DDQD_SPLITK) rides in bits 4-5
-    algo &= 0xff;
+    algo &= 0xff00ff;                                // algorithm + forced depth
     Plan p;
     int rc = make_plan(p, W, algo, T, m, l, n, batch, workspace_limit());
     if (rc) return rc;

@@ -49,6 +49,32 @@ def rec_shapes(m, l, n, T):
     return shapes
 
 
+def band_index_map(dims, a, b):
+    """Level-0 indices of the band [a, b) of the depth-d index range, ascending.
+
+    dims = [n_0, n_1, ..., n_d] with n_{j+1} = ceil(n_j / 2) (one dimension of the recursion's
+    level shapes). Index r of a level-(j+1) child is index r of the parent's top/left quadrant
+    and index n_{j+1} + r of its bottom/right quadrant (absent -- the virtual padding -- when
+    that is >= n_j). Going up from [a, b) at level d gives the set the band touches at every
+    level; taken in this order (top part, then bottom part) the compact sizes satisfy
+    H_{j+1} = ceil(H_j / 2), so the compact band recursed with the same depth reproduces, entry
+    for entry, the recursion of the whole problem (reading R21)."""
+    idx = list(range(a, b))
+    for j in range(len(dims) - 2, -1, -1):
+        h = dims[j + 1]
+        idx = idx + [h + r for r in idx if h + r < dims[j]]
+    return idx
+
+
+def band_grid(world: int):
+    """(G_r, G_c) with G_r * G_c = world and G_r <= G_c as close as possible: rows of C split
+    G_r ways, columns G_c ways (8 GPUs: 2 x 4)."""
+    gr = int(math.isqrt(world))
+    while world % gr:
+        gr -= 1
+    return gr, world // gr
+
+
 def balanced_slices(count: int, world: int):
     """Contiguous LPT split of `count` equal-cost units over `world` ranks."""
     base, extra = divmod(count, world)
@@ -121,6 +147,21 @@ class CudaBackend:
     def gemm_batched(self, A, B, C, algo, T):
         if A.shape[0]:
             self.ddqd.gemm_batched(A, B, C, algo, T)
+
+    def index(self, values, like):
+        import torch
+        return torch.tensor(values, dtype=torch.int64, device=like.device)
+
+    def band_copy(self, direction, full, compact, rmap, cmap):
+        self.ddqd.band_copy(direction, full, compact, rmap, cmap)
+
+    def gemm_depth(self, A, B, C, algo, depth, beta=0):
+        """C := (C -) A B with exactly `depth` recursion levels on contiguous [W, r, c] tensors."""
+        W, m, l = A.shape
+        n = B.shape[2]
+        self.ddqd._set_stream(A)
+        self.ddqd.gemm_ex(W, algo, 1, m, l, n, 1, A.data_ptr(), l, m * l, 0, B.data_ptr(), n, l * n, 0,
+                          C.data_ptr(), n, m * n, 0, beta, depth=depth if algo not in ("block", 0) else None)
 
     def gemm_rows(self, A, B, r0, r1, out, algo, T, beta=0):
         """out[:, :r1-r0, :] := (out -) A[:, r0:r1, :] B via strided views (no copies)."""
@@ -402,6 +443,139 @@ class DistributedGemm:
         if self.rank == 0:
             for r, (a, b) in enumerate(self.slices):
                 C[:, a:b, :].copy_(bufs["gather"][r][:, : b - a, :])
+        return C
+
+
+def _p2p(dist, ops):
+    """One group of point-to-point transfers (op, tensor, peer), waited for (empty: no-op)."""
+    if ops:
+        for q in dist.batch_isend_irecv([dist.P2POp(op, t, peer) for op, t, peer in ops]):
+            q.wait()
+
+
+class BandGemm:
+    """The band schedule: C := A B (beta = 0) or C := C - A B (beta = 1)
+    over the process group, each rank computing one (row band x column band) tile of C with the
+    WHOLE problem's recursion tree restricted to it -- bitwise the single-GPU result.
+
+    The ranks form a G_r x G_c grid (band_grid). The depth-d leaf rows [0, m_d) are cut into G_r
+    contiguous bands and the leaf columns [0, n_d) into G_c; band_index_map lifts a band to the
+    level-0 rows (columns) it touches. Rank (g_r, g_c) packs those rows of A and columns of B
+    (ddqd_band_copy), multiplies the compact operands with DDQD_DEPTH(d) (the same d levels of
+    pre-additions, leaves and post-additions, on 1/G of every level's positions) and sends its
+    compact C tile to rank 0, which unpacks every tile into C. No products or partial sums cross
+    the network and there is no combine tail on rank 0: the only traffic is the operand
+    broadcast and the tiles of C (with beta = 1, the tiles of C also go out first). Every
+    element follows the one-GPU operation sequence, so any world size gives the same bits."""
+
+    def __init__(self, W, algo, T, m, l, n, dist, device=None, backend=None, beta=0, replicated_inputs=False,
+                 grid=None, world=None):
+        self.W, self.algo, self.T, self.beta = W, algo, T, beta
+        self.m, self.l, self.n = m, l, n
+        self.dist = dist             # None: emulate() only, for a `world` of ranks on one device
+        self.rank = dist.get_rank() if dist is not None else 0
+        self.world = dist.get_world_size() if dist is not None else int(world)
+        self.backend = backend or CudaBackend()
+        self.replicated_inputs = replicated_inputs
+        block = algo in ("block", 0)
+        self.shapes = [(m, l, n)] if block else rec_shapes(m, l, n, T)
+        self.d = len(self.shapes) - 1
+        self.gr, self.gc = grid or band_grid(self.world)
+        if self.gr * self.gc != self.world:
+            raise ValueError("grid must multiply to the world size")
+        mdims = [s[0] for s in self.shapes]
+        ndims = [s[2] for s in self.shapes]
+        rb = balanced_slices(mdims[-1], self.gr)
+        cb = balanced_slices(ndims[-1], self.gc)
+        # rank g = g_r * G_c + g_c owns row band g_r and column band g_c
+        self.rows = [band_index_map(mdims, a, b) for a, b in rb]
+        self.cols = [band_index_map(ndims, a, b) for a, b in cb]
+        self._maps = None
+        self._bufs = None
+
+    def tile(self, g):
+        return self.rows[g // self.gc], self.cols[g % self.gc]
+
+    def run_tile(self, g, A, B, C, timer=None):
+        """Rank g's whole share on the current device: pack its operand bands out of the full
+        A and B, multiply them with the problem's depth, unpack the tile into C (beta = 1: C's
+        tile is packed first and updated). `timer(fn)` may wrap the compute call."""
+        bk, W = self.backend, self.W
+        rows, cols = self.tile(g)
+        if not rows or not cols:
+            return
+        rm, cm = bk.index(rows, A), bk.index(cols, A)
+        Ab = bk.empty((W, len(rows), self.l), A)
+        Bb = bk.empty((W, self.l, len(cols)), A)
+        Ct = bk.empty((W, len(rows), len(cols)), A)
+        bk.band_copy("pack", A, Ab, rm, None)
+        bk.band_copy("pack", B, Bb, None, cm)
+        if self.beta:
+            bk.band_copy("pack", C, Ct, rm, cm)
+        step = lambda: bk.gemm_depth(Ab, Bb, Ct, self.algo, self.d, self.beta)   # noqa: E731
+        timer(step) if timer else step()
+        bk.band_copy("unpack", C, Ct, rm, cm)
+
+    def emulate(self, A, B, C):
+        """Every rank's tile in turn on one device (no communication): the schedule's result,
+        for tests and for timing one rank's share on a single GPU."""
+        for g in range(self.world):
+            self.run_tile(g, A, B, C)
+        return C
+
+    def _setup(self, like):
+        if self._bufs is not None:
+            return self._bufs
+        bk, W = self.backend, self.W
+        rows, cols = self.tile(self.rank)
+        maps = {"r": bk.index(rows, like) if self.gr > 1 else None,
+                "c": bk.index(cols, like) if self.gc > 1 else None}
+        bufs = {"A": bk.empty((W, len(rows), self.l), like) if self.gr > 1 else None,
+                "B": bk.empty((W, self.l, len(cols)), like) if self.gc > 1 else None,
+                "C": bk.empty((W, len(rows), len(cols)), like)}
+        if self.rank == 0:
+            bufs["tiles"], maps["tiles"] = [], []
+            for g in range(self.world):
+                r, c = self.tile(g)
+                bufs["tiles"].append(bufs["C"] if g == 0 else bk.empty((W, len(r), len(c)), like))
+                maps["tiles"].append((bk.index(r, like), bk.index(c, like)))
+        self._maps, self._bufs = maps, bufs
+        return bufs
+
+    def __call__(self, A, B, C):
+        dist, bk = self.dist, self.backend
+        if not self.replicated_inputs:
+            dist.broadcast(A, 0)
+            dist.broadcast(B, 0)
+        bufs = self._setup(A)
+        maps = self._maps
+        Ct = bufs["C"]
+        if self.beta:
+            # C := C - A B: every rank's tile of C goes out first (rank 0 holds C)
+            # (the collectives are ordered after the pack kernels on the current stream)
+            if self.rank == 0:
+                for g in range(self.world):
+                    rm, cm = maps["tiles"][g]
+                    bk.band_copy("pack", C, bufs["tiles"][g], rm, cm)
+                _p2p(dist, [(dist.isend, bufs["tiles"][g], g) for g in range(1, self.world)])
+            else:
+                _p2p(dist, [(dist.irecv, Ct, 0)])
+        Ab, Bb = A, B
+        if bufs["A"] is not None:
+            bk.band_copy("pack", A, bufs["A"], maps["r"], None)
+            Ab = bufs["A"]
+        if bufs["B"] is not None:
+            bk.band_copy("pack", B, bufs["B"], None, maps["c"])
+            Bb = bufs["B"]
+        if Ct.shape[1] and Ct.shape[2]:
+            bk.gemm_depth(Ab, Bb, Ct, self.algo, self.d, self.beta)
+        if self.rank == 0:
+            _p2p(dist, [(dist.irecv, bufs["tiles"][g], g) for g in range(1, self.world)])
+            for g in range(self.world):
+                rm, cm = maps["tiles"][g]
+                bk.band_copy("unpack", C, bufs["tiles"][g], rm, cm)
+        else:
+            _p2p(dist, [(dist.isend, Ct, 0)])
         return C
 
 

@@ -958,3 +958,84 @@ def test_randomized_lu_sweep(orc):
         assert got[3] == ref[3] == 0, tag
         assert np.array_equal(np_(got[2]), ref[2]), tag
         assert same(np_(got[1]), ref[1]) and same(np_(got[0]), ref[0]), tag
+
+
+# ---- band schedule (BandGemm) and the DDQD_DEPTH flag on one GPU -----------------------------
+@pytest.mark.parametrize("W,algo,m,l,n,d", [(2, "winograd", 37, 29, 33, 3), (2, "strassen", 70, 65, 66, 2),
+                                              (4, "winograd", 21, 18, 25, 2), (2, "winograd", 200, 190, 170, 0)])
+def test_forced_depth_bitwise(orc, W, algo, m, l, n, d):
+    """DDQD_DEPTH(d): exactly d levels whatever the shape, bit-identical to the oracle's forced
+    depth (reading R21)."""
+    A, B = gen.matrix(W, m, l, 43, 0), gen.matrix(W, l, n, 43, 1)
+    C = torch.empty((W, m, n), dtype=torch.float64, device=DEV)
+    a, b = cu(A), cu(B)
+    ddqd._set_stream(a)
+    ddqd.gemm_ex(W, algo, 1, m, l, n, 1, a.data_ptr(), l, m * l, 0, b.data_ptr(), n, l * n, 0,
+                 C.data_ptr(), n, m * n, 0, 0, depth=d)
+    assert same(np_(C), orc.gemm(A, B, algo, threshold=1, depth=d))
+
+
+def test_band_copy_pack_unpack(orc):
+    from paper_1510_08642_b200.mgpu import band_index_map
+    rng = np.random.default_rng(3)
+    for W in (2, 4):
+        F = gen.matrix(W, 301, 257, 44, 0)
+        rows = sorted(rng.choice(301, 77, replace=False).tolist())
+        cols = band_index_map([257, 129, 65, 33], 5, 20)
+        f = cu(F)
+        c = torch.empty((W, len(rows), len(cols)), dtype=torch.float64, device=DEV)
+        rm = torch.tensor(rows, dtype=torch.int64, device=DEV)
+        cm = torch.tensor(cols, dtype=torch.int64, device=DEV)
+        ddqd.band_copy("pack", f, c, rm, cm)
+        assert same(np_(c), np.ascontiguousarray(F[:, np.array(rows)[:, None], np.array(cols)[None, :]]))
+        g = torch.zeros_like(f)
+        ddqd.band_copy("unpack", g, c, rm, cm)
+        want = np.zeros_like(F)
+        want[:, np.array(rows)[:, None], np.array(cols)[None, :]] = F[:, np.array(rows)[:, None], np.array(cols)[None, :]]
+        assert same(np_(g), want)
+        c2 = torch.empty((W, 301, len(cols)), dtype=torch.float64, device=DEV)
+        ddqd.band_copy("pack", f, c2, None, cm)     # identity row map
+        assert same(np_(c2), np.ascontiguousarray(F[:, :, cols]))
+
+
+@pytest.mark.parametrize("W,algo,T,m,l,n,world,beta", [
+    (2, "winograd", 64, 1023, 1025, 1021, 8, 0),    # c3-shaped, 2 x 4 grid
+    (2, "strassen", 32, 301, 257, 299, 4, 0),
+    (4, "winograd", 16, 200, 190, 170, 2, 0),       # QD
+    (2, "strassen", 64, 768, 256, 768, 3, 1),       # the LU update form C := C - A B
+    (2, "block", 64, 300, 200, 250, 4, 0),
+])
+def test_band_schedule_emulated_bitwise(orc, W, algo, T, m, l, n, world, beta):
+    """Every rank's share of the band schedule run in turn on this GPU (pack -> DDQD_DEPTH GEMM
+    -> unpack, the library's kernels): bit-identical to the one-GPU call, so the N-GPU result is
+    too (the ranks' kernels are these; only the transport differs)."""
+    from paper_1510_08642_b200.mgpu import BandGemm
+    A, B = gen.matrix(W, m, l, 45, 0), gen.matrix(W, l, n, 45, 1)
+    C0 = gen.matrix(W, m, n, 45, 2)
+    C = cu(C0)
+    BandGemm(W, algo, T, m, l, n, None, world=world, beta=beta).emulate(cu(A), cu(B), C)
+    a, b = cu(A), cu(B)
+    ref = cu(C0)
+    ddqd._set_stream(a)
+    ddqd.gemm_ex(W, algo, T, m, l, n, 1, a.data_ptr(), l, m * l, 0, b.data_ptr(), n, l * n, 0,
+                 ref.data_ptr(), n, m * n, 0, beta)
+    assert same(np_(C), np_(ref))
+    if m <= 400 and not beta:
+        assert same(np_(C), orc.gemm(A, B, algo, threshold=T))
+
+
+def test_band_schedule_nccl_world1(orc):
+    import socket
+    import torch.distributed as dist
+    from paper_1510_08642_b200.mgpu import BandGemm
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    try:
+        m, l, n, T = 301, 257, 299, 32
+        A = gen.dd_matrix(m, l, 17, 0); B = gen.dd_matrix(l, n, 17, 1)
+        C = torch.empty((2, m, n), dtype=torch.float64, device=DEV)
+        BandGemm(2, "winograd", T, m, l, n, dist)(cu(A), cu(B), C)
+        assert same(np_(C), orc.gemm(A, B, "winograd", threshold=T))
+    finally:
+        dist.destroy_process_group()

@@ -33,6 +33,9 @@ class OracleBackend:
         self.o = oracle
         self.W = W
         self.op = oracle.dd_op if W == 2 else oracle.qd_op
+        # one OpenMP thread per rank (omp_set_num_threads persists for this thread): several
+        # ranks each spinning a team over every core make the oracle ~1000x slower
+        oracle.gemm(np.zeros((W, 1, 1)), np.zeros((W, 1, 1)), nthreads=1)
 
     def empty(self, shape, like):
         return torch.empty(shape, dtype=torch.float64)
@@ -148,6 +151,25 @@ class OracleBackend:
         for b in range(A.shape[0]):
             C[b] = torch.from_numpy(self.o.gemm(A[b].numpy(), B[b].numpy(), algo, threshold=T))
 
+    def index(self, values, like):
+        return torch.tensor(values, dtype=torch.int64)
+
+    def band_copy(self, direction, full, compact, rmap, cmap):
+        W, r, c = compact.shape
+        ri = rmap if rmap is not None else torch.arange(r)
+        ci = cmap if cmap is not None else torch.arange(c)
+        if direction == "pack":
+            compact[:] = full[:, ri[:, None], ci[None, :]]
+        else:
+            full[:, ri[:, None], ci[None, :]] = compact
+
+    def gemm_depth(self, A, B, C, algo, depth, beta=0):
+        t = self.o.gemm(np.ascontiguousarray(A.numpy()), np.ascontiguousarray(B.numpy()), algo, threshold=1,
+                        depth=None if algo == "block" else depth)
+        if beta:
+            t = self._ew("sub", np.ascontiguousarray(C.numpy()), t)
+        C[:] = torch.from_numpy(t)
+
     def gemm_rows(self, A, B, r0, r1, out, algo, T, beta=0):
         t = self.o.gemm(np.ascontiguousarray(A[:, r0:r1, :].numpy()), B.numpy(), algo, threshold=T)
         if beta:
@@ -156,7 +178,8 @@ class OracleBackend:
 
 
 def _worker(rank, world, port, cfg, q, chunk=None, combine="nccl"):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    # one OpenMP thread per rank: several ranks spinning on all cores crawl
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), OMP_NUM_THREADS="1")
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1510_08642_b200.mgpu import DistributedGemm
@@ -224,7 +247,8 @@ def test_balancer():
 
 # ---- distributed LU (row f4) ------------------------------------------------------------------
 def _lu_worker(rank, world, port, cfg, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    # one OpenMP thread per rank: several ranks spinning on all cores crawl
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), OMP_NUM_THREADS="1")
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import oracle
@@ -310,7 +334,8 @@ def test_p2p_combine_matches_single_process(orc, cfg, world):
 
 
 def _auto_worker(rank, world, port, cfg, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    # one OpenMP thread per rank: several ranks spinning on all cores crawl
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), OMP_NUM_THREADS="1")
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1510_08642_b200.mgpu import AutoDistributedGemm, DistributedGemm
@@ -355,3 +380,58 @@ def test_c_tiles_and_auto_schedule(orc):
     expect = orc.gemm(A, B, algo, threshold=T) if choice1 == "products" else tiles
     assert np.array_equal(C.view(np.int64), expect.view(np.int64))
     assert not np.array_equal(tiles, orc.gemm(A, B, algo, threshold=T))   # the two schedules round differently
+
+
+# ---- band schedule (BandGemm: each rank one tile of C, the whole problem's tree) ---------------
+def _band_worker(rank, world, port, cfg, q):
+    # one OpenMP thread per rank: several ranks spinning on all cores crawl
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), OMP_NUM_THREADS="1")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1510_08642_b200.mgpu import BandGemm
+        W, algo, T, m, l, n, beta = cfg
+        A = torch.from_numpy(gen.matrix(W, m, l, 31, 0)) if rank == 0 else torch.zeros((W, m, l), dtype=torch.float64)
+        B = torch.from_numpy(gen.matrix(W, l, n, 31, 1)) if rank == 0 else torch.zeros((W, l, n), dtype=torch.float64)
+        C = torch.from_numpy(gen.matrix(W, m, n, 31, 2)) if rank == 0 else None
+        bg = BandGemm(W, algo, T, m, l, n, dist, backend=OracleBackend(W), beta=beta)
+        C0 = C.clone() if rank == 0 else None
+        bg(A, B, C)
+        if rank == 0 and beta:
+            C.copy_(C0)
+        bg(A, B, C)    # buffers are reused across steps
+        if rank == 0:
+            q.put(((bg.gr, bg.gc, bg.d), C.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,world", [
+    ((2, "winograd", 4, 37, 29, 33, 0), 2),     # 1 x 2 grid, odd shapes (virtual padding), d = 3
+    ((2, "strassen", 3, 40, 41, 42, 0), 3),     # 1 x 3 grid
+    ((2, "winograd", 3, 45, 30, 38, 0), 4),     # 2 x 2 grid, d = 4
+    ((4, "winograd", 2, 19, 23, 17, 0), 2),     # QD
+    ((2, "strassen", 4, 36, 16, 36, 1), 2),     # C := C - A B (the LU update form)
+    ((2, "block", 8, 31, 20, 25, 0), 4),        # Block: plain 2 x 2 C tiles
+])
+def test_band_schedule_matches_single_process(orc, cfg, world):
+    """BandGemm: every rank multiplies its packed (row band x column band) operands with the
+    whole problem's depth (DDQD_DEPTH); rank 0 unpacks the tiles -- bit-identical to the
+    single-process recursion for every grid."""
+    W, algo, T, m, l, n, beta = cfg
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_band_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    (gr, gc, d), C = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A, B = gen.matrix(W, m, l, 31, 0), gen.matrix(W, l, n, 31, 1)
+    ref = orc.gemm(A, B, algo, threshold=T)
+    if beta:
+        ref = (orc.dd_op if W == 2 else orc.qd_op)("sub", gen.matrix(W, m, n, 31, 2).reshape(W, -1),
+                                                   ref.reshape(W, -1)).reshape(W, m, n)
+    assert gr * gc == world and (algo == "block" or d >= 1)
+    assert np.array_equal(C.view(np.int64), ref.view(np.int64))
