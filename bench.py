@@ -88,15 +88,24 @@ def parse_args():
     ap.add_argument("--threshold", type=int, default=128)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--k", type=int, default=None, help="multi-GPU product depth (default: balancer)")
-    ap.add_argument("--schedule", default="products", choices=["products", "ctiles", "auto"],
-                    help="multi-GPU schedule: depth-k product distribution (bit-identical to one GPU), "
-                         "C row tiles each recursing on its slab, or whichever measures faster (BJ:5)")
+    ap.add_argument("--schedule", default="auto",
+                    choices=["auto", "bands", "products", "products_p2p", "ctiles", "auto-all"],
+                    help="multi-GPU schedule: auto = whichever of the bit-identical schedules measures "
+                         "fastest (BJ:5 (4)); bands = one tile of C per rank with the whole problem's "
+                         "tree; products = depth-k products to rank 0 (--combine); products_p2p = "
+                         "the same combined over CUDA IPC; ctiles = C row slabs (rounds differently); "
+                         "auto-all = auto including ctiles")
     ap.add_argument("--combine", default="nccl", choices=["nccl", "p2p"],
                     help="multi-GPU combine: products to rank 0 over NCCL point-to-point (default), or "
                          "the fused post-additions reading peers' products over CUDA IPC / NVLink")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--staged-transport", action="store_true",
+                    help="functional test of the N > 1 path on ONE GPU: every rank on cuda:0, exchanges "
+                         "over gloo staged through host memory (mgpu.HostStagedGroup); not a bench number")
+    ap.add_argument("--no-band-model", action="store_true",
+                    help="skip the one-GPU timing of the band schedule's per-rank tiles (N = 1 line)")
     ap.add_argument("--no-variant", action="store_true",
                     help="skip the extra fused / accurate measurements reported under 'variants'")
     ap.add_argument("--madd", default="canonical", choices=["canonical", "fused", "accurate"],
@@ -457,6 +466,113 @@ def lu_bench(args, wl, rank, world, local):
     return 0
 
 
+# ---- multi-GPU ---------------------------------------------------------------------
+def make_schedule(args, W, algo, T, m, l, n, dist, dev, replicated_inputs=False):
+    from paper_1510_08642_b200 import mgpu
+    if args.schedule in ("auto", "auto-all"):
+        cands = None if args.schedule == "auto" else ("bands", "products", "products_p2p", "ctiles")
+        return mgpu.AutoDistributedGemm(W, algo, T, m, l, n, dist, dev, candidates=cands, k=args.k,
+                                        replicated_inputs=replicated_inputs)
+    if args.schedule == "bands":
+        return mgpu.BandGemm(W, algo, T, m, l, n, dist, dev, replicated_inputs=replicated_inputs)
+    combine = "p2p" if args.schedule == "products_p2p" else args.combine
+    return mgpu.DistributedGemm(W, algo, T, m, l, n, dist, dev, k=0 if args.schedule == "ctiles" else args.k,
+                                combine=combine, replicated_inputs=replicated_inputs)
+
+
+def schedule_desc(args, sched, world):
+    if world == 1:
+        return "1 GPU"
+    d = f"{world} GPUs, schedule {args.schedule}"
+    if getattr(sched, "choice", None):
+        d += f" (chose {sched.choice})"
+    inner = sched.cands[sched.choice] if getattr(sched, "choice", None) else sched
+    if hasattr(inner, "gr"):
+        d += f", band grid {inner.gr} x {inner.gc}"
+    elif getattr(inner, "k", None) is not None:
+        d += f", product depth k = {inner.k}, {inner.combine} combine" if inner.k else ", C row slabs"
+    return d
+
+
+def mgpu_e2e(args, wl, A_h, B_h, A, B, C, dist, dev, rank, W, flops_per_step, choice=None):
+    """End to end at N GPUs: pinned host A, B on rank 0 -> H2D overlapped with the NCCL broadcast
+    (chunks) -> the schedule (the device-timed run's choice) -> C gathered on rank 0 -> D2H,
+    every step inside the timed region; device events on each rank, max over ranks."""
+    import argparse
+
+    import torch
+
+    from paper_1510_08642_b200 import mgpu
+    m, l, n = wl["m"], wl["l"], wl["n"]
+    a2 = argparse.Namespace(**vars(args))
+    if choice:
+        a2.schedule = choice
+    sched = make_schedule(a2, W, wl["algo"], wl["T"], m, l, n, dist, dev, replicated_inputs=True)
+    hA = A_h.pin_memory() if rank == 0 else None
+    hB = B_h.pin_memory() if rank == 0 else None
+    hC = torch.empty((W, m, n), dtype=torch.float64).pin_memory() if rank == 0 else None
+
+    def e2e_step():
+        mgpu.host_broadcast(hA, A, dist)
+        mgpu.host_broadcast(hB, B, dist)
+        sched(A, B, C)
+        if rank == 0:
+            hC.copy_(C, non_blocking=True)
+
+    e2e_step()       # the auto schedule measures its candidates here
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ems = float(t.item())
+    return {"value": flops_per_step * args.steps / (ems * 1e-3) / 1e9, "unit": "GFLOP/s",
+            "h2d_bytes_per_step": int((A.numel() + B.numel()) * 8),
+            "d2h_bytes_per_step": int(C.numel() * 8), "ms_per_step": ems / args.steps,
+            "path": "pinned host A, B on rank 0 -> H2D overlapped with the NCCL broadcast (8 chunks each) "
+                    "-> " + schedule_desc(a2, sched, dist.get_world_size()) + " -> C on rank 0 -> "
+                    "pinned host C (D2H); device events, max over ranks"}
+
+
+def band_model(args, wl, A, B, C, peak):
+    """One-GPU measurement of the band schedule's per-rank compute at 2, 4 and 8 GPUs: the
+    largest tile of each grid (pack + DDQD_DEPTH GEMM + unpack, the exact kernels a rank runs)
+    timed on this GPU. The N-GPU step is that plus the operand broadcast and the tile gather,
+    modelled at the measured NVLink rates of B200_PROFILING.md (no multi-GPU box here)."""
+    import torch
+
+    from paper_1510_08642_b200 import mgpu
+    W, m, l, n = wl["W"], wl["m"], wl["l"], wl["n"]
+    out = {}
+    for G in (2, 4, 8):
+        bg = mgpu.BandGemm(W, wl["algo"], wl["T"], m, l, n, None, world=G)
+        # tile 0 holds the largest bands (balanced_slices gives the extra rows to the first)
+        for _ in range(2):
+            bg.run_tile(0, A, B, C)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        reps = 3
+        for _ in range(reps):
+            bg.run_tile(0, A, B, C)
+        e1.record()
+        torch.cuda.synchronize()
+        tile_ms = e0.elapsed_time(e1) / reps
+        bcast_ms = (A.numel() + B.numel()) * 8 / 725e9 * 1e3       # NCCL bus bandwidth, 1 GiB class
+        rows, cols = bg.tile(0)
+        gather_ms = (G - 1) / G * C.numel() * 8 / 770e9 * 1e3      # tiles into rank 0 (peer copy rate)
+        out[str(G)] = {"grid": [bg.gr, bg.gc], "tile_rows": len(rows), "tile_cols": len(cols),
+                       "tile_ms_measured": tile_ms, "broadcast_ms_model": bcast_ms,
+                       "gather_ms_model": gather_ms, "step_ms_model": tile_ms + bcast_ms + gather_ms}
+    return out
+
+
 # ---- our arm ------------------------------------------------------------------------
 def main():
     args = parse_args()
@@ -484,12 +600,19 @@ def main():
     import ddqd_inputs as gen
     import paper_1510_08642_b200 as ddqd
 
+    if args.staged_transport:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if args.staged_transport:
+            from paper_1510_08642_b200.mgpu import HostStagedGroup
+            dist.init_process_group("gloo")
+            dist = HostStagedGroup(dist)
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     W, algo, T, m, l, n = wl["W"], wl["algo"], wl["T"], wl["m"], wl["l"], wl["n"]
     flops_per_step = 2.0 * m * l * n
@@ -506,13 +629,9 @@ def main():
     peak_dfma, _ = ddqd.fp64_peak("dfma")
     peak = max(peak_dadd, peak_dfma)
 
+    sched = None
     if world > 1:
-        from paper_1510_08642_b200 import mgpu
-        if args.schedule == "auto":
-            sched = mgpu.AutoDistributedGemm(W, algo, T, m, l, n, dist, dev, combine=args.combine)
-        else:
-            sched = mgpu.DistributedGemm(W, algo, T, m, l, n, dist, dev,
-                                         k=0 if args.schedule == "ctiles" else args.k, combine=args.combine)
+        sched = make_schedule(args, W, algo, T, m, l, n, dist, dev)
 
         def step():
             sched(A, B, C)
@@ -678,7 +797,23 @@ def main():
                         "(removes the host launch overhead; same kernels, same bits)"}
             del g
 
+    bitwise = None
+    if world > 1:
+        # the multi-GPU result against one GPU's dd_gemm/qd_gemm of the same inputs on rank 0
+        if rank == 0:
+            C1 = ddqd.gemm(A, B, algo, T, madd=args.madd)
+            torch.cuda.synchronize()
+            inner = sched.cands[sched.choice] if getattr(sched, "choice", None) else sched
+            bitwise = {"equal": bool(torch.equal(C1.view(torch.int64), C.view(torch.int64))),
+                       "schedule": getattr(sched, "choice", None) or args.schedule,
+                       "expected_bitwise": not (getattr(inner, "k", 1) == 0 and algo != "block")}
+            del C1
+        dist.barrier()
+
     e2e = None
+    if not args.no_e2e and world > 1:
+        e2e = mgpu_e2e(args, wl, A_h, B_h, A, B, C, dist, dev, rank, W, flops_per_step,
+                       choice=getattr(sched, "choice", None))
     if not args.no_e2e and world == 1:
         hA = A_h.pin_memory()
         hB = B_h.pin_memory()
@@ -699,8 +834,13 @@ def main():
                "path": "dd_gemm/qd_gemm with pinned HOST pointers (library stages H2D/D2H inside the call)"}
         del hA, hB, hC
 
+    bandm = None
+    if world == 1 and algo != "block" and not args.no_band_model and args.custom is None \
+            and args.workload in ("c3", "c2", "c1"):
+        bandm = band_model(args, wl, A, B, C, peak)
+
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:
         import oracle as orc
         orc.build()
         sA, sB, (ms_, ls_, ns_), desc = oracle_sample(wl)
@@ -719,9 +859,11 @@ def main():
                        "madd": args.madd,
                        "depth": d, "leaf_shape": list(shapes[-1]), "leaf_madds_per_step": leaf_madds_step,
                        "l2": "no flush: each operand (%.2f GB) exceeds the 126 MB L2" % (A.numel() * 8 / 1e9),
-                       "parallelism": f"{world} GPU" + (f"s, schedule {args.schedule}"
-                                                        + (f" (chose {sched.choice})" if args.schedule == "auto" else "")
-                                                        + f", {args.combine} combine" if world > 1 else "")},
+                       "parallelism": schedule_desc(args, sched, world),
+                       "schedule_timings_ms": ({k: v * 1e3 for k, v in sched.timings.items()}
+                                               if getattr(sched, "timings", None) else None),
+                       **({"transport": "FUNCTIONAL TEST ONLY: all ranks on one GPU, gloo staged through "
+                                        "host memory (not a bench number)"} if args.staged_transport else {})},
             "roofline": roofline,
             "fp64_roofline_fraction": {
                 "algorithmic_leaf": roofline["frac"],
@@ -732,6 +874,8 @@ def main():
                         "(BJ:5 literal; > 1 possible for Strassen/Winograd)" % (hbm_peak / 1e9, hbm_src)},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "bitwise_vs_1gpu": bitwise,
+            "band_schedule_model": bandm,
             "variants": variants,
             "paper_context": PAPER_CONTEXT.get(args.workload),
             "gpu_launches": int(launches),

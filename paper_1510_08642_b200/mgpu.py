@@ -21,11 +21,17 @@ Both schedules are numerically identical to the single-GPU call (same tree, same
 so results are bit-identical to the oracle for any world size. With beta = 1 the result is
 subtracted from C (C := C - A B), the form of the LU's Schur update.
 
+  Bands (BandGemm): C is partitioned into a G_r x G_c grid of tiles, each a row band x column
+    band of the depth-d LEAVES lifted to level 0, so every rank runs the whole problem's
+    recursion tree restricted to its tile (DDQD_DEPTH) -- no products cross the network and
+    nothing is combined on rank 0; bit-identical to one GPU.
+
 AutoDistributedGemm (BJ:5 (4) "the top-level 7 products are distributed over GPUs, or C is
 partitioned into tiles that each GPU recurses on, choosing whichever measures faster"): times
-both schedules once (max over ranks) and keeps the faster. The C-tile schedule recurses on row
-slabs of C (each slab its own Strassen/Winograd tree), so it rounds differently from the
-one-GPU call; it is bit-exact against the oracle run slab by slab.
+the candidate schedules once (max over ranks) and keeps the fastest; by default only the
+bit-identical ones compete. The C-row-slab schedule (k = 0) recurses on each slab as its own
+Strassen/Winograd tree, so it rounds differently from the one-GPU call; it is bit-exact against
+the oracle run slab by slab and competes only when asked for.
 
 DistributedLU: the blocked LU with its trailing update
 A22 := A22 - L21 U12 run by DistributedGemm over all ranks; rank 0 keeps the matrix
@@ -446,6 +452,22 @@ class DistributedGemm:
         return C
 
 
+def host_broadcast(hX, X, dist, chunks=8):
+    """X (device, every rank) := hX (pinned host tensor on rank 0), the host-to-device copy of
+    each chunk overlapping the NCCL broadcast of the previous one (the copy runs on the current
+    stream, the broadcast on NCCL's, which waits only for its own chunk's copy)."""
+    flat = X.view(-1)
+    src = hX.view(-1) if hX is not None else None
+    n = flat.numel()
+    step = max(1, -(-n // chunks))
+    for a in range(0, n, step):
+        b = min(n, a + step)
+        if dist.get_rank() == 0:
+            flat[a:b].copy_(src[a:b], non_blocking=True)
+        dist.broadcast(flat[a:b], 0)
+    return X
+
+
 def _p2p(dist, ops):
     """One group of point-to-point transfers (op, tensor, peer), waited for (empty: no-op)."""
     if ops:
@@ -619,19 +641,45 @@ class DistributedLU:
 
 
 class AutoDistributedGemm:
-    """C := A B with whichever of the two multi-GPU schedules measures faster on this machine
-    (BJ:5 (4)): "products" (depth-k product distribution, bit-identical to one GPU) or
-    "ctiles" (C row slabs, each rank recursing on its slab). The first call runs both, timed
-    with device syncs and a barrier on either side, takes the max over ranks (so every rank
-    makes the same choice) and leaves C from the chosen schedule; later calls run only it."""
+    """C := A B (or C := C - A B) with whichever multi-GPU schedule measures fastest on this
+    machine (BJ:5 (4) "... choosing whichever measures faster"). Candidates (default: the three
+    that are bit-identical to one GPU, so the result never depends on which one won):
+      "bands"        BandGemm: one tile of C per rank, the whole problem's tree (no combine);
+      "products"     DistributedGemm: depth-k products over the ranks, NCCL to rank 0, combine there;
+      "products_p2p" the same products, combined over CUDA IPC peer memory split over the ranks
+                     (beta = 0 only);
+      "ctiles"       C row slabs each recursing on its own (rounds differently: opt-in only).
+    The first call runs every candidate once, timed with device syncs and a barrier on either
+    side and the max over ranks (so every rank makes the same choice), then leaves C holding the
+    chosen schedule's result (with beta = 1, C is restored before each trial and the winner is
+    run once more on the original C); later calls run only the winner. `timings` (s) and
+    `choice` record the measurement."""
 
-    def __init__(self, W, algo, T, m, l, n, dist, device=None, backend=None, **kw):
+    BITWISE = ("bands", "products", "products_p2p")
+
+    def __init__(self, W, algo, T, m, l, n, dist, device=None, backend=None, beta=0, candidates=None, **kw):
         self.dist = dist
+        self.beta = beta
         self.backend = backend or CudaBackend()
-        self.cands = {
-            "products": DistributedGemm(W, algo, T, m, l, n, dist, device, backend=self.backend, **kw),
-            "ctiles": DistributedGemm(W, algo, T, m, l, n, dist, device, k=0, backend=self.backend, **kw),
+        self.rank = dist.get_rank()
+        names = list(candidates or self.BITWISE)
+        if beta:
+            names = [c for c in names if c != "products_p2p"]   # the p2p combine stores C
+        kw = {k: v for k, v in kw.items() if k != "combine"}
+        make = {
+            "bands": lambda: BandGemm(W, algo, T, m, l, n, dist, device, backend=self.backend, beta=beta,
+                                      replicated_inputs=kw.get("replicated_inputs", False)),
+            "products": lambda: DistributedGemm(W, algo, T, m, l, n, dist, device, backend=self.backend,
+                                                beta=beta, combine="nccl", **kw),
+            "products_p2p": lambda: DistributedGemm(W, algo, T, m, l, n, dist, device, backend=self.backend,
+                                                    combine="p2p", **kw),
+            "ctiles": lambda: DistributedGemm(W, algo, T, m, l, n, dist, device, k=0, backend=self.backend,
+                                              beta=beta, **kw),
         }
+        unknown = [c for c in names if c not in make]
+        if unknown:
+            raise ValueError(f"unknown schedules {unknown}")
+        self.cands = {c: make[c]() for c in names}
         self.choice = None
         self.timings = {}
 
@@ -649,10 +697,119 @@ class AutoDistributedGemm:
 
     def __call__(self, A, B, C):
         if self.choice is None:
-            for name in ("ctiles", "products"):
+            keep = C.clone() if (self.beta and C is not None) else None
+            last = None
+            for name in self.cands:
+                if keep is not None:
+                    C.copy_(keep)
                 self.timings[name] = self._timed(name, A, B, C)
+                last = name
             self.choice = min(self.timings, key=self.timings.get)
-            if self.choice != "products":          # C holds the last schedule's result
+            if keep is not None:
+                C.copy_(keep)
+            # (a collective decision: with beta = 1 only rank 0 holds C, but every rank reruns)
+            if self.beta or (self.choice != last and not
+                             (self.choice in self.BITWISE and last in self.BITWISE)):
                 self.cands[self.choice](A, B, C)
             return C
         return self.cands[self.choice](A, B, C)
+
+    def release(self):
+        for c in self.cands.values():
+            if hasattr(c, "release"):
+                c.release()
+
+
+class HostStagedGroup:
+    """A torch.distributed-like group over gloo that stages CUDA tensors through host memory:
+    the N-GPU code paths (schedules, bench.py's N > 1 line) run as N processes sharing ONE GPU
+    with no kernel ever waiting on another process (every exchange is a host-side gloo
+    transfer), which is how they are exercised where only one GPU exists. A functional test
+    transport, not a performance one: NCCL over NVLink is the real one."""
+
+    class _Done:
+        def wait(self):
+            return True
+
+    def __init__(self, dist):
+        self.d = dist
+        self.ReduceOp = dist.ReduceOp
+
+    # markers for P2POp
+    @staticmethod
+    def isend(*a, **k):
+        raise RuntimeError("use batch_isend_irecv")
+
+    @staticmethod
+    def irecv(*a, **k):
+        raise RuntimeError("use batch_isend_irecv")
+
+    class P2POp:
+        def __init__(self, op, tensor, peer):
+            self.op, self.tensor, self.peer = op, tensor, peer
+
+    def get_rank(self):
+        return self.d.get_rank()
+
+    def get_world_size(self):
+        return self.d.get_world_size()
+
+    def barrier(self):
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+        self.d.barrier()
+
+    def all_gather_object(self, out, obj):
+        self.d.all_gather_object(out, obj)
+
+    def _stage(self, t):
+        return t.detach().cpu().contiguous() if t.is_cuda else t
+
+    def broadcast(self, t, src):
+        c = self._stage(t)
+        self.d.broadcast(c, src)
+        if c is not t:
+            t.copy_(c)
+
+    def all_reduce(self, t, op=None):
+        c = self._stage(t)
+        self.d.all_reduce(c, op=op if op is not None else self.d.ReduceOp.SUM)
+        if c is not t:
+            t.copy_(c)
+
+    def batch_isend_irecv(self, ops):
+        sends, recvs = [], []
+        for o in ops:
+            if o.op is HostStagedGroup.isend:
+                c = self._stage(o.tensor)
+                sends.append((self.d.isend(c, o.peer), c))
+            else:
+                c = o.tensor.new_empty(o.tensor.shape, device="cpu") if o.tensor.is_cuda else o.tensor
+                recvs.append((self.d.irecv(c, o.peer), c, o.tensor))
+        for w, _ in sends:
+            w.wait()
+        for w, c, t in recvs:
+            w.wait()
+            if c is not t:
+                t.copy_(c)
+        return [HostStagedGroup._Done()]
+
+    def scatter(self, t, lst=None, src=0):
+        c = self._stage(t)
+        cl = [self._stage(x) for x in lst] if lst is not None else None
+        self.d.scatter(c, cl, src=src)
+        if c is not t:
+            t.copy_(c)
+
+    def gather(self, t, lst=None, dst=0):
+        c = self._stage(t)
+        cl = [x.new_empty(x.shape, device="cpu") if x.is_cuda else x for x in lst] if lst is not None else None
+        self.d.gather(c, cl, dst=dst)
+        if lst is not None:
+            for x, y in zip(lst, cl):
+                if x is not y:
+                    x.copy_(y)
+
+    def destroy_process_group(self):
+        self.d.destroy_process_group()

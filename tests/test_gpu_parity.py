@@ -1039,3 +1039,38 @@ def test_band_schedule_nccl_world1(orc):
         assert same(np_(C), orc.gemm(A, B, "winograd", threshold=T))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,world", [((2, "winograd", 64, 701, 513, 650), 2),
+                                       ((2, "strassen", 32, 300, 257, 299), 3),
+                                       ((4, "winograd", 32, 190, 170, 201), 2)])
+def test_multiprocess_schedules_staged_bitwise(orc, cfg, world):
+    """2-3 processes on this GPU run every multi-GPU schedule through the library (exchanges
+    over gloo staged through host memory): bands, products (rank-0 combine), products with the
+    p2p combine over CUDA IPC, the automatic choice, and bands with beta = 1 -- all
+    bit-identical to the one-GPU call."""
+    import multiprocessing as pymp
+    import socket
+    from tests import _p2p_worker
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    ctx = pymp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_p2p_worker.run_schedules, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+    assert "error" not in out, out
+    assert all(p.exitcode == 0 for p in procs)
+    W, algo, T, m, l, n = cfg
+    A, B = gen.matrix(W, m, l, 33, 0), gen.matrix(W, l, n, 33, 1)
+    ref = np_(ddqd.gemm(cu(A), cu(B), algo, T))
+    for name in ("bands", "products", "products_p2p", "auto"):
+        assert same(out[name], ref), name
+    C0 = cu(gen.matrix(W, m, n, 33, 2))
+    a, b = cu(A), cu(B)
+    ddqd._set_stream(a)
+    ddqd.gemm_ex(W, algo, T, m, l, n, 1, a.data_ptr(), l, m * l, 0, b.data_ptr(), n, l * n, 0,
+                 C0.data_ptr(), n, m * n, 0, 1)
+    assert same(out["bands_beta1"], np_(C0))

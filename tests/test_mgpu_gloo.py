@@ -344,21 +344,34 @@ def _auto_worker(rank, world, port, cfg, q):
         B = torch.from_numpy(gen.matrix(W, l, n, 23, 1)) if rank == 0 else torch.zeros((W, l, n), dtype=torch.float64)
         C = torch.zeros((W, m, n), dtype=torch.float64)
         C2 = torch.zeros((W, m, n), dtype=torch.float64)
+        C3 = torch.zeros((W, m, n), dtype=torch.float64)
         DistributedGemm(W, algo, T, m, l, n, dist, k=0, backend=OracleBackend(W))(A, B, C2)   # C tiles
-        ag = AutoDistributedGemm(W, algo, T, m, l, n, dist, backend=OracleBackend(W))
+        ag = AutoDistributedGemm(W, algo, T, m, l, n, dist, backend=OracleBackend(W))          # bitwise ones
         ag(A, B, C)
-        choice1 = ag.choice
+        choice1, t1 = ag.choice, dict(ag.timings)
         ag(A, B, C)
+        ag.release()
+        # every schedule incl. the C row slabs
+        ag3 = AutoDistributedGemm(W, algo, T, m, l, n, dist, backend=OracleBackend(W),
+                                  candidates=("ctiles", "bands", "products"))
+        ag3(A, B, C3)
+        # beta = 1 (C := C - A B): C restored before every trial, exactly one update in the end
+        C4 = torch.from_numpy(gen.matrix(W, m, n, 23, 2)) if rank == 0 else None
+        ag4 = AutoDistributedGemm(W, algo, T, m, l, n, dist, backend=OracleBackend(W), beta=1)
+        ag4(A, B, C4)
         if rank == 0:
-            q.put((choice1, ag.choice, C.numpy().copy(), C2.numpy().copy()))
+            q.put((choice1, ag.choice, sorted(t1), C.numpy().copy(), C2.numpy().copy(), ag3.choice,
+                   C3.numpy().copy(), C4.numpy().copy(), sorted(ag4.timings)))
     finally:
         dist.destroy_process_group()
 
 
 def test_c_tiles_and_auto_schedule(orc):
     """BJ:5 (4): the C-tile schedule (each rank recurses on its row slab of C) is bit-exact
-    against the oracle run slab by slab; AutoDistributedGemm times both schedules, makes the
-    same choice on every rank, and returns the chosen schedule's exact result."""
+    against the oracle run slab by slab; AutoDistributedGemm times its candidates, makes the same
+    choice on every rank and returns the chosen schedule's exact result -- by default only the
+    schedules bit-identical to one GPU compete, so the bits never depend on the timing; with
+    beta = 1 (the LU update) C is restored before every trial and updated exactly once."""
     from paper_1510_08642_b200.mgpu import balanced_slices
     cfg = (2, "winograd", 4, 37, 29, 33)
     ctx = mp.get_context("spawn")
@@ -367,21 +380,24 @@ def test_c_tiles_and_auto_schedule(orc):
     procs = [ctx.Process(target=_auto_worker, args=(r, 2, port, cfg, q)) for r in range(2)]
     for p in procs:
         p.start()
-    choice1, choice2, C, C2 = q.get(timeout=300)
+    choice1, choice2, names, C, C2, choice3, C3, C4, names4 = q.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     W, algo, T, m, l, n = cfg
     A, B = gen.matrix(W, m, l, 23, 0), gen.matrix(W, l, n, 23, 1)
+    whole = orc.gemm(A, B, algo, threshold=T)
     tiles = np.concatenate([orc.gemm(np.ascontiguousarray(A[:, a:b]), B, algo, threshold=T)
                             for a, b in balanced_slices(m, 2)], axis=1)
     assert np.array_equal(C2.view(np.int64), tiles.view(np.int64))
-    assert choice1 == choice2 and choice1 in ("products", "ctiles")
-    expect = orc.gemm(A, B, algo, threshold=T) if choice1 == "products" else tiles
-    assert np.array_equal(C.view(np.int64), expect.view(np.int64))
-    assert not np.array_equal(tiles, orc.gemm(A, B, algo, threshold=T))   # the two schedules round differently
-
-
+    assert names == ["bands", "products", "products_p2p"] and choice1 == choice2 and choice1 in names
+    assert np.array_equal(C.view(np.int64), whole.view(np.int64))
+    assert choice3 in ("ctiles", "bands", "products")
+    assert np.array_equal(C3.view(np.int64), (tiles if choice3 == "ctiles" else whole).view(np.int64))
+    assert names4 == ["bands", "products"]
+    ref4 = orc.dd_op("sub", gen.matrix(W, m, n, 23, 2).reshape(W, -1), whole.reshape(W, -1)).reshape(W, m, n)
+    assert np.array_equal(C4.view(np.int64), ref4.view(np.int64))
+    assert not np.array_equal(tiles, whole)   # the two schedules round differently
 # ---- band schedule (BandGemm: each rank one tile of C, the whole problem's tree) ---------------
 def _band_worker(rank, world, port, cfg, q):
     # one OpenMP thread per rank: several ranks spinning on all cores crawl
