@@ -191,10 +191,23 @@ __global__ void lu_rank1_kernel(double *A, int64_t n, int64_t k, int64_t jend, c
 // entries) published to a double-buffered global scratch -> ONE grid barrier -> every CTA
 // reduces the G candidates identically, interchanges the rows it owns, forms rinv = 1/u_kk,
 // scales its column entries and does its part of the rank-1 update.
+//
+// Diagonal fast path (spec = 1). The pivot-free LU always takes row k; under partial
+// pivoting the diagonal is SPECULATED: row k's owner publishes it, ONE grid barrier, every CTA
+// takes it as the pivot row and, while scaling its rows, checks that none of them is larger in
+// the DD/QD magnitude order (|a_ik| > |a_kk| for an i > k, exactly the test that makes the
+// argmax -- ties to the lowest row -- pick r = k). No candidates are published or merged. A CTA
+// that sees a larger entry raises the step's flag; every CTA reads step kk-1's flag after
+// barrier kk (so all break at the same step), nothing is written back, the slab is reloaded
+// from A and the column loop below (the full pivot search) factors the panel from the start.
+// When the speculation holds, every step is the one the search would have taken (r = k, the
+// pivot row = row k's values), so the factors are bit-identical either way. For BJ:11's
+// c4 matrix (column diagonally dominant) it always holds.
 template <int W>
 __global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n, int64_t p, int kb,
                                                             int rows_per, int pivot, int64_t *ipiv,
-                                                            LuAux *aux, double *scr, int probe) {
+                                                            LuAux *aux, double *scr, int probe, int spec,
+                                                            double *fscr) {
     using E = elem<W>;
     using T = typename E::T;
     namespace cg = cooperative_groups;
@@ -222,6 +235,92 @@ __global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n
         sts<W>(S, SS, e, ldA<W>(A, n, r0 + li, p + j));
     }
     __syncthreads();
+
+    if (spec) {
+        // fscr: pivot rows [2][W][kb] (double-buffered by step parity) | per-step flags [kb]
+        int *flag = reinterpret_cast<int *>(fscr + (size_t)2 * W * kb);
+        if (blockIdx.x == 0)
+            for (int j = tid; j < kb; j += blockDim.x) flag[j] = 0;
+        long long zero_k = -1;               // first exactly-zero pivot (CTA-uniform)
+        bool failed = false;
+        for (int kk = 0; kk < kb; kk++) {
+            const int64_t k = p + kk;
+            double *krow = fscr + (size_t)(kk & 1) * W * kb;
+            const bool own_k = k >= r0 && k < r0 + nrows;
+            if (own_k) {
+                const int li = (int)(k - r0);
+                for (int j = tid; j < kb; j += blockDim.x)
+                    for (int w = 0; w < W; w++) krow[(size_t)w * kb + j] = S[w * SS + li * kb + j];
+            }
+            grid.sync();
+            if (pivot && kk > 0 && *reinterpret_cast<volatile int *>(flag + kk - 1)) { failed = true; break; }
+            for (int j = tid; j < kb; j += blockDim.x)
+                for (int w = 0; w < W; w++) U[w * kb + j] = __ldcg(krow + (size_t)w * kb + j);
+            __syncthreads();
+            if (tid == 0) {
+                const T piv = lds<W>(U, kb, kk);
+                if (blockIdx.x == 0) ipiv[k] = k;
+                if (E::word(piv, 0) == 0.0) {
+                    s_skip = 1;
+                    if (zero_k < 0) zero_k = k;
+                } else {
+                    const T rvv = E::div(E::one(), piv);
+                    for (int w = 0; w < W; w++) s_rinv[w] = E::word(rvv, w);
+                    s_skip = 0;
+                }
+            }
+            __syncthreads();
+            const T akk = lds<W>(U, kb, kk);
+            bool bigger = false;             // an owned row below k outranks the diagonal
+            if (s_skip) {
+                if (pivot)
+                    for (int li = tid; li < nrows; li += blockDim.x)
+                        if (r0 + li > k && E::abs_gt(lds<W>(S, SS, li * kb + kk), akk)) bigger = true;
+                if (bigger) flag[kk] = 1;
+                continue;
+            }
+            const T rinv = lds<W>(s_rinv, 1, 0);
+            for (int li = tid; li < nrows; li += blockDim.x) {
+                if (r0 + li <= k) continue;
+                const T a = lds<W>(S, SS, li * kb + kk);
+                if (pivot && E::abs_gt(a, akk)) bigger = true;
+                const T lv = E::mul(a, rinv);
+                sts<W>(S, SS, li * kb + kk, lv);
+                sts<W>(L, rows_per, li, lv);
+            }
+            if (bigger) flag[kk] = 1;
+            __syncthreads();
+            {
+                const int64_t first = k + 1 - r0;
+                const int li0 = first <= 0 ? 0 : (first >= nrows ? nrows : (int)first);
+                const int nwarp = blockDim.x >> 5, lane = tid & 31, wrp = tid >> 5;
+                for (int j = kk + 1 + lane; j < kb; j += 32) {
+                    const T u = lds<W>(U, kb, j);
+                    for (int li = li0 + wrp; li < nrows; li += nwarp) {
+                        const T a = lds<W>(S, SS, li * kb + j);
+                        sts<W>(S, SS, li * kb + j, E::sub(a, E::mul(lds<W>(L, rows_per, li), u)));
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        grid.sync();
+        if (pivot && !failed && *reinterpret_cast<volatile int *>(flag + kb - 1)) failed = true;
+        if (!failed) {
+            if (blockIdx.x == 0 && tid == 0 && zero_k >= 0 && aux->info == 0) aux->info = (int)(zero_k + 1);
+            for (int e = tid; e < nrows * kb; e += blockDim.x) {
+                const int li = e / kb, j = e % kb;
+                stA<W>(A, n, r0 + li, p + j, lds<W>(S, SS, e));
+            }
+            return;
+        }
+        // the speculation failed: A still holds the panel; factor it with the pivot search
+        for (int e = tid; e < nrows * kb; e += blockDim.x) {
+            const int li = e / kb, j = e % kb;
+            sts<W>(S, SS, e, ldA<W>(A, n, r0 + li, p + j));
+        }
+        __syncthreads();
+    }
 
     long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long tlast = clock64();
@@ -1059,6 +1158,17 @@ static bool use_coop_panel() {
     return v == 1;
 }
 
+// DDQD_LU_SPEC=0 disables the diagonal fast path of the cooperative panel (every column then runs
+// the full candidate exchange, as in round 1); the factors are the same bits either way
+static bool spec_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_LU_SPEC");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 // returns 1 if the cooperative path was launched, 0 if the caller should use the per-column path
 template <int W>
 static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot, int64_t *ipiv, LuAux *aux,
@@ -1082,7 +1192,8 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
     const size_t smem = sizeof(double) * W * ((size_t)rows_per * kb + (size_t)kb + (size_t)rows_per);
     if (smem > 200 * 1024) return 0;
     const size_t per_buf = (size_t)G * (W + 1) * kLuCrep + (size_t)G * W * kb + (size_t)W * kb;
-    if (2 * per_buf * sizeof(double) > scr_bytes) return 0;
+    const size_t fast_bytes = sizeof(double) * (2 * (size_t)W * kb + (size_t)kb);   // pivot rows + flags
+    if (2 * per_buf * sizeof(double) + fast_bytes > scr_bytes) return 0;
     static size_t attr_dev[64];
     size_t &attr = attr_dev[dv];
     if (smem > 48 * 1024 && smem > attr) {
@@ -1103,7 +1214,9 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
         const char *e = getenv("DDQD_LU_PROBE");
         probe = (e && e[0] == '1') ? 1 : 0;
     }
-    void *args[] = {&A, &n, &p, &kbi, (void *)&rows_per, &piv, &ipiv, &aux, &scr, &probe};
+    int spec = spec_enabled() ? 1 : 0;
+    double *fscr = scr + 2 * per_buf;
+    void *args[] = {&A, &n, &p, &kbi, (void *)&rows_per, &piv, &ipiv, &aux, &scr, &probe, &spec, &fscr};
     cudaError_t e = cudaLaunchCooperativeKernel((void *)lu_panel_coop_kernel<W>, dim3(G), dim3(256), args, smem, s);
     count_launch();
     if (e != cudaSuccess) {
@@ -1286,7 +1399,10 @@ struct LuMem {
 static int lu_mem(int W, int64_t n, int64_t K, LuMem *m) {
     int st = DDQD_OK;
     const size_t ybytes = (sizeof(double) * W * (size_t)n + 255) & ~size_t(255);
-    m->scr_bytes = sizeof(double) * 2 * ((size_t)160 * ((W + 1) * kLuCrep + W * (size_t)K) + W * (size_t)K);
+    // two candidate buffers for up to one CTA per SM, plus the fast path's pivot rows and flags
+    const size_t G = (size_t)std::max(sm_count(), 1);
+    m->scr_bytes = sizeof(double) * (2 * (G * ((W + 1) * kLuCrep + W * (size_t)K) + W * (size_t)K) +
+                                     2 * (size_t)W * K + (size_t)K);
     char *mem = static_cast<char *>(aux_get(256 + ybytes + m->scr_bytes, &st));
     if (st) return st;
     m->aux = reinterpret_cast<LuAux *>(mem);
