@@ -204,7 +204,7 @@ __global__ void lu_rank1_kernel(double *A, int64_t n, int64_t k, int64_t jend, c
 // pivot row = row k's values), so the factors are bit-identical either way. For BJ:11's
 // c4 matrix (column diagonally dominant) it always holds.
 template <int W>
-__global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n, int64_t p, int kb,
+__global__ void __launch_bounds__(512) lu_panel_coop_kernel(double *A, int64_t n, int64_t p, int kb,
                                                             int rows_per, int pivot, int64_t *ipiv,
                                                             LuAux *aux, double *scr, int probe, int spec,
                                                             double *fscr) {
@@ -230,13 +230,177 @@ __global__ void __launch_bounds__(256) lu_panel_coop_kernel(double *A, int64_t n
     // scratch per buffer parity: cand value [W][G], cand idx [G], cand rows [G][W][kb], krow [W][kb]
     const size_t per_buf = (size_t)G * (W + 1) * kLuCrep + (size_t)G * W * kb + (size_t)W * kb;
 
-    for (int e = tid; e < nrows * kb; e += blockDim.x) {
-        const int li = e / kb, j = e % kb;
-        sts<W>(S, SS, e, ldA<W>(A, n, r0 + li, p + j));
+    if (spec != 2) {   // (the split-barrier fast path loads its own, cyclic, layout)
+        for (int e = tid; e < nrows * kb; e += blockDim.x) {
+            const int li = e / kb, j = e % kb;
+            sts<W>(S, SS, e, ldA<W>(A, n, r0 + li, p + j));
+        }
+        __syncthreads();
     }
-    __syncthreads();
 
-    if (spec) {
+    if (spec == 2) {
+        // Split-barrier form of the fast path, rows dealt CYCLICALLY (CTA b owns panel rows
+        // p + b + G*li), so successive pivot rows belong to successive CTAs: the owner of row
+        // k+1 scales and updates that row FIRST in step k, publishes it with its reciprocal and
+        // arrives at barrier k+1; every other CTA arrives as soon as it has read row k, and then
+        // scales and rank-1-updates its rows while the barrier completes. Step k's verification
+        // flags are read after barrier k+2 (raised before the detector arrives there), so every
+        // CTA breaks at the same step. The fallback reloads the slab in the block layout below.
+        // fscr: [2][W][kb + 1] pivot rows (+ reciprocal in slot kb) | flags [kb] | counter
+        const int RS = kb + 1;
+        int *flag = reinterpret_cast<int *>(fscr + (size_t)2 * W * RS);
+        unsigned *ctr = reinterpret_cast<unsigned *>(flag + kb);
+        const int64_t R = n - p;
+        const int b = blockIdx.x;
+        const int cr = b < R ? (int)((R - b + G - 1) / G) : 0;      // rows of this CTA (<= rows_per)
+        auto grow = [&](int li) { return p + b + (int64_t)G * li; };
+        for (int e = tid; e < cr * kb; e += blockDim.x) {
+            const int li = e / kb, j = e % kb;
+            sts<W>(S, SS, e, ldA<W>(A, n, grow(li), p + j));
+        }
+        auto publish = [&](int kk1, int li) {
+            // (warp 0) row p+kk1, local row li, and its reciprocal -> the pivot-row buffer
+            double *kr = fscr + (size_t)(kk1 & 1) * W * RS;
+            for (int j = tid; j < kb; j += 32)
+                for (int w = 0; w < W; w++) kr[(size_t)w * RS + j] = S[w * SS + li * kb + j];
+            if (tid == 0) {
+                const T d = lds<W>(S, SS, li * kb + kk1);
+                const T rv2 = (E::word(d, 0) == 0.0) ? E::zero() : E::div(E::one(), d);
+                for (int w = 0; w < W; w++) kr[(size_t)w * RS + kb] = E::word(rv2, w);
+            }
+        };
+        if (blockIdx.x == 0) {
+            for (int j = tid; j < kb; j += blockDim.x) flag[j] = 0;
+            if (tid == 0) *ctr = 0u;
+        }
+        __syncthreads();
+        if (tid < 32 && b == 0 && cr > 0) publish(0, 0);     // row p: CTA 0, local row 0
+        grid.sync();   // flags and counter reset, row p published
+        long long zero_k = -1;
+        bool failed = false;
+        long long q[6] = {0, 0, 0, 0, 0, 0};
+        long long qt = clock64();
+        auto qmark = [&](int ph) {   // DDQD_LU_PROBE: per-phase cycles of this path
+            if (probe) { __syncthreads(); const long long t = clock64(); q[ph] += t - qt; qt = t; }
+        };
+        for (int kk = 0; kk < kb; kk++) {
+            const int64_t k = p + kk;
+            qmark(5);
+            if (kk > 0 && tid == 0) {
+                const unsigned target = (unsigned)G * (unsigned)kk;
+                unsigned v;
+                do {
+                    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+                } while (v < target);
+            }
+            __syncthreads();
+            qmark(0);
+            if (pivot && kk >= 2 && __ldcg(flag + kk - 2)) { failed = true; break; }
+            const double *kr = fscr + (size_t)(kk & 1) * W * RS;
+            for (int j = tid; j < kb; j += blockDim.x)
+                for (int w = 0; w < W; w++) U[w * kb + j] = __ldcg(kr + (size_t)w * RS + j);
+            if (tid < W) s_rinv[tid] = __ldcg(kr + (size_t)tid * RS + kb);
+            __syncthreads();
+            qmark(1);
+            const T akk = lds<W>(U, kb, kk);
+            const bool skip = E::word(akk, 0) == 0.0;
+            if (tid == 0) {
+                if (blockIdx.x == 0) ipiv[k] = k;
+                if (skip && zero_k < 0) zero_k = k;
+            }
+            const T rinv = lds<W>(s_rinv, 1, 0);
+            // first owned row below k, and the owner of row k+1 (local li1)
+            const int64_t dk = k - p - b;
+            const int li0 = dk < 0 ? 0 : (int)(dk / G) + 1;
+            const int li1 = (kk + 1 < kb && (kk + 1) % G == b) ? (kk + 1) / G : -1;
+            // warp 0 arrives at barrier kk+1 as soon as the CTA has read row k (the barrier after
+            // the fetch) -- after publishing row k+1 when this CTA owns it; the other warps go
+            // straight on to the scaling and the update. The release fence orders this CTA's
+            // reads of row k, its flags of step kk-1 and the published row before the arrival.
+            auto arrive = [&]() {
+                __syncwarp();
+                if (tid == 0) {
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    atomicAdd(ctr, 1u);
+                }
+            };
+            if (tid < 32 && li1 < 0) arrive();
+            if (li1 >= 0 && tid < 32) {
+                const T a = lds<W>(S, SS, li1 * kb + kk);
+                if (!skip) {
+                    if (pivot && tid == 0 && E::abs_gt(a, akk)) flag[kk] = 1;
+                    const T lv = E::mul(a, rinv);
+                    for (int j = kk + 1 + tid; j < kb; j += 32)
+                        sts<W>(S, SS, li1 * kb + j, E::sub(lds<W>(S, SS, li1 * kb + j), E::mul(lv, lds<W>(U, kb, j))));
+                    __syncwarp();
+                    if (tid == 0) { sts<W>(S, SS, li1 * kb + kk, lv); sts<W>(L, rows_per, li1, lv); }
+                    __syncwarp();
+                } else if (pivot && tid == 0 && E::abs_gt(a, akk)) {
+                    flag[kk] = 1;
+                }
+                publish(kk + 1, li1);
+                arrive();
+            }
+            qmark(2);
+            bool bigger = false;
+            if (skip) {
+                if (pivot)
+                    for (int li = li0 + tid; li < cr; li += blockDim.x)
+                        if (li != li1 && E::abs_gt(lds<W>(S, SS, li * kb + kk), akk)) bigger = true;
+                if (bigger) flag[kk] = 1;
+                continue;
+            }
+            for (int li = li0 + tid; li < cr; li += blockDim.x) {
+                if (li == li1) continue;
+                const T a = lds<W>(S, SS, li * kb + kk);
+                if (pivot && E::abs_gt(a, akk)) bigger = true;
+                const T lv = E::mul(a, rinv);
+                sts<W>(S, SS, li * kb + kk, lv);
+                sts<W>(L, rows_per, li, lv);
+            }
+            if (bigger) flag[kk] = 1;
+            __syncthreads();
+            qmark(3);
+            {
+                // rows in pairs, both loaded before either is stored: two independent DD chains
+                // per thread (the loop is latency-bound at one CTA per SM)
+                const int nwarp = blockDim.x >> 5, lane = tid & 31, wrp = tid >> 5;
+                for (int j = kk + 1 + lane; j < kb; j += 32) {
+                    const T u = lds<W>(U, kb, j);
+                    int li = li0 + wrp;
+                    for (; li + nwarp < cr; li += 2 * nwarp) {
+                        const int lb = li + nwarp;
+                        const T a0 = lds<W>(S, SS, li * kb + j), a1 = lds<W>(S, SS, lb * kb + j);
+                        const T l0 = lds<W>(L, rows_per, li), l1 = lds<W>(L, rows_per, lb);
+                        const T r0v = E::sub(a0, E::mul(l0, u)), r1v = E::sub(a1, E::mul(l1, u));
+                        if (li != li1) sts<W>(S, SS, li * kb + j, r0v);
+                        if (lb != li1) sts<W>(S, SS, lb * kb + j, r1v);
+                    }
+                    if (li < cr && li != li1)
+                        sts<W>(S, SS, li * kb + j, E::sub(lds<W>(S, SS, li * kb + j), E::mul(lds<W>(L, rows_per, li), u)));
+                }
+            }
+            __syncthreads();
+        }
+        if (probe && tid == 0 && (blockIdx.x == 0 || blockIdx.x == 1 || blockIdx.x == G / 2))
+            printf("LUPROBE2 p=%lld G=%d cta=%d wait %lld fetch %lld owner+arrive %lld scale %lld update %lld\n",
+                   (long long)p, G, blockIdx.x, q[0], q[1], q[2], q[3], q[5]);
+        grid.sync();
+        if (pivot && !failed && (__ldcg(flag + kb - 1) || (kb >= 2 && __ldcg(flag + kb - 2)))) failed = true;
+        if (!failed) {
+            if (blockIdx.x == 0 && tid == 0 && zero_k >= 0 && aux->info == 0) aux->info = (int)(zero_k + 1);
+            for (int e = tid; e < cr * kb; e += blockDim.x) {
+                const int li = e / kb, j = e % kb;
+                stA<W>(A, n, grow(li), p + j, lds<W>(S, SS, e));
+            }
+            return;
+        }
+        for (int e = tid; e < nrows * kb; e += blockDim.x) {
+            const int li = e / kb, j = e % kb;
+            sts<W>(S, SS, e, ldA<W>(A, n, r0 + li, p + j));
+        }
+        __syncthreads();
+    } else if (spec == 1) {
         // fscr: pivot rows [2][W][kb] (double-buffered by step parity) | per-step flags [kb]
         int *flag = reinterpret_cast<int *>(fscr + (size_t)2 * W * kb);
         if (blockIdx.x == 0)
@@ -1158,15 +1322,16 @@ static bool use_coop_panel() {
     return v == 1;
 }
 
-// DDQD_LU_SPEC=0 disables the diagonal fast path of the cooperative panel (every column then runs
-// the full candidate exchange, as in round 1); the factors are the same bits either way
-static bool spec_enabled() {
+// Diagonal fast path of the cooperative panel: DDQD_LU_SPEC=0 off (every column runs the full
+// candidate exchange, as in round 1), =1 one grid barrier per column, default (2) the split
+// arrive/wait barrier; the factors are the same bits in every mode
+static int spec_mode() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("DDQD_LU_SPEC");
-        v = (e && e[0] == '0') ? 0 : 1;
+        v = (e && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : 2;
     }
-    return v == 1;
+    return v;
 }
 
 // returns 1 if the cooperative path was launched, 0 if the caller should use the per-column path
@@ -1192,7 +1357,7 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
     const size_t smem = sizeof(double) * W * ((size_t)rows_per * kb + (size_t)kb + (size_t)rows_per);
     if (smem > 200 * 1024) return 0;
     const size_t per_buf = (size_t)G * (W + 1) * kLuCrep + (size_t)G * W * kb + (size_t)W * kb;
-    const size_t fast_bytes = sizeof(double) * (2 * (size_t)W * kb + (size_t)kb);   // pivot rows + flags
+    const size_t fast_bytes = sizeof(double) * (2 * (size_t)W * (kb + 1) + (size_t)kb + 2);   // rows + flags + counter
     if (2 * per_buf * sizeof(double) + fast_bytes > scr_bytes) return 0;
     static size_t attr_dev[64];
     size_t &attr = attr_dev[dv];
@@ -1205,7 +1370,12 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
         attr = smem;
     }
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lu_panel_coop_kernel<W>, 256, smem);
+    static int nthr = -1;   // DDQD_LU_THREADS=256|512: threads of the panel CTA
+    if (nthr < 0) {
+        const char *e = getenv("DDQD_LU_THREADS");
+        nthr = (e && std::string(e) == "256") ? 256 : 512;
+    }
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lu_panel_coop_kernel<W>, nthr, smem);
     if (occ < 1 || G > occ * nsm) return 0;
     int kbi = (int)kb;
     int piv = pivot;
@@ -1214,10 +1384,10 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
         const char *e = getenv("DDQD_LU_PROBE");
         probe = (e && e[0] == '1') ? 1 : 0;
     }
-    int spec = spec_enabled() ? 1 : 0;
+    int spec = spec_mode();
     double *fscr = scr + 2 * per_buf;
     void *args[] = {&A, &n, &p, &kbi, (void *)&rows_per, &piv, &ipiv, &aux, &scr, &probe, &spec, &fscr};
-    cudaError_t e = cudaLaunchCooperativeKernel((void *)lu_panel_coop_kernel<W>, dim3(G), dim3(256), args, smem, s);
+    cudaError_t e = cudaLaunchCooperativeKernel((void *)lu_panel_coop_kernel<W>, dim3(G), dim3(nthr), args, smem, s);
     count_launch();
     if (e != cudaSuccess) {
         set_error(std::string("cooperative panel launch: ") + cudaGetErrorString(e));
@@ -1402,7 +1572,7 @@ static int lu_mem(int W, int64_t n, int64_t K, LuMem *m) {
     // two candidate buffers for up to one CTA per SM, plus the fast path's pivot rows and flags
     const size_t G = (size_t)std::max(sm_count(), 1);
     m->scr_bytes = sizeof(double) * (2 * (G * ((W + 1) * kLuCrep + W * (size_t)K) + W * (size_t)K) +
-                                     2 * (size_t)W * K + (size_t)K);
+                                     2 * (size_t)W * (K + 1) + (size_t)K + 2);
     char *mem = static_cast<char *>(aux_get(256 + ybytes + m->scr_bytes, &st));
     if (st) return st;
     m->aux = reinterpret_cast<LuAux *>(mem);
