@@ -267,13 +267,75 @@ static bool small_enabled();
 static int launch_leaf_one(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
                            const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s);
 
+int launch_leaf_flat(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
+                     const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s);   // leaf_small.cu
+bool leaf_pack_fits(int W, int64_t m, int64_t l, int64_t n);                                       // leaf_small.cu
+int launch_leaf_pack(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
+                     const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s);   // leaf_small.cu
+
+// DDQD_LEAF_RAGGED=0 disables the interior / strip split and the flat leaf (A/B measurements)
+static bool ragged_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_LEAF_RAGGED");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// DDQD_LEAF_PACK=1 routes tiny leaves to the shared-memory packed kernel (A/B experiments)
+static bool pack_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_LEAF_PACK");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+static MatDesc rows_from(MatDesc d, int64_t r0, int64_t rows) { d.p += r0 * d.ld; d.rows = rows; return d; }
+static MatDesc cols_from(MatDesc d, int64_t c0, int64_t cols) { d.p += c0; d.cols = cols; return d; }
+
 int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A,
                      const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s) {
     if (m == 0 || n == 0 || batch == 0) return DDQD_OK;
     // mv: arithmetic variant (low 4 bits) | log2(split-k) << 4
     const int split = 1 << ((mv >> 4) & 3);
+    if (split > 1) return launch_leaf_splitk(W, split, m, l, n, batch, A, B, C, beta, mv & 0xf, s);
     mv &= 0xf;
-    if (split > 1) return launch_leaf_splitk(W, split, m, l, n, batch, A, B, C, beta, mv, s);
+    // Ragged leaves (n = 1025 at threshold 128: 65 x 65; at 32: 17 x 17). The tile kernels pad
+    // every leaf to whole CTA tiles: a 65 x 65 leaf is 4 tiles of 64 of which 3 are slivers
+    // running the full k loop, a 17 x 17 leaf uses 28% of a 32 x 32 tile. Instead the tile-
+    // aligned interior of ALL leaves runs as one batched tile launch (strided views of the same
+    // leaves) and the remaining row / column strips -- or, for leaves below one tile, the whole
+    // leaves -- go to the flat 2x2-per-thread kernel. Each element keeps its operation order.
+    if (ragged_enabled() && leaf_cfg_override() < 0) {
+        const int64_t TL = (W == 2 && m > 32 && n > 32) ? 64 : 32;
+        const int64_t mt = m / TL * TL, nt = n / TL * TL;
+        const double used = (double)m * (double)n /
+                            (double)(((m + TL - 1) / TL * TL) * ((n + TL - 1) / TL * TL));
+        if (used < 0.8) {
+            if (mt == 0 || nt == 0) {   // below one tile: the flat kernel takes the whole leaves
+                // (staging 3 such leaves per CTA through shared memory, leaf_pack_kernel, measured
+                // slower: DD Strassen(32) n = 1025 2.07 vs 1.64 ms, QD 12.6 vs 11.0 ms)
+                if (pack_enabled() && leaf_pack_fits(W, m, l, n))
+                    return launch_leaf_pack(W, m, l, n, batch, A, B, C, beta, mv, s);
+                return launch_leaf_flat(W, m, l, n, batch, A, B, C, beta, mv, s);
+            }
+            int rc = launch_leaf_gemm(W, mt, l, nt, batch, rows_from(A, 0, mt), cols_from(B, 0, nt),
+                                      cols_from(rows_from(C, 0, mt), 0, nt), beta, mv, s);
+            if (rc) return rc;
+            // right strip: rows [0, mt) x cols [nt, n); bottom strip: rows [mt, m) x all columns
+            auto strip = [&](int64_t sm, int64_t sn, const MatDesc &a, const MatDesc &b, const MatDesc &c) {
+                if (sm == 0 || sn == 0) return (int)DDQD_OK;
+                if (sm < 32 || sn < 32) return launch_leaf_flat(W, sm, l, sn, batch, a, b, c, beta, mv, s);
+                return launch_leaf_gemm(W, sm, l, sn, batch, a, b, c, beta, mv, s);
+            };
+            if ((rc = strip(mt, n - nt, rows_from(A, 0, mt), cols_from(B, nt, n - nt),
+                            cols_from(rows_from(C, 0, mt), nt, n - nt)))) return rc;
+            return strip(m - mt, n, rows_from(A, mt, m - mt), B, rows_from(C, mt, m - mt));
+        }
+    }
     // Tail split (DD): a batch of 64x64-tile leaves whose last wave would leave most of the
     // GPU idle runs its whole waves with 64x64 tiles and the remaining leaves with 32x32 tiles
     // (4x the CTAs for the same work) -- same per-element order, so the same bits.

@@ -1074,3 +1074,43 @@ def test_multiprocess_schedules_staged_bitwise(orc, cfg, world):
     ddqd.gemm_ex(W, algo, T, m, l, n, 1, a.data_ptr(), l, m * l, 0, b.data_ptr(), n, l * n, 0,
                  C0.data_ptr(), n, m * n, 0, 1)
     assert same(out["bands_beta1"], np_(C0))
+
+
+# ---- ragged leaves: interior / strip split and the flat leaf ------------
+@pytest.mark.parametrize("W", [2, 4])
+@pytest.mark.parametrize("w", [17, 65, 129, 257])
+def test_ragged_leaf_widths_bitwise(orc, W, w):
+    """Leaves of width 17, 65, 129, 257 (n = 1025-type recursions): Block leaves directly, a
+    batch of such leaves through one recursion level (Strassen with threshold w so the seven
+    children are w x w), and a non-square ragged leaf; bit-identical to the oracle."""
+    A, B = gen.matrix(W, w, w + 3, 47, 0), gen.matrix(W, w + 3, w, 47, 1)
+    assert same(np_(ddqd.gemm(cu(A), cu(B), "block", 128)), orc.gemm(A, B, "block"))
+    m = 2 * w - 1
+    A2, B2 = gen.matrix(W, m, m, 48, 0), gen.matrix(W, m, m, 48, 1)
+    for algo in ("strassen", "winograd"):
+        got = np_(ddqd.gemm(cu(A2), cu(B2), algo, w))
+        assert same(got, orc.gemm(A2, B2, algo, threshold=w)), algo
+    A3, B3 = gen.matrix(W, w + 40, 33, 49, 0), gen.matrix(W, 33, w, 49, 1)
+    assert same(np_(ddqd.gemm(cu(A3), cu(B3), "block", 128)), orc.gemm(A3, B3, "block"))
+
+
+def test_ragged_split_same_bits_as_unsplit(tmp_path):
+    """DDQD_LEAF_RAGGED=0 (whole leaves on padded CTA tiles) and the default interior / strip
+    split give the same bits (subprocesses: the switch is read once per process)."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, ddqd_inputs as gen, paper_1510_08642_b200 as d\n"
+        "out = []\n"
+        "for W, n, T in ((2, 1025, 128), (2, 1025, 32), (4, 517, 64), (4, 263, 16)):\n"
+        "    A, B = gen.bench_pair(n, W)\n"
+        "    for algo in ('strassen', 'winograd'):\n"
+        "        out.append(d.gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), algo, T).cpu().numpy().ravel())\n"
+        "np.save(r'%s', np.concatenate(out))\n")
+    outs = []
+    for mode in ("0", "1"):
+        f = tmp_path / f"r{mode}.npy"
+        env = dict(os.environ, DDQD_LEAF_RAGGED=mode)
+        subprocess.check_call([sys.executable, "-c", code % f], env=env, cwd=ROOT)
+        outs.append(np.load(f))
+    assert same(outs[0], outs[1])

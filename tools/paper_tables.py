@@ -6,7 +6,7 @@ against the closed form c_ij = sqrt(15) * S(i, n) within 4 n eps 18^
 Times are CUDA-event medians of 5 runs (inputs resident). Paper times: 1 and 8 OpenMP
 threads on a Xeon E5-2620 v2, context only.
 
-    python tools/paper_tables.py [--out profiles/r01/paper_tables.md]
+    python tools/paper_tables.py [--out profiles/r02/paper_tables.md]
 """
 import argparse
 import json
@@ -31,7 +31,7 @@ PAPER = {  # (prec, algo, n) -> (1PE s, 8PE s)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01", "paper_tables.md"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02", "paper_tables.md"))
     args = ap.parse_args()
     import numpy as np
     import torch
