@@ -102,6 +102,9 @@ __global__ void __launch_bounds__(256) pre_add_kernel(int64_t P, MatDesc X, MatD
         pre_ops<E, ALGO, SIDE>(x11, x12, x21, x22, o);
 #pragma unroll
         for (int c = 0; c < 7; c++) E::store(Y.p + (7 * b + c) * Y.bs + i * Y.ld + j, Y.ps, o[c]);
+        if (j == hc - 1 && Y.ld > hc)   // padded leading dimension: fill the gap so no sector is partial
+#pragma unroll
+            for (int c = 0; c < 7; c++) E::store(Y.p + (7 * b + c) * Y.bs + i * Y.ld + hc, Y.ps, E::zero());
     }
 }
 
@@ -166,6 +169,10 @@ __global__ void __launch_bounds__(ADD2_THREADS, ADD2_MINB) pre_add2_kernel(int64
             for (int c2 = 0; c2 < 7; c2++)
                 E::store(Y.p + (49 * b + 7 * c1 + c2) * Y.bs + i * Y.ld + j, Y.ps, o[c2]);
         }
+        // padded leading dimension (the TMA-aligned leaf level): fill the gap as well, so no
+        // sector is left partially written (partial sectors cost DRAM read-fills on eviction)
+        if (j == hc - 1 && Y.ld > hc)
+            for (int g = 0; g < 49; g++) E::store(Y.p + (49 * b + g) * Y.bs + i * Y.ld + hc, Y.ps, E::zero());
     }
 }
 

@@ -234,6 +234,8 @@ static int leaf_cfg_override() {
 
 int try_leaf_tma(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A, const MatDesc &B,
                  const MatDesc &C, int beta, int mv, cudaStream_t s, int *rc);   // leaf_tma.cu
+int try_leaf_tma_qd(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A, const MatDesc &B,
+                    const MatDesc &C, int beta, int mv, cudaStream_t s, int *rc);   // leaf_tma.cu
 
 // DDQD_LEAF_TMA=0 disables the TMA + mbarrier DD leaf (A/B comparisons); default on
 static bool tma_enabled() {
@@ -417,14 +419,22 @@ static int launch_leaf_one(int W, int64_t m, int64_t l, int64_t n, int64_t batch
         }
     }
     if (mv == 1) {   // fused DD / QD madd (numerics.md s.2-3, row f3)
-        if (W == 4) return launch_cfg<4, 32, 32, 16, 2, 2, 3, 2, 1>(m, l, n, batch, A, B, C, beta, s);
+        if (W == 4) {
+            int rc = DDQD_OK;
+            if (try_leaf_tma_qd(m, l, n, batch, A, B, C, beta, mv, s, &rc)) return rc;
+            return launch_cfg<4, 32, 32, 16, 2, 2, 3, 2, 1>(m, l, n, batch, A, B, C, beta, s);
+        }
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
         if (big_tiles >= 2 * sm_count() && m > 32 && n > 32)
             return launch_cfg<2, 64, 64, 8, 4, 4, 4, 2, 1>(m, l, n, batch, A, B, C, beta, s);
         return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2, 1>(m, l, n, batch, A, B, C, beta, s);
     }
     if (mv == 2) {   // accurate adds (numerics.md s.2-3, row f3)
-        if (W == 4) return launch_cfg<4, 32, 32, 16, 2, 2, 3, 2, 2>(m, l, n, batch, A, B, C, beta, s);
+        if (W == 4) {
+            int rc = DDQD_OK;
+            if (try_leaf_tma_qd(m, l, n, batch, A, B, C, beta, mv, s, &rc)) return rc;
+            return launch_cfg<4, 32, 32, 16, 2, 2, 3, 2, 2>(m, l, n, batch, A, B, C, beta, s);
+        }
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
         if (big_tiles >= 2 * sm_count() && m > 32 && n > 32)
             return launch_cfg<2, 64, 64, 8, 4, 4, 4, 2, 2>(m, l, n, batch, A, B, C, beta, s);
@@ -451,7 +461,11 @@ static int launch_leaf_one(int W, int64_t m, int64_t l, int64_t n, int64_t batch
             return launch_cfg<2, 64, 64, 8, 4, 4, 4, 2>(m, l, n, batch, A, B, C, beta, s);
         return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2>(m, l, n, batch, A, B, C, beta, s);
     }
-    if (W == 4) return launch_cfg<4, 32, 32, 16, 2, 2, 3, 2>(m, l, n, batch, A, B, C, beta, s);
+    if (W == 4) {
+        int rc = DDQD_OK;
+        if (try_leaf_tma_qd(m, l, n, batch, A, B, C, beta, mv, s, &rc)) return rc;
+        return launch_cfg<4, 32, 32, 16, 2, 2, 3, 2>(m, l, n, batch, A, B, C, beta, s);
+    }
     set_error("leaf GEMM: precision must be 2 (DD) or 4 (QD)");
     return DDQD_EINVAL;
 }

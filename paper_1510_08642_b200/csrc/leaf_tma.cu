@@ -13,6 +13,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "ddqd_arith.cuh"
@@ -34,6 +35,13 @@ constexpr int A_STAGE = W * BM * BK;                // doubles
 constexpr int B_STAGE = W * BK * BN;
 constexpr unsigned STAGE_BYTES = (unsigned)(sizeof(double) * (A_STAGE + B_STAGE));
 constexpr size_t SMEM = sizeof(double) * (size_t)S * (A_STAGE + B_STAGE) + 2 * S * sizeof(uint64_t) + 1024;
+// row-pair A stage: even rows [W][BM/2][BK + 2] from column k0, odd rows [W][BM/2][BK + 2] from
+// column ld + k0 - 1 (one early, so that the box starts 16-byte aligned: TMA faults on an
+// unaligned start); one box shape for both, so every thread reads its rows with one stride
+constexpr int BKO = BK + 2;
+constexpr int A_EVEN = W * (BM / 2) * BKO, A_ODD = W * (BM / 2) * BKO, A_STAGE_P = A_EVEN + A_ODD;
+constexpr unsigned STAGE_BYTES_P = (unsigned)(sizeof(double) * (A_STAGE_P + B_STAGE));
+constexpr size_t SMEM_P = sizeof(double) * (size_t)S * (A_STAGE_P + B_STAGE) + 2 * S * sizeof(uint64_t) + 1024;
 }  // namespace tma
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -73,16 +81,28 @@ __device__ __forceinline__ void tma_load_4d(void *smem_dst, const CUtensorMap *m
         : "memory");
 }
 
-template <int MV>
+// APAIR: A is addressed as a tensor of ROW PAIRS -- pair p = rows 2p and 2p+1 back to back, so
+// its stride is 2 ld doubles = 16 ld bytes, a multiple of 16 whatever ld is. This puts odd
+// leading dimensions (c3's 256 x 257 A leaves, ld 257) on TMA without padding the workspace:
+// each stage loads the even rows (pair columns k0 .. k0+7, map tmA) and the odd rows (pair
+// columns ld + k0 - 1 .. ld + k0 + 8, map tmA2: one column early, because a box must start on a
+// 16-byte boundary -- tools/tma_align_probe showed an odd float64 start faulting) as two boxes.
+// Entries past l in the even box are the odd row's first columns, not zeros -- the k loop
+// never reads past l (kmax), so they are never used.
+template <int MV, int APAIR>
 __global__ void __launch_bounds__(tma::NT, 2)
-leaf_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t m,
-                int64_t l, int64_t n, MatDesc C, int beta, int64_t batch0) {
+leaf_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmA2,
+                const __grid_constant__ CUtensorMap tmB, int64_t m, int64_t l, int64_t n, int64_t lda, MatDesc C,
+                int beta, int64_t batch0) {
     using namespace tma;
     using E = elem<2>;
     using T = dd;
     extern __shared__ unsigned char smraw[];
-    double *As = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-    double *Bs = As + S * A_STAGE;
+    constexpr int AST = APAIR ? A_STAGE_P : A_STAGE;
+    // 1024-byte aligned start, by an offset from the shared array itself (a cast through an integer
+    // would drop the shared address space and turn every fragment read into a generic LD)
+    double *As = reinterpret_cast<double *>(smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u));
+    double *Bs = As + S * AST;
     uint64_t *full = reinterpret_cast<uint64_t *>(Bs + S * B_STAGE);
     uint64_t *empty = full + S;
 
@@ -95,6 +115,7 @@ leaf_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if (tid == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+        if (APAIR) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA2)) : "memory");
         for (int s = 0; s < S; s++) {
             mbar_init(full + s, 1);
             mbar_init(empty + s, NT / 32);
@@ -105,8 +126,13 @@ leaf_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 
     auto produce = [&](int t) {   // thread 0 only: tile t into stage t % S
         const int st = t % S;
-        mbar_arrive_expect_tx(full + st, STAGE_BYTES);
-        tma_load_4d(As + st * A_STAGE, &tmA, t * BK, row0, 0, (int)b, full + st);
+        mbar_arrive_expect_tx(full + st, APAIR ? STAGE_BYTES_P : STAGE_BYTES);
+        if (APAIR) {
+            tma_load_4d(As + st * AST, &tmA2, t * BK, row0 / 2, 0, (int)b, full + st);
+            tma_load_4d(As + st * AST + A_EVEN, &tmA2, (int)lda + t * BK - 1, row0 / 2, 0, (int)b, full + st);
+        } else {
+            tma_load_4d(As + st * AST, &tmA, t * BK, row0, 0, (int)b, full + st);
+        }
         tma_load_4d(Bs + st * B_STAGE, &tmB, col0, t * BK, 0, (int)b, full + st);
     };
     if (tid == 0)
@@ -121,17 +147,21 @@ leaf_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     for (int kt = 0; kt < KT; kt++) {
         const int st = kt % S;
         mbar_wait(full + st, (unsigned)((kt / S) & 1));
-        const double *as = As + st * A_STAGE;   // [W][BM][BK]
+        // [W][BM][BK]; row pairs: even [W][BM/2][BK], odd [W][BM/2][BK+2] from column 1; a
+        // thread's rows all share ty's parity
+        const double *as = As + st * AST + (APAIR ? (ty & 1) * (A_EVEN + 1) : 0);
         const double *bs = Bs + st * B_STAGE;   // [W][BK][BN]
         const int krem = (int)(l - (int64_t)kt * BK);
         const int kmax = krem < BK ? krem : BK;   // uniform: no madds past l
-#pragma unroll kLeafTmaKkUnroll
+#pragma unroll (MV ? 1 : kLeafTmaKkUnroll)
         for (int kk = 0; kk < kmax; kk++) {
             double av[W][TM], bv[W][TN];
 #pragma unroll
             for (int w = 0; w < W; w++) {
 #pragma unroll
-                for (int i = 0; i < TM; i++) av[w][i] = as[(w * BM + ty + 16 * i) * BK + kk];
+                for (int i = 0; i < TM; i++)
+                    av[w][i] = APAIR ? as[(w * (BM / 2) + ((ty + 16 * i) >> 1)) * BKO + kk]
+                                     : as[(w * BM + ty + 16 * i) * BK + kk];
                 const double *brow = bs + (w * BK + kk) * BN;
 #pragma unroll
                 for (int j = 0; j < TN; j += 2) {
@@ -174,6 +204,116 @@ leaf_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
 }
 
+// ---- QD: the same pipeline with 4-plane boxes --------------------------------------------------
+// 32x32 CTA tile, 2x2 QD micro-tile per thread (256 threads), 16-deep k slabs in 3 stages, 2 CTAs
+// per SM -- the cp.async QD leaf's configuration. A arrives as [4][32 rows][18 k] (two columns
+// beyond the slab, zero or unused, so that the 144-byte row stride spreads a warp's four rows over
+// distinct banks), B as [4][16 k][32 cols]. Edge-tile entries outside C skip their madds, as in
+// the cp.async leaf (one renormalisation path per warp); same per-element order, same bits.
+namespace tmaq {
+constexpr int BM = 32, BN = 32, BK = 16, BKA = 18, TM = 2, TN = 2, S = 3, W = 4;
+constexpr int NT = (BM / TM) * (BN / TN);           // 256
+constexpr int A_STAGE = W * BM * BKA, B_STAGE = W * BK * BN;
+constexpr unsigned STAGE_BYTES = (unsigned)(sizeof(double) * (A_STAGE + B_STAGE));
+constexpr size_t SMEM = sizeof(double) * (size_t)S * (A_STAGE + B_STAGE) + 2 * S * sizeof(uint64_t) + 1024;
+}  // namespace tmaq
+
+template <int MV>
+__global__ void __launch_bounds__(tmaq::NT, 2)
+leaf_tma_qd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t m,
+                   int64_t l, int64_t n, MatDesc C, int beta, int64_t batch0) {
+    using namespace tmaq;
+    using E = arith<4, MV>;
+    using T = qd;
+    extern __shared__ unsigned char smraw[];
+    // 1024-byte aligned start, by an offset from the shared array itself (a cast through an integer
+    // would drop the shared address space and turn every fragment read into a generic LD)
+    double *As = reinterpret_cast<double *>(smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u));
+    double *Bs = As + S * A_STAGE;
+    uint64_t *full = reinterpret_cast<uint64_t *>(Bs + S * B_STAGE);
+    uint64_t *empty = full + S;
+
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+    const int64_t b = batch0 + blockIdx.z;
+    const int row0 = (int)blockIdx.y * BM, col0 = (int)blockIdx.x * BN;
+    const int KT = (int)((l + BK - 1) / BK);
+
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+        for (int st = 0; st < S; st++) {
+            mbar_init(full + st, 1);
+            mbar_init(empty + st, NT / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto produce = [&](int t) {
+        const int st = t % S;
+        mbar_arrive_expect_tx(full + st, STAGE_BYTES);
+        tma_load_4d(As + st * A_STAGE, &tmA, t * BK, row0, 0, (int)b, full + st);
+        tma_load_4d(Bs + st * B_STAGE, &tmB, col0, t * BK, 0, (int)b, full + st);
+    };
+    if (tid == 0)
+        for (int t = 0; t < S - 1 && t < KT; t++) produce(t);
+
+    T acc[TM][TN];
+    bool live[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; i++)
+#pragma unroll
+        for (int j = 0; j < TN; j++) {
+            acc[i][j] = E::zero();
+            live[i][j] = row0 + 2 * ty + i < m && col0 + 2 * tx + j < n;
+        }
+
+    for (int kt = 0; kt < KT; kt++) {
+        const int st = kt % S;
+        mbar_wait(full + st, (unsigned)((kt / S) & 1));
+        const double *as = As + st * A_STAGE;   // [W][BM][BKA]
+        const double *bs = Bs + st * B_STAGE;   // [W][BK][BN]
+        const int krem = (int)(l - (int64_t)kt * BK);
+        const int kmax = krem < BK ? krem : BK;
+        for (int kk = 0; kk < kmax; kk++) {
+            T a[TM], bb[TN];
+#pragma unroll
+            for (int w = 0; w < W; w++) {
+#pragma unroll
+                for (int i = 0; i < TM; i++) a[i].w[w] = as[(w * BM + 2 * ty + i) * BKA + kk];
+                const double2 v = *reinterpret_cast<const double2 *>(bs + (w * BK + kk) * BN + 2 * tx);
+                bb[0].w[w] = v.x;
+                bb[1].w[w] = v.y;
+            }
+#pragma unroll
+            for (int i = 0; i < TM; i++)
+#pragma unroll
+                for (int j = 0; j < TN; j++)
+                    if (live[i][j]) acc[i][j] = E::madd(acc[i][j], a[i], bb[j]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + st);
+        if (tid == 0 && kt + S - 1 < KT) {
+            const int t = kt + S - 1;
+            if (t >= S) mbar_wait(empty + t % S, (unsigned)(((t - S) / S) & 1));
+            produce(t);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < TM; i++) {
+        const int64_t gi = row0 + 2 * ty + i;
+        if (gi >= m) continue;
+#pragma unroll
+        for (int j = 0; j < TN; j++) {
+            const int64_t gj = col0 + 2 * tx + j;
+            if (gj >= n) continue;
+            double *cp = C.p + b * C.bs + gi * C.ld + gj;
+            if (beta) E::store(cp, C.ps, E::sub(E::load(cp, C.ps), acc[i][j]));
+            else E::store(cp, C.ps, acc[i][j]);
+        }
+    }
+}
+
 // ---- host side --------------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
@@ -192,20 +332,37 @@ static bool encoder() {
     return g_encode != nullptr;
 }
 
-// 4-D map over a batch of planar matrices: dims {cols, rows, W, batch}; box {bc, br, W, 1}
-static bool make_map(CUtensorMap *map, const MatDesc &d, int64_t batch, unsigned bc, unsigned br) {
+// 4-D map over a batch of planar matrices: dims {cols, rows, W, batch}; box {bc, br, W, 1}.
+// pair = true: the row-pair view {ld + cols, rows / 2, W, batch} (rows must be even).
+static bool make_map(CUtensorMap *map, const MatDesc &d, int64_t batch, unsigned bc, unsigned br, bool pair = false,
+                     int W = 2) {
     const uint64_t al = 16;
-    if (reinterpret_cast<uintptr_t>(d.p) % al || (d.ld * 8) % al || (d.ps * 8) % al) return false;
-    const int64_t bs = batch > 1 ? d.bs : 2 * d.ps;
+    const int64_t rs = pair ? 2 * d.ld : d.ld;   // row (pair) stride in doubles
+    if (reinterpret_cast<uintptr_t>(d.p) % al || (rs * 8) % al || (d.ps * 8) % al) return false;
+    if (pair && (d.rows % 2)) return false;
+    const int64_t bs = batch > 1 ? d.bs : W * d.ps;
     if ((bs * 8) % al || d.ld < d.cols || d.cols <= 0 || d.rows <= 0) return false;
-    cuuint64_t dims[4] = {(cuuint64_t)d.cols, (cuuint64_t)d.rows, 2, (cuuint64_t)batch};
-    cuuint64_t strides[3] = {(cuuint64_t)d.ld * 8, (cuuint64_t)d.ps * 8, (cuuint64_t)bs * 8};
-    cuuint32_t box[4] = {bc, br, 2, 1};
+    cuuint64_t dims[4] = {(cuuint64_t)(pair ? d.ld + d.cols : d.cols), (cuuint64_t)(pair ? d.rows / 2 : d.rows),
+                          (cuuint64_t)W, (cuuint64_t)batch};
+    cuuint64_t strides[3] = {(cuuint64_t)rs * 8, (cuuint64_t)d.ps * 8, (cuuint64_t)bs * 8};
+    cuuint32_t box[4] = {bc, br, (cuuint32_t)W, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     const CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, d.p, dims, strides, box, es,
                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
+}
+
+// Odd-ld A operands (c3's 256 x 257 leaves) take TMA through the row-pair view; DDQD_LEAF_APAIR=0
+// keeps them on the cp.async leaf. Measured on c3 (profiles/r02/c3_leaf_load_paths.md): 0.939 of
+// the FP64 peak with row-pair TMA vs 0.923 cp.async (343.2 vs 349.8 ms per step).
+static bool apair_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_LEAF_APAIR");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
 }
 
 // Returns 1 if launched (rc = status), 0 if the shape/strides do not qualify (caller falls back).
@@ -215,9 +372,75 @@ int try_leaf_tma(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &
     *rc = DDQD_OK;
     if (l == 0 || batch > 0x7fffffffLL || m > 0x7fffffffLL || l > 0x7fffffffLL || !encoder()) return 0;
     CUtensorMap ma, mb;
-    if (!make_map(&ma, A, batch, BK, BM) || !make_map(&mb, B, batch, BN, BK)) return 0;
-    auto kern = mv ? leaf_tma_kernel<1> : leaf_tma_kernel<0>;
-    static bool attr_set[2][64] = {};   // per variant and device
+    if (!make_map(&mb, B, batch, BN, BK)) return 0;
+    // A: the plain view when its rows are 16-byte aligned, else the row-pair view
+    CUtensorMap ma2;
+    int pair = 0;
+    if (!make_map(&ma, A, batch, BK, BM)) {
+        // row pairs: the odd rows' boxes start at ld + k0 - 1, 16-byte aligned only for odd ld
+        if (!apair_enabled() || A.ld % 2 == 0 || !make_map(&ma, A, batch, BK, BM / 2, true) ||
+            !make_map(&ma2, A, batch, BKO, BM / 2, true))
+            return 0;
+        pair = 1;
+    } else {
+        ma2 = ma;
+    }
+    auto kern = mv ? (pair ? leaf_tma_kernel<1, 1> : leaf_tma_kernel<1, 0>)
+                   : (pair ? leaf_tma_kernel<0, 1> : leaf_tma_kernel<0, 0>);
+    static bool attr_set[4][64] = {};   // per variant and device
+    bool &attr = attr_set[2 * mv + pair][current_device()];
+    const size_t smem = pair ? SMEM_P : SMEM;
+    if (!attr) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        attr = true;
+    }
+    const int64_t gx = (n + BN - 1) / BN, gy = (m + BM - 1) / BM;
+    if (gx > 0x7fffffff || gy > 65535) return 0;
+    prof_begin(0, s);
+    for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+        const int64_t bz = (batch - b0) < 65535 ? (batch - b0) : 65535;
+        // the maps index the batch absolutely: shift the problem index by b0 inside the kernel
+        kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)bz), NT, smem, s>>>(ma, ma2, mb, m, l, n, A.ld, C, beta, b0);
+        count_launch();
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            set_error(std::string("TMA leaf launch: ") + cudaGetErrorString(e));
+            *rc = DDQD_ECUDA;
+            return 1;
+        }
+    }
+    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s);
+    return 1;
+}
+
+}  // namespace ddqd
+
+namespace ddqd {
+
+// DDQD_LEAF_TMA_QD=0 keeps QD on the cp.async leaf (A/B measurements)
+static bool tma_qd_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_LEAF_TMA_QD");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// QD TMA leaf; returns 1 if launched (rc = status), 0 if the shape/strides do not qualify.
+int try_leaf_tma_qd(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A, const MatDesc &B,
+                    const MatDesc &C, int beta, int mv, cudaStream_t s, int *rc) {
+    using namespace tmaq;
+    *rc = DDQD_OK;
+    if (!tma_qd_enabled() || l == 0 || batch > 0x7fffffffLL || m > 0x7fffffffLL || l > 0x7fffffffLL || !encoder())
+        return 0;
+    CUtensorMap ma, mb;
+    if (!make_map(&ma, A, batch, BKA, BM, false, 4) || !make_map(&mb, B, batch, BN, BK, false, 4)) return 0;
+    auto kern = mv == 1 ? leaf_tma_qd_kernel<1> : mv == 2 ? leaf_tma_qd_kernel<2> : leaf_tma_qd_kernel<0>;
+    static bool attr_set[3][64] = {};
     bool &attr = attr_set[mv][current_device()];
     if (!attr) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess) {
@@ -231,12 +454,11 @@ int try_leaf_tma(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &
     prof_begin(0, s);
     for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
         const int64_t bz = (batch - b0) < 65535 ? (batch - b0) : 65535;
-        // the maps index the batch absolutely: shift the problem index by b0 inside the kernel
         kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)bz), NT, SMEM, s>>>(ma, mb, m, l, n, C, beta, b0);
         count_launch();
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) {
-            set_error(std::string("TMA leaf launch: ") + cudaGetErrorString(e));
+            set_error(std::string("QD TMA leaf launch: ") + cudaGetErrorString(e));
             *rc = DDQD_ECUDA;
             return 1;
         }

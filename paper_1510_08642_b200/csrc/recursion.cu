@@ -42,17 +42,27 @@ struct Plan {
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
-// workspace leading dimension: tight by default. DDQD_WS_PAD=1 pads it to even so every row is
-// 16-byte aligned and odd-width leaves qualify for the TMA leaf; measured on c3 this costs
-// more in the pre-additions (row gaps break their contiguous stores: 23.6 vs 20.3 ms/step)
-// than TMA gains in the leaf (equal FP64-pipe rate), so it is off.
-static int64_t ws_ld(int64_t cols) {
+// workspace leading dimension. DDQD_WS_PAD=1 pads every level's to even so every row is 16-byte
+// aligned and odd-width leaves qualify for the TMA leaf; measured on c3 in round 1 (one-level
+// additions) this cost more in the pre-additions (23.6 vs 20.3 ms/step) than TMA gained in the
+// leaf. =2 pads only the LEAF level (the operands the leaf kernel reads, written once by the
+// last pre-addition pass), so c3's 256 x 257 A leaves get ld 258 and take the TMA path. 0 = tight.
+static int ws_pad_mode() {
     static int pad = -1;
     if (pad < 0) {
         const char *e = getenv("DDQD_WS_PAD");
-        pad = (e && e[0] == '1') ? 1 : 0;
+        pad = (e && (e[0] == '0' || e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
     }
-    return pad ? ((cols + 1) & ~int64_t(1)) : cols;
+    return pad;
+}
+static int64_t ws_ld(int64_t cols) {
+    return ws_pad_mode() == 1 ? ((cols + 1) & ~int64_t(1)) : cols;
+}
+
+// leading dimension of the level-`level` workspace operands
+static int64_t ws_ld_at(const Plan &p, int level, int64_t cols) {
+    const int mode = ws_pad_mode();
+    return (mode == 1 || (mode == 2 && level == p.d)) ? ((cols + 1) & ~int64_t(1)) : cols;
 }
 
 static void plan_shapes(Plan &p, int64_t m, int64_t l, int64_t n) {
@@ -83,9 +93,9 @@ static size_t plan_layout(Plan &p, int64_t batch, int s, int lanes, bool fill) {
         if (j + 1 == s) { off = align256(off); lane0 = off; }   // start of the per-lane region
         const int64_t k = cnt[j + 1];
         const size_t W = (size_t)p.W;
-        const size_t a = (size_t)k * W * p.m[j + 1] * ws_ld(p.l[j + 1]) * sizeof(double);
-        const size_t b = (size_t)k * W * p.l[j + 1] * ws_ld(p.n[j + 1]) * sizeof(double);
-        const size_t c = (size_t)k * W * p.m[j + 1] * ws_ld(p.n[j + 1]) * sizeof(double);
+        const size_t a = (size_t)k * W * p.m[j + 1] * ws_ld_at(p, j + 1, p.l[j + 1]) * sizeof(double);
+        const size_t b = (size_t)k * W * p.l[j + 1] * ws_ld_at(p, j + 1, p.n[j + 1]) * sizeof(double);
+        const size_t c = (size_t)k * W * p.m[j + 1] * ws_ld_at(p, j + 1, p.n[j + 1]) * sizeof(double);
         oa[j + 1] = off; off = align256(off + a);
         ob[j + 1] = off; off = align256(off + b);
         om[j + 1] = off; off = align256(off + c);
@@ -148,7 +158,7 @@ static MatDesc child(const Plan &p, char *ws, const std::vector<size_t> &off, in
                      int64_t rows, int64_t cols, int lane) {
     MatDesc d;
     d.p = reinterpret_cast<double *>(ws + off[level] + (level >= p.s ? (size_t)lane * p.lane_bytes : 0));
-    d.rows = rows; d.cols = cols; d.ld = ws_ld(cols); d.ps = rows * d.ld; d.bs = (int64_t)p.W * d.ps;
+    d.rows = rows; d.cols = cols; d.ld = ws_ld_at(p, level, cols); d.ps = rows * d.ld; d.bs = (int64_t)p.W * d.ps;
     return d;
 }
 
