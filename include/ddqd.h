@@ -256,6 +256,11 @@ int64_t ddqd_launch_count(void);
  * n^2 for c = 5); cap = number of doubles in out (18 for all classes). */
 int ddqd_profile_start(void);
 int ddqd_profile_stop(double *out, int cap);
+/* Per-kernel breakdown of the last ddqd_profile_stop: one line per kernel (leaf variants are
+ * named separately, e.g. "leaf_tma_kernel (TMA, row-pair A)" / "leaf_gemm_kernel<...> (cp.async)"),
+ * "name \t class \t total ms \t launches \t work \n", NUL-terminated, truncated to cap bytes.
+ * Returns the bytes needed (including the NUL); out = NULL / cap = 0 only measures. */
+int ddqd_profile_kernels(char *out, size_t cap);
 
 /* FP64-pipe throughput probe: op 0 = DFMA, 1 = DADD stream; returns lane-operations per
  * second on the current device (and the per-launch ms). Roofline denominator of the leaf. */

@@ -83,6 +83,7 @@ def _load():
     L.ddqd_post_add.argtypes = [i32, i32, i64, ctypes.POINTER(Mat), ctypes.POINTER(Mat), i32]
     L.ddqd_profile_stop.argtypes = [ctypes.POINTER(ctypes.c_double), i32]
     L.ddqd_fp64_peak.argtypes = [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    L.ddqd_profile_kernels.argtypes = [ctypes.c_char_p, ctypes.c_size_t]
     return L
 
 
@@ -94,7 +95,7 @@ EXPORTED = ["dd_gemm", "qd_gemm", "ddqd_gemm_ex", "dd_lu_solve", "qd_lu_solve", 
             "ddqd_workspace_bytes", "ddqd_set_workspace", "ddqd_set_workspace_limit",
             "ddqd_launch_count", "ddqd_release", "ddqd_last_error", "ddqd_version",
             "ddqd_profile_start", "ddqd_profile_stop", "ddqd_fp64_peak", "ddqd_pre_add", "ddqd_post_add",
-            "ddqd_band_copy"]
+            "ddqd_band_copy", "ddqd_profile_kernels"]
 
 
 def _check(rc: int, what: str) -> int:
@@ -425,6 +426,18 @@ def profile_stop():
     v = list(buf)
     names = ["leaf", "pre", "post", "lu_panel", "lu_trsm", "lu_solve"]
     return {nm: tuple(v[3 * i:3 * i + 3]) for i, nm in enumerate(names)}
+
+
+def profile_kernels():
+    """Per-kernel totals of the last profile_stop(): {name: (class, ms, launches, work)}."""
+    need = lib.ddqd_profile_kernels(None, 0)
+    buf = ctypes.create_string_buffer(max(int(need), 1))
+    lib.ddqd_profile_kernels(buf, len(buf))
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cls, ms, launches, work = line.split("\t")
+        out[name] = (int(cls), float(ms), int(float(launches)), float(work))
+    return out
 
 
 def fp64_peak(op="dfma"):

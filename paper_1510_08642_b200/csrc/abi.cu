@@ -31,7 +31,13 @@ struct ProfRec {
     int cls;
     double work;
     cudaEvent_t e0, e1;
+    const char *name;
 };
+struct ProfAgg {
+    int cls;
+    double ms, launches, work;
+};
+static thread_local std::vector<std::pair<std::string, ProfAgg>> t_kern;   // per-kernel totals of the last stop
 static thread_local bool t_prof = false;
 static thread_local std::vector<ProfRec> t_recs;
 static thread_local cudaEvent_t t_open = nullptr;
@@ -42,12 +48,12 @@ void prof_begin(int cls, cudaStream_t s) {
     cudaEventCreate(&t_open);
     cudaEventRecord(t_open, s);
 }
-void prof_end(int cls, double work, cudaStream_t s) {
+void prof_end(int cls, double work, cudaStream_t s, const char *name) {
     if (!t_prof || !t_open) return;
     cudaEvent_t e1;
     cudaEventCreate(&e1);
     cudaEventRecord(e1, s);
-    t_recs.push_back(ProfRec{cls, work, t_open, e1});
+    t_recs.push_back(ProfRec{cls, work, t_open, e1, name});
     t_open = nullptr;
 }
 cudaStream_t cur_stream() { return t_stream; }
@@ -486,7 +492,9 @@ int ddqd_profile_start(void) {
 }
 
 int ddqd_profile_stop(double *out, int cap) {
+    static const char *kClassNames[] = {"leaf", "pre_add", "post_add", "lu_panel", "lu_trsm", "lu_solve"};
     t_prof = false;
+    t_kern.clear();
     for (int i = 0; i < cap; i++) out[i] = 0.0;
     for (auto &r : t_recs) {
         cudaEventSynchronize(r.e1);
@@ -497,12 +505,34 @@ int ddqd_profile_stop(double *out, int cap) {
             out[3 * r.cls + 1] += 1.0;
             out[3 * r.cls + 2] += r.work;
         }
+        const std::string nm = r.name ? r.name : (r.cls >= 0 && r.cls < 6 ? kClassNames[r.cls] : "?");
+        auto it = t_kern.begin();
+        for (; it != t_kern.end() && it->first != nm; ++it) {}
+        if (it == t_kern.end()) { t_kern.push_back({nm, ProfAgg{r.cls, 0.0, 0.0, 0.0}}); it = t_kern.end() - 1; }
+        it->second.ms += ms;
+        it->second.launches += 1.0;
+        it->second.work += r.work;
         cudaEventDestroy(r.e0);
         cudaEventDestroy(r.e1);
     }
     t_recs.clear();
     DDQD_CUDA_CHECK(cudaGetLastError());
     return DDQD_OK;
+}
+
+int ddqd_profile_kernels(char *out, size_t cap) {
+    std::string s;
+    for (auto &kv : t_kern) {
+        char line[512];
+        snprintf(line, sizeof(line), "%s\t%d\t%.6f\t%.0f\t%.6e\n", kv.first.c_str(), kv.second.cls, kv.second.ms,
+                 kv.second.launches, kv.second.work);
+        s += line;
+    }
+    if (!out || cap == 0) return (int)s.size() + 1;
+    const size_t k = s.size() < cap - 1 ? s.size() : cap - 1;
+    memcpy(out, s.data(), k);
+    out[k] = 0;
+    return (int)s.size() + 1;
 }
 
 int ddqd_fp64_peak(int op, double *lane_ops_per_s, double *ms) {

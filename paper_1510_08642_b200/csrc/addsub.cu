@@ -278,7 +278,7 @@ static int pre_dispatch(int algo, int side, int64_t P, const MatDesc &X, const M
     else if (side == 0) pre_add_kernel<W, 2, 0, V><<<g, 256, 0, s>>>(P, X, Y);
     else pre_add_kernel<W, 2, 1, V><<<g, 256, 0, s>>>(P, X, Y);
     DDQD_LAUNCH_CHECK();
-    prof_end(1, (double)total * W * 8.0 * 11.0, s);   // 4 quadrant reads + 7 operand writes
+    prof_end(1, (double)total * W * 8.0 * 11.0, s, "pre_add_kernel");   // 4 quadrant reads + 7 operand writes
     return DDQD_OK;
 }
 
@@ -303,7 +303,7 @@ static int pre2_dispatch(int algo, int side, int64_t P, const MatDesc &X, int64_
     else if (side == 0) pre_add2_kernel<W, 2, 0, V><<<g, TB, 0, s>>>(P, X, h1r, h1c, Y);
     else pre_add2_kernel<W, 2, 1, V><<<g, TB, 0, s>>>(P, X, h1r, h1c, Y);
     DDQD_LAUNCH_CHECK();
-    prof_end(1, (double)total * W * 8.0 * 65.0, s);   // 16 level-j reads + 49 level-(j+2) writes
+    prof_end(1, (double)total * W * 8.0 * 65.0, s, "pre_add2_kernel (two levels)");   // 16 level-j reads + 49 level-(j+2) writes
     return DDQD_OK;
 }
 
@@ -328,7 +328,7 @@ static int post2_dispatch(int algo, int64_t P, const MatDesc &M, int64_t h1m, in
     if (algo == 1) post_add2_kernel<W, 1, V><<<g, TB, 0, s>>>(P, M, h1m, h1n, C, beta);
     else post_add2_kernel<W, 2, V><<<g, TB, 0, s>>>(P, M, h1m, h1n, C, beta);
     DDQD_LAUNCH_CHECK();
-    prof_end(2, (double)total * W * 8.0 * (beta ? 81.0 : 65.0), s);   // 49 reads + 16 (32) C
+    prof_end(2, (double)total * W * 8.0 * (beta ? 81.0 : 65.0), s, "post_add2_kernel (two levels)");   // 49 reads + 16 (32) C
     return DDQD_OK;
 }
 
@@ -350,7 +350,7 @@ static int post_dispatch(int algo, int64_t P, const MatDesc &M, const MatDesc &C
     if (algo == 1) post_add_kernel<W, 1, V><<<g, 256, 0, s>>>(P, M, C, beta);
     else post_add_kernel<W, 2, V><<<g, 256, 0, s>>>(P, M, C, beta);
     DDQD_LAUNCH_CHECK();
-    prof_end(2, (double)total * W * 8.0 * (beta ? 15.0 : 11.0), s);   // 7 product reads + 4 (8) C
+    prof_end(2, (double)total * W * 8.0 * (beta ? 15.0 : 11.0), s, "post_add_kernel");   // 7 product reads + 4 (8) C
     return DDQD_OK;
 }
 
@@ -381,7 +381,7 @@ static int post_quad_dispatch(int algo, int q, const MatDesc &M, const MatDesc &
         else post_add_kernel<W, 2, V, 3><<<g, 256, 0, s>>>(1, M, C, 0);
     }
     DDQD_LAUNCH_CHECK();
-    prof_end(2, (double)total * W * 8.0 * (reads[algo == 2][q] + 1.0), s);
+    prof_end(2, (double)total * W * 8.0 * (reads[algo == 2][q] + 1.0), s, "post_add_kernel (one C quadrant)");
     return DDQD_OK;
 }
 
@@ -450,7 +450,7 @@ int launch_post_add_ptrs(int W, int algo, int64_t P, const double *const *ch, in
     }
 #undef DDQD_PP
     DDQD_LAUNCH_CHECK();
-    prof_end(2, (double)total * W * 8.0 * (beta ? 15.0 : 11.0), s);
+    prof_end(2, (double)total * W * 8.0 * (beta ? 15.0 : 11.0), s, "post_add_ptrs_kernel (peer pointers)");
     return DDQD_OK;
 }
 

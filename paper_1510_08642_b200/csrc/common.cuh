@@ -35,7 +35,9 @@ struct NvtxRange {
 // only between ddqd_profile_start/stop. Classes: 0 leaf GEMM (work = madds), 1 pre-add
 // (work = algorithmic bytes), 2 post-add (bytes), 3 LU kernels.
 void prof_begin(int cls, cudaStream_t s);
-void prof_end(int cls, double work, cudaStream_t s);
+// name: a string literal (or other static storage) naming the kernel, for the per-kernel
+// breakdown of ddqd_profile_kernels; null = the class name
+void prof_end(int cls, double work, cudaStream_t s, const char *name = nullptr);
 int fp64_peak(int op, double *lane_ops_per_s, double *ms, cudaStream_t s);
 
 #define DDQD_CUDA_CHECK(expr)                                                            \

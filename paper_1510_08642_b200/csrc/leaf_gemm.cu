@@ -217,7 +217,11 @@ static int launch_cfg(int64_t m, int64_t l, int64_t n, int64_t batch, const MatD
         kern<<<grid, Cfg::NT, Cfg::SMEM, s>>>(m, l, n, A, B, C, beta, b0);
         DDQD_LAUNCH_CHECK();
     }
-    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s);
+    static const std::string nm = "leaf_gemm_kernel<" + std::to_string(W) + "," + std::to_string(BM) + "," +
+                                  std::to_string(BN) + "," + std::to_string(BK) + "," + std::to_string(TM) + "," +
+                                  std::to_string(TN) + "," + std::to_string(STAGES) + "," + std::to_string(MINB) + "," +
+                                  std::to_string(MV) + "> (cp.async)";
+    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s, nm.c_str());
     return DDQD_OK;
 }
 

@@ -137,7 +137,7 @@ int launch_small(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &
             m, l, n, A, B, C, beta, b0);
         DDQD_LAUNCH_CHECK();
     }
-    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s);
+    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s, "leaf_small_kernel");
     return DDQD_OK;
 }
 
@@ -224,7 +224,7 @@ int launch_flat(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A
     prof_begin(0, s);
     leaf_flat_kernel<W, MV, RM, RN><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(m, l, n, total, A, B, C, beta);
     DDQD_LAUNCH_CHECK();
-    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s);
+    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s, "leaf_flat_kernel");
     return DDQD_OK;
 }
 
@@ -310,7 +310,7 @@ int launch_pack(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A
     prof_begin(0, s);
     leaf_pack_kernel<W, MV><<<(unsigned)blocks, 256, smem, s>>>(m, l, n, batch, NL, A, B, C, beta);
     DDQD_LAUNCH_CHECK();
-    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s);
+    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s, "leaf_pack_kernel");
     return DDQD_OK;
 }
 

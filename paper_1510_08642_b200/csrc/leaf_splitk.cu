@@ -140,7 +140,7 @@ static int launch_splitk_t(int64_t m, int64_t l, int64_t n, int64_t batch, const
             return DDQD_ECUDA;
         }
     }
-    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s);
+    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s, "leaf_splitk_kernel (cluster DSMEM tree)");
     return DDQD_OK;
 }
 

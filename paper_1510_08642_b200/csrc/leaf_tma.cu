@@ -412,7 +412,8 @@ int try_leaf_tma(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &
             return 1;
         }
     }
-    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s);
+    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s,
+             pair ? "leaf_tma_kernel (TMA, row-pair A)" : "leaf_tma_kernel (TMA)");
     return 1;
 }
 
@@ -463,7 +464,7 @@ int try_leaf_tma_qd(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDes
             return 1;
         }
     }
-    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s);
+    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s, "leaf_tma_qd_kernel (TMA)");
     return 1;
 }
 

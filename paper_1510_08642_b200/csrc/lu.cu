@@ -1440,7 +1440,8 @@ static int lu_panel_w(int64_t n, int pivot, double *A, int64_t *ipiv, int64_t p,
             DDQD_LAUNCH_CHECK();
         }
     }
-    prof_end(3, (double)kb * (double)(n - p) * (double)kb / 2.0, s);   // panel madds (approx.)
+    prof_end(3, (double)kb * (double)(n - p) * (double)kb / 2.0, s,   // panel madds (approx.)
+             coop ? "lu_panel_coop_kernel (+ lu_laswp_kernel)" : "lu_pivot_kernel + lu_rank1_kernel");
     const int64_t n2 = n - p - kb;
     if (n2 <= 0) return DDQD_OK;
     // one CTA per SM when possible: cw = ceil(n2 / #SMs), capped by shared memory
@@ -1481,7 +1482,7 @@ static int lu_panel_w(int64_t n, int pivot, double *A, int64_t *ipiv, int64_t p,
         lu_trsm_kernel<W><<<(unsigned)((n2 + cw - 1) / cw), tthreads, smem, s>>>(A, n, p, kb, p + kb, cw);
     }
     DDQD_LAUNCH_CHECK();
-    prof_end(4, (double)kb * (double)kb / 2.0 * (double)n2, s);
+    prof_end(4, (double)kb * (double)kb / 2.0 * (double)n2, s, "lu_trsm_*_kernel (U12)");
     return DDQD_OK;
 }
 
@@ -1556,7 +1557,7 @@ static int lu_trsv_w(int64_t n, const double *A, const int64_t *ipiv, const doub
             DDQD_LAUNCH_CHECK();
         }
     }
-    prof_end(5, (double)n * (double)n, s);
+    prof_end(5, (double)n * (double)n, s, "lu solves (perm, trsv_diag_blk, trsv_update_co)");
     return DDQD_OK;
 }
 
