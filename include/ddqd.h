@@ -20,13 +20,29 @@
  * for the overlap; pageable memory works, with the copies serialised.
  *
  * Ownership: the caller owns every buffer passed in; the library never frees caller
- * memory. The library owns a per-device workspace (grown on demand, freed by
- * ddqd_release) unless the calling thread installed one with ddqd_set_workspace.
+ * memory. The library owns a per-device workspace, LU auxiliary and host-path staging
+ * buffers (grown on demand, freed by ddqd_release) unless the calling thread installed
+ * a workspace with ddqd_set_workspace.
  *
  * Synchronisation: device-pointer GEMM calls are asynchronous on the calling
  * thread's stream (ddqd_set_stream; default = legacy default stream), like cuBLAS;
  * kernel faults surface at the next synchronisation. dd_lu_solve synchronises once
  * at the end to read `info`.
+ *
+ * Concurrency: calls from several host threads and on several streams are safe. A call
+ * that uses the library-owned buffers (Strassen/Winograd recursion workspace, LU, host
+ * pointers) holds the device's call lock while it enqueues, and when the previous such
+ * call was on another stream its stream first waits for that call's kernels (an event),
+ * so those calls serialise on the device; calls that use no library buffer (Block on
+ * device pointers, or with a per-thread caller workspace) run fully concurrently.
+ *
+ * CUDA graphs: calls may be captured. The library buffers a captured call uses must
+ * already be large enough (make the same call once before capturing, or install a
+ * caller workspace); growing one during capture fails with DDQD_ENOTSUP. Once a call
+ * has been captured, buffers the library outgrows are kept (not freed) until
+ * ddqd_release, so a captured graph never points at freed memory; do not call
+ * ddqd_release while captured graphs that use library buffers may still be replayed.
+ * A captured call does not wait for library calls on other streams outside the graph.
  *
  * Errors: every entry point returns an int status. 0 = success; negative values are
  * the DDQD_E* codes below (no C++ exception crosses the ABI); a human-readable
@@ -113,6 +129,9 @@ int qd_gemm(int64_t m, int64_t l, int64_t n, const double *A, const double *B, d
 
 /* Strided / batched / accumulate form used by the LU and the multi-GPU driver.
  * Element (b, i, j) word w of X lives at X[b*bs + w*ps + i*ld + j] (device pointers only).
+ * DDQD_EINVAL if ld < cols, ps < rows*ld, or (batch > 1) bs < words*ps; DDQD_EALIAS if C shares
+ * an element with A or B (exact for single views with equal ld and ps -- e.g. disjoint
+ * sub-blocks of one matrix are accepted; conservative, by address extent, otherwise).
  * beta = 0: C := A B.  beta = 1: C := C - A B, where A B is first formed from +0 and then
  * subtracted elementwise (dd_sub / qd_sub) -- the LU Schur update of P:131.
  * batch >= 1 independent problems of identical shape share one schedule. */

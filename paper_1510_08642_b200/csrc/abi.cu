@@ -82,15 +82,36 @@ int sm_count() {
     return cache[d];
 }
 
-// Library-owned per-device buffers. Growth frees the old buffer (cudaFree synchronises the
-// device, so no in-flight kernel can still be using it).
+// Library-owned per-device buffers (GEMM workspace, LU auxiliary, host-path staging), shared by
+// every host thread and stream of the device. Ordering between users:
+//  * the first use of a library buffer inside an entry point takes the device's CALL LOCK (held
+//    until the entry point has enqueued everything, LibCall below), so two threads never
+//    enqueue work on the same buffers at once;
+//  * if the previous user enqueued on a different stream, the new stream first waits for that
+//    user's last kernels (an event recorded at the end of every call that touched the buffers);
+//  * calls that touch no library buffer (Block GEMMs on device pointers, caller workspace via
+//    ddqd_set_workspace) take neither and stay fully concurrent.
+// Growth frees the old buffer (cudaFree synchronises the device) -- unless a CUDA graph has
+// captured a call that used library buffers: from then on old buffers are retired and freed
+// only by ddqd_release, so a captured graph never points at freed memory; growing a buffer
+// DURING capture is refused (allocation is not capturable), see ddqd.h.
 struct DevBuf {
     void *p = nullptr;
     size_t bytes = 0;
 };
+struct DevSync {
+    std::mutex call;
+    cudaEvent_t done = nullptr;
+    cudaStream_t last = nullptr;
+    bool have = false;
+};
 static std::mutex g_mu;
 static DevBuf g_ws[64], g_aux[64], g_stage[64];
+static DevSync g_sync[64];
+static std::vector<void *> g_retired[64];
+static bool g_captured = false;
 static size_t g_limit = 0;
+static thread_local int t_lock_dev = -1;   // device whose call lock this thread holds (-1: none)
 
 static int cur_dev() {
     int d = 0;
@@ -98,11 +119,65 @@ static int cur_dev() {
     return d;
 }
 
+static bool capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return st != cudaStreamCaptureStatusNone;
+}
+
+// first library-buffer use of this entry point: take the call lock, order after the last user
+static void lib_acquire() {
+    const int d = cur_dev() & 63;
+    if (t_lock_dev == d) return;
+    g_sync[d].call.lock();
+    t_lock_dev = d;
+    DevSync &y = g_sync[d];
+    if (capturing(t_stream)) {
+        g_captured = true;   // (a captured graph must not wait on work outside the capture)
+        return;
+    }
+    if (y.have && y.last != t_stream) cudaStreamWaitEvent(t_stream, y.done, 0);
+}
+
+// RAII guard of every entry point that may use library buffers
+struct LibCall {
+    ~LibCall() {
+        if (t_lock_dev < 0) return;
+        DevSync &y = g_sync[t_lock_dev];
+        if (!capturing(t_stream)) {
+            if (!y.done) cudaEventCreateWithFlags(&y.done, cudaEventDisableTiming);
+            if (y.done && cudaEventRecord(y.done, t_stream) == cudaSuccess) {
+                y.last = t_stream;
+                y.have = true;
+            } else {
+                cudaGetLastError();
+            }
+        }
+        t_lock_dev = -1;
+        y.call.unlock();
+    }
+};
+
 static void *buf_get(DevBuf *arr, size_t bytes, int *status, const char *what) {
+    lib_acquire();
     std::lock_guard<std::mutex> lk(g_mu);
-    DevBuf &b = arr[cur_dev() & 63];
+    const int dv = cur_dev() & 63;
+    DevBuf &b = arr[dv];
     if (b.bytes < bytes) {
-        if (b.p) cudaFree(b.p);
+        if (capturing(t_stream)) {
+            set_error(std::string("the library's ") + what + " must grow to " + std::to_string(bytes) +
+                      " bytes, which cannot happen during stream capture: make the same call once before "
+                      "capturing, or install a caller workspace (ddqd_set_workspace)");
+            *status = DDQD_ENOTSUP;
+            return nullptr;
+        }
+        if (b.p) {
+            if (g_captured) g_retired[dv].push_back(b.p);   // a captured graph may still use it
+            else cudaFree(b.p);
+        }
         b.p = nullptr;
         b.bytes = 0;
         if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
@@ -251,6 +326,7 @@ static int copy_res(CopyRes **out) {
 static int gemm_entry(int W, int64_t m, int64_t l, int64_t n, const double *A, const double *B,
                        double *C, int algo, int64_t T) {
     NvtxRange nv(W == 2 ? "dd_gemm" : "qd_gemm");
+    LibCall guard;
     t_err.clear();
     int rc = check_gemm_args(m, l, n, algo, T);
     if (rc) return rc;
@@ -352,8 +428,36 @@ int qd_gemm(int64_t m, int64_t l, int64_t n, const double *A, const double *B, d
     return gemm_entry(4, m, l, n, A, B, C, algo, threshold);
 }
 
+// Do two strided planar views share an element? Exact for two single (batch 1) views with the
+// same ld and plane stride -- the LU's and the multi-GPU schedule's sub-blocks of one matrix;
+// otherwise conservative (overlapping address extents count as aliasing).
+struct View {
+    const double *p;
+    int64_t rows, cols, ld, ps, bs, batch;
+};
+static const double *view_end(const View &v, int W) {   // one past the last element
+    return v.p + (v.batch - 1) * v.bs + (int64_t)(W - 1) * v.ps + (v.rows - 1) * v.ld + v.cols;
+}
+static bool views_alias(const View &a, const View &c, int W) {
+    if (a.rows == 0 || a.cols == 0 || c.rows == 0 || c.cols == 0 || a.batch == 0 || c.batch == 0) return false;
+    if (!(a.p < view_end(c, W) && c.p < view_end(a, W))) return false;   // disjoint extents
+    if (a.batch != 1 || c.batch != 1 || a.ld != c.ld || a.ps != c.ps || a.ld <= 0 || a.ps <= 0) return true;
+    const View &lo = a.p <= c.p ? a : c, &hi = a.p <= c.p ? c : a;
+    const int64_t delta = hi.p - lo.p;
+    const int64_t q = delta / lo.ps, r = delta % lo.ps;           // plane, then row / column offsets
+    const int64_t row = r / lo.ld, col = r % lo.ld;
+    if (q >= W) return false;                                     // all planes disjoint
+    if (col + hi.cols > lo.ld) return true;                       // wraps a row: be conservative
+    const bool rows_meet = row < lo.rows && 0 < row + hi.rows;
+    const bool cols_meet = col < lo.cols && 0 < col + hi.cols;
+    // plane k of the higher view sits at plane q + k of the lower one (q < W: some planes meet),
+    // at the same (row, col) offset in every plane
+    return rows_meet && cols_meet;
+}
+
 int ddqd_gemm_ex(const ddqd_gemm_desc *d) {
     NvtxRange nv("ddqd_gemm_ex");
+    LibCall guard;
     t_err.clear();
     if (!d) { set_error("null descriptor"); return DDQD_EINVAL; }
     if (d->prec != 2 && d->prec != 4) { set_error("prec must be DDQD_DD or DDQD_QD"); return DDQD_EINVAL; }
@@ -362,6 +466,19 @@ int ddqd_gemm_ex(const ddqd_gemm_desc *d) {
     if (d->batch < 0 || (d->beta != 0 && d->beta != 1)) { set_error("bad batch or beta"); return DDQD_EINVAL; }
     if (d->lda < d->l || d->ldb < d->n || d->ldc < d->n) { set_error("leading dimension too small"); return DDQD_EINVAL; }
     if (d->m == 0 || d->n == 0 || d->batch == 0) return DDQD_OK;
+    const int W = d->prec;
+    // plane strides must clear a plane, batch strides a whole W-word matrix
+    if ((d->l && d->psA < d->m * d->lda) || d->psB < d->l * d->ldb || d->psC < d->m * d->ldc ||
+        (d->batch > 1 && ((d->l && d->bsA < W * d->psA) || d->bsB < W * d->psB || d->bsC < W * d->psC))) {
+        set_error("plane stride < rows * ld, or batch stride < words * plane stride");
+        return DDQD_EINVAL;
+    }
+    {
+        const View va{d->A, d->m, d->l, d->lda, d->psA, d->bsA, d->batch};
+        const View vb{d->B, d->l, d->n, d->ldb, d->psB, d->bsB, d->batch};
+        const View vc{d->C, d->m, d->n, d->ldc, d->psC, d->bsC, d->batch};
+        if (views_alias(va, vc, W) || views_alias(vb, vc, W)) { set_error("C overlaps A or B"); return DDQD_EALIAS; }
+    }
     if (where(d->A) || where(d->B) || where(d->C)) { set_error("ddqd_gemm_ex takes device pointers only"); return DDQD_ENOTSUP; }
     MatDesc A{const_cast<double *>(d->A), d->m, d->l, d->lda, d->psA, d->bsA};
     MatDesc B{const_cast<double *>(d->B), d->l, d->n, d->ldb, d->psB, d->bsB};
@@ -372,10 +489,12 @@ int ddqd_gemm_ex(const ddqd_gemm_desc *d) {
 int ddqd_lu_solve(int prec, int pivot, int64_t n, double *A, const double *b, double *x, int64_t *ipiv,
                   int64_t panel, int algo, int64_t threshold) {
     NvtxRange nv("ddqd_lu_solve");
+    LibCall guard;
     t_err.clear();
     if (prec != 2 && prec != 4) { set_error("prec must be DDQD_DD or DDQD_QD"); return DDQD_EINVAL; }
     if (pivot != 0 && pivot != 1) { set_error("pivot must be 0 or 1"); return DDQD_EINVAL; }
     if (n < 0 || panel < 1) { set_error("n must be >= 0 and panel >= 1"); return DDQD_EINVAL; }
+    if (panel > 1024 && n > panel) { set_error("panel > 1024 is not supported by the TRSM kernels (n > panel)"); return DDQD_ENOTSUP; }
     int rc = check_gemm_args(n, panel, n, algo, threshold);
     if (rc) return rc;
     if (algo & DDQD_ADD_ACCURATE) { set_error("the accurate-add variant is a GEMM variant (LU: canonical)"); return DDQD_ENOTSUP; }
@@ -389,10 +508,12 @@ int ddqd_lu_solve(int prec, int pivot, int64_t n, double *A, const double *b, do
 }
 
 int ddqd_lu_panel(int prec, int pivot, int64_t n, double *A, int64_t *ipiv, int64_t p, int64_t kb) {
+    LibCall guard;
     t_err.clear();
     if (prec != 2 && prec != 4) { set_error("prec must be DDQD_DD or DDQD_QD"); return DDQD_EINVAL; }
     if (pivot != 0 && pivot != 1) { set_error("pivot must be 0 or 1"); return DDQD_EINVAL; }
     if (n < 0 || p < 0 || kb < 1 || p + kb > n) { set_error("need 0 <= p, 1 <= kb, p + kb <= n"); return DDQD_EINVAL; }
+    if (kb > 1024 && p + kb < n) { set_error("panel > 1024 is not supported by the TRSM kernels"); return DDQD_ENOTSUP; }
     if (!A || !ipiv) { set_error("null pointer"); return DDQD_EINVAL; }
     if (where(A) || where(ipiv)) { set_error("LU takes device pointers only"); return DDQD_ENOTSUP; }
     int info = 0;
@@ -402,6 +523,7 @@ int ddqd_lu_panel(int prec, int pivot, int64_t n, double *A, int64_t *ipiv, int6
 }
 
 int ddqd_lu_trsv(int prec, int64_t n, const double *LU, const int64_t *ipiv, const double *b, double *x) {
+    LibCall guard;
     t_err.clear();
     if (prec != 2 && prec != 4) { set_error("prec must be DDQD_DD or DDQD_QD"); return DDQD_EINVAL; }
     if (n < 0) { set_error("n must be >= 0"); return DDQD_EINVAL; }
@@ -541,13 +663,17 @@ int ddqd_fp64_peak(int op, double *lane_ops_per_s, double *ms) {
 }
 
 int ddqd_release(void) {
-    std::lock_guard<std::mutex> lk(g_mu);
     const int d = cur_dev() & 63;
+    std::lock_guard<std::mutex> cl(g_sync[d].call);   // no call of another thread is enqueuing
+    std::lock_guard<std::mutex> lk(g_mu);
     for (DevBuf *arr : {g_ws, g_aux, g_stage}) {
         if (arr[d].p) cudaFree(arr[d].p);
         arr[d].p = nullptr;
         arr[d].bytes = 0;
     }
+    for (void *p : g_retired[d]) cudaFree(p);
+    g_retired[d].clear();
+    g_sync[d].have = false;
     return DDQD_OK;
 }
 

@@ -1114,3 +1114,80 @@ def test_ragged_split_same_bits_as_unsplit(tmp_path):
         subprocess.check_call([sys.executable, "-c", code % f], env=env, cwd=ROOT)
         outs.append(np.load(f))
     assert same(outs[0], outs[1])
+
+
+# ---- ABI hardening: aliasing / stride checks, threads and streams, graph capture ----
+def test_gemm_ex_alias_and_stride_checks(orc):
+    """ddqd_gemm_ex rejects C overlapping A or B (EALIAS) and impossible strides (EINVAL), and
+    accepts disjoint sub-blocks of one matrix (the LU's form)."""
+    import ctypes
+    n = 96
+    M = cu(gen.dd_matrix(n, n, 51, 0))
+    base = M.data_ptr()
+    ps = n * n
+
+    def call(a_off, b_off, c_off, m, l, k, psA=ps, beta=1):
+        return ddqd.lib.ddqd_gemm_ex(ctypes.byref(ddqd.GemmDesc(
+            2, 1, 16, m, l, k, 1, base + 8 * a_off, n, psA, 0, base + 8 * b_off, n, ps, 0,
+            base + 8 * c_off, n, ps, 0, beta)))
+    ddqd._set_stream(M)
+    # LU-like disjoint blocks: L21 = rows 32.., cols 0..32; U12 = rows 0..32, cols 32..; A22
+    assert call(32 * n, 32, 32 * n + 32, 64, 32, 64) == 0
+    # C overlapping A (C's block starts inside A's block)
+    assert call(0, 32, 16 * n + 16, 48, 32, 48) == -2
+    # C overlapping B in the second plane only region still overlaps (same rectangles)
+    assert call(32 * n, 32, 32, 32, 32, 32) == -2
+    # plane stride smaller than rows * ld
+    assert call(32 * n, 32, 32 * n + 32, 64, 32, 64, psA=10) == -1
+    torch.cuda.synchronize()
+    # panels wider than the TRSM kernels take are refused before anything runs
+    assert ddqd.lib.ddqd_lu_panel(2, 1, 4000, M.data_ptr(), M.data_ptr(), 0, 1100) == -5
+
+
+def test_threads_and_streams_share_the_workspace(orc):
+    """Strassen/Winograd calls from two host threads, each on its own stream, with the
+    library-owned workspace: every result bit-exact (the call lock + cross-stream events)."""
+    import threading
+    A, B = gen.dd_matrix(300, 280, 52, 0), gen.dd_matrix(280, 310, 52, 1)
+    refs = {a: orc.gemm(A, B, a, threshold=32) for a in ("strassen", "winograd")}
+    out, errs = {}, []
+
+    def work(algo):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                a, b = cu(A), cu(B)
+                res = [ddqd.gemm(a, b, algo, 32) for _ in range(6)]
+                st.synchronize()
+                out[algo] = [r.cpu().numpy() for r in res]
+        except Exception as e:   # noqa: BLE001
+            errs.append(repr(e))
+    ts = [threading.Thread(target=work, args=(a,)) for a in ("strassen", "winograd")]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for algo, res in out.items():
+        assert all(same(r, refs[algo]) for r in res), algo
+
+
+def test_graph_capture_workspace_rules(orc):
+    """A captured Strassen call whose workspace is already large enough replays correctly even
+    after a later, larger call grows the workspace (the old buffer is retired, not freed)."""
+    A, B = gen.dd_matrix(200, 200, 53, 0), gen.dd_matrix(200, 200, 53, 1)
+    a, b = cu(A), cu(B)
+    C = ddqd.gemm(a, b, "strassen", 32)                 # sizes the workspace outside capture
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        ddqd.gemm(a, b, "strassen", 32, out=C)
+    A2, B2 = gen.dd_matrix(700, 700, 54, 0), gen.dd_matrix(700, 700, 54, 1)
+    big = ddqd.gemm(cu(A2), cu(B2), "strassen", 32)     # grows the workspace
+    C.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert same(np_(C), orc.gemm(A, B, "strassen", threshold=32))
+    assert same(np_(big), orc.gemm(A2, B2, "strassen", threshold=32))
