@@ -144,6 +144,25 @@ class CudaBackend:
     def post_add_ptrs(self, algo, children, C, r0, r1):
         return self.ddqd.post_add_ptrs(algo, children, C, r0, r1)
 
+    # interprocess events: stream-ordered dependencies on other ranks' kernels (no host sync)
+    def ipc_event(self, like):
+        import torch
+        with torch.cuda.device(like.device):
+            e = torch.cuda.Event(enable_timing=False, interprocess=True)
+            e.record()   # an event needs a record before its handle can be taken
+            return e, e.ipc_handle()
+
+    def open_event(self, handle, like):
+        import torch
+        return torch.cuda.Event.from_ipc_handle(like.device, handle)
+
+    def record(self, e):
+        e.record()
+
+    def wait(self, e):
+        import torch
+        torch.cuda.current_stream().wait_event(e)
+
     def lu_panel(self, A, ipiv, p, kb, pivot):
         return self.ddqd.lu_panel(A, ipiv, p, kb, pivot)
 
@@ -326,6 +345,9 @@ class DistributedGemm:
             return self._p2p
         W, bk, dist = self.W, self.backend, self.dist
         local, handles, frees = {}, {}, []
+        # one interprocess event per level (k: the products, k-1 .. 0: the combine levels)
+        events = [bk.ipc_event(like) for _ in range(self.k + 1)]
+        handles["events"] = [h for _, h in events]
         for level in range(1, self.k + 1):
             mj, _, nj = self.shapes[level]
             sl = self.slices if level == self.k else self.pslices[level]
@@ -357,7 +379,20 @@ class DistributedGemm:
             v, c = bk.ipc_open(allh[0]["C"], (W, self.m, self.n), like)
             views["C"] = v
             closes.append(c)
-        self._p2p = {"local": local, "views": views, "frees": frees, "closes": closes}
+        ev = {"own": [e for e, _ in events],
+              "peers": {r: [bk.open_event(h, like) for h in allh[r]["events"]]
+                        for r in range(self.world) if r != self.rank}}
+        # host-only rendezvous for the per-level barriers: an NCCL barrier is a device collective
+        # that waits for this rank's queued kernels, which is what the events are there to avoid
+        hb = dist.barrier
+        try:
+            if hasattr(dist, "new_group") and dist.get_backend() == "nccl":
+                grp = dist.new_group(backend="gloo")
+                hb = lambda: dist.barrier(group=grp)   # noqa: E731
+        except Exception:   # noqa: BLE001  (no gloo: the NCCL barrier is still correct)
+            hb = dist.barrier
+        self._p2p = {"local": local, "views": views, "frees": frees, "closes": closes, "events": ev,
+                     "host_barrier": hb}
         return self._p2p
 
     def _p2p_call(self, A, B, C):
@@ -381,10 +416,16 @@ class DistributedGemm:
         for c0 in range(lo, hi, self.chunk):
             c1 = min(hi, c0 + self.chunk)
             bk.gemm_batched(X[c0:c1], Y[c0:c1], Mk[c0 - lo:c1 - lo], self.algo, self.T)
+        ev = st["events"]
+        bk.record(ev["own"][k])
         keep = []
         for j in range(k - 1, -1, -1):
-            bk.sync()
-            dist.barrier()            # level j+1 complete on every rank
+            # level j reads every rank's level-(j+1) results: each rank recorded an interprocess
+            # event after that level; the host barrier only guarantees the records are enqueued,
+            # the wait itself is stream-ordered (no device synchronisation per level)
+            st["host_barrier"]()
+            for r, evs in ev["peers"].items():
+                bk.wait(evs[j + 1])
             if j > 0:
                 a, b = self.pslices[j][self.rank]
                 if b > a:
@@ -402,8 +443,11 @@ class DistributedGemm:
                         o, off = self._owner(1, c)
                         children.append(st["views"][(1, o)][off])
                     keep.append(bk.post_add_ptrs(self.algo, children, st["views"]["C"], r0, r1))
+            bk.record(ev["own"][j])
+        # every rank's rows of C are in rank 0's buffer, and no peer still reads this rank's
+        # buffers when the next call overwrites them
         bk.sync()
-        dist.barrier()                # every rank's rows of C are in rank 0's buffer
+        dist.barrier()
         if self.rank == 0:
             C.copy_(st["local"]["C"])
         return C

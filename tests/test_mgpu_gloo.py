@@ -66,6 +66,19 @@ class OracleBackend:
     def ipc_free(self, path):
         os.remove(path)
 
+    # CPU: every backend call completes before it returns, so events are no-ops
+    def ipc_event(self, like):
+        return None, b""
+
+    def open_event(self, handle, like):
+        return None
+
+    def record(self, e):
+        pass
+
+    def wait(self, e):
+        pass
+
     def post_add_ptrs(self, algo, children, C, r0, r1):
         """Position rows [r0, r1) of the one-level post-addition, children given as tensors."""
         add = lambda a, b: self._ew("add", a, b)   # noqa: E731
