@@ -490,4 +490,170 @@ int launch_elementwise(int W, int op, int64_t count, const double *x, const doub
     return DDQD_OK;
 }
 
+// ---- the last recursion level fused with its leaves (tiny leaves) ------------------------------
+// For leaves of at most 32 x 32 x 32 (Strassen/Winograd(32) at n = 1025: 33^3 parents, 17^3
+// leaves) one CTA takes one level-(d-1) parent: its threads form the 7 A and 7 B children in
+// shared memory straight from the parent in global memory (pre_add_kernel's formulas, reads
+// outside the parent are exact zeros -- the virtual padding), then each thread owns output
+// positions (i, j) of the children: it forms the 7 products at (i, j) (7 independent chains,
+// acc from +0, k ascending, E::madd) and combines them with the post-addition formulas straight
+// into the parent's C (crop, beta). Every element sees the operation sequence of
+// pre_add_kernel -> leaf -> post_add_kernel, so the bits are those of the unfused schedule; the
+// children and the products never touch HBM.
+constexpr int kFusedNT = 160;   // a 17 x 17 leaf: 17 rows x 9 position pairs = 153 DD tasks
+
+struct FusedLastDims {
+    int hm, hl, hn;   // child (leaf) dims
+};
+
+__host__ __device__ inline size_t fused_last_smem_doubles(int W, int hm, int hl, int hn) {
+    return (size_t)7 * W * hm * hl + (size_t)7 * W * hl * hn;
+}
+
+template <int W, int ALGO, int VA, int MV>
+__global__ void __launch_bounds__(kFusedNT) fused_last_kernel(int64_t P, MatDesc X, MatDesc Y, MatDesc C, int beta,
+                                                              FusedLastDims dd) {
+    using EA = arith<W, VA>;   // additions (canonical or accurate)
+    using EM = arith<W, MV>;   // the leaf's multiply-add
+    using T = typename EA::T;
+    extern __shared__ double fs[];
+    const int hm = dd.hm, hl = dd.hl, hn = dd.hn;
+    const size_t psa = (size_t)hm * hl, psb = (size_t)hl * hn;
+    double *CA = fs;                              // [7][W][hm][hl]
+    double *CB = fs + (size_t)7 * W * psa;        // [7][W][hl][hn]
+    const int tid = threadIdx.x;
+    auto sld = [&](const double *base, size_t ps, int e) {
+        T v;
+#pragma unroll
+        for (int w = 0; w < W; w++) EA::set_word(v, w, base[w * ps + e]);
+        return v;
+    };
+    auto sst = [&](double *base, size_t ps, int e, const T &v) {
+#pragma unroll
+        for (int w = 0; w < W; w++) base[w * ps + e] = EA::word(v, w);
+    };
+    const int per = hm * hn;
+    for (int64_t b = blockIdx.x; b < P; b += gridDim.x) {
+        const double *xb = X.p + b * X.bs, *yb = Y.p + b * Y.bs;
+        // 1. the 7 children of each side, read from the parent (4 quadrant values, zero outside)
+        for (int e = tid; e < hm * hl; e += kFusedNT) {
+            const int i = e / hl, k = e % hl;
+            const bool r2 = i + hm < X.rows, c2 = k + hl < X.cols;
+            const T x11 = ld_or_zero<W>(xb + i * X.ld + k, X.ps, true);
+            const T x12 = ld_or_zero<W>(xb + i * X.ld + k + hl, X.ps, c2);
+            const T x21 = ld_or_zero<W>(xb + (i + hm) * X.ld + k, X.ps, r2);
+            const T x22 = ld_or_zero<W>(xb + (i + hm) * X.ld + k + hl, X.ps, r2 && c2);
+            T o[7];
+            pre_ops<EA, ALGO, 0>(x11, x12, x21, x22, o);
+#pragma unroll
+            for (int c = 0; c < 7; c++) sst(CA + (size_t)c * W * psa, psa, e, o[c]);
+        }
+        for (int e = tid; e < hl * hn; e += kFusedNT) {
+            const int k = e / hn, j = e % hn;
+            const bool r2 = k + hl < Y.rows, c2 = j + hn < Y.cols;
+            const T y11 = ld_or_zero<W>(yb + k * Y.ld + j, Y.ps, true);
+            const T y12 = ld_or_zero<W>(yb + k * Y.ld + j + hn, Y.ps, c2);
+            const T y21 = ld_or_zero<W>(yb + (k + hl) * Y.ld + j, Y.ps, r2);
+            const T y22 = ld_or_zero<W>(yb + (k + hl) * Y.ld + j + hn, Y.ps, r2 && c2);
+            T o[7];
+            pre_ops<EA, ALGO, 1>(y11, y12, y21, y22, o);
+#pragma unroll
+            for (int c = 0; c < 7; c++) sst(CB + (size_t)c * W * psb, psb, e, o[c]);
+        }
+        __syncthreads();
+        // 2. per position: the 7 products (independent chains), then the post-additions. A
+        // thread owns RP positions of one row (i, j .. j+RP-1), so each A value it loads feeds RP
+        // chains (shared-memory loads per madd: (1 + RP) / RP words instead of 2)
+        double *cb = C.p + b * C.bs;
+        constexpr int RP = W == 2 ? 2 : 1;
+        const int hnb = (hn + RP - 1) / RP;
+        auto post_put = [&](int i, int j, const T pv[7]) {
+            T c11, c12, c21, c22;
+            post_ops<EA, ALGO>(pv, c11, c12, c21, c22);
+            const bool r2 = i + hm < C.rows, cc2 = j + hn < C.cols;
+            auto put = [&](int64_t r, int64_t c, const T &v) {
+                double *q = cb + r * C.ld + c;
+                if (beta) EA::store(q, C.ps, EA::sub(EA::load(q, C.ps), v));
+                else EA::store(q, C.ps, v);
+            };
+            if (i < C.rows && j < C.cols) put(i, j, c11);
+            if (i < C.rows && cc2) put(i, j + hn, c12);
+            if (r2 && j < C.cols) put(i + hm, j, c21);
+            if (r2 && cc2) put(i + hm, j + hn, c22);
+        };
+        for (int e = tid; e < hm * hnb; e += kFusedNT) {
+            const int i = e / hnb, j0 = (e % hnb) * RP;
+            T pv[RP][7];
+#pragma unroll
+            for (int r = 0; r < RP; r++)
+#pragma unroll
+                for (int c = 0; c < 7; c++) pv[r][c] = EM::zero();
+            for (int k = 0; k < hl; k++) {
+#pragma unroll
+                for (int c = 0; c < 7; c++) {
+                    const T a = sld(CA + (size_t)c * W * psa, psa, i * hl + k);
+#pragma unroll
+                    for (int r = 0; r < RP; r++) {
+                        const int jj = j0 + r < hn ? j0 + r : j0;   // (a duplicate, never stored)
+                        pv[r][c] = EM::madd(pv[r][c], a, sld(CB + (size_t)c * W * psb, psb, k * hn + jj));
+                    }
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < RP; r++)
+                if (j0 + r < hn) post_put(i, j0 + r, pv[r]);
+        }
+        __syncthreads();   // the children buffers are reused by the next parent
+    }
+}
+
+// shared memory a fused last level needs (bytes), or 0 when the leaves are too large for it
+size_t fused_last_smem(int W, int64_t hm, int64_t hl, int64_t hn) {
+    if (hm < 1 || hl < 1 || hn < 1 || hm > 32 || hl > 32 || hn > 32) return 0;
+    const size_t b = sizeof(double) * fused_last_smem_doubles(W, (int)hm, (int)hl, (int)hn);
+    return b <= 220 * 1024 ? b : 0;
+}
+
+template <int W, int ALGO, int VA, int MV>
+static int fused_last_go(int64_t P, const MatDesc &X, const MatDesc &Y, const MatDesc &C, int beta, FusedLastDims dd,
+                         size_t smem, cudaStream_t s) {
+    auto kern = fused_last_kernel<W, ALGO, VA, MV>;
+    static bool attr[64] = {};
+    if (!attr[current_device()]) {
+        DDQD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        attr[current_device()] = true;
+    }
+    const int64_t per_sm = (int64_t)((228 * 1024) / (smem + 1024));
+    const int64_t cap = (per_sm < 1 ? 1 : per_sm) * 8 * sm_count();
+    const int64_t blocks = P < cap ? P : cap;
+    prof_begin(0, s);
+    kern<<<(unsigned)blocks, kFusedNT, smem, s>>>(P, X, Y, C, beta, dd);
+    DDQD_LAUNCH_CHECK();
+    prof_end(0, 7.0 * dd.hm * (double)dd.hl * dd.hn * (double)P, s, "fused_last_kernel (pre-add + leaves + post-add)");
+    return DDQD_OK;
+}
+
+// P parents X (A side), Y (B side) -> parents C, one recursion level + its leaves in one kernel.
+// mv: the leaf's arithmetic variant (0 canonical, 1 fused madd, 2 accurate adds everywhere).
+int launch_fused_last(int W, int algo, int mv, int64_t P, const MatDesc &X, const MatDesc &Y, const MatDesc &C,
+                      int beta, int64_t hm, int64_t hl, int64_t hn, cudaStream_t s) {
+    const size_t smem = fused_last_smem(W, hm, hl, hn);
+    if (!smem) { set_error("fused last level: leaves too large"); return DDQD_EINVAL; }
+    if (P == 0) return DDQD_OK;
+    const FusedLastDims dd{(int)hm, (int)hl, (int)hn};
+    algo &= 0xff;
+#define FL_GO(WW, AL, VA, MV) return fused_last_go<WW, AL, VA, MV>(P, X, Y, C, beta, dd, smem, s)
+    if (W == 2) {
+        if (algo == 1) { if (mv == 1) FL_GO(2, 1, 0, 1); if (mv == 2) FL_GO(2, 1, 2, 2); FL_GO(2, 1, 0, 0); }
+        if (mv == 1) FL_GO(2, 2, 0, 1);
+        if (mv == 2) FL_GO(2, 2, 2, 2);
+        FL_GO(2, 2, 0, 0);
+    }
+    if (algo == 1) { if (mv == 1) FL_GO(4, 1, 0, 1); if (mv == 2) FL_GO(4, 1, 2, 2); FL_GO(4, 1, 0, 0); }
+    if (mv == 1) FL_GO(4, 2, 0, 1);
+    if (mv == 2) FL_GO(4, 2, 2, 2);
+    FL_GO(4, 2, 0, 0);
+#undef FL_GO
+}
+
 }  // namespace ddqd

@@ -79,6 +79,10 @@ int launch_post_quad(int W, int algo, int q, const MatDesc &M, const MatDesc &C,
 int launch_post_add_ptrs(int W, int algo, int64_t P, const double *const *ch, int64_t hm, int64_t hn,
                          int64_t ld, int64_t ps, int64_t r0, int64_t r1, const MatDesc &C, int beta,
                          cudaStream_t s);
+// The last recursion level fused with its (tiny) leaves (addsub.cu): P parents -> parents C.
+size_t fused_last_smem(int W, int64_t hm, int64_t hl, int64_t hn);   // 0: leaves too large
+int launch_fused_last(int W, int algo, int mv, int64_t P, const MatDesc &X, const MatDesc &Y, const MatDesc &C,
+                      int beta, int64_t hm, int64_t hl, int64_t hn, cudaStream_t s);
 // Band pack (dir 0) / unpack (dir 1) through row / column index maps (band.cu).
 int launch_band_copy(int W, int dir, int64_t rows, int64_t cols, const int64_t *rmap, const int64_t *cmap,
                      const MatDesc &full, const MatDesc &compact, cudaStream_t s);

@@ -29,6 +29,7 @@ size_t workspace_limit();                          // abi.cu
 struct Plan {
     int W = 2, algo = 0, d = 0, s = 0, mv = 0;
     int fd = -1;                        // DDQD_DEPTH(fd): recurse exactly fd levels (T unused)
+    bool fuse_last = false;             // level d-1 runs fused with its leaves (fused_last_kernel)
     int64_t T = 1;
     std::vector<int64_t> m, l, n;       // level shapes, 0..d
     std::vector<int64_t> chunk;         // parents per chunk at level j (j < d)
@@ -205,7 +206,10 @@ static int exec_level(const Plan &p, char *ws, int j, int64_t cnt, const MatDesc
 static int exec_chunk(const Plan &p, char *ws, int j, int64_t p0, int64_t pc, const MatDesc &A,
                       const MatDesc &B, const MatDesc &C, int beta, cudaStream_t s, int lane) {
     const int var = p.mv & 0xf;
-    const bool two = fuse2_enabled() && p.W == 2 && var != 2 && j + 2 <= p.d && ((p.d - j) % 2 == 0);
+    // two-level passes are paired from the last materialised level up (d, or d-1 when the last
+    // level is fused with the leaves)
+    const int de = p.fuse_last ? p.d - 1 : p.d;
+    const bool two = fuse2_enabled() && p.W == 2 && var != 2 && j + 2 <= de && ((de - j) % 2 == 0);
     const int add_algo = p.algo | (var == 2 ? DDQD_ADD_ACCURATE : 0);   // the additions' variant
     int rc;
     if (two && p.chunk[j + 1] >= 7 * pc) {
@@ -227,6 +231,15 @@ static int exec_chunk(const Plan &p, char *ws, int j, int64_t p0, int64_t pc, co
     return launch_post_add(p.W, add_algo, pc, cM, shift(C, p0), beta, s);
 }
 
+static bool fuse_last_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("DDQD_FUSE_LAST");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
 static const char *kLevelNames[] = {"level 0", "level 1", "level 2", "level 3", "level 4", "level 5",
                                      "level 6", "level 7", "level 8+"};
 
@@ -235,6 +248,11 @@ static int exec_level(const Plan &p, char *ws, int j, int64_t cnt, const MatDesc
     if (j == p.d) {
         NvtxRange nv("leaf GEMM");
         return launch_leaf_gemm(p.W, p.m[j], p.l[j], p.n[j], cnt, A, B, C, beta, p.mv, s);
+    }
+    if (p.fuse_last && j == p.d - 1) {
+        NvtxRange nv("last level fused with its leaves");
+        const int add_algo = p.algo | ((p.mv & 0xf) == 2 ? DDQD_ADD_ACCURATE : 0);
+        return launch_fused_last(p.W, add_algo, p.mv & 0xf, cnt, A, B, C, beta, p.m[p.d], p.l[p.d], p.n[p.d], s);
     }
     NvtxRange nv(kLevelNames[j < 8 ? j : 8]);
     const int64_t nch = (cnt + p.chunk[j] - 1) / p.chunk[j];
@@ -273,6 +291,12 @@ int run_gemm(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n, int64_
     if (rc) return rc;
     p.mv = mv;
     if (p.d == 0) return launch_leaf_gemm(W, m, l, n, batch, A, B, C, beta, mv, s);
+    // tiny leaves (<= 32 per side, e.g. Strassen(32) at n = 1025): the last level and its leaves
+    // as one kernel, when its shared-memory footprint fits; DDQD_FUSE_LAST=0 disables it
+    // (DD only: the QD version, 200-instruction madds x 7 chains at one 160-thread CTA per SM,
+    // measured 15.5 vs 11.0 ms on QD Strassen(32) at n = 1025)
+    p.fuse_last = fuse_last_enabled() && W == 2 && ((mv >> 4) & 3) == 0 &&
+                  fused_last_smem(W, p.m[p.d], p.l[p.d], p.n[p.d]) > 0;
     int st = DDQD_OK;
     char *ws = static_cast<char *>(workspace_get(p.bytes, &st));
     if (st) return st;

@@ -1191,3 +1191,30 @@ def test_graph_capture_workspace_rules(orc):
     torch.cuda.synchronize()
     assert same(np_(C), orc.gemm(A, B, "strassen", threshold=32))
     assert same(np_(big), orc.gemm(A2, B2, "strassen", threshold=32))
+
+
+def test_fused_last_level_same_bits(tmp_path, orc):
+    """The last recursion level fused with its tiny leaves (fused_last_kernel) gives the bits of
+    the unfused schedule (DDQD_FUSE_LAST=0), DD and QD, Strassen and Winograd, canonical and
+    the fused/accurate variants, and matches the oracle on a small case."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, ddqd_inputs as gen, paper_1510_08642_b200 as d\n"
+        "out = []\n"
+        "for W, n, T in ((2, 1025, 32), (4, 517, 16), (2, 99, 6), (4, 70, 5)):\n"
+        "    A, B = gen.bench_pair(n, W) if n > 500 else (gen.matrix(W, n, n - 3, 61, 0), gen.matrix(W, n - 3, n + 2, 61, 1))\n"
+        "    for algo in ('strassen', 'winograd'):\n"
+        "        for madd in ('canonical', 'fused', 'accurate'):\n"
+        "            out.append(d.gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), algo, T, madd=madd).cpu().numpy().ravel())\n"
+        "np.save(r'%s', np.concatenate(out))\n")
+    outs = []
+    for mode in ("0", "1"):
+        f = tmp_path / f"f{mode}.npy"
+        env = dict(os.environ, DDQD_FUSE_LAST=mode)
+        subprocess.check_call([sys.executable, "-c", code % f], env=env, cwd=ROOT)
+        outs.append(np.load(f))
+    assert same(outs[0], outs[1])
+    A, B = gen.matrix(2, 99, 96, 61, 0), gen.matrix(2, 96, 101, 61, 1)
+    for algo in ("strassen", "winograd"):
+        assert same(np_(ddqd.gemm(cu(A), cu(B), algo, 6)), orc.gemm(A, B, algo, threshold=6))
