@@ -1000,6 +1000,28 @@ __global__ void __launch_bounds__(1024) lu_perm_kernel(const double *b, double *
         for (int64_t i = threadIdx.x; i < (int64_t)W * n; i += blockDim.x) y[i] = sy[i];
 }
 
+// The swaps of one panel, [p, p+kb), applied in order to y (the forward solve run panel by
+// panel, alongside the factorisation): one warp, only the actual interchanges visited.
+__global__ void __launch_bounds__(32) lu_yswap_kernel(double *y, const int64_t *ipiv, int W, int64_t n, int64_t p,
+                                                      int64_t kb) {
+    const int lane = threadIdx.x;
+    for (int64_t k0 = p; k0 < p + kb; k0 += 32) {
+        const int64_t k = k0 + lane;
+        const int64_t r_l = k < p + kb ? ipiv[k] : k;
+        unsigned mask = __ballot_sync(0xffffffffu, r_l != k);
+        while (mask) {
+            const int j = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const int64_t kk = k0 + j, r = __shfl_sync(0xffffffffu, r_l, j);
+            if (lane < W) {
+                const double t = y[lane * n + kk];
+                y[lane * n + kk] = y[lane * n + r];
+                y[lane * n + r] = t;
+            }
+        }
+    }
+}
+
 // y vectors: planar [W][n]
 template <int W>
 __device__ __forceinline__ typename elem<W>::T ldv(const double *y, int64_t n, int64_t i) {
@@ -1337,7 +1359,7 @@ static int spec_mode() {
 // returns 1 if the cooperative path was launched, 0 if the caller should use the per-column path
 template <int W>
 static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot, int64_t *ipiv, LuAux *aux,
-                          double *scr, size_t scr_bytes, cudaStream_t s, int *rc) {
+                          double *scr, size_t scr_bytes, cudaStream_t s, int *rc, cudaEvent_t pre_swap) {
     *rc = DDQD_OK;
     const int64_t R = n - p;
     const int dv = current_device();
@@ -1395,6 +1417,9 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
         return 1;
     }
     if (pivot && n - kb > 0) {
+        // the interchanges move rows of the earlier panels' L columns: a reader of those (the
+        // panel-by-panel forward solve on another stream) must be done with them first
+        if (pre_swap) DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, pre_swap, 0));
         const int64_t threads = (int64_t)W * (n - kb);
         lu_laswp_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(A, W, n, p, kb, ipiv);
         count_launch();
@@ -1423,12 +1448,16 @@ static int trsm_mode() {
 // the per-column pair), interchanges of the other columns, U12 := L11^{-1} A12.
 template <int W>
 static int lu_panel_w(int64_t n, int pivot, double *A, int64_t *ipiv, int64_t p, int64_t kb, LuAux *aux,
-                      double *scr, size_t scr_bytes, cudaStream_t s) {
+                      double *scr, size_t scr_bytes, cudaStream_t s, cudaEvent_t pre_swap = nullptr) {
     NvtxRange nv("LU panel + TRSM");
     prof_begin(3, s);
     int crc = DDQD_OK;
-    const bool coop = use_coop_panel() && try_panel_coop<W>(A, n, p, kb, pivot, ipiv, aux, scr, scr_bytes, s, &crc);
+    // the per-column kernels swap whole rows as they go: order them after the reader up front
+    if (pre_swap && !use_coop_panel()) DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, pre_swap, 0));
+    const bool coop = use_coop_panel() && try_panel_coop<W>(A, n, p, kb, pivot, ipiv, aux, scr, scr_bytes, s, &crc,
+                                                            pre_swap);
     if (crc) return crc;
+    if (!coop && pre_swap && use_coop_panel()) DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, pre_swap, 0));
     for (int64_t k = p; !coop && k < p + kb; k++) {
         lu_pivot_kernel<W><<<1, 1024, 0, s>>>(A, n, k, pivot, ipiv, aux);
         DDQD_LAUNCH_CHECK();
@@ -1497,47 +1526,47 @@ static bool trsv_fast_enabled() {
     return v == 1;
 }
 
-// Eq. (2) with the factors: y := P b, forward (unit L), backward (numerics.md s.5).
+// shared-memory sizes / attributes of the solve kernels (set once per device)
 template <int W>
-static int lu_trsv_w(int64_t n, const double *A, const int64_t *ipiv, const double *b, double *x, double *y,
-                     cudaStream_t s) {
-    NvtxRange nv("LU solves");
-    const int use_smem = ((int64_t)W * n * (int64_t)sizeof(double) <= 200 * 1024) ? 1 : 0;
-    const size_t psmem = use_smem ? (size_t)W * n * sizeof(double) : 0;
-    if (psmem > 48 * 1024)
-        DDQD_CUDA_CHECK(cudaFuncSetAttribute(lu_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)psmem));
-    prof_begin(5, s);
-    lu_perm_kernel<<<1, 1024, psmem, s>>>(b, y, ipiv, W, n, use_smem);
-    DDQD_LAUNCH_CHECK();
-    const int NB = 256;
-    const bool fast = trsv_fast_enabled();
+static int trsv_setup(size_t *usm_out) {
     const size_t usm = sizeof(double) * W * (256 + 2 * (size_t)TuCc<W>::v * TU_LD);
     static bool tattr[64] = {};
-    if (fast && !tattr[current_device()]) {
+    if (trsv_fast_enabled() && !tattr[current_device()]) {
         DDQD_CUDA_CHECK(cudaFuncSetAttribute(trsv_update_co<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
         DDQD_CUDA_CHECK(cudaFuncSetAttribute(trsv_update_co<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
         tattr[current_device()] = true;
     }
-    for (int64_t J = 0; J < n; J += NB) {
-        const int nb = (int)std::min<int64_t>(NB, n - J);
-        const int64_t rows = n - J - nb;
-        if (fast && nb % 32 == 0) {
-            trsv_diag_blk<W, true><<<1, W == 2 ? 288 : 256, 0, s>>>(A, n, y, nullptr, J, nb);
-            DDQD_LAUNCH_CHECK();
-            if (rows > 0) {
-                trsv_update_co<W, true><<<(unsigned)((rows + TU_ROWS - 1) / TU_ROWS), TU_ROWS, usm, s>>>(A, n, y, nullptr, J, nb);
-                DDQD_LAUNCH_CHECK();
-            }
-            continue;
-        }
-        trsv_fwd_diag<W><<<1, 256, 0, s>>>(A, n, y, J, nb);
+    *usm_out = usm;
+    return DDQD_OK;
+}
+
+// forward (unit L) for the diagonal block [J, J+nb) and the fold of its columns into rows >= J+nb
+template <int W>
+static int trsv_fwd_block(int64_t n, const double *A, double *y, int64_t J, int nb, size_t usm, cudaStream_t s) {
+    const int64_t rows = n - J - nb;
+    if (trsv_fast_enabled() && nb % 32 == 0) {
+        trsv_diag_blk<W, true><<<1, W == 2 ? 288 : 256, 0, s>>>(A, n, y, nullptr, J, nb);
         DDQD_LAUNCH_CHECK();
         if (rows > 0) {
-            trsv_fwd_update<W><<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(A, n, y, J, nb);
+            trsv_update_co<W, true><<<(unsigned)((rows + TU_ROWS - 1) / TU_ROWS), TU_ROWS, usm, s>>>(A, n, y, nullptr, J, nb);
             DDQD_LAUNCH_CHECK();
         }
+        return DDQD_OK;
     }
+    trsv_fwd_diag<W><<<1, 256, 0, s>>>(A, n, y, J, nb);
+    DDQD_LAUNCH_CHECK();
+    if (rows > 0) {
+        trsv_fwd_update<W><<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(A, n, y, J, nb);
+        DDQD_LAUNCH_CHECK();
+    }
+    return DDQD_OK;
+}
+
+// backward (upper, x_j = div(y_j, u_jj)), 256-row blocks from the bottom
+template <int W>
+static int trsv_bwd_all(int64_t n, const double *A, double *y, double *x, size_t usm, cudaStream_t s) {
+    const int NB = 256;
+    const bool fast = trsv_fast_enabled();
     const int64_t last = ((n - 1) / NB) * NB;
     for (int64_t J = last; J >= 0; J -= NB) {
         const int nb = (int)std::min<int64_t>(NB, n - J);
@@ -1557,6 +1586,29 @@ static int lu_trsv_w(int64_t n, const double *A, const int64_t *ipiv, const doub
             DDQD_LAUNCH_CHECK();
         }
     }
+    return DDQD_OK;
+}
+
+// Eq. (2) with the factors: y := P b, forward (unit L), backward (numerics.md s.5).
+template <int W>
+static int lu_trsv_w(int64_t n, const double *A, const int64_t *ipiv, const double *b, double *x, double *y,
+                     cudaStream_t s) {
+    NvtxRange nv("LU solves");
+    const int use_smem = ((int64_t)W * n * (int64_t)sizeof(double) <= 200 * 1024) ? 1 : 0;
+    const size_t psmem = use_smem ? (size_t)W * n * sizeof(double) : 0;
+    if (psmem > 48 * 1024)
+        DDQD_CUDA_CHECK(cudaFuncSetAttribute(lu_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)psmem));
+    size_t usm = 0;
+    int rc = trsv_setup<W>(&usm);
+    if (rc) return rc;
+    prof_begin(5, s);
+    lu_perm_kernel<<<1, 1024, psmem, s>>>(b, y, ipiv, W, n, use_smem);
+    DDQD_LAUNCH_CHECK();
+    const int NB = 256;
+    for (int64_t J = 0; J < n; J += NB)
+        if ((rc = trsv_fwd_block<W>(n, A, y, J, (int)std::min<int64_t>(NB, n - J), usm, s))) return rc;
+    if ((rc = trsv_bwd_all<W>(n, A, y, x, usm, s))) return rc;
     prof_end(5, (double)n * (double)n, s, "lu solves (perm, trsv_diag_blk, trsv_update_co)");
     return DDQD_OK;
 }
@@ -1582,6 +1634,34 @@ static int lu_mem(int W, int64_t n, int64_t K, LuMem *m) {
     return DDQD_OK;
 }
 
+// side stream + events of the LU's panel-by-panel forward solve, per host thread and device
+struct LuSide {
+    cudaStream_t ss = nullptr;
+    cudaEvent_t start = nullptr, panel = nullptr, done = nullptr;
+};
+static int lu_side(LuSide **out) {
+    static thread_local LuSide res[64];
+    LuSide &r = res[current_device()];
+    if (!r.ss) {
+        DDQD_CUDA_CHECK(cudaStreamCreateWithFlags(&r.ss, cudaStreamNonBlocking));
+        DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.start, cudaEventDisableTiming));
+        DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.panel, cudaEventDisableTiming));
+        DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming));
+    }
+    *out = &r;
+    return DDQD_OK;
+}
+
+// DDQD_LU_FWD_OVERLAP=0 keeps the forward solve after the factorisation (A/B measurements)
+static bool fwd_overlap_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_LU_FWD_OVERLAP");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 template <int W>
 static int lu_solve_w(int64_t n, int pivot, double *A, const double *b, double *x, int64_t *ipiv, int64_t K,
                       int algo, int64_t T, cudaStream_t s, int *info_out) {
@@ -1591,9 +1671,40 @@ static int lu_solve_w(int64_t n, int pivot, double *A, const double *b, double *
     int rc = lu_mem(W, n, K, &mem);
     if (rc) return rc;
     DDQD_CUDA_CHECK(cudaMemsetAsync(mem.aux, 0, sizeof(LuAux), s));
+    size_t usm = 0;
+    if ((rc = trsv_setup<W>(&usm))) return rc;
+    // The forward solve y := L^{-1} P b runs panel by panel on a side stream, each panel's part
+    // (its interchanges applied to y, its diagonal block, the fold of its L21 columns into the rows
+    // below) right after the panel is factored, alongside the Schur update -- b is the extra
+    // column of a right-looking LU. Every y element still receives l_ij y_j for j ascending with
+    // the same operands (its row and its L row move together under the later interchanges),
+    // so the bits are those of the solve after the factorisation. The next panel's interchanges
+    // wait for the side stream's reads of the L columns they move. Not under stream capture.
+    LuSide *sd = nullptr;
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cst) != cudaSuccess) { cudaGetLastError(); cst = cudaStreamCaptureStatusActive; }
+    const bool overlap = fwd_overlap_enabled() && cst == cudaStreamCaptureStatusNone && !lu_side(&sd);
+    if (overlap) {
+        DDQD_CUDA_CHECK(cudaMemcpyAsync(mem.y, b, sizeof(double) * W * (size_t)n, cudaMemcpyDeviceToDevice, s));
+        DDQD_CUDA_CHECK(cudaEventRecord(sd->start, s));
+        DDQD_CUDA_CHECK(cudaStreamWaitEvent(sd->ss, sd->start, 0));
+    }
+    bool side_pending = false;
     for (int64_t p = 0; p < n; p += K) {
         const int64_t kb = std::min(K, n - p);
-        if ((rc = lu_panel_w<W>(n, pivot, A, ipiv, p, kb, mem.aux, mem.scr, mem.scr_bytes, s))) return rc;
+        if ((rc = lu_panel_w<W>(n, pivot, A, ipiv, p, kb, mem.aux, mem.scr, mem.scr_bytes, s,
+                                side_pending ? sd->done : nullptr))) return rc;
+        if (overlap) {
+            DDQD_CUDA_CHECK(cudaEventRecord(sd->panel, s));
+            DDQD_CUDA_CHECK(cudaStreamWaitEvent(sd->ss, sd->panel, 0));
+            if (pivot) {
+                lu_yswap_kernel<<<1, 32, 0, sd->ss>>>(mem.y, ipiv, W, n, p, kb);
+                DDQD_LAUNCH_CHECK();
+            }
+            if ((rc = trsv_fwd_block<W>(n, A, mem.y, p, (int)kb, usm, sd->ss))) return rc;
+            DDQD_CUDA_CHECK(cudaEventRecord(sd->done, sd->ss));
+            side_pending = true;
+        }
         const int64_t n2 = n - p - kb;
         if (n2 <= 0) continue;
         MatDesc L21{A + (p + kb) * n + p, n2, kb, n, n * n, 0};
@@ -1601,7 +1712,14 @@ static int lu_solve_w(int64_t n, int pivot, double *A, const double *b, double *
         MatDesc A22{A + (p + kb) * n + (p + kb), n2, n2, n, n * n, 0};
         if ((rc = run_gemm(W, algo, T, n2, kb, n2, 1, L21, U12, A22, 1, s))) return rc;
     }
-    if ((rc = lu_trsv_w<W>(n, A, ipiv, b, x, mem.y, s))) return rc;
+    if (overlap) {
+        DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, sd->done, 0));
+        prof_begin(5, s);
+        if ((rc = trsv_bwd_all<W>(n, A, mem.y, x, usm, s))) return rc;
+        prof_end(5, (double)n * (double)n / 2.0, s, "lu backward solve (trsv_diag_blk, trsv_update_co)");
+    } else if ((rc = lu_trsv_w<W>(n, A, ipiv, b, x, mem.y, s))) {
+        return rc;
+    }
     int info_h = 0;
     DDQD_CUDA_CHECK(cudaMemcpyAsync(&info_h, &mem.aux->info, sizeof(int), cudaMemcpyDeviceToHost, s));
     DDQD_CUDA_CHECK(cudaStreamSynchronize(s));
