@@ -33,6 +33,13 @@ namespace ddqd {
 // (Every warp merging all candidates itself instead of one pass per CTA made the hot spot 8x
 // worse: 82.5 ms.)
 constexpr int kLuCrep = LU_CREP;
+// replicas of the published pivot row in the speculated-pivot panel (CTA b reads replica b % R).
+// Measured on c4 (ms per solve): R = 1 41.98, 4 42.22, 8 42.99, 16 44.70 -- the owner's extra
+// stores cost more than the spread reads gain, so one copy.
+#ifndef LU_RREP
+#define LU_RREP 1
+#endif
+constexpr int kLuRrep = LU_RREP;
 
 void *aux_get(size_t bytes, int *status);   // abi.cu (separate from the GEMM workspace)
 
@@ -246,9 +253,9 @@ __global__ void __launch_bounds__(512) lu_panel_coop_kernel(double *A, int64_t n
         // scales and rank-1-updates its rows while the barrier completes. Step k's verification
         // flags are read after barrier k+2 (raised before the detector arrives there), so every
         // CTA breaks at the same step. The fallback reloads the slab in the block layout below.
-        // fscr: [2][W][kb + 1] pivot rows (+ reciprocal in slot kb) | flags [kb] | counter
+        // fscr: [2][R][W][kb + 1] pivot rows (+ reciprocal in slot kb) | flags [kb] | counter
         const int RS = kb + 1;
-        int *flag = reinterpret_cast<int *>(fscr + (size_t)2 * W * RS);
+        int *flag = reinterpret_cast<int *>(fscr + (size_t)2 * kLuRrep * W * RS);
         unsigned *ctr = reinterpret_cast<unsigned *>(flag + kb);
         const int64_t R = n - p;
         const int b = blockIdx.x;
@@ -259,14 +266,19 @@ __global__ void __launch_bounds__(512) lu_panel_coop_kernel(double *A, int64_t n
             sts<W>(S, SS, e, ldA<W>(A, n, grow(li), p + j));
         }
         auto publish = [&](int kk1, int li) {
-            // (warp 0) row p+kk1, local row li, and its reciprocal -> the pivot-row buffer
-            double *kr = fscr + (size_t)(kk1 & 1) * W * RS;
-            for (int j = tid; j < kb; j += 32)
-                for (int w = 0; w < W; w++) kr[(size_t)w * RS + j] = S[w * SS + li * kb + j];
+            // (warp 0) row p+kk1, local row li, and its reciprocal -> every replica of the
+            // pivot-row buffer (columns < kk1 are never read)
+            double *kr = fscr + (size_t)(kk1 & 1) * kLuRrep * W * RS;
+            for (int j = kk1 + tid; j < kb; j += 32)
+                for (int w = 0; w < W; w++) {
+                    const double v = S[w * SS + li * kb + j];
+                    for (int q = 0; q < kLuRrep; q++) kr[((size_t)q * W + w) * RS + j] = v;
+                }
             if (tid == 0) {
                 const T d = lds<W>(S, SS, li * kb + kk1);
                 const T rv2 = (E::word(d, 0) == 0.0) ? E::zero() : E::div(E::one(), d);
-                for (int w = 0; w < W; w++) kr[(size_t)w * RS + kb] = E::word(rv2, w);
+                for (int q = 0; q < kLuRrep; q++)
+                    for (int w = 0; w < W; w++) kr[((size_t)q * W + w) * RS + kb] = E::word(rv2, w);
             }
         };
         if (blockIdx.x == 0) {
@@ -296,8 +308,8 @@ __global__ void __launch_bounds__(512) lu_panel_coop_kernel(double *A, int64_t n
             __syncthreads();
             qmark(0);
             if (pivot && kk >= 2 && __ldcg(flag + kk - 2)) { failed = true; break; }
-            const double *kr = fscr + (size_t)(kk & 1) * W * RS;
-            for (int j = tid; j < kb; j += blockDim.x)
+            const double *kr = fscr + ((size_t)(kk & 1) * kLuRrep + (b % kLuRrep)) * W * RS;
+            for (int j = kk + tid; j < kb; j += blockDim.x)   // columns < kk are never read
                 for (int w = 0; w < W; w++) U[w * kb + j] = __ldcg(kr + (size_t)w * RS + j);
             if (tid < W) s_rinv[tid] = __ldcg(kr + (size_t)tid * RS + kb);
             __syncthreads();
@@ -317,18 +329,21 @@ __global__ void __launch_bounds__(512) lu_panel_coop_kernel(double *A, int64_t n
             // the fetch) -- after publishing row k+1 when this CTA owns it; the other warps go
             // straight on to the scaling and the update. The release fence orders this CTA's
             // reads of row k, its flags of step kk-1 and the published row before the arrival.
-            auto arrive = [&]() {
+            // Only the owner's arrival publishes data (row k+1), so only it needs the release
+            // fence; the others signal "row k has been read" (their loads have returned), and a
+            // raised flag carries its own fence where it is raised (the rare miss path).
+            auto arrive = [&](bool release) {
                 __syncwarp();
                 if (tid == 0) {
-                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    if (release) asm volatile("fence.acq_rel.gpu;" ::: "memory");
                     atomicAdd(ctr, 1u);
                 }
             };
-            if (tid < 32 && li1 < 0) arrive();
+            if (tid < 32 && li1 < 0) arrive(false);
             if (li1 >= 0 && tid < 32) {
                 const T a = lds<W>(S, SS, li1 * kb + kk);
                 if (!skip) {
-                    if (pivot && tid == 0 && E::abs_gt(a, akk)) flag[kk] = 1;
+                    if (pivot && tid == 0 && E::abs_gt(a, akk)) { flag[kk] = 1; __threadfence(); }
                     const T lv = E::mul(a, rinv);
                     for (int j = kk + 1 + tid; j < kb; j += 32)
                         sts<W>(S, SS, li1 * kb + j, E::sub(lds<W>(S, SS, li1 * kb + j), E::mul(lv, lds<W>(U, kb, j))));
@@ -339,18 +354,20 @@ __global__ void __launch_bounds__(512) lu_panel_coop_kernel(double *A, int64_t n
                     flag[kk] = 1;
                 }
                 publish(kk + 1, li1);
-                arrive();
+                arrive(true);
             }
             qmark(2);
             bool bigger = false;
+            // the scaling starts at warp 1, so warp 0's arrival / owner work runs beside it
+            const int ts = (tid + (int)blockDim.x - 32) % (int)blockDim.x;
             if (skip) {
                 if (pivot)
-                    for (int li = li0 + tid; li < cr; li += blockDim.x)
+                    for (int li = li0 + ts; li < cr; li += blockDim.x)
                         if (li != li1 && E::abs_gt(lds<W>(S, SS, li * kb + kk), akk)) bigger = true;
-                if (bigger) flag[kk] = 1;
+                if (bigger) { flag[kk] = 1; __threadfence(); }
                 continue;
             }
-            for (int li = li0 + tid; li < cr; li += blockDim.x) {
+            for (int li = li0 + ts; li < cr; li += blockDim.x) {
                 if (li == li1) continue;
                 const T a = lds<W>(S, SS, li * kb + kk);
                 if (pivot && E::abs_gt(a, akk)) bigger = true;
@@ -358,7 +375,7 @@ __global__ void __launch_bounds__(512) lu_panel_coop_kernel(double *A, int64_t n
                 sts<W>(S, SS, li * kb + kk, lv);
                 sts<W>(L, rows_per, li, lv);
             }
-            if (bigger) flag[kk] = 1;
+            if (bigger) { flag[kk] = 1; __threadfence(); }
             __syncthreads();
             qmark(3);
             {
@@ -1379,7 +1396,7 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
     const size_t smem = sizeof(double) * W * ((size_t)rows_per * kb + (size_t)kb + (size_t)rows_per);
     if (smem > 200 * 1024) return 0;
     const size_t per_buf = (size_t)G * (W + 1) * kLuCrep + (size_t)G * W * kb + (size_t)W * kb;
-    const size_t fast_bytes = sizeof(double) * (2 * (size_t)W * (kb + 1) + (size_t)kb + 2);   // rows + flags + counter
+    const size_t fast_bytes = sizeof(double) * (2 * (size_t)kLuRrep * W * (kb + 1) + (size_t)kb + 2);   // rows + flags + counter
     if (2 * per_buf * sizeof(double) + fast_bytes > scr_bytes) return 0;
     static size_t attr_dev[64];
     size_t &attr = attr_dev[dv];
@@ -1625,7 +1642,7 @@ static int lu_mem(int W, int64_t n, int64_t K, LuMem *m) {
     // two candidate buffers for up to one CTA per SM, plus the fast path's pivot rows and flags
     const size_t G = (size_t)std::max(sm_count(), 1);
     m->scr_bytes = sizeof(double) * (2 * (G * ((W + 1) * kLuCrep + W * (size_t)K) + W * (size_t)K) +
-                                     2 * (size_t)W * (K + 1) + (size_t)K + 2);
+                                     2 * (size_t)kLuRrep * W * (K + 1) + (size_t)K + 2);
     char *mem = static_cast<char *>(aux_get(256 + ybytes + m->scr_bytes, &st));
     if (st) return st;
     m->aux = reinterpret_cast<LuAux *>(mem);
