@@ -240,6 +240,8 @@ int try_leaf_tma(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &
                  const MatDesc &C, int beta, int mv, cudaStream_t s, int *rc);   // leaf_tma.cu
 int try_leaf_tma_qd(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A, const MatDesc &B,
                     const MatDesc &C, int beta, int mv, cudaStream_t s, int *rc);   // leaf_tma.cu
+int try_leaf_tma32_dd(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A, const MatDesc &B,
+                      const MatDesc &C, int beta, int mv, cudaStream_t s, int *rc);   // leaf_tma.cu
 
 // DDQD_LEAF_TMA=0 disables the TMA + mbarrier DD leaf (A/B comparisons); default on
 static bool tma_enabled() {
@@ -362,6 +364,7 @@ int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, cons
                 int rc = launch_leaf_one(W, m, l, n, b1, A, B, C, beta, mv, s);
                 if (rc) return rc;
                 const MatDesc A2 = shift_batch(A, b1), B2 = shift_batch(B, b1), C2 = shift_batch(C, b1);
+                if (tma_enabled() && try_leaf_tma32_dd(m, l, n, batch - b1, A2, B2, C2, beta, mv, s, &rc)) return rc;
                 if (mv == 1) return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2, 1>(m, l, n, batch - b1, A2, B2, C2, beta, s);
                 if (mv == 2) return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2, 2>(m, l, n, batch - b1, A2, B2, C2, beta, s);
                 return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2>(m, l, n, batch - b1, A2, B2, C2, beta, s);
@@ -463,6 +466,10 @@ static int launch_leaf_one(int W, int64_t m, int64_t l, int64_t n, int64_t batch
         const int64_t big_tiles = ((m + 63) / 64) * ((n + 63) / 64) * batch;
         if (big_tiles >= 2 * sm_count() && m > 32 && n > 32)   // tools/tune_leaf.py: BK = 8 x 4 stages is the fastest DD tile
             return launch_cfg<2, 64, 64, 8, 4, 4, 4, 2>(m, l, n, batch, A, B, C, beta, s);
+        {
+            int rc = DDQD_OK;
+            if (tma_enabled() && try_leaf_tma32_dd(m, l, n, batch, A, B, C, beta, mv, s, &rc)) return rc;
+        }
         return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2>(m, l, n, batch, A, B, C, beta, s);
     }
     if (W == 4) {

@@ -204,27 +204,31 @@ leaf_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
 }
 
-// ---- QD: the same pipeline with 4-plane boxes --------------------------------------------------
-// 32x32 CTA tile, 2x2 QD micro-tile per thread (256 threads), 16-deep k slabs in 3 stages, 2 CTAs
-// per SM -- the cp.async QD leaf's configuration. A arrives as [4][32 rows][18 k] (two columns
-// beyond the slab, zero or unused, so that the 144-byte row stride spreads a warp's four rows over
-// distinct banks), B as [4][16 k][32 cols]. Edge-tile entries outside C skip their madds, as in
-// the cp.async leaf (one renormalisation path per warp); same per-element order, same bits.
-namespace tmaq {
-constexpr int BM = 32, BN = 32, BK = 16, BKA = 18, TM = 2, TN = 2, S = 3, W = 4;
-constexpr int NT = (BM / TM) * (BN / TN);           // 256
-constexpr int A_STAGE = W * BM * BKA, B_STAGE = W * BK * BN;
-constexpr unsigned STAGE_BYTES = (unsigned)(sizeof(double) * (A_STAGE + B_STAGE));
-constexpr size_t SMEM = sizeof(double) * (size_t)S * (A_STAGE + B_STAGE) + 2 * S * sizeof(uint64_t) + 1024;
-}  // namespace tmaq
+// ---- 32x32 tiles: QD (4-plane boxes) and the DD tail --------------------------------------------
+// 32x32 CTA tile, 2x2 micro-tile per thread (256 threads), 16-deep k slabs in 3 stages -- the
+// cp.async 32x32 leaf's configuration (QD: 2 CTAs per SM; DD, the tail of a 64x64 batch and small
+// grids: 4). A arrives as [W][32 rows][18 k] (two columns beyond the slab, zero or unused, so that
+// the 144-byte row stride spreads a warp's four rows over distinct banks), B as [W][16 k][32
+// cols]. Edge-tile entries outside C skip their madds, as in the cp.async leaf (QD: one
+// renormalisation path per warp); same per-element order, same bits.
+template <int W_> struct Tq {
+    static constexpr int BM = 32, BN = 32, BK = 16, BKA = 18, TM = 2, TN = 2, S = 3, W = W_;
+    static constexpr int NT = (BM / TM) * (BN / TN);   // 256
+    static constexpr int A_STAGE = W * BM * BKA, B_STAGE = W * BK * BN;
+    static constexpr unsigned STAGE_BYTES = (unsigned)(sizeof(double) * (A_STAGE + B_STAGE));
+    static constexpr size_t SMEM = sizeof(double) * (size_t)S * (A_STAGE + B_STAGE) + 2 * S * sizeof(uint64_t) + 1024;
+};
 
-template <int MV>
-__global__ void __launch_bounds__(tmaq::NT, 2)
+template <int W, int MV>
+__global__ void __launch_bounds__(256, W == 2 ? 4 : 2)
 leaf_tma_qd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t m,
                    int64_t l, int64_t n, MatDesc C, int beta, int64_t batch0) {
-    using namespace tmaq;
-    using E = arith<4, MV>;
-    using T = qd;
+    using Q = Tq<W>;
+    constexpr int BM = Q::BM, BN = Q::BN, BK = Q::BK, BKA = Q::BKA, TM = Q::TM, TN = Q::TN, S = Q::S, NT = Q::NT;
+    constexpr int A_STAGE = Q::A_STAGE, B_STAGE = Q::B_STAGE;
+    constexpr unsigned STAGE_BYTES = Q::STAGE_BYTES;
+    using E = arith<W, MV>;
+    using T = typename E::T;
     extern __shared__ unsigned char smraw[];
     // 1024-byte aligned start, by an offset from the shared array itself (a cast through an integer
     // would drop the shared address space and turn every fragment read into a generic LD)
@@ -280,10 +284,10 @@ leaf_tma_qd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
 #pragma unroll
             for (int w = 0; w < W; w++) {
 #pragma unroll
-                for (int i = 0; i < TM; i++) a[i].w[w] = as[(w * BM + 2 * ty + i) * BKA + kk];
+                for (int i = 0; i < TM; i++) E::set_word(a[i], w, as[(w * BM + 2 * ty + i) * BKA + kk]);
                 const double2 v = *reinterpret_cast<const double2 *>(bs + (w * BK + kk) * BN + 2 * tx);
-                bb[0].w[w] = v.x;
-                bb[1].w[w] = v.y;
+                E::set_word(bb[0], w, v.x);
+                E::set_word(bb[1], w, v.y);
             }
 #pragma unroll
             for (int i = 0; i < TM; i++)
@@ -431,16 +435,19 @@ static bool tma_qd_enabled() {
     return v == 1;
 }
 
-// QD TMA leaf; returns 1 if launched (rc = status), 0 if the shape/strides do not qualify.
-int try_leaf_tma_qd(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A, const MatDesc &B,
-                    const MatDesc &C, int beta, int mv, cudaStream_t s, int *rc) {
-    using namespace tmaq;
+// 32x32-tile TMA leaf (QD, and the DD tail / small grids); returns 1 if launched (rc = status),
+// 0 if the shape/strides do not qualify.
+template <int W>
+static int try_tma32(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A, const MatDesc &B,
+                     const MatDesc &C, int beta, int mv, cudaStream_t s, int *rc) {
+    using Q = Tq<W>;
+    constexpr int BM = Q::BM, BN = Q::BN, BK = Q::BK, BKA = Q::BKA, NT = Q::NT;
+    constexpr size_t SMEM = Q::SMEM;
     *rc = DDQD_OK;
-    if (!tma_qd_enabled() || l == 0 || batch > 0x7fffffffLL || m > 0x7fffffffLL || l > 0x7fffffffLL || !encoder())
-        return 0;
+    if (l == 0 || batch > 0x7fffffffLL || m > 0x7fffffffLL || l > 0x7fffffffLL || !encoder()) return 0;
     CUtensorMap ma, mb;
-    if (!make_map(&ma, A, batch, BKA, BM, false, 4) || !make_map(&mb, B, batch, BN, BK, false, 4)) return 0;
-    auto kern = mv == 1 ? leaf_tma_qd_kernel<1> : mv == 2 ? leaf_tma_qd_kernel<2> : leaf_tma_qd_kernel<0>;
+    if (!make_map(&ma, A, batch, BKA, BM, false, W) || !make_map(&mb, B, batch, BN, BK, false, W)) return 0;
+    auto kern = mv == 1 ? leaf_tma_qd_kernel<W, 1> : mv == 2 ? leaf_tma_qd_kernel<W, 2> : leaf_tma_qd_kernel<W, 0>;
     static bool attr_set[3][64] = {};
     bool &attr = attr_set[mv][current_device()];
     if (!attr) {
@@ -459,13 +466,40 @@ int try_leaf_tma_qd(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDes
         count_launch();
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) {
-            set_error(std::string("QD TMA leaf launch: ") + cudaGetErrorString(e));
+            set_error(std::string("32x32 TMA leaf launch: ") + cudaGetErrorString(e));
             *rc = DDQD_ECUDA;
             return 1;
         }
     }
-    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s, "leaf_tma_qd_kernel (TMA)");
+    prof_end(0, (double)m * (double)l * (double)n * (double)batch, s,
+             W == 4 ? "leaf_tma_qd_kernel (TMA)" : "leaf_tma32_kernel (TMA, DD 32x32)");
     return 1;
+}
+
+int try_leaf_tma_qd(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A, const MatDesc &B,
+                    const MatDesc &C, int beta, int mv, cudaStream_t s, int *rc) {
+    *rc = DDQD_OK;
+    if (!tma_qd_enabled()) return 0;
+    return try_tma32<4>(m, l, n, batch, A, B, C, beta, mv, s, rc);
+}
+
+// DDQD_LEAF_TMA32=1 puts DD 32x32 tiles (the tail of a 64x64 batch, small grids) on this TMA leaf.
+// Off by default: on c1's tail it measured 0.656 of the FP64 peak against 0.698 for the cp.async
+// 32x32 leaf (both are bound by the 2x2 micro-tile's four dependent DD chains per thread).
+static bool tma32_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_LEAF_TMA32");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+int try_leaf_tma32_dd(int64_t m, int64_t l, int64_t n, int64_t batch, const MatDesc &A, const MatDesc &B,
+                      const MatDesc &C, int beta, int mv, cudaStream_t s, int *rc) {
+    *rc = DDQD_OK;
+    if (!tma32_enabled()) return 0;
+    return try_tma32<2>(m, l, n, batch, A, B, C, beta, mv, s, rc);
 }
 
 }  // namespace ddqd
