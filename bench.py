@@ -898,6 +898,7 @@ def main():
         }
         print(json.dumps(line), flush=True)
     if dist:
+        dist.barrier()   # rank 0's oracle sample and print are done before anyone tears down
         dist.destroy_process_group()
     return 0
 
