@@ -266,7 +266,19 @@ static int check_gemm_args(int64_t m, int64_t l, int64_t n, int algo, int64_t T)
 size_t streamed_top_bytes(int W, int64_t m, int64_t l, int64_t n);   // recursion.cu
 int run_gemm_streamed(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n, const MatDesc &A,
                       const MatDesc &B, const MatDesc &C, char *tws, cudaEvent_t rest_ready,
-                      cudaStream_t s, int (*on_quad)(int q, void *ctx), void *ctx);
+                      cudaStream_t s, int (*on_quad)(int q, void *ctx), void *ctx, cudaEvent_t mid_ready,
+                      char *tws2);
+
+// DDQD_HOST_DEEP=0 keeps M1's inputs as one copy stage (A/B measurements), =2 uses two stages
+// whatever the size (tests); default: two stages when A11 + B11 are >= 64 MB
+static int host_deep_mode() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_HOST_DEEP");
+        v = (e && (e[0] == '0' || e[0] == '2')) ? e[0] - '0' : 1;
+    }
+    return v;
+}
 
 // DDQD_HOST_STREAM=0 disables the overlapped host path (A/B measurements)
 static bool host_stream_enabled() {
@@ -281,7 +293,7 @@ static bool host_stream_enabled() {
 // copy stream + events of the overlapped host path, per host thread and device
 struct CopyRes {
     cudaStream_t cs = nullptr;
-    cudaEvent_t start = nullptr, first = nullptr, rest = nullptr, quad = nullptr;
+    cudaEvent_t start = nullptr, first = nullptr, mid = nullptr, rest = nullptr, quad = nullptr;
 };
 
 // device-to-host copy of one finished C quadrant on the copy stream (run_gemm_streamed's hook)
@@ -316,6 +328,7 @@ static int copy_res(CopyRes **out) {
         DDQD_CUDA_CHECK(cudaStreamCreateWithFlags(&r.cs, cudaStreamNonBlocking));
         DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.start, cudaEventDisableTiming));
         DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.first, cudaEventDisableTiming));
+        DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.mid, cudaEventDisableTiming));
         DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.rest, cudaEventDisableTiming));
         DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.quad, cudaEventDisableTiming));
     }
@@ -347,10 +360,16 @@ static int gemm_entry(int W, int64_t m, int64_t l, int64_t n, const double *A, c
     // host path: stage through library-owned device memory, copy back, synchronise
     const bool streamed = (algo & 0xff) == DDQD_WINOGRAD && !(algo & 0xff0000) &&
                           std::min(std::min(m, l), n) > T && host_stream_enabled();
+    const int64_t qm = (m + 1) / 2, ql = (l + 1) / 2, qn = (n + 1) / 2;
+    // two-stage arrival of A11, B11 (their own leading quadrants first, so M1's first product
+    // starts after 1/16 of the inputs) when M1 itself recurses and the copies are large
+    const bool deep = streamed && std::min(std::min(qm, ql), qn) > T && host_deep_mode() &&
+                      (host_deep_mode() == 2 || (size_t)W * (qm * ql + ql * qn) * sizeof(double) >= (size_t(64) << 20));
     const size_t oB = (bA + 255) & ~size_t(255), oC = oB + ((bB + 255) & ~size_t(255)),
                  oT = oC + ((bC + 255) & ~size_t(255));
+    const size_t oT2 = oT + (streamed ? streamed_top_bytes(W, m, l, n) : 0);
     int st = DDQD_OK;
-    char *dev = static_cast<char *>(buf_get(g_stage, oT + (streamed ? streamed_top_bytes(W, m, l, n) : 0) + 256,
+    char *dev = static_cast<char *>(buf_get(g_stage, oT2 + (deep ? streamed_top_bytes(W, qm, ql, qn) : 0) + 256,
                                             &st, "staging buffers"));
     if (st) return st;
     double *dA = reinterpret_cast<double *>(dev);
@@ -367,13 +386,30 @@ static int gemm_entry(int W, int64_t m, int64_t l, int64_t n, const double *A, c
         cudaStream_t cs = cr->cs;
         DDQD_CUDA_CHECK(cudaEventRecord(cr->start, s));
         DDQD_CUDA_CHECK(cudaStreamWaitEvent(cs, cr->start, 0));
-        for (int w = 0; w < W; w++) {
-            DDQD_CUDA_CHECK(cudaMemcpy2DAsync(dA + w * m * l, l * d8, A + w * m * l, l * d8, hl * d8, hm,
-                                              cudaMemcpyHostToDevice, cs));
-            DDQD_CUDA_CHECK(cudaMemcpy2DAsync(dB + w * l * n, n * d8, B + w * l * n, n * d8, hn * d8, hl,
-                                              cudaMemcpyHostToDevice, cs));
+        // a rows x cols block at (r0, c0) of every plane of X (ld = cols of X) to the device copy
+        auto blk = [&](double *dX, const double *hX, int64_t xr, int64_t xc, int64_t r0, int64_t c0, int64_t rows,
+                       int64_t cols) -> int {
+            if (rows <= 0 || cols <= 0) return DDQD_OK;
+            for (int w = 0; w < W; w++) {
+                const int64_t off = w * xr * xc + r0 * xc + c0;
+                DDQD_CUDA_CHECK(cudaMemcpy2DAsync(dX + off, xc * d8, hX + off, xc * d8, cols * d8, rows,
+                                                  cudaMemcpyHostToDevice, cs));
+            }
+            return DDQD_OK;
+        };
+        if (deep) {
+            // stage 1: A11's and B11's leading quadrants; stage 2: the rest of A11 and B11
+            const int64_t hm2 = (hm + 1) / 2, hl2 = (hl + 1) / 2, hn2 = (hn + 1) / 2;
+            if ((rc = blk(dA, A, m, l, 0, 0, hm2, hl2)) || (rc = blk(dB, B, l, n, 0, 0, hl2, hn2))) return rc;
+            DDQD_CUDA_CHECK(cudaEventRecord(cr->first, cs));
+            if ((rc = blk(dA, A, m, l, 0, hl2, hm2, hl - hl2)) || (rc = blk(dA, A, m, l, hm2, 0, hm - hm2, hl)) ||
+                (rc = blk(dB, B, l, n, 0, hn2, hl2, hn - hn2)) || (rc = blk(dB, B, l, n, hl2, 0, hl - hl2, hn)))
+                return rc;
+            DDQD_CUDA_CHECK(cudaEventRecord(cr->mid, cs));
+        } else {
+            if ((rc = blk(dA, A, m, l, 0, 0, hm, hl)) || (rc = blk(dB, B, l, n, 0, 0, hl, hn))) return rc;
+            DDQD_CUDA_CHECK(cudaEventRecord(cr->first, cs));
         }
-        DDQD_CUDA_CHECK(cudaEventRecord(cr->first, cs));
         for (int w = 0; w < W; w++) {
             DDQD_CUDA_CHECK(cudaMemcpy2DAsync(dA + w * m * l + hl, l * d8, A + w * m * l + hl, l * d8,
                                               (l - hl) * d8, hm, cudaMemcpyHostToDevice, cs));
@@ -392,7 +428,7 @@ static int gemm_entry(int W, int64_t m, int64_t l, int64_t n, const double *A, c
         const bool quads = (size_t)W * hm * hn * d8 >= (size_t(32) << 20);
         QuadCopy qc{cr, s, W, m, n, dC, C};
         rc = run_gemm_streamed(W, algo, T, m, l, n, mA, mB, mC, dev + oT, cr->rest, s,
-                               quads ? copy_quad : nullptr, &qc);
+                               quads ? copy_quad : nullptr, &qc, deep ? cr->mid : nullptr, dev + oT2);
         // the copy stream must not outlive the call into the caller's buffers
         cudaError_t e = cudaStreamSynchronize(cs);
         if (rc) return rc;

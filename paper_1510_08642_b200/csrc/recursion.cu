@@ -319,6 +319,12 @@ namespace ddqd {
 // copy). Each product is the same recursion as in run_gemm (the
 // planner's chunking never changes the arithmetic), so the result is bitwise that of the
 // device-pointer call.
+#define return_if_err(expr)        \
+    do {                           \
+        const int rc__ = (expr);   \
+        if (rc__) return rc__;     \
+    } while (0)
+
 static void top_shapes(int64_t m, int64_t l, int64_t n, int64_t *hm, int64_t *hl, int64_t *hn) {
     *hm = (m + 1) / 2; *hl = (l + 1) / 2; *hn = (n + 1) / 2;
 }
@@ -332,7 +338,8 @@ size_t streamed_top_bytes(int W, int64_t m, int64_t l, int64_t n) {
 
 int run_gemm_streamed(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n, const MatDesc &A,
                       const MatDesc &B, const MatDesc &C, char *tws, cudaEvent_t rest_ready,
-                      cudaStream_t s, int (*on_quad)(int q, void *ctx), void *ctx) {
+                      cudaStream_t s, int (*on_quad)(int q, void *ctx), void *ctx, cudaEvent_t mid_ready,
+                      char *tws2) {
     int64_t hm, hl, hn;
     top_shapes(m, l, n, &hm, &hl, &hn);
     const size_t w = (size_t)7 * W * sizeof(double);
@@ -351,7 +358,16 @@ int run_gemm_streamed(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t 
         NvtxRange nv("M1 = A11 B11 (overlaps the H2D copy)");
         MatDesc a11 = A, b11 = B;
         a11.rows = hm; a11.cols = hl; b11.rows = hl; b11.cols = hn;
-        if ((rc = run_gemm(W, algo, T, hm, hl, hn, 1, a11, b11, cM, 0, s))) return rc;
+        if (mid_ready) {
+            // M1 streamed one level deeper: its own first product (A11's and B11's leading
+            // quadrants, copied first) runs while the rest of A11 and B11 arrives, then its other
+            // six products as one batch and one post-addition -- the subproblem's recursion, so
+            // the same bits as run_gemm on it
+            return_if_err(run_gemm_streamed(W, algo, T, hm, hl, hn, a11, b11, cM, tws2, mid_ready, s, nullptr,
+                                            nullptr, nullptr, nullptr));
+        } else if ((rc = run_gemm(W, algo, T, hm, hl, hn, 1, a11, b11, cM, 0, s))) {
+            return rc;
+        }
     }
     DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, rest_ready, 0));
     NvtxRange nv("level 0 (streamed)");

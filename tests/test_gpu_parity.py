@@ -1218,3 +1218,30 @@ def test_fused_last_level_same_bits(tmp_path, orc):
     A, B = gen.matrix(2, 99, 96, 61, 0), gen.matrix(2, 96, 101, 61, 1)
     for algo in ("strassen", "winograd"):
         assert same(np_(ddqd.gemm(cu(A), cu(B), algo, 6)), orc.gemm(A, B, algo, threshold=6))
+
+
+def test_host_streamed_two_stage_bitwise(tmp_path, orc):
+    """Host-pointer Winograd with M1 streamed one level deeper (DDQD_HOST_DEEP=2: A11's and B11's
+    leading quadrants copied first, M1's first product overlapping the rest): bit-identical to
+    the device-pointer call and the oracle, DD and QD, odd shapes."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, ddqd_inputs as gen, paper_1510_08642_b200 as d\n"
+        "out = []\n"
+        "for W, m, l, n, T in ((2, 301, 277, 263, 32), (4, 150, 133, 141, 16), (2, 517, 515, 513, 64)):\n"
+        "    A, B = gen.matrix(W, m, l, 71, 0), gen.matrix(W, l, n, 71, 1)\n"
+        "    h = d.gemm(torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory(), 'winograd', T).numpy()\n"
+        "    g = d.gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), 'winograd', T).cpu().numpy()\n"
+        "    out += [h.ravel(), g.ravel()]\n"
+        "np.save(r'%s', np.concatenate(out))\n")
+    f = tmp_path / "deep.npy"
+    env = dict(os.environ, DDQD_HOST_DEEP="2")
+    subprocess.check_call([sys.executable, "-c", code % f], env=env, cwd=ROOT)
+    v = np.load(f)
+    refs = []
+    for W, m, l, n, T in ((2, 301, 277, 263, 32), (4, 150, 133, 141, 16), (2, 517, 515, 513, 64)):
+        A, B = gen.matrix(W, m, l, 71, 0), gen.matrix(W, l, n, 71, 1)
+        r = orc.gemm(A, B, "winograd", threshold=T).ravel()
+        refs += [r, r]
+    assert same(v, np.concatenate(refs))
