@@ -89,7 +89,7 @@ def parse_args():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--k", type=int, default=None, help="multi-GPU product depth (default: balancer)")
     ap.add_argument("--schedule", default="auto",
-                    choices=["auto", "bands", "products", "products_p2p", "ctiles", "auto-all"],
+                    choices=["auto", "bands", "products", "products_rows", "products_p2p", "ctiles", "auto-all"],
                     help="multi-GPU schedule: auto = whichever of the bit-identical schedules measures "
                          "fastest (BJ:5 (4)); bands = one tile of C per rank with the whole problem's "
                          "tree; products = depth-k products to rank 0 (--combine); products_p2p = "
@@ -473,12 +473,12 @@ def lu_bench(args, wl, rank, world, local):
 def make_schedule(args, W, algo, T, m, l, n, dist, dev, replicated_inputs=False):
     from paper_1510_08642_b200 import mgpu
     if args.schedule in ("auto", "auto-all"):
-        cands = None if args.schedule == "auto" else ("bands", "products", "products_p2p", "ctiles")
+        cands = None if args.schedule == "auto" else ("bands", "products_rows", "products", "products_p2p", "ctiles")
         return mgpu.AutoDistributedGemm(W, algo, T, m, l, n, dist, dev, candidates=cands, k=args.k,
                                         replicated_inputs=replicated_inputs)
     if args.schedule == "bands":
         return mgpu.BandGemm(W, algo, T, m, l, n, dist, dev, replicated_inputs=replicated_inputs)
-    combine = "p2p" if args.schedule == "products_p2p" else args.combine
+    combine = {"products_p2p": "p2p", "products_rows": "rows"}.get(args.schedule, args.combine)
     return mgpu.DistributedGemm(W, algo, T, m, l, n, dist, dev, k=0 if args.schedule == "ctiles" else args.k,
                                 combine=combine, replicated_inputs=replicated_inputs)
 
@@ -570,9 +570,35 @@ def band_model(args, wl, A, B, C, peak):
         bcast_ms = (A.numel() + B.numel()) * 8 / 725e9 * 1e3       # NCCL bus bandwidth, 1 GiB class
         rows, cols = bg.tile(0)
         gather_ms = (G - 1) / G * C.numel() * 8 / 770e9 * 1e3      # tiles into rank 0 (peer copy rate)
-        out[str(G)] = {"grid": [bg.gr, bg.gc], "tile_rows": len(rows), "tile_cols": len(cols),
-                       "tile_ms_measured": tile_ms, "broadcast_ms_model": bcast_ms,
-                       "gather_ms_model": gather_ms, "step_ms_model": tile_ms + bcast_ms + gather_ms}
+        ent = {"grid": [bg.gr, bg.gc], "tile_rows": len(rows), "tile_cols": len(cols),
+               "tile_ms_measured": tile_ms, "broadcast_ms_model": bcast_ms,
+               "gather_ms_model": gather_ms, "step_ms_model": tile_ms + bcast_ms + gather_ms}
+        # the product schedule with the row-band combine: rank 0 (the largest slice) measured
+        # the same way; plus the all-to-all of product row bands, modelled
+        dg = mgpu.DistributedGemm(W, wl["algo"], wl["T"], m, l, n, None, combine="rows", world=G, rank=0)
+        dg.compute_share(A, B)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            dg.compute_share(A, B)
+        e1.record()
+        torch.cuda.synchronize()
+        share_ms = e0.elapsed_time(e1) / reps
+        mk, _, nk = dg.shapes[dg.k]
+        lo, hi = dg.slices[0]
+        a2a_bytes = (hi - lo) * W * mk * nk * 8 * (G - 1) / G         # sent = received per rank
+        a2a_ms = a2a_bytes / 770e9 * 1e3
+        # each chunk's row bands are exchanged while the next chunk computes: only the last
+        # chunk's exchange is exposed
+        last = (hi - lo) - ((hi - lo - 1) // dg.chunk) * dg.chunk
+        a2a_exposed = a2a_ms * last / (hi - lo)
+        ent["products_rows"] = {"k": dg.k, "products_rank0": hi - lo, "share_ms_measured": share_ms,
+                                "all_to_all_bytes_per_rank": a2a_bytes, "all_to_all_ms_model": a2a_ms,
+                                "all_to_all_exposed_ms_model": a2a_exposed,
+                                "rank0_receive_bytes": (G - 1) / G * C.numel() * 8,
+                                "step_ms_model": share_ms + bcast_ms + a2a_exposed + gather_ms}
+        del dg
+        out[str(G)] = ent
     return out
 
 

@@ -166,6 +166,10 @@ typedef struct {
 } ddqd_mat;
 
 int ddqd_pre_add(int prec, int algo, int side, int64_t P, const ddqd_mat *X, const ddqd_mat *Y);
+/* ddqd_pre_add storing only the children with index 7b + c in [keep_lo, keep_hi) (the others are
+ * left untouched): the multi-GPU schedules form only the ancestors of a rank's own products. */
+int ddqd_pre_add_range(int prec, int algo, int side, int64_t P, const ddqd_mat *X, const ddqd_mat *Y,
+                       int64_t keep_lo, int64_t keep_hi);
 int ddqd_post_add(int prec, int algo, int64_t P, const ddqd_mat *M, const ddqd_mat *C, int beta);
 
 /* The multi-GPU fused combine: one recursion level's post-additions with the

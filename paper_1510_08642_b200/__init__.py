@@ -80,6 +80,7 @@ def _load():
     L.ddqd_launch_count.restype = i64
     L.ddqd_last_error.restype = ctypes.c_char_p
     L.ddqd_pre_add.argtypes = [i32, i32, i32, i64, ctypes.POINTER(Mat), ctypes.POINTER(Mat)]
+    L.ddqd_pre_add_range.argtypes = [i32, i32, i32, i64, ctypes.POINTER(Mat), ctypes.POINTER(Mat), i64, i64]
     L.ddqd_post_add.argtypes = [i32, i32, i64, ctypes.POINTER(Mat), ctypes.POINTER(Mat), i32]
     L.ddqd_profile_stop.argtypes = [ctypes.POINTER(ctypes.c_double), i32]
     L.ddqd_fp64_peak.argtypes = [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
@@ -95,7 +96,7 @@ EXPORTED = ["dd_gemm", "qd_gemm", "ddqd_gemm_ex", "dd_lu_solve", "qd_lu_solve", 
             "ddqd_workspace_bytes", "ddqd_set_workspace", "ddqd_set_workspace_limit",
             "ddqd_launch_count", "ddqd_release", "ddqd_last_error", "ddqd_version",
             "ddqd_profile_start", "ddqd_profile_stop", "ddqd_fp64_peak", "ddqd_pre_add", "ddqd_post_add",
-            "ddqd_band_copy", "ddqd_profile_kernels"]
+            "ddqd_band_copy", "ddqd_profile_kernels", "ddqd_pre_add_range"]
 
 
 def _check(rc: int, what: str) -> int:
@@ -216,13 +217,16 @@ def _add_algo(algo, madd):
     return _algo(algo) | (ADD_ACCURATE if madd == "accurate" else 0)
 
 
-def pre_add(algo, side, X, Y, madd="canonical"):
-    """One level's fused pre-additions: X [P,W,r,c] -> Y [7P,W,ceil(r/2),ceil(c/2)]."""
+def pre_add(algo, side, X, Y, madd="canonical", keep=None):
+    """One level's fused pre-additions: X [P,W,r,c] -> Y [7P,W,ceil(r/2),ceil(c/2)]; keep = (lo, hi)
+    stores only children 7b + c in [lo, hi)."""
     P = 1 if X.dim() == 3 else X.shape[0]
     W = X.shape[-3]
     _set_stream(X)
     x, y = batch_mat(X), batch_mat(Y)
-    _check(lib.ddqd_pre_add(W, _add_algo(algo, madd), side, P, ctypes.byref(x), ctypes.byref(y)), "pre_add")
+    lo, hi = keep if keep is not None else (0, 7 * P)
+    _check(lib.ddqd_pre_add_range(W, _add_algo(algo, madd), side, P, ctypes.byref(x), ctypes.byref(y), lo, hi),
+           "pre_add")
 
 
 def post_add(algo, M, C, beta=0, madd="canonical"):

@@ -582,7 +582,16 @@ int qd_lu_solve(int64_t n, double *A, const double *b, double *x, int64_t *ipiv,
 static MatDesc to_desc(const ddqd_mat *x) { return MatDesc{x->p, x->rows, x->cols, x->ld, x->ps, x->bs}; }
 
 int ddqd_pre_add(int prec, int algo, int side, int64_t P, const ddqd_mat *X, const ddqd_mat *Y) {
+    return ddqd_pre_add_range(prec, algo, side, P, X, Y, 0, 7 * P);
+}
+
+int ddqd_pre_add_range(int prec, int algo, int side, int64_t P, const ddqd_mat *X, const ddqd_mat *Y,
+                       int64_t keep_lo, int64_t keep_hi) {
     t_err.clear();
+    if (keep_lo < 0 || keep_hi < keep_lo || keep_hi > 7 * P) {
+        set_error("pre_add: keep range must satisfy 0 <= lo <= hi <= 7P");
+        return DDQD_EINVAL;
+    }
     const int a = algo & ~DDQD_ADD_ACCURATE;   // the accurate-add variant may be OR-ed in
     if ((prec != 2 && prec != 4) || (a != 1 && a != 2) || (side != 0 && side != 1) || P < 0 || !X || !Y) {
         set_error("bad pre_add arguments");
@@ -592,7 +601,7 @@ int ddqd_pre_add(int prec, int algo, int side, int64_t P, const ddqd_mat *X, con
         set_error("pre_add: child shape must be ceil(parent/2)");
         return DDQD_EINVAL;
     }
-    return launch_pre_add(prec, algo, side, P, to_desc(X), to_desc(Y), t_stream);
+    return launch_pre_add(prec, algo, side, P, to_desc(X), to_desc(Y), t_stream, keep_lo, keep_hi);
 }
 
 int ddqd_post_add(int prec, int algo, int64_t P, const ddqd_mat *M, const ddqd_mat *C, int beta) {

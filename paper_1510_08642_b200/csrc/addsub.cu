@@ -83,7 +83,8 @@ __device__ __forceinline__ void post_ops(const typename E::T p[7], typename E::T
 
 // side 0 = A operands, side 1 = B operands; algo 1 = Strassen, 2 = Winograd
 template <int W, int ALGO, int SIDE, int V>
-__global__ void __launch_bounds__(256) pre_add_kernel(int64_t P, MatDesc X, MatDesc Y) {
+__global__ void __launch_bounds__(256) pre_add_kernel(int64_t P, MatDesc X, MatDesc Y, int64_t keep_lo,
+                                                      int64_t keep_hi) {
     using E = arith<W, V>;
     using T = typename E::T;
     const int64_t hr = Y.rows, hc = Y.cols;
@@ -100,11 +101,17 @@ __global__ void __launch_bounds__(256) pre_add_kernel(int64_t P, MatDesc X, MatD
         const T x22 = ld_or_zero<W>(xb + (i + hr) * X.ld + (j + hc), X.ps, r2 && c2);
         T o[7];
         pre_ops<E, ALGO, SIDE>(x11, x12, x21, x22, o);
+        // children outside [keep_lo, keep_hi) are not stored (the multi-GPU schedules form only
+        // the ancestors of a rank's own products)
 #pragma unroll
-        for (int c = 0; c < 7; c++) E::store(Y.p + (7 * b + c) * Y.bs + i * Y.ld + j, Y.ps, o[c]);
+        for (int c = 0; c < 7; c++)
+            if (7 * b + c >= keep_lo && 7 * b + c < keep_hi)
+                E::store(Y.p + (7 * b + c) * Y.bs + i * Y.ld + j, Y.ps, o[c]);
         if (j == hc - 1 && Y.ld > hc)   // padded leading dimension: fill the gap so no sector is partial
 #pragma unroll
-            for (int c = 0; c < 7; c++) E::store(Y.p + (7 * b + c) * Y.bs + i * Y.ld + hc, Y.ps, E::zero());
+            for (int c = 0; c < 7; c++)
+                if (7 * b + c >= keep_lo && 7 * b + c < keep_hi)
+                    E::store(Y.p + (7 * b + c) * Y.bs + i * Y.ld + hc, Y.ps, E::zero());
     }
 }
 
@@ -268,26 +275,31 @@ static unsigned grid_for(int64_t total, int threads = 256) {
 // Dispatch. `algo` is 1 (Strassen) or 2 (Winograd), optionally | DDQD_ADD_ACCURATE (every
 // addition the accurate one, numerics.md s.2-3).
 template <int W, int V>
-static int pre_dispatch(int algo, int side, int64_t P, const MatDesc &X, const MatDesc &Y, cudaStream_t s) {
+static int pre_dispatch(int algo, int side, int64_t P, const MatDesc &X, const MatDesc &Y, cudaStream_t s,
+                        int64_t klo, int64_t khi) {
     const int64_t total = P * Y.rows * Y.cols;
     if (total == 0) return DDQD_OK;
     const unsigned g = grid_for(total);
     prof_begin(1, s);
-    if (algo == 1 && side == 0) pre_add_kernel<W, 1, 0, V><<<g, 256, 0, s>>>(P, X, Y);
-    else if (algo == 1) pre_add_kernel<W, 1, 1, V><<<g, 256, 0, s>>>(P, X, Y);
-    else if (side == 0) pre_add_kernel<W, 2, 0, V><<<g, 256, 0, s>>>(P, X, Y);
-    else pre_add_kernel<W, 2, 1, V><<<g, 256, 0, s>>>(P, X, Y);
+    if (algo == 1 && side == 0) pre_add_kernel<W, 1, 0, V><<<g, 256, 0, s>>>(P, X, Y, klo, khi);
+    else if (algo == 1) pre_add_kernel<W, 1, 1, V><<<g, 256, 0, s>>>(P, X, Y, klo, khi);
+    else if (side == 0) pre_add_kernel<W, 2, 0, V><<<g, 256, 0, s>>>(P, X, Y, klo, khi);
+    else pre_add_kernel<W, 2, 1, V><<<g, 256, 0, s>>>(P, X, Y, klo, khi);
     DDQD_LAUNCH_CHECK();
     prof_end(1, (double)total * W * 8.0 * 11.0, s, "pre_add_kernel");   // 4 quadrant reads + 7 operand writes
     return DDQD_OK;
 }
 
 int launch_pre_add(int W, int algo, int side, int64_t P, const MatDesc &X, const MatDesc &Y,
-                   cudaStream_t s) {
+                   cudaStream_t s, int64_t keep_lo, int64_t keep_hi) {
     const bool acc = (algo & DDQD_ADD_ACCURATE) != 0;
     algo &= 0xff;
-    if (W == 2) return acc ? pre_dispatch<2, 2>(algo, side, P, X, Y, s) : pre_dispatch<2, 0>(algo, side, P, X, Y, s);
-    return acc ? pre_dispatch<4, 2>(algo, side, P, X, Y, s) : pre_dispatch<4, 0>(algo, side, P, X, Y, s);
+    if (keep_hi < 0) keep_hi = 7 * P;
+    if (W == 2)
+        return acc ? pre_dispatch<2, 2>(algo, side, P, X, Y, s, keep_lo, keep_hi)
+                   : pre_dispatch<2, 0>(algo, side, P, X, Y, s, keep_lo, keep_hi);
+    return acc ? pre_dispatch<4, 2>(algo, side, P, X, Y, s, keep_lo, keep_hi)
+               : pre_dispatch<4, 0>(algo, side, P, X, Y, s, keep_lo, keep_hi);
 }
 
 template <int W, int V>

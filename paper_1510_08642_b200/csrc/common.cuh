@@ -64,8 +64,9 @@ int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, cons
                      const MatDesc &B, const MatDesc &C, int beta, int mv, cudaStream_t s);
 
 // Strassen/Winograd pre/post additions (addsub.cu).
+// keep_lo/keep_hi: only children with index (7b + c) in [keep_lo, keep_hi) are stored (-1: all)
 int launch_pre_add(int W, int algo, int side, int64_t P, const MatDesc &X, const MatDesc &Y,
-                   cudaStream_t s);
+                   cudaStream_t s, int64_t keep_lo = 0, int64_t keep_hi = -1);
 int launch_post_add(int W, int algo, int64_t P, const MatDesc &M, const MatDesc &C, int beta,
                     cudaStream_t s);
 // Two levels at once (j -> j+2; h1r x h1c / h1m x h1n = the skipped level-(j+1) extent).

@@ -118,8 +118,8 @@ class CudaBackend:
         import torch
         return torch.empty(n, dtype=torch.int64, device=like.device)
 
-    def pre_add(self, algo, side, X, Y):
-        self.ddqd.pre_add(algo, side, X, Y)
+    def pre_add(self, algo, side, X, Y, keep=None):
+        self.ddqd.pre_add(algo, side, X, Y, keep=keep)
 
     def post_add(self, algo, M, C, beta=0):
         self.ddqd.post_add(algo, M, C, beta)
@@ -205,22 +205,24 @@ class DistributedGemm:
     holds the operands and C; C may be a strided view with unit-stride rows)."""
 
     def __init__(self, W, algo, T, m, l, n, dist, device=None, k=None, backend=None, chunk=None, beta=0,
-                 combine="nccl", replicated_inputs=False):
+                 combine="nccl", replicated_inputs=False, world=None, rank=0):
         self.W, self.algo, self.T, self.beta = W, algo, T, beta
         # combine = "nccl": products stream to rank 0 over NCCL point-to-point, rank 0 post-adds;
         # "p2p": products stay resident, the post-adds read peers' buffers through CUDA IPC
         # mappings (fused gather + combine kernels, levels split over the ranks, each rank writes
         # its rows of C straight into rank 0's C buffer). beta = 1 needs combine = "nccl".
-        if combine not in ("nccl", "p2p"):
-            raise ValueError("combine must be 'nccl' or 'p2p'")
+        # "rows": products exchanged by row bands (all-to-all), every rank combines its band of C
+        # through all k levels, rank 0 gathers the bands -- no combine tail on rank 0
+        if combine not in ("nccl", "p2p", "rows"):
+            raise ValueError("combine must be 'nccl', 'p2p' or 'rows'")
         if combine == "p2p" and beta:
             raise ValueError("the p2p combine computes C := A B (beta = 0)")
         self.combine = combine
         self.replicated_inputs = replicated_inputs   # every rank already holds A and B
         self.m, self.l, self.n = m, l, n
-        self.dist = dist
-        self.rank = dist.get_rank()
-        self.world = dist.get_world_size()
+        self.dist = dist             # None: compute_share() only, as `rank` of `world` on one device
+        self.rank = dist.get_rank() if dist is not None else int(rank)
+        self.world = dist.get_world_size() if dist is not None else int(world)
         self.backend = backend or CudaBackend()
         self.shapes = rec_shapes(m, l, n, T) if algo not in ("block", 0) else [(m, l, n)]
         d = len(self.shapes) - 1
@@ -267,6 +269,24 @@ class DistributedGemm:
         self._bufs = bufs
         return bufs
 
+    def _pruned_pre_adds(self, A, B, bufs):
+        """The top-k pre-additions, breadth-first, pruned to the ancestors of this rank's products:
+        at level j only the parents above them, and of their children only those that are
+        ancestors (or the products) themselves. Returns the level-k operand buffers."""
+        bk, k = self.backend, self.k
+        X, Y = A, B
+        for j in range(k):
+            a, b = self._ancestor_range(j)
+            if b > a:
+                Xs = X if j == 0 else X[a:b]
+                Ys = Y if j == 0 else Y[a:b]
+                c0, c1 = self._ancestor_range(j + 1) if j + 1 < k else self.slices[self.rank]
+                keep = (c0 - 7 * a, c1 - 7 * a)
+                bk.pre_add(self.algo, 0, Xs, bufs["A"][j][7 * a:7 * b], keep=keep)
+                bk.pre_add(self.algo, 1, Ys, bufs["B"][j][7 * a:7 * b], keep=keep)
+            X, Y = bufs["A"][j], bufs["B"][j]
+        return X, Y
+
     def _ancestor_range(self, j):
         """Parents at level j (0 <= j < k) whose subtrees contain this rank's products."""
         lo, hi = self.slices[self.rank]
@@ -282,20 +302,14 @@ class DistributedGemm:
             dist.broadcast(B, 0)
         if self.k > 0 and self.combine == "p2p":
             return self._p2p_call(A, B, C)
+        if self.k > 0 and self.combine == "rows":
+            return self._rows_call(A, B, C)
         bufs = self._alloc(A)
         if self.k == 0:
             return self._row_slabs(A, B, C, bufs)
         bk = self.backend
         # top-k pre-additions, breadth-first, pruned to the ancestors of this rank's products
-        X, Y = A, B
-        for j in range(self.k):
-            a, b = self._ancestor_range(j)
-            if b > a:
-                Xs = X if j == 0 else X[a:b]
-                Ys = Y if j == 0 else Y[a:b]
-                bk.pre_add(self.algo, 0, Xs, bufs["A"][j][7 * a:7 * b])
-                bk.pre_add(self.algo, 1, Ys, bufs["B"][j][7 * a:7 * b])
-            X, Y = bufs["A"][j], bufs["B"][j]
+        X, Y = self._pruned_pre_adds(A, B, bufs)
         lo, hi = self.slices[self.rank]
         # this rank's products, in chunks; each finished chunk streams to rank 0 while the next
         # one computes (point-to-point sends on the NCCL stream overlap the library's stream)
@@ -329,6 +343,126 @@ class DistributedGemm:
                 sends += dist.batch_isend_irecv([dist.P2POp(dist.isend, part, 0)])
             for q in sends:
                 q.wait()
+        return C
+
+    def compute_share(self, A, B):
+        """This rank's compute of the product schedule on the current device, no communication:
+        the pruned top-k pre-additions and its slice of the depth-k products, then (combine =
+        'rows') the k post-addition levels on its row band (over whatever the band buffer holds:
+        timing only). For the one-GPU model of the multi-GPU step (bench.py)."""
+        bk, k = self.backend, self.k
+        bufs = self._alloc_operands(A)
+        X, Y = self._pruned_pre_adds(A, B, bufs)
+        lo, hi = self.slices[self.rank]
+        st = self._rows_setup(A)
+        for c0 in range(lo, hi, self.chunk):
+            c1 = min(hi, c0 + self.chunk)
+            bk.gemm_batched(X[c0:c1], Y[c0:c1], st["local"][c0 - lo:c1 - lo], self.algo, self.T)
+        if self.combine == "rows" and st["H"][0]:
+            for j in range(k - 1, -1, -1):
+                bk.post_add(self.algo, st["lev"][j + 1], st["lev"][j], 0)
+
+    # ---- row-band combine ------------------------------------------------------------------------
+    def _rows_setup(self, like):
+        if getattr(self, "_rows", None) is not None:
+            return self._rows
+        W, bk, G = self.W, self.backend, self.world
+        mdims = [s[0] for s in self.shapes[: self.k + 1]]
+        bands = balanced_slices(mdims[self.k], G)           # level-k product rows per rank
+        maps = [band_index_map(mdims, a, b) for a, b in bands]
+        # compact heights of this rank's band at every level 0..k
+        a, b = bands[self.rank]
+        H = [len(band_index_map(mdims[j:], a, b)) for j in range(self.k + 1)]
+        lo, hi = self.slices[self.rank]
+        mk, _, nk = self.shapes[self.k]
+        st = {
+            "bands": bands, "H": H,
+            "local": bk.empty((max(hi - lo, 1), W, mk, nk), like),          # this rank's products
+            "lev": [bk.empty((7 ** j, W, H[j], self.shapes[j][2]), like) for j in range(self.k + 1)],
+            "rmap": bk.index(maps[self.rank], like) if H[0] else None,
+        }
+        if self.rank == 0:
+            st["gather"] = [bk.empty((W, len(maps[g]), self.n), like) for g in range(G)]
+            st["gmaps"] = [bk.index(maps[g], like) if maps[g] else None for g in range(G)]
+        self._rows = st
+        return st
+
+    def _rows_call(self, A, B, C):
+        """Products by depth-k units (as the NCCL combine), then (1) an all-to-all of product ROW
+        BANDS: rank r receives rows [a_r, b_r) of every level-k product (each sender packs its
+        products' band rows in product order, so a receive lands contiguously); (2) every rank
+        runs the k levels of post-additions on its compact band (the band rows lifted level by
+        level as in the band schedule: the same formulas on 1/G of the positions); (3) rank 0
+        gathers the compact bands of C and unpacks their rows. Same operations per element as one
+        GPU, so the same bits; rank 0 receives (G-1)/G of C instead of (G-1)/G of every product."""
+        dist, bk, W, k = self.dist, self.backend, self.W, self.k
+        st = self._rows_setup(A)
+        bufs = self._alloc_operands(A)
+        X, Y = self._pruned_pre_adds(A, B, bufs)
+        # (1) products chunk by chunk; each finished chunk's row bands go to their ranks (and the
+        # peers' chunks of the same round come in) while the next chunk computes -- the
+        # exchanges run on NCCL's stream, ordered after the chunk that produced them
+        lev_k = st["lev"][k]
+        a_me, b_me = st["bands"][self.rank]
+        Mk = st["local"]
+        chunks = [[(c0, min(phi, c0 + self.chunk)) for c0 in range(plo, phi, self.chunk)]
+                  for plo, phi in self.slices]
+        lo = self.slices[self.rank][0]
+        reqs, keep = [], []
+        for rnd in range(max(len(c) for c in chunks)):
+            ops = []
+            if rnd < len(chunks[self.rank]):
+                c0, c1 = chunks[self.rank][rnd]
+                bk.gemm_batched(X[c0:c1], Y[c0:c1], Mk[c0 - lo:c1 - lo], self.algo, self.T)
+                for r, (a, b) in enumerate(st["bands"]):
+                    if b <= a:
+                        continue
+                    part = Mk[c0 - lo:c1 - lo, :, a:b, :]
+                    if r == self.rank:
+                        lev_k[c0:c1].copy_(part)
+                    else:
+                        packed = part.contiguous()     # [chunk][W][band rows][n_k], product order
+                        keep.append(packed)
+                        ops.append((dist.isend, packed, r))
+            if b_me > a_me:
+                for o in range(self.world):
+                    if o != self.rank and rnd < len(chunks[o]):
+                        pc0, pc1 = chunks[o][rnd]
+                        ops.append((dist.irecv, lev_k[pc0:pc1], o))
+            if ops:
+                reqs += dist.batch_isend_irecv([dist.P2POp(op, t, peer) for op, t, peer in ops])
+        for q in reqs:
+            q.wait()
+        del keep
+        # beta = 1: this rank's rows of C arrive first (rank 0 holds C)
+        Cb = st["lev"][0][0]
+        if self.beta:
+            if self.rank == 0:
+                sends = []
+                for g in range(self.world):
+                    if st["gmaps"][g] is None:
+                        continue
+                    bk.band_copy("pack", C, st["gather"][g], st["gmaps"][g], None)
+                    if g == 0:
+                        Cb.copy_(st["gather"][0])
+                    else:
+                        sends.append((dist.isend, st["gather"][g], g))
+                _p2p(dist, sends)
+            elif st["H"][0]:
+                _p2p(dist, [(dist.irecv, Cb, 0)])
+        # (2) the k levels of post-additions on the compact band
+        if st["H"][0]:
+            for j in range(k - 1, -1, -1):
+                bk.post_add(self.algo, st["lev"][j + 1], st["lev"][j], self.beta if j == 0 else 0)
+        # (3) gather the compact bands of C on rank 0 and unpack their rows
+        if self.rank == 0:
+            _p2p(dist, [(dist.irecv, st["gather"][g], g) for g in range(1, self.world) if st["gmaps"][g] is not None])
+            for g in range(self.world):
+                if st["gmaps"][g] is None:
+                    continue
+                bk.band_copy("unpack", C, Cb if g == 0 else st["gather"][g], st["gmaps"][g], None)
+        elif st["H"][0]:
+            _p2p(dist, [(dist.isend, Cb, 0)])
         return C
 
     # ---- p2p combine ----------------------------------------------------------------------------
@@ -402,15 +536,7 @@ class DistributedGemm:
         dist, bk, W, k = self.dist, self.backend, self.W, self.k
         st = self._p2p_setup(A)
         bufs = self._alloc_operands(A)
-        X, Y = A, B
-        for j in range(k):
-            a, b = self._ancestor_range(j)
-            if b > a:
-                Xs = X if j == 0 else X[a:b]
-                Ys = Y if j == 0 else Y[a:b]
-                bk.pre_add(self.algo, 0, Xs, bufs["A"][j][7 * a:7 * b])
-                bk.pre_add(self.algo, 1, Ys, bufs["B"][j][7 * a:7 * b])
-            X, Y = bufs["A"][j], bufs["B"][j]
+        X, Y = self._pruned_pre_adds(A, B, bufs)
         lo, hi = self.slices[self.rank]
         Mk = st["local"][k]
         for c0 in range(lo, hi, self.chunk):
@@ -678,7 +804,7 @@ class DistributedLU:
                 U12 = bk.empty((W, kb, n2), A)
                 C = None
             DistributedGemm(W, self.algo, self.T, n2, kb, n2, self.dist, k=self.k, backend=bk,
-                            beta=1)(L21, U12, C)
+                            beta=1, combine="rows")(L21, U12, C)
         if not root:
             return None, None, None
         return bk.lu_trsv(A, ipiv, b), ipiv, info
@@ -699,7 +825,7 @@ class AutoDistributedGemm:
     run once more on the original C); later calls run only the winner. `timings` (s) and
     `choice` record the measurement."""
 
-    BITWISE = ("bands", "products", "products_p2p")
+    BITWISE = ("bands", "products_rows", "products", "products_p2p")
 
     def __init__(self, W, algo, T, m, l, n, dist, device=None, backend=None, beta=0, candidates=None, **kw):
         self.dist = dist
@@ -715,6 +841,8 @@ class AutoDistributedGemm:
                                       replicated_inputs=kw.get("replicated_inputs", False)),
             "products": lambda: DistributedGemm(W, algo, T, m, l, n, dist, device, backend=self.backend,
                                                 beta=beta, combine="nccl", **kw),
+            "products_rows": lambda: DistributedGemm(W, algo, T, m, l, n, dist, device, backend=self.backend,
+                                                     beta=beta, combine="rows", **kw),
             "products_p2p": lambda: DistributedGemm(W, algo, T, m, l, n, dist, device, backend=self.backend,
                                                     combine="p2p", **kw),
             "ctiles": lambda: DistributedGemm(W, algo, T, m, l, n, dist, device, k=0, backend=self.backend,

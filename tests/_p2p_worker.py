@@ -66,6 +66,8 @@ def run_schedules(rank, world, port, cfg, q):
                          ("products", lambda: mgpu.DistributedGemm(W, algo, T, m, l, n, dist, dev)),
                          ("products_p2p", lambda: mgpu.DistributedGemm(W, algo, T, m, l, n, dist, dev,
                                                                        combine="p2p")),
+                         ("products_rows", lambda: mgpu.DistributedGemm(W, algo, T, m, l, n, dist, dev,
+                                                                        combine="rows")),
                          ("auto", lambda: mgpu.AutoDistributedGemm(W, algo, T, m, l, n, dist, dev))):
             A, B = inputs()
             C = torch.zeros((W, m, n), dtype=torch.float64, device=dev)
@@ -82,6 +84,12 @@ def run_schedules(rank, world, port, cfg, q):
         torch.cuda.synchronize()
         if rank == 0:
             out["bands_beta1"] = C.cpu().numpy().copy()
+        A, B = inputs()
+        C = torch.from_numpy(gen.matrix(W, m, n, 33, 2)).to(dev) if rank == 0 else None
+        mgpu.DistributedGemm(W, algo, T, m, l, n, dist, dev, beta=1, combine="rows")(A, B, C)
+        torch.cuda.synchronize()
+        if rank == 0:
+            out["rows_beta1"] = C.cpu().numpy().copy()
             q.put(out)
     except Exception as e:   # surface the failure to the parent
         q.put({"error": repr(e)})

@@ -1066,7 +1066,7 @@ def test_multiprocess_schedules_staged_bitwise(orc, cfg, world):
     W, algo, T, m, l, n = cfg
     A, B = gen.matrix(W, m, l, 33, 0), gen.matrix(W, l, n, 33, 1)
     ref = np_(ddqd.gemm(cu(A), cu(B), algo, T))
-    for name in ("bands", "products", "products_p2p", "auto"):
+    for name in ("bands", "products", "products_p2p", "products_rows", "auto"):
         assert same(out[name], ref), name
     C0 = cu(gen.matrix(W, m, n, 33, 2))
     a, b = cu(A), cu(B)
@@ -1074,6 +1074,7 @@ def test_multiprocess_schedules_staged_bitwise(orc, cfg, world):
     ddqd.gemm_ex(W, algo, T, m, l, n, 1, a.data_ptr(), l, m * l, 0, b.data_ptr(), n, l * n, 0,
                  C0.data_ptr(), n, m * n, 0, 1)
     assert same(out["bands_beta1"], np_(C0))
+    assert same(out["rows_beta1"], np_(C0))
 
 
 # ---- ragged leaves: interior / strip split and the flat leaf ------------

@@ -119,7 +119,7 @@ class OracleBackend:
         P[:, :r, :c] = X
         return P[:, :hr, :hc], P[:, :hr, hc:], P[:, hr:, :hc], P[:, hr:, hc:]
 
-    def pre_add(self, algo, side, X, Y):
+    def pre_add(self, algo, side, X, Y, keep=None):   # (forms every child; `keep` only saves work)
         Xn = X.numpy().reshape((-1,) + tuple(X.shape[-3:]))
         hr, hc = Y.shape[-2], Y.shape[-1]
         add = lambda a, b: self._ew("add", a, b)   # noqa: E731
@@ -403,11 +403,11 @@ def test_c_tiles_and_auto_schedule(orc):
     tiles = np.concatenate([orc.gemm(np.ascontiguousarray(A[:, a:b]), B, algo, threshold=T)
                             for a, b in balanced_slices(m, 2)], axis=1)
     assert np.array_equal(C2.view(np.int64), tiles.view(np.int64))
-    assert names == ["bands", "products", "products_p2p"] and choice1 == choice2 and choice1 in names
+    assert names == ["bands", "products", "products_p2p", "products_rows"] and choice1 == choice2 and choice1 in names
     assert np.array_equal(C.view(np.int64), whole.view(np.int64))
     assert choice3 in ("ctiles", "bands", "products")
     assert np.array_equal(C3.view(np.int64), (tiles if choice3 == "ctiles" else whole).view(np.int64))
-    assert names4 == ["bands", "products"]
+    assert names4 == ["bands", "products", "products_rows"]
     ref4 = orc.dd_op("sub", gen.matrix(W, m, n, 23, 2).reshape(W, -1), whole.reshape(W, -1)).reshape(W, m, n)
     assert np.array_equal(C4.view(np.int64), ref4.view(np.int64))
     assert not np.array_equal(tiles, whole)   # the two schedules round differently
@@ -464,3 +464,18 @@ def test_band_schedule_matches_single_process(orc, cfg, world):
                                                    ref.reshape(W, -1)).reshape(W, m, n)
     assert gr * gc == world and (algo == "block" or d >= 1)
     assert np.array_equal(C.view(np.int64), ref.view(np.int64))
+
+
+@pytest.mark.parametrize("cfg,world", [
+    ((2, "winograd", 4, 37, 29, 33, None), 2),     # k chosen by the balancer (k = 2)
+    ((2, "strassen", 3, 40, 41, 42, 2), 3),        # three ranks, odd band heights
+    ((4, "winograd", 2, 19, 23, 17, 2), 2),        # QD
+    ((2, "winograd", 3, 30, 27, 29, 2), 4),        # four ranks
+])
+def test_rows_combine_matches_single_process(orc, cfg, world):
+    """combine='rows': products exchanged by row bands, every rank combines its band of C
+    through the k levels, rank 0 gathers -- bit-identical to the single-process recursion."""
+    W, algo, T, m, l, n, _ = cfg
+    k, C = _run(cfg, world=world, combine="rows")
+    ref = orc.gemm(gen.matrix(W, m, l, 21, 0), gen.matrix(W, l, n, 21, 1), algo, threshold=T)
+    assert k >= 1 and np.array_equal(C.view(np.int64), ref.view(np.int64))
