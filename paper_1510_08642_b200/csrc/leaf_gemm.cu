@@ -227,6 +227,18 @@ static int launch_cfg(int64_t m, int64_t l, int64_t n, int64_t batch, const MatD
 
 // DDQD_LEAF_CFG selects an alternative tile configuration (tuning experiments only;
 // tools/tune_leaf.py). Every configuration computes the same bits.
+// DDQD_TAIL_CFG (experiments): the DD tail tile -- 0 32x32 (2x2 micro-tile, 256 threads),
+// 1 32x32 (4x4, 64 threads), 2 32x64 (4x4, 128 threads). Measured on c1's tail (fraction of the
+// FP64 peak): 0.699 / 0.648 / 0.669, step 0.969 / 0.982 / 0.976 ms -- the default stays.
+static int tail_cfg() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_TAIL_CFG");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
 static int leaf_cfg_override() {
     static int v = -2;
     if (v == -2) {
@@ -367,6 +379,10 @@ int launch_leaf_gemm(int W, int64_t m, int64_t l, int64_t n, int64_t batch, cons
                 if (tma_enabled() && try_leaf_tma32_dd(m, l, n, batch - b1, A2, B2, C2, beta, mv, s, &rc)) return rc;
                 if (mv == 1) return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2, 1>(m, l, n, batch - b1, A2, B2, C2, beta, s);
                 if (mv == 2) return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2, 2>(m, l, n, batch - b1, A2, B2, C2, beta, s);
+                if (tail_cfg() == 1)   // 64-thread CTAs with 4x4 micro-tiles (16 chains per thread)
+                    return launch_cfg<2, 32, 32, 8, 4, 4, 4, 8>(m, l, n, batch - b1, A2, B2, C2, beta, s);
+                if (tail_cfg() == 2)
+                    return launch_cfg<2, 32, 64, 8, 4, 4, 4, 4>(m, l, n, batch - b1, A2, B2, C2, beta, s);
                 return launch_cfg<2, 32, 32, 16, 2, 2, 3, 2>(m, l, n, batch - b1, A2, B2, C2, beta, s);
             }
         }
