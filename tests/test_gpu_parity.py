@@ -1246,3 +1246,18 @@ def test_host_streamed_two_stage_bitwise(tmp_path, orc):
         r = orc.gemm(A, B, "winograd", threshold=T).ravel()
         refs += [r, r]
     assert same(v, np.concatenate(refs))
+
+
+@pytest.mark.parametrize("m,l", [(128, 257), (192, 129), (127, 257)])
+def test_row_pair_tma_leaf_bitwise(orc, m, l):
+    """Batched Block leaves whose A rows are not 16-byte aligned (odd ld) but whose B rows are:
+    even row counts take the row-pair TMA view (c3's leaf path), an odd row count falls back to
+    the cp.async leaf; both bit-identical to the oracle, element by element, for every leaf."""
+    batch, n = 80, 128
+    A = np.stack([gen.dd_matrix(m, l, 81, b) for b in range(batch)])
+    B = np.stack([gen.dd_matrix(l, n, 82, b) for b in range(batch)])
+    C = torch.empty((batch, 2, m, n), dtype=torch.float64, device=DEV)
+    ddqd.gemm_batched(cu(A), cu(B), C, "block", 1)
+    got = np_(C)
+    for b in range(0, batch, 9):
+        assert same(got[b], orc.gemm(A[b], B[b], "block")), b
