@@ -426,7 +426,13 @@ __global__ void __launch_bounds__(256) post_add_ptr_kernel(int64_t P, const doub
         const int64_t b = t / per, rem = t % per, i = r0 + rem / hn, j = rem % hn;
         T p[7];
 #pragma unroll
-        for (int c = 0; c < 7; c++) p[c] = E::load(ch[7 * b + c] + i * ld + j, ps);
+        for (int c = 0; c < 7; c++) {
+            // the children may live in peer GPUs' memory (CUDA IPC mappings): global loads,
+            // cached in L2 only (a generic load through the pointer table would also work, slower)
+            const double *q = ch[7 * b + c] + i * ld + j;
+#pragma unroll
+            for (int w = 0; w < W; w++) E::set_word(p[c], w, __ldcg(q + w * ps));
+        }
         T c11, c12, c21, c22;
         post_ops<E, ALGO>(p, c11, c12, c21, c22);
         double *cb = C.p + b * C.bs;
