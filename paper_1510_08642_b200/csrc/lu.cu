@@ -855,10 +855,12 @@ __global__ void __launch_bounds__(TB_NT) lu_trsm_blk_kernel(double *A, int64_t n
     using E = elem<W>;
     using T = typename E::T;
     extern __shared__ double sm[];
+    // Ld and Lo rows are padded by one double (33, 225): the staging stores walk i / ii with r
+    // fixed, and an unpadded 32- / 224-double stride put all of them in one bank
     double *Us = sm;                                  // [W][kb][TB_CW]
-    double *Ld = Us + (size_t)W * kb * TB_CW;         // [W][32][32]: Ld[w][i][r]
-    double *Lo = Ld + (size_t)W * 32 * 32;            // [W][TB_LC][224]: Lo[w][ii][r']
-    const int US = kb * TB_CW, LDS_ = 32 * 32, LOS = TB_LC * 224;
+    double *Ld = Us + (size_t)W * kb * TB_CW;         // [W][32][33]: Ld[w][i][r]
+    double *Lo = Ld + (size_t)W * 32 * 33;            // [W][TB_LC][225]: Lo[w][ii][r']
+    const int US = kb * TB_CW, LDS_ = 32 * 33, LOS = TB_LC * 225;
     const int tid = threadIdx.x, lane = tid & 31, wrp = tid >> 5;
     const int64_t col0 = c0 + (int64_t)blockIdx.x * TB_CW;
     const int nc = (int)((c0 + ncols - col0) < TB_CW ? (c0 + ncols - col0) : TB_CW);
@@ -877,7 +879,7 @@ __global__ void __launch_bounds__(TB_NT) lu_trsm_blk_kernel(double *A, int64_t n
             const int r = e / bs, i = e % bs;
             const T l = ldA<W>(A, n, p + b0 + r, p + b0 + i);
 #pragma unroll
-            for (int w = 0; w < W; w++) Ld[w * LDS_ + i * 32 + r] = E::word(l, w);
+            for (int w = 0; w < W; w++) Ld[w * LDS_ + i * 33 + r] = E::word(l, w);
         }
         __syncthreads();
         // (a) diagonal block: warp wrp solves columns wrp (and wrp + 8), lane = row b0 + lane
@@ -897,7 +899,7 @@ __global__ void __launch_bounds__(TB_NT) lu_trsm_blk_kernel(double *A, int64_t n
                 for (int w = 0; w < W; w++) {
                     E::set_word(xa, w, __shfl_sync(0xffffffffu, E::word(va, w), i));
                     E::set_word(xb, w, __shfl_sync(0xffffffffu, E::word(vb, w), i));
-                    E::set_word(l, w, Ld[w * LDS_ + i * 32 + lane]);
+                    E::set_word(l, w, Ld[w * LDS_ + i * 33 + lane]);
                 }
                 const T na = E::sub(va, E::mul(l, xa));
                 const T nb = E::sub(vb, E::mul(l, xb));
@@ -933,7 +935,7 @@ __global__ void __launch_bounds__(TB_NT) lu_trsm_blk_kernel(double *A, int64_t n
                 const int r = e / lc, ii = e % lc;
                 const T l = ldA<W>(A, n, p + rb + r, p + b0 + i0 + ii);
 #pragma unroll
-                for (int w = 0; w < W; w++) Lo[w * LOS + ii * 224 + r] = E::word(l, w);
+                for (int w = 0; w < W; w++) Lo[w * LOS + ii * 225 + r] = E::word(l, w);
             }
             __syncthreads();
             for (int ii = 0; ii < lc; ii++) {
@@ -948,7 +950,7 @@ __global__ void __launch_bounds__(TB_NT) lu_trsm_blk_kernel(double *A, int64_t n
                         const int rr = r < R ? r : R - 1;
                         T l;
 #pragma unroll
-                        for (int w = 0; w < W; w++) E::set_word(l, w, Lo[w * LOS + ii * 224 + rr]);
+                        for (int w = 0; w < W; w++) E::set_word(l, w, Lo[w * LOS + ii * 225 + rr]);
                         const T nv = E::sub(v[k], E::mul(l, x));
                         if (r < R) v[k] = nv;
                     }
@@ -1504,7 +1506,7 @@ static int lu_panel_w(int64_t n, int pivot, double *A, int64_t *ipiv, int64_t p,
         // with half the chain): the per-CTA chain, not the FP64 rate, bounds small panels
         static bool battr[2][64] = {};
         const bool wide = (n2 + 15) / 16 >= 3 * sm_count() / 2;
-        const size_t bsmem = sizeof(double) * W * ((size_t)256 * (wide ? 16 : 8) + 32 * 32 + (size_t)TB_LC * 224);
+        const size_t bsmem = sizeof(double) * W * ((size_t)256 * (wide ? 16 : 8) + 32 * 33 + (size_t)TB_LC * 225);
         auto kfn = wide ? lu_trsm_blk_kernel<W, 256, 16> : lu_trsm_blk_kernel<W, 256, 8>;
         if (!battr[wide][current_device()]) {
             DDQD_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
