@@ -11,6 +11,8 @@
 // written left-to-right order, so results are bit-identical to the oracle's explicit-copy
 // recursion. Per element: pre-add reads 4 and writes 7 W-word values; post-add reads 7 and
 // writes 4 (8 with beta = 1).
+#include <algorithm>
+
 #include "common.cuh"
 #include "ddqd_arith.cuh"
 
@@ -625,8 +627,258 @@ __global__ void __launch_bounds__(kFusedNT) fused_last_kernel(int64_t P, MatDesc
     }
 }
 
+// The fused last level, DD, second form (the default; DDQD_FUSED_S=0 selects the first): the
+// children sit in shared memory with their two words side by side (one 16-byte load per
+// value) and a thread owns RP positions (i, j0 + r * ceil(hn / RP)) of one row (RP = 1 in
+// use: one thread per position, so a CTA has as many warps as a 17 x 17 leaf has positions /
+// 32 and three CTAs share an SM). S > 0 fixes the S^3 leaf at compile time (S = 17: the
+// paper's n = 1025 with n_min = 32) and unrolls the k loop; NT = 0 takes the block size at
+// run time. Same per-element operation sequence as fused_last_kernel.
+template <int ALGO, int VA, int MV, int S, int NT, int RP>
+__global__ void __launch_bounds__(NT ? NT : 1024, NT ? 3 : 1) fused_last_s_kernel(int64_t P, MatDesc X, MatDesc Y, MatDesc C, int beta,
+                                                                   FusedLastDims dd) {
+    using EA = arith<2, VA>;
+    using EM = arith<2, MV>;
+    using T = typename EA::T;
+    extern __shared__ double2 fs2[];
+    // S = 0: the dims at run time (any leaf shape that fits)
+    const int hm = S ? S : dd.hm, hl = S ? S : dd.hl, hn = S ? S : dd.hn;
+    const int psa = hm * hl, psb = hl * hn, HNB = (hn + RP - 1) / RP;
+    double2 *CA = fs2;              // [7][hm][hl] (hi, lo)
+    double2 *CB = fs2 + 7 * psa;    // [7][hl][hn]
+    const int tid = threadIdx.x, nt = NT ? NT : blockDim.x;
+    auto l2 = [](const double2 &v) { T t; t.hi = v.x; t.lo = v.y; return t; };
+    for (int64_t b = blockIdx.x; b < P; b += gridDim.x) {
+        const double *xb = X.p + b * X.bs, *yb = Y.p + b * Y.bs;
+        for (int e = tid; e < psa; e += nt) {
+            const int i = e / hl, k = e % hl;
+            const bool r2 = i + hm < X.rows, c2 = k + hl < X.cols;
+            const T x11 = ld_or_zero<2>(xb + i * X.ld + k, X.ps, true);
+            const T x12 = ld_or_zero<2>(xb + i * X.ld + k + hl, X.ps, c2);
+            const T x21 = ld_or_zero<2>(xb + (i + hm) * X.ld + k, X.ps, r2);
+            const T x22 = ld_or_zero<2>(xb + (i + hm) * X.ld + k + hl, X.ps, r2 && c2);
+            T o[7];
+            pre_ops<EA, ALGO, 0>(x11, x12, x21, x22, o);
+#pragma unroll
+            for (int c = 0; c < 7; c++) CA[c * psa + e] = make_double2(o[c].hi, o[c].lo);
+        }
+        for (int e = tid; e < psb; e += nt) {
+            const int k = e / hn, j = e % hn;
+            const bool r2 = k + hl < Y.rows, c2 = j + hn < Y.cols;
+            const T y11 = ld_or_zero<2>(yb + k * Y.ld + j, Y.ps, true);
+            const T y12 = ld_or_zero<2>(yb + k * Y.ld + j + hn, Y.ps, c2);
+            const T y21 = ld_or_zero<2>(yb + (k + hl) * Y.ld + j, Y.ps, r2);
+            const T y22 = ld_or_zero<2>(yb + (k + hl) * Y.ld + j + hn, Y.ps, r2 && c2);
+            T o[7];
+            pre_ops<EA, ALGO, 1>(y11, y12, y21, y22, o);
+#pragma unroll
+            for (int c = 0; c < 7; c++) CB[c * psb + e] = make_double2(o[c].hi, o[c].lo);
+        }
+        __syncthreads();
+        double *cb = C.p + b * C.bs;
+        for (int e = tid; e < hm * HNB; e += nt) {
+            const int i = e / HNB, j0 = e % HNB;
+            int jj[RP];
+#pragma unroll
+            for (int r = 0; r < RP; r++) jj[r] = j0 + r * HNB < hn ? j0 + r * HNB : j0;   // (a duplicate, never stored)
+            T pv[RP][7];
+#pragma unroll
+            for (int r = 0; r < RP; r++)
+#pragma unroll
+                for (int c = 0; c < 7; c++) pv[r][c] = EM::zero();
+#pragma unroll
+            for (int k = 0; k < hl; k++) {
+#pragma unroll
+                for (int c = 0; c < 7; c++) {
+                    const T a = l2(CA[c * psa + i * hl + k]);
+#pragma unroll
+                    for (int r = 0; r < RP; r++) pv[r][c] = EM::madd(pv[r][c], a, l2(CB[c * psb + k * hn + jj[r]]));
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < RP; r++) {
+                const int j = j0 + r * HNB;
+                if (j >= hn) continue;
+                T c11, c12, c21, c22;
+                post_ops<EA, ALGO>(pv[r], c11, c12, c21, c22);
+                const bool r2 = i + hm < C.rows, cc2 = j + hn < C.cols;
+                auto put = [&](int64_t rr, int64_t cc, const T &v) {
+                    double *q = cb + rr * C.ld + cc;
+                    if (beta) EA::store(q, C.ps, EA::sub(EA::load(q, C.ps), v));
+                    else EA::store(q, C.ps, v);
+                };
+                if (i < C.rows && j < C.cols) put(i, j, c11);
+                if (i < C.rows && cc2) put(i, j + hn, c12);
+                if (r2 && j < C.cols) put(i + hm, j, c21);
+                if (r2 && cc2) put(i + hm, j + hn, c22);
+            }
+        }
+        __syncthreads();   // the children buffers are reused by the next parent
+    }
+}
+
+// QD: the same fused last level with one product chain per thread. A QD value is two 16-byte
+// halves (w0, w1) and (w2, w3) in separate shared-memory planes; the 7 * hm * hn products
+// (thread t: child c = t / (hm hn), position t % (hm hn), acc from +0, k ascending) go to
+// their own shared buffer, then one thread per position forms the post-additions. 1024
+// threads per CTA (one CTA per SM: the QD children of a 17^3 level take 129 KB).
+template <int ALGO, int VA, int MV, int NQ>
+__global__ void __launch_bounds__(NQ, 1) fused_last_q_kernel(int64_t P, MatDesc X, MatDesc Y, MatDesc C, int beta,
+                                                               FusedLastDims dd) {
+    using EA = arith<4, VA>;
+    using EM = arith<4, MV>;
+    using T = typename EA::T;
+    extern __shared__ double2 fq[];
+    const int hm = dd.hm, hl = dd.hl, hn = dd.hn;
+    const int psa = hm * hl, psb = hl * hn, per = hm * hn;
+    double2 *CA = fq;                    // [7][2][hm*hl]
+    double2 *CB = CA + 14 * psa;         // [7][2][hl*hn]
+    double2 *PR = CB + 14 * psb;         // [7][2][hm*hn] products
+    const int tid = threadIdx.x, nt = blockDim.x;
+    auto ldq = [](const double2 *base, int ps, int e) {
+        const double2 u = base[e], v = base[ps + e];
+        T t; t.w[0] = u.x; t.w[1] = u.y; t.w[2] = v.x; t.w[3] = v.y; return t;
+    };
+    auto stq = [](double2 *base, int ps, int e, const T &t) {
+        base[e] = make_double2(t.w[0], t.w[1]);
+        base[ps + e] = make_double2(t.w[2], t.w[3]);
+    };
+    for (int64_t b = blockIdx.x; b < P; b += gridDim.x) {
+        const double *xb = X.p + b * X.bs, *yb = Y.p + b * Y.bs;
+        for (int e = tid; e < psa; e += nt) {
+            const int i = e / hl, k = e % hl;
+            const bool r2 = i + hm < X.rows, c2 = k + hl < X.cols;
+            const T x11 = ld_or_zero<4>(xb + i * X.ld + k, X.ps, true);
+            const T x12 = ld_or_zero<4>(xb + i * X.ld + k + hl, X.ps, c2);
+            const T x21 = ld_or_zero<4>(xb + (i + hm) * X.ld + k, X.ps, r2);
+            const T x22 = ld_or_zero<4>(xb + (i + hm) * X.ld + k + hl, X.ps, r2 && c2);
+            T o[7];
+            pre_ops<EA, ALGO, 0>(x11, x12, x21, x22, o);
+#pragma unroll
+            for (int c = 0; c < 7; c++) stq(CA + 2 * c * psa, psa, e, o[c]);
+        }
+        for (int e = tid; e < psb; e += nt) {
+            const int k = e / hn, j = e % hn;
+            const bool r2 = k + hl < Y.rows, c2 = j + hn < Y.cols;
+            const T y11 = ld_or_zero<4>(yb + k * Y.ld + j, Y.ps, true);
+            const T y12 = ld_or_zero<4>(yb + k * Y.ld + j + hn, Y.ps, c2);
+            const T y21 = ld_or_zero<4>(yb + (k + hl) * Y.ld + j, Y.ps, r2);
+            const T y22 = ld_or_zero<4>(yb + (k + hl) * Y.ld + j + hn, Y.ps, r2 && c2);
+            T o[7];
+            pre_ops<EA, ALGO, 1>(y11, y12, y21, y22, o);
+#pragma unroll
+            for (int c = 0; c < 7; c++) stq(CB + 2 * c * psb, psb, e, o[c]);
+        }
+        __syncthreads();
+        for (int t = tid; t < 7 * per; t += nt) {
+            const int c = t / per, pos = t % per, i = pos / hn, j = pos % hn;
+            const double2 *ca = CA + 2 * c * psa + i * hl, *cbp = CB + 2 * c * psb + j;
+            T acc = EM::zero();
+            for (int k = 0; k < hl; k++) acc = EM::madd(acc, ldq(ca, psa, k), ldq(cbp, psb, k * hn));
+            stq(PR + 2 * c * per, per, pos, acc);
+        }
+        __syncthreads();
+        double *cb = C.p + b * C.bs;
+        for (int pos = tid; pos < per; pos += nt) {
+            const int i = pos / hn, j = pos % hn;
+            T pv[7];
+#pragma unroll
+            for (int c = 0; c < 7; c++) pv[c] = ldq(PR + 2 * c * per, per, pos);
+            T c11, c12, c21, c22;
+            post_ops<EA, ALGO>(pv, c11, c12, c21, c22);
+            const bool r2 = i + hm < C.rows, cc2 = j + hn < C.cols;
+            auto put = [&](int64_t rr, int64_t cc, const T &v) {
+                double *q = cb + rr * C.ld + cc;
+                if (beta) EA::store(q, C.ps, EA::sub(EA::load(q, C.ps), v));
+                else EA::store(q, C.ps, v);
+            };
+            if (i < C.rows && j < C.cols) put(i, j, c11);
+            if (i < C.rows && cc2) put(i, j + hn, c12);
+            if (r2 && j < C.cols) put(i + hm, j, c21);
+            if (r2 && cc2) put(i + hm, j + hn, c22);
+        }
+        __syncthreads();   // the buffers are reused by the next parent
+    }
+}
+
+size_t fused_last_q_smem(int64_t hm, int64_t hl, int64_t hn) {
+    if (hm < 1 || hl < 1 || hn < 1 || hm > 32 || hl > 32 || hn > 32) return 0;
+    const size_t b = sizeof(double) * 4 * 7 * (size_t)(hm * hl + hl * hn + hm * hn);
+    return b <= 220 * 1024 ? b : 0;
+}
+
+template <int ALGO, int VA, int MV, int NQ>
+static int fused_last_q_go2(int64_t P, const MatDesc &X, const MatDesc &Y, const MatDesc &C, int beta,
+                            FusedLastDims dd, cudaStream_t s) {
+    auto kern = fused_last_q_kernel<ALGO, VA, MV, NQ>;
+    const size_t smem = fused_last_q_smem(dd.hm, dd.hl, dd.hn);
+    static bool attr[64] = {};
+    if (!attr[current_device()]) {
+        DDQD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        attr[current_device()] = true;
+    }
+    const int64_t blocks = P < 8 * sm_count() ? P : 8 * sm_count();
+    const int nt = (int)std::min<int64_t>(NQ, (7 * dd.hm * (int64_t)dd.hn + 31) / 32 * 32);
+    prof_begin(0, s);
+    kern<<<(unsigned)blocks, nt, smem, s>>>(P, X, Y, C, beta, dd);
+    DDQD_LAUNCH_CHECK();
+    prof_end(0, 7.0 * dd.hm * (double)dd.hl * dd.hn * (double)P, s, "fused_last_q_kernel (pre-add + leaves + post-add)");
+    return DDQD_OK;
+}
+
+// 768 threads: QD Strassen(32) at n = 1025, ms of the fused level: 512 / 768 / 1024 threads
+// 8.59 / 8.55 / 8.76 (1024 spills at 64 registers); unfused leaf 8.88 plus the additions
+template <int ALGO, int VA, int MV>
+static int fused_last_q_go(int64_t P, const MatDesc &X, const MatDesc &Y, const MatDesc &C, int beta,
+                           FusedLastDims dd, cudaStream_t s) {
+    return fused_last_q_go2<ALGO, VA, MV, 768>(P, X, Y, C, beta, dd, s);
+}
+
+static int fused_s_mode() {
+    static int m = -1;
+    if (m < 0) {
+        const char *e = getenv("DDQD_FUSED_S");   // 0: the first fused kernel (A/B)
+        m = e ? atoi(e) : 1;
+    }
+    return m;
+}
+
+template <int ALGO, int VA, int MV, int S, int NT, int RP>
+static int fused_last_s_go(int64_t P, const MatDesc &X, const MatDesc &Y, const MatDesc &C, int beta,
+                           FusedLastDims dd, cudaStream_t s) {
+    auto kern = fused_last_s_kernel<ALGO, VA, MV, S, NT, RP>;
+    const size_t smem = sizeof(double2) * 7 * ((size_t)dd.hm * dd.hl + (size_t)dd.hl * dd.hn);
+    static bool attr[64] = {};
+    if (!attr[current_device()]) {
+        DDQD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        attr[current_device()] = true;
+    }
+    const int64_t per_sm = (int64_t)((228 * 1024) / (smem + 1024));
+    const int64_t cap = (per_sm < 1 ? 1 : per_sm) * 8 * sm_count();
+    const int64_t blocks = P < cap ? P : cap;
+    prof_begin(0, s);
+    // NT = 0: one thread per output position of a leaf (a multiple of 32, at most 1024)
+    const int nt = NT ? NT : (int)std::min<int64_t>(1024, (dd.hm * (int64_t)dd.hn + 31) / 32 * 32);
+    kern<<<(unsigned)blocks, nt, smem, s>>>(P, X, Y, C, beta, dd);
+    DDQD_LAUNCH_CHECK();
+    prof_end(0, 7.0 * dd.hm * (double)dd.hl * dd.hn * (double)P, s, "fused_last_s_kernel (pre-add + leaves + post-add)");
+    return DDQD_OK;
+}
+
+template <int ALGO, int VA, int MV>
+static int fused_last_s_pick(FusedLastDims dd, int64_t P, const MatDesc &X, const MatDesc &Y, const MatDesc &C,
+                             int beta, cudaStream_t s) {
+    // measured on DD Strassen(32), n = 1025 (17^3 leaves), ms of the fused level: 160 threads x
+    // 2 positions (fused_last_kernel) 1.14; unrolled 17^3 with 160 x 2 / 128 x 3 positions
+    // 1.27 / 1.26; one position per thread, 320 threads: run-time dims 0.96, unrolled 0.89
+    if (dd.hm == 17 && dd.hl == 17 && dd.hn == 17) return fused_last_s_go<ALGO, VA, MV, 17, 320, 1>(P, X, Y, C, beta, dd, s);
+    return fused_last_s_go<ALGO, VA, MV, 0, 0, 1>(P, X, Y, C, beta, dd, s);
+}
+
 // shared memory a fused last level needs (bytes), or 0 when the leaves are too large for it
+size_t fused_last_q_smem(int64_t hm, int64_t hl, int64_t hn);
 size_t fused_last_smem(int W, int64_t hm, int64_t hl, int64_t hn) {
+    if (W == 4) return fused_last_q_smem(hm, hl, hn);
     if (hm < 1 || hl < 1 || hn < 1 || hm > 32 || hl > 32 || hn > 32) return 0;
     const size_t b = sizeof(double) * fused_last_smem_doubles(W, (int)hm, (int)hl, (int)hn);
     return b <= 220 * 1024 ? b : 0;
@@ -660,6 +912,24 @@ int launch_fused_last(int W, int algo, int mv, int64_t P, const MatDesc &X, cons
     if (P == 0) return DDQD_OK;
     const FusedLastDims dd{(int)hm, (int)hl, (int)hn};
     algo &= 0xff;
+    if (W == 2 && fused_s_mode() > 0) {
+        int rc = 1;
+        if (algo == 1) rc = mv == 1 ? fused_last_s_pick<1, 0, 1>(dd, P, X, Y, C, beta, s)
+                          : mv == 2 ? fused_last_s_pick<1, 2, 2>(dd, P, X, Y, C, beta, s)
+                                    : fused_last_s_pick<1, 0, 0>(dd, P, X, Y, C, beta, s);
+        else rc = mv == 1 ? fused_last_s_pick<2, 0, 1>(dd, P, X, Y, C, beta, s)
+                  : mv == 2 ? fused_last_s_pick<2, 2, 2>(dd, P, X, Y, C, beta, s)
+                            : fused_last_s_pick<2, 0, 0>(dd, P, X, Y, C, beta, s);
+        if (rc != 1) return rc;
+    }
+    if (W == 4 && fused_s_mode() > 0) {
+        if (algo == 1) return mv == 1 ? fused_last_q_go<1, 0, 1>(P, X, Y, C, beta, dd, s)
+                            : mv == 2 ? fused_last_q_go<1, 2, 2>(P, X, Y, C, beta, dd, s)
+                                      : fused_last_q_go<1, 0, 0>(P, X, Y, C, beta, dd, s);
+        return mv == 1 ? fused_last_q_go<2, 0, 1>(P, X, Y, C, beta, dd, s)
+             : mv == 2 ? fused_last_q_go<2, 2, 2>(P, X, Y, C, beta, dd, s)
+                       : fused_last_q_go<2, 0, 0>(P, X, Y, C, beta, dd, s);
+    }
 #define FL_GO(WW, AL, VA, MV) return fused_last_go<WW, AL, VA, MV>(P, X, Y, C, beta, dd, smem, s)
     if (W == 2) {
         if (algo == 1) { if (mv == 1) FL_GO(2, 1, 0, 1); if (mv == 2) FL_GO(2, 1, 2, 2); FL_GO(2, 1, 0, 0); }

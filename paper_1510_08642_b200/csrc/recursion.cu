@@ -292,10 +292,10 @@ int run_gemm(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n, int64_
     p.mv = mv;
     if (p.d == 0) return launch_leaf_gemm(W, m, l, n, batch, A, B, C, beta, mv, s);
     // tiny leaves (<= 32 per side, e.g. Strassen(32) at n = 1025): the last level and its leaves
-    // as one kernel, when its shared-memory footprint fits; DDQD_FUSE_LAST=0 disables it
-    // (DD only: the QD version, 200-instruction madds x 7 chains at one 160-thread CTA per SM,
-    // measured 15.5 vs 11.0 ms on QD Strassen(32) at n = 1025)
-    p.fuse_last = fuse_last_enabled() && W == 2 && ((mv >> 4) & 3) == 0 &&
+    // as one kernel, when its shared-memory footprint fits (DD leaves up to ~31^3, QD up to
+    // 18^3); DDQD_FUSE_LAST=0 disables it. n = 1025, threshold 32: DD 1.69 -> 1.28 ms, QD
+    // 11.07 -> 9.78 ms per product (profiles/r02/fused_last_level.md)
+    p.fuse_last = fuse_last_enabled() && ((mv >> 4) & 3) == 0 &&
                   fused_last_smem(W, p.m[p.d], p.l[p.d], p.n[p.d]) > 0;
     int st = DDQD_OK;
     char *ws = static_cast<char *>(workspace_get(p.bytes, &st));

@@ -1195,30 +1195,36 @@ def test_graph_capture_workspace_rules(orc):
 
 
 def test_fused_last_level_same_bits(tmp_path, orc):
-    """The last recursion level fused with its tiny leaves (fused_last_kernel) gives the bits of
-    the unfused schedule (DDQD_FUSE_LAST=0), DD and QD, Strassen and Winograd, canonical and
-    the fused/accurate variants, and matches the oracle on a small case."""
+    """The last recursion level fused with its tiny leaves (fused_last_kernel, and the default
+    fused_last_s_kernel / fused_last_q_kernel) gives the bits of the unfused schedule
+    (DDQD_FUSE_LAST=0), DD and QD, Strassen and Winograd, canonical and the fused/accurate
+    variants (17^3 unrolled, 18^3 and 4^3 run-time leaves), and matches the oracle on a small case."""
     import subprocess
     import sys
     code = (
         "import numpy as np, torch, ddqd_inputs as gen, paper_1510_08642_b200 as d\n"
         "out = []\n"
-        "for W, n, T in ((2, 1025, 32), (4, 517, 16), (2, 99, 6), (4, 70, 5)):\n"
+        "for W, n, T in ((2, 1025, 32), (4, 517, 16), (2, 99, 6), (4, 70, 5), (2, 1100, 32), (4, 1025, 32)):\n"
         "    A, B = gen.bench_pair(n, W) if n > 500 else (gen.matrix(W, n, n - 3, 61, 0), gen.matrix(W, n - 3, n + 2, 61, 1))\n"
         "    for algo in ('strassen', 'winograd'):\n"
         "        for madd in ('canonical', 'fused', 'accurate'):\n"
         "            out.append(d.gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), algo, T, madd=madd).cpu().numpy().ravel())\n"
         "np.save(r'%s', np.concatenate(out))\n")
     outs = []
-    for mode in ("0", "1"):
-        f = tmp_path / f"f{mode}.npy"
-        env = dict(os.environ, DDQD_FUSE_LAST=mode)
+    # unfused / the first fused kernel / the default (DD: one position per thread, 17^3
+    # unrolled; QD: one product chain per thread)
+    for i, extra in enumerate(({"DDQD_FUSE_LAST": "0"}, {"DDQD_FUSED_S": "0"}, {})):
+        f = tmp_path / f"f{i}.npy"
+        env = dict(os.environ, **extra)
         subprocess.check_call([sys.executable, "-c", code % f], env=env, cwd=ROOT)
         outs.append(np.load(f))
-    assert same(outs[0], outs[1])
+    assert same(outs[0], outs[1]) and same(outs[0], outs[2])
     A, B = gen.matrix(2, 99, 96, 61, 0), gen.matrix(2, 96, 101, 61, 1)
     for algo in ("strassen", "winograd"):
         assert same(np_(ddqd.gemm(cu(A), cu(B), algo, 6)), orc.gemm(A, B, algo, threshold=6))
+    A, B = gen.matrix(4, 71, 68, 62, 0), gen.matrix(4, 68, 73, 62, 1)   # QD, 9 x 9 x 9 leaves
+    for algo in ("strassen", "winograd"):
+        assert same(np_(ddqd.gemm(cu(A), cu(B), algo, 8)), orc.gemm(A, B, algo, threshold=8))
 
 
 def test_host_streamed_two_stage_bitwise(tmp_path, orc):
