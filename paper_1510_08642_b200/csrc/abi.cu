@@ -265,18 +265,26 @@ static int check_gemm_args(int64_t m, int64_t l, int64_t n, int algo, int64_t T)
 
 size_t streamed_top_bytes(int W, int64_t m, int64_t l, int64_t n);   // recursion.cu
 int run_gemm_streamed(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n, const MatDesc &A,
-                      const MatDesc &B, const MatDesc &C, char *tws, cudaEvent_t rest_ready,
-                      cudaStream_t s, int (*on_quad)(int q, void *ctx), void *ctx, cudaEvent_t mid_ready,
-                      char *tws2);
+                      const MatDesc &B, const MatDesc &C, char *const *tws, const cudaEvent_t *ready, int front,
+                      int tail, cudaStream_t s, int (*on_block)(int64_t r0, int64_t nr, int64_t c0, int64_t nc, void *ctx),
+                      void *ctx);
 
-// DDQD_HOST_DEEP=0 keeps M1's inputs as one copy stage (A/B measurements), =2 uses two stages
-// whatever the size (tests); default: two stages when A11 + B11 are >= 64 MB
+// DDQD_HOST_DEEP=0 keeps M1's inputs as one copy stage (A/B measurements), =2 nests as deep as
+// the recursion allows (up to 3, tests); default: one level deeper while that level's leading
+// blocks of A and B are >= 64 MB. DDQD_HOST_TAIL: the same for the last product's split
+// (0 off, 2 as deep as possible; default while the blocks it completes are >= 16 MB).
+static int host_mode(const char *name) {
+    const char *e = getenv(name);
+    return (e && (e[0] == '0' || e[0] == '2')) ? e[0] - '0' : 1;
+}
 static int host_deep_mode() {
     static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("DDQD_HOST_DEEP");
-        v = (e && (e[0] == '0' || e[0] == '2')) ? e[0] - '0' : 1;
-    }
+    if (v < 0) v = host_mode("DDQD_HOST_DEEP");
+    return v;
+}
+static int host_tail_mode() {
+    static int v = -1;
+    if (v < 0) v = host_mode("DDQD_HOST_TAIL");
     return v;
 }
 
@@ -291,12 +299,14 @@ static bool host_stream_enabled() {
 }
 
 // copy stream + events of the overlapped host path, per host thread and device
+constexpr int kHostLevels = 4;   // nested streamed levels (M1 front, M4 tail) + the top level
 struct CopyRes {
     cudaStream_t cs = nullptr;
-    cudaEvent_t start = nullptr, first = nullptr, mid = nullptr, rest = nullptr, quad = nullptr;
+    cudaEvent_t start = nullptr, first = nullptr, quad = nullptr;
+    cudaEvent_t ready[kHostLevels] = {};   // ready[j]: the level-j leading blocks of A and B resident
 };
 
-// device-to-host copy of one finished C quadrant on the copy stream (run_gemm_streamed's hook)
+// device-to-host copy of one finished block of C on the copy stream (run_gemm_streamed's hook)
 struct QuadCopy {
     CopyRes *cr;
     cudaStream_t s;
@@ -305,12 +315,9 @@ struct QuadCopy {
     const double *dC;
     double *hC;
 };
-static int copy_quad(int q, void *ctx) {
+static int copy_block(int64_t r0, int64_t nr, int64_t c0, int64_t nc, void *ctx) {
     const QuadCopy &c = *static_cast<QuadCopy *>(ctx);
-    const int64_t hm = (c.m + 1) / 2, hn = (c.n + 1) / 2;
-    const int64_t r0 = q >= 2 ? hm : 0, nr = q >= 2 ? c.m - hm : hm;
-    const int64_t c0 = (q & 1) ? hn : 0, nc = (q & 1) ? c.n - hn : hn;
-    if (nr == 0 || nc == 0) return DDQD_OK;
+    if (nr <= 0 || nc <= 0) return DDQD_OK;
     DDQD_CUDA_CHECK(cudaEventRecord(c.cr->quad, c.s));
     DDQD_CUDA_CHECK(cudaStreamWaitEvent(c.cr->cs, c.cr->quad, 0));
     const size_t d8 = sizeof(double);
@@ -328,9 +335,8 @@ static int copy_res(CopyRes **out) {
         DDQD_CUDA_CHECK(cudaStreamCreateWithFlags(&r.cs, cudaStreamNonBlocking));
         DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.start, cudaEventDisableTiming));
         DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.first, cudaEventDisableTiming));
-        DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.mid, cudaEventDisableTiming));
-        DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.rest, cudaEventDisableTiming));
         DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&r.quad, cudaEventDisableTiming));
+        for (auto &e : r.ready) DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     *out = &r;
     return DDQD_OK;
@@ -360,29 +366,47 @@ static int gemm_entry(int W, int64_t m, int64_t l, int64_t n, const double *A, c
     // host path: stage through library-owned device memory, copy back, synchronise
     const bool streamed = (algo & 0xff) == DDQD_WINOGRAD && !(algo & 0xff0000) &&
                           std::min(std::min(m, l), n) > T && host_stream_enabled();
-    const int64_t qm = (m + 1) / 2, ql = (l + 1) / 2, qn = (n + 1) / 2;
-    // two-stage arrival of A11, B11 (their own leading quadrants first, so M1's first product
-    // starts after 1/16 of the inputs) when M1 itself recurses and the copies are large
-    const bool deep = streamed && std::min(std::min(qm, ql), qn) > T && host_deep_mode() &&
-                      (host_deep_mode() == 2 || (size_t)W * (qm * ql + ql * qn) * sizeof(double) >= (size_t(64) << 20));
+    // the nested levels' shapes (ceil halving) and children workspaces
+    int64_t dm[kHostLevels + 1], dl[kHostLevels + 1], dn[kHostLevels + 1];
+    dm[0] = m; dl[0] = l; dn[0] = n;
+    for (int j = 0; j < kHostLevels; j++) { dm[j + 1] = (dm[j] + 1) / 2; dl[j + 1] = (dl[j] + 1) / 2; dn[j + 1] = (dn[j] + 1) / 2; }
+    auto recurses = [&](int j) { return std::min(std::min(dm[j], dl[j]), dn[j]) > T; };
+    const size_t d8 = sizeof(double);
+    // front: M1 streamed this many levels deeper (its own leading blocks first)
+    int front = 0;
+    if (streamed && host_deep_mode())
+        while (front + 1 < kHostLevels && recurses(front + 1) &&
+               (host_deep_mode() == 2 || (size_t)W * (dm[front + 1] * dl[front + 1] + dl[front + 1] * dn[front + 1]) * d8 >= (size_t(64) << 20)))
+            front++;
+    // C copied back block by block (each block while the next products run) when a quadrant is
+    // >= 32 MB; measured on c2 (8 MB quadrants) the split products cost more than the
+    // overlapped copy gains (10.5 vs 10.2 ms), on c3 (268 MB) it saves 14 ms per call
+    const bool quads = streamed && (size_t)W * dm[1] * dn[1] * d8 >= (size_t(32) << 20);
+    // tail: the last product split this many levels deep (only its last block waits)
+    int tail = 0;
+    if (quads && host_tail_mode())
+        while (tail + 1 < kHostLevels && recurses(tail + 1) &&
+               (host_tail_mode() == 2 || (size_t)W * dm[tail + 2] * dn[tail + 2] * d8 >= (size_t(16) << 20)))
+            tail++;
     const size_t oB = (bA + 255) & ~size_t(255), oC = oB + ((bB + 255) & ~size_t(255)),
                  oT = oC + ((bC + 255) & ~size_t(255));
-    const size_t oT2 = oT + (streamed ? streamed_top_bytes(W, m, l, n) : 0);
+    size_t ot[kHostLevels + 1];
+    ot[0] = oT;
+    const int nlev = streamed ? 1 + std::max(front, tail) : 0;
+    for (int j = 0; j < kHostLevels; j++) ot[j + 1] = ot[j] + (j < nlev ? streamed_top_bytes(W, dm[j], dl[j], dn[j]) : 0);
     int st = DDQD_OK;
-    char *dev = static_cast<char *>(buf_get(g_stage, oT2 + (deep ? streamed_top_bytes(W, qm, ql, qn) : 0) + 256,
-                                            &st, "staging buffers"));
+    char *dev = static_cast<char *>(buf_get(g_stage, ot[kHostLevels] + 256, &st, "staging buffers"));
     if (st) return st;
     double *dA = reinterpret_cast<double *>(dev);
     double *dB = reinterpret_cast<double *>(dev + oB);
     double *dC = reinterpret_cast<double *>(dev + oC);
     MatDesc mA{dA, m, l, l, m * l, 0}, mB{dB, l, n, n, l * n, 0}, mC{dC, m, n, n, m * n, 0};
     if (streamed) {
-        // Winograd: A11 and B11 first on the copy stream; M1 = A11 B11 runs while the rest of
-        // A and B is copied (run_gemm_streamed); bitwise the same result as the plain path
+        // Winograd: the innermost leading blocks of A and B first on the copy stream; M1 (its
+        // own M1 first, `front` levels deep) runs while the rest of A and B is copied
+        // (run_gemm_streamed); bitwise the same result as the plain path
         CopyRes *cr;
         if ((rc = copy_res(&cr))) return rc;
-        const int64_t hm = (m + 1) / 2, hl = (l + 1) / 2, hn = (n + 1) / 2;
-        const size_t d8 = sizeof(double);
         cudaStream_t cs = cr->cs;
         DDQD_CUDA_CHECK(cudaEventRecord(cr->start, s));
         DDQD_CUDA_CHECK(cudaStreamWaitEvent(cs, cr->start, 0));
@@ -397,38 +421,27 @@ static int gemm_entry(int W, int64_t m, int64_t l, int64_t n, const double *A, c
             }
             return DDQD_OK;
         };
-        if (deep) {
-            // stage 1: A11's and B11's leading quadrants; stage 2: the rest of A11 and B11
-            const int64_t hm2 = (hm + 1) / 2, hl2 = (hl + 1) / 2, hn2 = (hn + 1) / 2;
-            if ((rc = blk(dA, A, m, l, 0, 0, hm2, hl2)) || (rc = blk(dB, B, l, n, 0, 0, hl2, hn2))) return rc;
-            DDQD_CUDA_CHECK(cudaEventRecord(cr->first, cs));
-            if ((rc = blk(dA, A, m, l, 0, hl2, hm2, hl - hl2)) || (rc = blk(dA, A, m, l, hm2, 0, hm - hm2, hl)) ||
-                (rc = blk(dB, B, l, n, 0, hn2, hl2, hn - hn2)) || (rc = blk(dB, B, l, n, hl2, 0, hl - hl2, hn)))
+        // stage 1: the level-(front + 1) leading blocks; then, level by level outwards, the rest
+        // of the level-j leading blocks (ready[j]); ready[0]: all of A and B
+        const int f1 = front + 1;
+        if ((rc = blk(dA, A, m, l, 0, 0, dm[f1], dl[f1])) || (rc = blk(dB, B, l, n, 0, 0, dl[f1], dn[f1]))) return rc;
+        DDQD_CUDA_CHECK(cudaEventRecord(cr->first, cs));
+        for (int j = front; j >= 0; j--) {
+            // level j's leading blocks (all of A and B at j = 0) minus level j + 1's
+            const int64_t am = j ? dm[j] : m, al = j ? dl[j] : l, bn = j ? dn[j] : n;
+            if ((rc = blk(dA, A, m, l, 0, dl[j + 1], dm[j + 1], al - dl[j + 1])) ||
+                (rc = blk(dA, A, m, l, dm[j + 1], 0, am - dm[j + 1], al)) ||
+                (rc = blk(dB, B, l, n, 0, dn[j + 1], dl[j + 1], bn - dn[j + 1])) ||
+                (rc = blk(dB, B, l, n, dl[j + 1], 0, al - dl[j + 1], bn)))
                 return rc;
-            DDQD_CUDA_CHECK(cudaEventRecord(cr->mid, cs));
-        } else {
-            if ((rc = blk(dA, A, m, l, 0, 0, hm, hl)) || (rc = blk(dB, B, l, n, 0, 0, hl, hn))) return rc;
-            DDQD_CUDA_CHECK(cudaEventRecord(cr->first, cs));
+            DDQD_CUDA_CHECK(cudaEventRecord(cr->ready[j], cs));
         }
-        for (int w = 0; w < W; w++) {
-            DDQD_CUDA_CHECK(cudaMemcpy2DAsync(dA + w * m * l + hl, l * d8, A + w * m * l + hl, l * d8,
-                                              (l - hl) * d8, hm, cudaMemcpyHostToDevice, cs));
-            DDQD_CUDA_CHECK(cudaMemcpyAsync(dA + w * m * l + hm * l, A + w * m * l + hm * l, (m - hm) * l * d8,
-                                            cudaMemcpyHostToDevice, cs));
-            DDQD_CUDA_CHECK(cudaMemcpy2DAsync(dB + w * l * n + hn, n * d8, B + w * l * n + hn, n * d8,
-                                              (n - hn) * d8, hl, cudaMemcpyHostToDevice, cs));
-            DDQD_CUDA_CHECK(cudaMemcpyAsync(dB + w * l * n + hl * n, B + w * l * n + hl * n, (l - hl) * n * d8,
-                                            cudaMemcpyHostToDevice, cs));
-        }
-        DDQD_CUDA_CHECK(cudaEventRecord(cr->rest, cs));
         DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, cr->first, 0));
-        // C quadrant by quadrant (each copied back while the next products run) when a quadrant
-        // is >= 32 MB; measured on c2 (8 MB quadrants) the split products cost more than the
-        // overlapped copy gains (10.5 vs 10.2 ms), on c3 (268 MB) it saves 14 ms per call
-        const bool quads = (size_t)W * hm * hn * d8 >= (size_t(32) << 20);
         QuadCopy qc{cr, s, W, m, n, dC, C};
-        rc = run_gemm_streamed(W, algo, T, m, l, n, mA, mB, mC, dev + oT, cr->rest, s,
-                               quads ? copy_quad : nullptr, &qc, deep ? cr->mid : nullptr, dev + oT2);
+        char *tws[kHostLevels];
+        for (int j = 0; j < kHostLevels; j++) tws[j] = dev + ot[j];
+        rc = run_gemm_streamed(W, algo, T, m, l, n, mA, mB, mC, tws, cr->ready, front, tail, s,
+                               quads ? copy_block : nullptr, &qc);
         // the copy stream must not outlive the call into the caller's buffers
         cudaError_t e = cudaStreamSynchronize(cs);
         if (rc) return rc;

@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(ADD2_THREADS, ADD2_MINB) pre_add2_kernel(int64
 // Q >= 0 forms only C quadrant Q (0 = C11, 1 = C12, 2 = C21, 3 = C22; the other values and the
 // products they alone read are dead code): the host-streamed top level writes C quadrant by
 // quadrant so each one's device-to-host copy overlaps the remaining products.
-template <int W, int ALGO, int V, int Q = -1>
+template <int W, int ALGO, int V>
 __global__ void __launch_bounds__(256) post_add_kernel(int64_t P, MatDesc M, MatDesc C, int beta) {
     using E = arith<W, V>;
     using T = typename E::T;
@@ -210,10 +210,10 @@ __global__ void __launch_bounds__(256) post_add_kernel(int64_t P, MatDesc M, Mat
             if (beta) E::store(q, C.ps, E::sub(E::load(q, C.ps), v));
             else E::store(q, C.ps, v);
         };
-        if ((Q < 0 || Q == 0) && i < C.rows && j < C.cols) put(i, j, c11);
-        if ((Q < 0 || Q == 1) && i < C.rows && cc2) put(i, j + hn, c12);
-        if ((Q < 0 || Q == 2) && r2 && j < C.cols) put(i + hm, j, c21);
-        if ((Q < 0 || Q == 3) && r2 && cc2) put(i + hm, j + hn, c22);
+        if (i < C.rows && j < C.cols) put(i, j, c11);
+        if (i < C.rows && cc2) put(i, j + hn, c12);
+        if (r2 && j < C.cols) put(i + hm, j, c21);
+        if (r2 && cc2) put(i + hm, j + hn, c22);
     }
 }
 
@@ -376,36 +376,61 @@ int launch_post_add(int W, int algo, int64_t P, const MatDesc &M, const MatDesc 
     return acc ? post_dispatch<4, 2>(algo, P, M, C, beta, s) : post_dispatch<4, 0>(algo, P, M, C, beta, s);
 }
 
-template <int W, int V>
-static int post_quad_dispatch(int algo, int q, const MatDesc &M, const MatDesc &C, cudaStream_t s) {
-    const int64_t total = M.rows * M.cols;
-    if (total == 0) return DDQD_OK;
+// One C quadrant Q of a single parent's post-addition, restricted to the positions
+// [r0, r0 + nr) x [c0, c0 + nc) of the hm x hn product grid (hm, hn = M.rows, M.cols): the
+// host-streamed top level forms a quadrant block by block as its products complete.
+template <int W, int ALGO, int V, int Q>
+__global__ void __launch_bounds__(256) post_region_kernel(MatDesc M, MatDesc C, int64_t r0, int64_t nr, int64_t c0,
+                                                          int64_t nc) {
+    using E = arith<W, V>;
+    using T = typename E::T;
+    const int64_t hm = M.rows, hn = M.cols;
+    const int64_t total = nr * nc;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = r0 + t / nc, j = c0 + t % nc;
+        T p[7];
+#pragma unroll
+        for (int c = 0; c < 7; c++) p[c] = E::load(M.p + c * M.bs + i * M.ld + j, M.ps);
+        T c11, c12, c21, c22;
+        post_ops<E, ALGO>(p, c11, c12, c21, c22);
+        const int64_t r = i + (Q >= 2 ? hm : 0), cc = j + ((Q & 1) ? hn : 0);
+        if (r < C.rows && cc < C.cols)
+            E::store(C.p + r * C.ld + cc, C.ps, Q == 0 ? c11 : Q == 1 ? c12 : Q == 2 ? c21 : c22);
+    }
+}
+
+template <int W, int V, int ALGO>
+static int post_region_dispatch(int q, const MatDesc &M, const MatDesc &C, int64_t r0, int64_t nr, int64_t c0,
+                                int64_t nc, cudaStream_t s) {
+    const int64_t total = nr * nc;
+    if (total <= 0) return DDQD_OK;
     const unsigned g = grid_for(total);
     static const double reads[2][4] = {{4, 2, 2, 4}, {2, 4, 4, 4}};   // products read: Strassen, Winograd
     prof_begin(2, s);
-    if (algo == 1) {
-        if (q == 0) post_add_kernel<W, 1, V, 0><<<g, 256, 0, s>>>(1, M, C, 0);
-        else if (q == 1) post_add_kernel<W, 1, V, 1><<<g, 256, 0, s>>>(1, M, C, 0);
-        else if (q == 2) post_add_kernel<W, 1, V, 2><<<g, 256, 0, s>>>(1, M, C, 0);
-        else post_add_kernel<W, 1, V, 3><<<g, 256, 0, s>>>(1, M, C, 0);
-    } else {
-        if (q == 0) post_add_kernel<W, 2, V, 0><<<g, 256, 0, s>>>(1, M, C, 0);
-        else if (q == 1) post_add_kernel<W, 2, V, 1><<<g, 256, 0, s>>>(1, M, C, 0);
-        else if (q == 2) post_add_kernel<W, 2, V, 2><<<g, 256, 0, s>>>(1, M, C, 0);
-        else post_add_kernel<W, 2, V, 3><<<g, 256, 0, s>>>(1, M, C, 0);
-    }
+    if (q == 0) post_region_kernel<W, ALGO, V, 0><<<g, 256, 0, s>>>(M, C, r0, nr, c0, nc);
+    else if (q == 1) post_region_kernel<W, ALGO, V, 1><<<g, 256, 0, s>>>(M, C, r0, nr, c0, nc);
+    else if (q == 2) post_region_kernel<W, ALGO, V, 2><<<g, 256, 0, s>>>(M, C, r0, nr, c0, nc);
+    else post_region_kernel<W, ALGO, V, 3><<<g, 256, 0, s>>>(M, C, r0, nr, c0, nc);
     DDQD_LAUNCH_CHECK();
-    prof_end(2, (double)total * W * 8.0 * (reads[algo == 2][q] + 1.0), s, "post_add_kernel (one C quadrant)");
+    prof_end(2, (double)total * W * 8.0 * (reads[ALGO == 2][q] + 1.0), s, "post_region_kernel (one C quadrant)");
     return DDQD_OK;
 }
 
-// one C quadrant of a single parent's post-addition (the host-streamed top level)
-int launch_post_quad(int W, int algo, int q, const MatDesc &M, const MatDesc &C, cudaStream_t s) {
+// one C quadrant of a single parent's post-addition (the host-streamed top level), over the
+// position block [r0, r0 + nr) x [c0, c0 + nc) (nr < 0: the whole M.rows x M.cols grid)
+int launch_post_quad(int W, int algo, int q, const MatDesc &M, const MatDesc &C, cudaStream_t s, int64_t r0,
+                     int64_t nr, int64_t c0, int64_t nc) {
     const bool acc = (algo & DDQD_ADD_ACCURATE) != 0;
     algo &= 0xff;
     if (q < 0 || q > 3 || (algo != 1 && algo != 2)) { set_error("launch_post_quad: bad quadrant/algo"); return DDQD_EINVAL; }
-    if (W == 2) return acc ? post_quad_dispatch<2, 2>(algo, q, M, C, s) : post_quad_dispatch<2, 0>(algo, q, M, C, s);
-    return acc ? post_quad_dispatch<4, 2>(algo, q, M, C, s) : post_quad_dispatch<4, 0>(algo, q, M, C, s);
+    if (nr < 0) { r0 = 0; nr = M.rows; c0 = 0; nc = M.cols; }
+#define PQ(WW, VV) return algo == 1 ? post_region_dispatch<WW, VV, 1>(q, M, C, r0, nr, c0, nc, s) \
+                                    : post_region_dispatch<WW, VV, 2>(q, M, C, r0, nr, c0, nc, s)
+    if (W == 2) { if (acc) PQ(2, 2); PQ(2, 0); }
+    if (acc) PQ(4, 2);
+    PQ(4, 0);
+#undef PQ
 }
 
 // ---- post-addition over peer memory (the multi-GPU fused combine) --------

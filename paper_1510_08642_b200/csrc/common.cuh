@@ -74,8 +74,10 @@ int launch_pre_add2(int W, int algo, int side, int64_t P, const MatDesc &X, int6
                     int64_t h1c, const MatDesc &Y, cudaStream_t s);
 int launch_post_add2(int W, int algo, int64_t P, const MatDesc &M, int64_t h1m, int64_t h1n,
                      const MatDesc &C, int beta, cudaStream_t s);
-// One C quadrant q (0 C11, 1 C12, 2 C21, 3 C22) of a single parent's post-addition.
-int launch_post_quad(int W, int algo, int q, const MatDesc &M, const MatDesc &C, cudaStream_t s);
+// One C quadrant q (0 C11, 1 C12, 2 C21, 3 C22) of a single parent's post-addition, over the
+// product-grid positions [r0, r0 + nr) x [c0, c0 + nc) (nr < 0: all of them).
+int launch_post_quad(int W, int algo, int q, const MatDesc &M, const MatDesc &C, cudaStream_t s, int64_t r0 = 0,
+                     int64_t nr = -1, int64_t c0 = 0, int64_t nc = 0);
 // Post-addition with the 7P children addressed through a device pointer array (peer memory).
 int launch_post_add_ptrs(int W, int algo, int64_t P, const double *const *ch, int64_t hm, int64_t hn,
                          int64_t ld, int64_t ps, int64_t r0, int64_t r1, const MatDesc &C, int beta,

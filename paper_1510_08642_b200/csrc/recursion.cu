@@ -17,6 +17,7 @@
 // split-k factor of the leaves.
 #include <algorithm>
 #include <cstdlib>
+#include <functional>
 #include <vector>
 
 #include "common.cuh"
@@ -310,15 +311,16 @@ namespace ddqd {
 // ---- host-streamed top level (the host-pointer entry, Winograd) -----------------------------
 // Winograd's first product M1 = A11 B11 reads only the leading quadrants, so the host
 // path copies A11 and B11 first and runs M1 while the copy engine brings in the rest of A and
-// B; then the top level's pre-additions and the other products in an order that completes C
+// B (`front` levels deep: M1's own M1 first, on the leading quadrants of A11 and B11, ...);
+// then the top level's pre-additions and the other products in an order that completes C
 // quadrant by quadrant -- C11 = U1 after M2; C22 = U7 after M6, M7, M5; C12 = U5 after M3;
-// C21 = U6 after M4 -- each quadrant formed by its own post-addition pass (the same chain of
-// DD/QD operations per element) and handed to on_quad, which starts its device-to-host copy
-// while the next products run (for a small C -- on_quad null -- M2..M7 run as one batch and
-// one post-addition forms C: there the batch's fuller waves are worth more than the overlapped
-// copy). Each product is the same recursion as in run_gemm (the
-// planner's chunking never changes the arithmetic), so the result is bitwise that of the
-// device-pointer call.
+// C21 = U6 after M4 (itself split `tail` levels deep, so C21 completes block by block) --
+// each block formed by its own post-addition pass (the same chain of DD/QD operations per
+// element) and handed to on_block, which starts its device-to-host copy while the next
+// products run (for a small C -- on_block null -- M2..M7 run as one batch and one
+// post-addition forms C: there the batch's fuller waves are worth more than the overlapped
+// copy). Each product is the same recursion as in run_gemm (the planner's chunking never
+// changes the arithmetic), so the result is bitwise that of the device-pointer call.
 #define return_if_err(expr)        \
     do {                           \
         const int rc__ = (expr);   \
@@ -329,6 +331,14 @@ static void top_shapes(int64_t m, int64_t l, int64_t n, int64_t *hm, int64_t *hl
     *hm = (m + 1) / 2; *hl = (l + 1) / 2; *hn = (n + 1) / 2;
 }
 
+// the 7 children (r x c, planar, workspace leading dimension) of one streamed level at base
+static MatDesc kid_desc(int W, char *base, int64_t r, int64_t c) {
+    MatDesc d;
+    d.p = reinterpret_cast<double *>(base);
+    d.rows = r; d.cols = c; d.ld = ws_ld(c); d.ps = r * d.ld; d.bs = (int64_t)W * d.ps;
+    return d;
+}
+
 size_t streamed_top_bytes(int W, int64_t m, int64_t l, int64_t n) {
     int64_t hm, hl, hn;
     top_shapes(m, l, n, &hm, &hl, &hn);
@@ -336,56 +346,105 @@ size_t streamed_top_bytes(int W, int64_t m, int64_t l, int64_t n) {
     return align256(w * hm * ws_ld(hl)) + align256(w * hl * ws_ld(hn)) + align256(w * hm * ws_ld(hn));
 }
 
+// The last product one level deeper per level of `levels` (Winograd): Aop Bop -> Mout
+// (hm x hl x hn) formed as the subproblem's recursion -- pre-additions into tws[0], the
+// children in the order {M1, M2} {M5, M6, M7} {M3} {M4}, each group followed by the
+// post-addition of the Mout block it completes (C11 = U1, C22 = U7, C12 = U5, C21 = U6) and
+// done(block) -- with the last child (M4) itself split the same way while levels remain. The
+// same operations per element as run_gemm on the subproblem, so the same bits.
+using BlockDone = std::function<int(int64_t r0, int64_t nr, int64_t c0, int64_t nc)>;
+static int tail_rec(int W, int algo, int add_algo, int64_t T, int64_t hm, int64_t hl, int64_t hn, const MatDesc &Aop,
+                    const MatDesc &Bop, const MatDesc &Mout, char *const *tws, int levels, cudaStream_t s,
+                    const BlockDone &done) {
+    if (levels <= 0 || std::min(std::min(hm, hl), hn) <= T) {
+        return_if_err(run_gemm(W, algo, T, hm, hl, hn, 1, Aop, Bop, Mout, 0, s));
+        return done(0, hm, 0, hn);
+    }
+    int64_t h2m, h2l, h2n;
+    top_shapes(hm, hl, hn, &h2m, &h2l, &h2n);
+    const size_t w = (size_t)7 * W * sizeof(double);
+    const MatDesc sA = kid_desc(W, tws[0], h2m, h2l);
+    const MatDesc sB = kid_desc(W, tws[0] + align256(w * h2m * ws_ld(h2l)), h2l, h2n);
+    const MatDesc sM = kid_desc(W, tws[0] + align256(w * h2m * ws_ld(h2l)) + align256(w * h2l * ws_ld(h2n)), h2m, h2n);
+    return_if_err(launch_pre_add(W, add_algo, 0, 1, Aop, sA, s));
+    return_if_err(launch_pre_add(W, add_algo, 1, 1, Bop, sB, s));
+    // Mout's block of child-grid positions [r0, r0 + nr) x [c0, c0 + nc) in quadrant q is final
+    auto sub_done = [&](int q, int64_t r0, int64_t nr, int64_t c0, int64_t nc) -> int {
+        return_if_err(launch_post_quad(W, add_algo, q, sM, Mout, s, r0, nr, c0, nc));
+        const int64_t mr = r0 + (q >= 2 ? h2m : 0), mc = c0 + ((q & 1) ? h2n : 0);
+        nr = std::min(nr, hm - mr);
+        nc = std::min(nc, hn - mc);
+        return nr > 0 && nc > 0 ? done(mr, nr, mc, nc) : DDQD_OK;
+    };
+    static const int sub[3][3] = {{0, 2, 0}, {4, 3, 3}, {2, 1, 1}};
+    for (const auto &ss : sub) {
+        return_if_err(run_gemm(W, algo, T, h2m, h2l, h2n, ss[1], shift(sA, ss[0]), shift(sB, ss[0]),
+                               shift(sM, ss[0]), 0, s));
+        return_if_err(sub_done(ss[2], 0, h2m, 0, h2n));
+    }
+    MatDesc m4 = shift(sM, 3);
+    m4.bs = 0;
+    return tail_rec(W, algo, add_algo, T, h2m, h2l, h2n, shift(sA, 3), shift(sB, 3), m4, tws + 1, levels - 1, s,
+                    [&](int64_t r0, int64_t nr, int64_t c0, int64_t nc) { return sub_done(2, r0, nr, c0, nc); });
+}
+
 int run_gemm_streamed(int W, int algo, int64_t T, int64_t m, int64_t l, int64_t n, const MatDesc &A,
-                      const MatDesc &B, const MatDesc &C, char *tws, cudaEvent_t rest_ready,
-                      cudaStream_t s, int (*on_quad)(int q, void *ctx), void *ctx, cudaEvent_t mid_ready,
-                      char *tws2) {
+                      const MatDesc &B, const MatDesc &C, char *const *tws, const cudaEvent_t *ready, int front,
+                      int tail, cudaStream_t s, int (*on_block)(int64_t r0, int64_t nr, int64_t c0, int64_t nc, void *ctx),
+                      void *ctx) {
     int64_t hm, hl, hn;
     top_shapes(m, l, n, &hm, &hl, &hn);
     const size_t w = (size_t)7 * W * sizeof(double);
-    auto kid = [&](char *base, int64_t r, int64_t c) {
-        MatDesc d;
-        d.p = reinterpret_cast<double *>(base);
-        d.rows = r; d.cols = c; d.ld = ws_ld(c); d.ps = r * d.ld; d.bs = (int64_t)W * d.ps;
-        return d;
-    };
-    const MatDesc cA = kid(tws, hm, hl);
-    const MatDesc cB = kid(tws + align256(w * hm * ws_ld(hl)), hl, hn);
-    const MatDesc cM = kid(tws + align256(w * hm * ws_ld(hl)) + align256(w * hl * ws_ld(hn)), hm, hn);
+    const MatDesc cA = kid_desc(W, tws[0], hm, hl);
+    const MatDesc cB = kid_desc(W, tws[0] + align256(w * hm * ws_ld(hl)), hl, hn);
+    const MatDesc cM = kid_desc(W, tws[0] + align256(w * hm * ws_ld(hl)) + align256(w * hl * ws_ld(hn)), hm, hn);
     const int add_algo = (algo & 0xff) | (algo & DDQD_ADD_ACCURATE);
-    int rc;
     {
         NvtxRange nv("M1 = A11 B11 (overlaps the H2D copy)");
         MatDesc a11 = A, b11 = B;
         a11.rows = hm; a11.cols = hl; b11.rows = hl; b11.cols = hn;
-        if (mid_ready) {
+        if (front > 0 && std::min(std::min(hm, hl), hn) > T) {
             // M1 streamed one level deeper: its own first product (A11's and B11's leading
-            // quadrants, copied first) runs while the rest of A11 and B11 arrives, then its other
-            // six products as one batch and one post-addition -- the subproblem's recursion, so
-            // the same bits as run_gemm on it
-            return_if_err(run_gemm_streamed(W, algo, T, hm, hl, hn, a11, b11, cM, tws2, mid_ready, s, nullptr,
-                                            nullptr, nullptr, nullptr));
-        } else if ((rc = run_gemm(W, algo, T, hm, hl, hn, 1, a11, b11, cM, 0, s))) {
-            return rc;
+            // quadrants, copied first) runs while the rest of A11 and B11 arrives (ready[1]),
+            // then its other six products as one batch and one post-addition -- the
+            // subproblem's recursion, so the same bits as run_gemm on it
+            return_if_err(run_gemm_streamed(W, algo, T, hm, hl, hn, a11, b11, cM, tws + 1, ready + 1, front - 1, 0, s,
+                                            nullptr, nullptr));
+        } else {
+            return_if_err(run_gemm(W, algo, T, hm, hl, hn, 1, a11, b11, cM, 0, s));
         }
     }
-    DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, rest_ready, 0));
+    DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, ready[0], 0));
     NvtxRange nv("level 0 (streamed)");
-    if ((rc = launch_pre_add(W, add_algo, 0, 1, A, cA, s))) return rc;
-    if ((rc = launch_pre_add(W, add_algo, 1, 1, B, cB, s))) return rc;
-    if (!on_quad) {   // small C: M2..M7 as one batch (better filled waves), one post-addition
-        if ((rc = run_gemm(W, algo, T, hm, hl, hn, 6, shift(cA, 1), shift(cB, 1), shift(cM, 1), 0, s))) return rc;
+    return_if_err(launch_pre_add(W, add_algo, 0, 1, A, cA, s));
+    return_if_err(launch_pre_add(W, add_algo, 1, 1, B, cB, s));
+    if (!on_block) {   // small C: M2..M7 as one batch (better filled waves), one post-addition
+        return_if_err(run_gemm(W, algo, T, hm, hl, hn, 6, shift(cA, 1), shift(cB, 1), shift(cM, 1), 0, s));
         return launch_post_add(W, add_algo, 1, cM, C, 0, s);
     }
+    // C's quadrant-q block of product-grid positions [r0, r0 + nr) x [c0, c0 + nc) is final:
+    // form it and hand it over (its device-to-host copy starts while the next products run)
+    auto quad_done = [&](int q, int64_t r0, int64_t nr, int64_t c0, int64_t nc) -> int {
+        return_if_err(launch_post_quad(W, add_algo, q, cM, C, s, r0, nr, c0, nc));
+        const int64_t cr = r0 + (q >= 2 ? hm : 0), cc = c0 + ((q & 1) ? hn : 0);
+        nr = std::min(nr, m - cr);
+        nc = std::min(nc, n - cc);
+        return nr > 0 && nc > 0 ? on_block(cr, nr, cc, nc, ctx) : DDQD_OK;
+    };
     // (first product index, count) of each step, then the quadrant it completes
-    static const int steps[4][3] = {{1, 1, 0}, {4, 3, 3}, {2, 1, 1}, {3, 1, 2}};
+    static const int steps[3][3] = {{1, 1, 0}, {4, 3, 3}, {2, 1, 1}};
     for (const auto &st : steps) {
-        if ((rc = run_gemm(W, algo, T, hm, hl, hn, st[1], shift(cA, st[0]), shift(cB, st[0]),
-                           shift(cM, st[0]), 0, s))) return rc;
-        if ((rc = launch_post_quad(W, add_algo, st[2], cM, C, s))) return rc;
-        if (on_quad && (rc = on_quad(st[2], ctx))) return rc;
+        return_if_err(run_gemm(W, algo, T, hm, hl, hn, st[1], shift(cA, st[0]), shift(cB, st[0]),
+                               shift(cM, st[0]), 0, s));
+        return_if_err(quad_done(st[2], 0, hm, 0, hn));
     }
-    return DDQD_OK;
+    // the last product M4 (which only C21 = U3 - M4 waits for), `tail` levels deeper: C21 is
+    // formed and copied back block by block, only its last block after the compute
+    NvtxRange nv4("M4 (C21 block by block)");
+    MatDesc m4 = shift(cM, 3);
+    m4.bs = 0;
+    return tail_rec(W, algo, add_algo, T, hm, hl, hn, shift(cA, 3), shift(cB, 3), m4, tws + 1, tail, s,
+                    [&](int64_t r0, int64_t nr, int64_t c0, int64_t nc) { return quad_done(2, r0, nr, c0, nc); });
 }
 
 }  // namespace ddqd

@@ -1254,6 +1254,38 @@ def test_host_streamed_two_stage_bitwise(tmp_path, orc):
     assert same(v, np.concatenate(refs))
 
 
+def test_host_streamed_tail_blocks_bitwise(tmp_path):
+    """Host-pointer Winograd large enough for the block-by-block copy-back (C quadrants >= 32 MB):
+    the last product M4 runs one or more levels deeper and C21 is formed and copied back block
+    by block; M1 streamed as deep as the recursion allows with DDQD_HOST_DEEP=2. Bit-identical
+    to the device-pointer call and to DDQD_HOST_TAIL=0 / DDQD_HOST_DEEP=0 (M4 in one pass, M1
+    on one copy stage), DD and QD, odd shapes (ragged halves at every level)."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, ddqd_inputs as gen, paper_1510_08642_b200 as d\n"
+        "out = []\n"
+        "for W, m, l, n, T in ((2, 3001, 263, 2999, 64), (4, 2049, 133, 2051, 32)):\n"
+        "    A, B = gen.matrix(W, m, l, 73, 0), gen.matrix(W, l, n, 73, 1)\n"
+        "    h = d.gemm(torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory(), 'winograd', T).numpy()\n"
+        "    g = d.gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), 'winograd', T).cpu().numpy()\n"
+        "    out += [h.ravel(), g.ravel()]\n"
+        "np.save(r'%s', np.concatenate(out))\n")
+    outs = []
+    for i, extra in enumerate(({}, {"DDQD_HOST_TAIL": "0", "DDQD_HOST_DEEP": "0"},
+                               {"DDQD_HOST_TAIL": "2", "DDQD_HOST_DEEP": "2"})):
+        f = tmp_path / f"t{i}.npy"
+        subprocess.check_call([sys.executable, "-c", code % f], env=dict(os.environ, **extra), cwd=ROOT)
+        outs.append(np.load(f))
+    assert same(outs[0], outs[1]) and same(outs[0], outs[2])
+    v = outs[0]
+    k = 0
+    for W, m, n in ((2, 3001, 2999), (4, 2049, 2051)):
+        sz = W * m * n
+        assert same(v[k:k + sz], v[k + sz:k + 2 * sz])   # host == device pointers
+        k += 2 * sz
+
+
 @pytest.mark.parametrize("m,l", [(128, 257), (192, 129), (127, 257)])
 def test_row_pair_tma_leaf_bitwise(orc, m, l):
     """Batched Block leaves whose A rows are not 16-byte aligned (odd ld) but whose B rows are:
