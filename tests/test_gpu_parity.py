@@ -264,6 +264,30 @@ def test_gemm_ex_strided_beta1(orc, algo):
     assert same(np_(g)[:, 70:70 + m, 65:65 + n], ref)
 
 
+@pytest.mark.parametrize("W", [2, 4])
+@pytest.mark.parametrize("algo", ["strassen", "winograd"])
+def test_gemm_ex_beta1_fused_last_level(orc, W, algo):
+    """C := C - A B where the fused last level is the top level (its beta = 1 epilogue): the
+    unrolled 17^3 DD kernel (34^3, T = 32), run-time leaves (30 x 20 x 31, T = 16), and a
+    fused level below an unfused one (60 x 40 x 62, T = 16), strided sub-blocks, DD and QD."""
+    N = 140
+    big = gen.matrix(W, N, N, 12, 0)
+    for (m, l, n, T) in ((34, 34, 34, 32), (30, 20, 31, 16), (60, 40, 62, 16)):
+        A = big[:, 3:3 + m, 70:70 + l].copy()
+        B = big[:, 72:72 + l, 1:1 + n].copy()
+        C0 = big[:, 75:75 + m, 71:71 + n].copy()
+        Tm = orc.gemm(A, B, algo, threshold=T)
+        op = orc.dd_op if W == 2 else orc.qd_op
+        ref = op("sub", C0.reshape(W, -1), Tm.reshape(W, -1)).reshape(W, m, n)
+        g = cu(big)
+        base, ps = g.data_ptr(), N * N
+        ddqd.gemm_ex(W, algo, T, m, l, n, 1,
+                     base + 8 * (3 * N + 70), N, ps, 0,
+                     base + 8 * (72 * N + 1), N, ps, 0,
+                     base + 8 * (75 * N + 71), N, ps, 0, beta=1)
+        assert same(np_(g)[:, 75:75 + m, 71:71 + n], ref), (m, l, n, T)
+
+
 # ---- paper benchmark pair (P:61) ----------------------------------------------------
 @pytest.mark.parametrize("n", [1023, 1024, 1025])
 def test_paper_pair_columns_and_parity(orc, n):
