@@ -901,8 +901,11 @@ def main():
                        "depth": d, "leaf_shape": list(shapes[-1]), "leaf_madds_per_step": leaf_madds_step,
                        "l2": "no flush: each operand (%.2f GB) exceeds the 126 MB L2" % (A.numel() * 8 / 1e9),
                        "parallelism": schedule_desc(args, sched, world),
-                       "schedule_timings_ms": ({k: v * 1e3 for k, v in sched.timings.items()}
+                       "schedule_timings_ms": ({k: (v * 1e3 if math.isfinite(v) else None)
+                                                for k, v in sched.timings.items()}
                                                if getattr(sched, "timings", None) else None),
+                       **({"schedules_unavailable": sched.unavailable}
+                          if getattr(sched, "unavailable", None) else {}),
                        **({"transport": "FUNCTIONAL TEST ONLY: all ranks on one GPU, gloo staged through "
                                         "host memory (not a bench number)"} if args.staged_transport else {})},
             "roofline": roofline,

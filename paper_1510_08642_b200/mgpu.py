@@ -47,6 +47,10 @@ from __future__ import annotations
 import math
 
 
+class ScheduleUnavailable(RuntimeError):
+    """A schedule cannot run on this machine; raised on every rank at the same point."""
+
+
 def rec_shapes(m, l, n, T):
     shapes = [(m, l, n)]
     while min(m, l, n) > T:
@@ -479,43 +483,67 @@ class DistributedGemm:
             return self._p2p
         W, bk, dist = self.W, self.backend, self.dist
         local, handles, frees = {}, {}, []
-        # one interprocess event per level (k: the products, k-1 .. 0: the combine levels)
-        events = [bk.ipc_event(like) for _ in range(self.k + 1)]
-        handles["events"] = [h for _, h in events]
-        for level in range(1, self.k + 1):
-            mj, _, nj = self.shapes[level]
-            sl = self.slices if level == self.k else self.pslices[level]
-            cnt = max(1, max(hi - lo for lo, hi in sl))
-            t, h, f = bk.ipc_alloc((cnt, W, mj, nj), like)
-            local[level], handles[level] = t, h
-            frees.append(f)
-        if self.rank == 0:
-            t, h, f = bk.ipc_alloc((W, self.m, self.n), like)
-            local["C"], handles["C"] = t, h
-            frees.append(f)
+        # Every local failure (allocation, exporting or opening a peer's handle) is agreed on by
+        # all ranks before anyone leaves the setup, so a machine without CUDA IPC between its
+        # GPUs makes every rank raise ScheduleUnavailable at the same point (and the automatic
+        # choice drops the schedule) instead of leaving the other ranks waiting in a collective.
+        err = None
+        events = []
+        try:
+            # one interprocess event per level (k: the products, k-1 .. 0: the combine levels)
+            events = [bk.ipc_event(like) for _ in range(self.k + 1)]
+            handles["events"] = [h for _, h in events]
+            for level in range(1, self.k + 1):
+                mj, _, nj = self.shapes[level]
+                sl = self.slices if level == self.k else self.pslices[level]
+                cnt = max(1, max(hi - lo for lo, hi in sl))
+                t, h, f = bk.ipc_alloc((cnt, W, mj, nj), like)
+                local[level], handles[level] = t, h
+                frees.append(f)
+            if self.rank == 0:
+                t, h, f = bk.ipc_alloc((W, self.m, self.n), like)
+                local["C"], handles["C"] = t, h
+                frees.append(f)
+        except Exception as e:   # noqa: BLE001  (reported collectively below)
+            err = f"rank {self.rank}: {type(e).__name__}: {e}"
+        handles["error"] = err
         allh = [None] * self.world
         dist.all_gather_object(allh, handles)
-        views, closes = {}, []
-        for level in range(1, self.k + 1):
-            mj, _, nj = self.shapes[level]
-            sl = self.slices if level == self.k else self.pslices[level]
-            for r in range(self.world):
-                if r == self.rank:
-                    views[(level, r)] = local[level]
+        errs = [h["error"] for h in allh if h.get("error")]
+        views, closes, ev = {}, [], None
+        if not errs:
+            try:
+                for level in range(1, self.k + 1):
+                    mj, _, nj = self.shapes[level]
+                    sl = self.slices if level == self.k else self.pslices[level]
+                    for r in range(self.world):
+                        if r == self.rank:
+                            views[(level, r)] = local[level]
+                        else:
+                            cnt = max(1, max(hi - lo for lo, hi in sl))
+                            v, c = bk.ipc_open(allh[r][level], (cnt, W, mj, nj), like)
+                            views[(level, r)] = v
+                            closes.append(c)
+                if self.rank == 0:
+                    views["C"] = local["C"]
                 else:
-                    cnt = max(1, max(hi - lo for lo, hi in sl))
-                    v, c = bk.ipc_open(allh[r][level], (cnt, W, mj, nj), like)
-                    views[(level, r)] = v
+                    v, c = bk.ipc_open(allh[0]["C"], (W, self.m, self.n), like)
+                    views["C"] = v
                     closes.append(c)
-        if self.rank == 0:
-            views["C"] = local["C"]
-        else:
-            v, c = bk.ipc_open(allh[0]["C"], (W, self.m, self.n), like)
-            views["C"] = v
-            closes.append(c)
-        ev = {"own": [e for e, _ in events],
-              "peers": {r: [bk.open_event(h, like) for h in allh[r]["events"]]
-                        for r in range(self.world) if r != self.rank}}
+                ev = {"own": [e for e, _ in events],
+                      "peers": {r: [bk.open_event(h, like) for h in allh[r]["events"]]
+                                for r in range(self.world) if r != self.rank}}
+            except Exception as e:   # noqa: BLE001
+                err = f"rank {self.rank}: {type(e).__name__}: {e}"
+            allerr = [None] * self.world
+            dist.all_gather_object(allerr, err)
+            errs = [x for x in allerr if x]
+        if errs:
+            for c in closes:
+                bk.ipc_close(c)
+            for f in frees:
+                bk.ipc_free(f)
+            raise ScheduleUnavailable("p2p combine unavailable: " + "; ".join(errs))
         # host-only rendezvous for the per-level barriers: an NCCL barrier is a device collective
         # that waits for this rank's queued kernels, which is what the events are there to avoid
         hb = dist.barrier
@@ -854,6 +882,7 @@ class AutoDistributedGemm:
         self.cands = {c: make[c]() for c in names}
         self.choice = None
         self.timings = {}
+        self.unavailable = {}
 
     def _timed(self, name, A, B, C):
         import time
@@ -874,7 +903,12 @@ class AutoDistributedGemm:
             for name in self.cands:
                 if keep is not None:
                     C.copy_(keep)
-                self.timings[name] = self._timed(name, A, B, C)
+                try:
+                    self.timings[name] = self._timed(name, A, B, C)
+                except ScheduleUnavailable as e:   # raised on every rank alike: drop it
+                    self.timings[name] = float("inf")
+                    self.unavailable[name] = str(e)
+                    continue
                 last = name
             self.choice = min(self.timings, key=self.timings.get)
             if keep is not None:

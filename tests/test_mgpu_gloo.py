@@ -411,6 +411,66 @@ def test_c_tiles_and_auto_schedule(orc):
     ref4 = orc.dd_op("sub", gen.matrix(W, m, n, 23, 2).reshape(W, -1), whole.reshape(W, -1)).reshape(W, m, n)
     assert np.array_equal(C4.view(np.int64), ref4.view(np.int64))
     assert not np.array_equal(tiles, whole)   # the two schedules round differently
+class _NoPeerBackend(OracleBackend):
+    """Rank `bad` cannot map peer memory (a box without CUDA IPC between its GPUs)."""
+
+    def __init__(self, W, bad):
+        super().__init__(W)
+        self.bad = bad
+
+    def ipc_open(self, handle, shape, like):
+        if dist.get_rank() == self.bad:
+            raise RuntimeError("cudaIpcOpenMemHandle: peer access unsupported")
+        return super().ipc_open(handle, shape, like)
+
+
+def _unavail_worker(rank, world, port, cfg, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), OMP_NUM_THREADS="1")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1510_08642_b200.mgpu import AutoDistributedGemm, DistributedGemm, ScheduleUnavailable
+        W, algo, T, m, l, n = cfg
+        A = torch.from_numpy(gen.matrix(W, m, l, 29, 0)) if rank == 0 else torch.zeros((W, m, l), dtype=torch.float64)
+        B = torch.from_numpy(gen.matrix(W, l, n, 29, 1)) if rank == 0 else torch.zeros((W, l, n), dtype=torch.float64)
+        C = torch.zeros((W, m, n), dtype=torch.float64)
+        raised = None
+        try:   # the p2p schedule alone: every rank raises, none is left in a collective
+            DistributedGemm(W, algo, T, m, l, n, dist, backend=_NoPeerBackend(W, 1), combine="p2p")(A, B, C)
+        except ScheduleUnavailable as e:
+            raised = str(e)
+        ag = AutoDistributedGemm(W, algo, T, m, l, n, dist, backend=_NoPeerBackend(W, 1))
+        ag(A, B, C)
+        dist.barrier()
+        q.put((rank, raised, ag.choice, sorted(ag.unavailable), C.numpy().copy() if rank == 0 else None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_p2p_unavailable_is_dropped_on_every_rank(orc):
+    """A rank that cannot open its peers' memory makes the p2p combine raise ScheduleUnavailable
+    on EVERY rank at the same point (the failure is agreed on before anyone leaves the setup),
+    and the automatic choice (BJ:5 (4)) drops it and returns another bit-identical schedule's
+    result -- the driver's multi-GPU run must not hang or crash on a box without CUDA IPC."""
+    cfg = (2, "strassen", 4, 21, 19, 23)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_unavail_worker, args=(r, 2, port, cfg, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    W, algo, T, m, l, n = cfg
+    whole = orc.gemm(gen.matrix(W, m, l, 29, 0), gen.matrix(W, l, n, 29, 1), algo, threshold=T)
+    for rank, raised, choice, unavailable, _ in res:
+        assert raised and "rank 1" in raised and "peer access unsupported" in raised
+        assert unavailable == ["products_p2p"] and choice in ("bands", "products", "products_rows")
+    assert res[0][2] == res[1][2]
+    assert np.array_equal(res[0][4].view(np.int64), whole.view(np.int64))
+
+
 # ---- band schedule (BandGemm: each rank one tile of C, the whole problem's tree) ---------------
 def _band_worker(rank, world, port, cfg, q):
     # one OpenMP thread per rank: several ranks spinning on all cores crawl
