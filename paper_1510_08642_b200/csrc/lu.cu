@@ -69,6 +69,8 @@ struct LuAux {
     int info;
     int skip;
     double rinv[4];
+    int miss;   // split panel: some row outranked the speculated pivot, or a zero pivot
+    int pad;
 };
 
 // is candidate (a, ia) preferred over (b, ib)? larger magnitude; ties -> lower row; -1 = none
@@ -214,10 +216,13 @@ template <int W>
 __global__ void __launch_bounds__(512) lu_panel_coop_kernel(double *A, int64_t n, int64_t p, int kb,
                                                             int rows_per, int pivot, int64_t *ipiv,
                                                             LuAux *aux, double *scr, int probe, int spec,
-                                                            double *fscr) {
+                                                            double *fscr, const int *gate) {
     using E = elem<W>;
     using T = typename E::T;
     namespace cg = cooperative_groups;
+    // gate: the split panel's miss flag -- the fallback launch runs only when the split path's
+    // speculation failed (every CTA reads the same value, so all return together)
+    if (gate && __ldcg(gate) == 0) return;
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double sm[];
     const int G = gridDim.x;
@@ -666,6 +671,268 @@ __global__ void __launch_bounds__(512) lu_panel_coop_kernel(double *A, int64_t n
     }
 }
 
+// ---- blocked speculated panel: 64-column sub-panels, no grid-wide barrier -----------------------
+// The speculated-pivot panel (r = k at every step, verified) as a blocked LU of the panel itself.
+// With the pivot rows known in advance, sub-panel q (columns [p0, p0 + w), w <= 64) splits into
+//  D. its w x w diagonal block: the sequential part, ONE CTA with the block in shared memory
+//     (two CTA barriers per column, no cross-SM traffic);
+//  B. the rows below it, columns [p0, p0 + w): each row needs only D's U rows, so warps
+//     eliminate their own rows column by column (lanes hold columns, the multiplier is
+//     broadcast with shuffles);
+//  T. the block's rows right of it: U12 := L11^-1 A12 (the warp TRSM kernel, column-parallel);
+//  G. the rows below x the columns right: a_ij := a_ij - l_ik u_kj for k = p0 .. p0+w-1 in order.
+// Every element receives exactly the operations of the right-looking column steps
+// (l_ik = a_ik * (1 / u_kk), a_ij := a_ij - l_ik * u_kj, k ascending), so the factors are the
+// bits of the cooperative kernel and the oracle when the speculation holds. At column k every
+// row below checks that it does not outrank u_kk in the DD/QD magnitude order (the test that
+// makes the argmax pick row k); a zero pivot also counts as a miss. The panel is snapshotted
+// first; after a miss the later kernels return at once, the snapshot is restored and the gated
+// cooperative kernel factors the panel with the full pivot search.
+constexpr int kSubSB = 32;     // sub-panel width
+constexpr int kSubDiagNT = 288; // 8 bulk warps + the chain warp
+
+// D: the w x w (w <= 32) diagonal block of sub-panel [p0, p0 + w). Warp 8 (the chain warp) owns
+// row kk+1 in step kk: it scales it, updates it and forms the next reciprocal 1/u_{kk+1,kk+1}
+// (the dependent chain mul -> sub(mul) -> div of every column) while warps 0-7 update rows
+// kk+2.. (warp wr: rows kk+2+wr+8t; lane: column kk+1+lane); one CTA barrier per column.
+template <int W>
+__global__ void __launch_bounds__(kSubDiagNT, 1) lu_subdiag_kernel(double *A, int64_t n, int64_t p0, int w, int pivot,
+                                                                   int *miss, double *rv_out) {
+    using E = elem<W>;
+    using T = typename E::T;
+    if (__ldcg(miss)) return;
+    constexpr int SB = kSubSB, SS = SB * SB, NT = kSubDiagNT;
+    __shared__ double S[W * SS];        // [W][SB][SB]
+    __shared__ double s_r[2 * 4];       // 1 / u_kk, by step parity
+    const int tid = threadIdx.x, lane = tid & 31, wr = tid >> 5;
+    {
+        T v[(SS + NT - 1) / NT];
+#pragma unroll
+        for (int it = 0; it < (SS + NT - 1) / NT; it++) {
+            const int e = tid + NT * it, i = e / SB, j = e % SB;
+            v[it] = (e < SS && i < w && j < w) ? ldA<W>(A, n, p0 + i, p0 + j) : E::zero();
+        }
+#pragma unroll
+        for (int it = 0; it < (SS + NT - 1) / NT; it++)
+            if (tid + NT * it < SS) sts<W>(S, SS, tid + NT * it, v[it]);
+    }
+    __syncthreads();
+    if (tid == 0) sts<W>(s_r, 1, 0, E::div(E::one(), lds<W>(S, SS, 0)));
+    __syncthreads();
+    bool bad = false;
+    for (int kk = 0; kk < w; kk++) {
+        const T akk = lds<W>(S, SS, kk * SB + kk);
+        const T rinv = lds<W>(s_r + (kk & 1) * W, 1, 0);
+        if (tid == 0) {
+            if (E::word(akk, 0) == 0.0) bad = true;
+            for (int ww = 0; ww < W; ww++) rv_out[ww * SB + kk] = E::word(rinv, ww);   // for B
+        }
+        const int j = kk + 1 + lane;
+        if (wr == 8) {
+            const int i = kk + 1;
+            if (i < w) {
+                const T a = lds<W>(S, SS, i * SB + kk);
+                if (pivot && lane == 0 && E::abs_gt(a, akk)) bad = true;
+                const T lv = E::mul(a, rinv);
+                if (j < w) {
+                    const T v = E::sub(lds<W>(S, SS, i * SB + j), E::mul(lv, lds<W>(S, SS, kk * SB + j)));
+                    sts<W>(S, SS, i * SB + j, v);
+                    if (lane == 0) sts<W>(s_r + ((kk + 1) & 1) * W, 1, 0, E::div(E::one(), v));
+                }
+                __syncwarp();
+                if (lane == 0) sts<W>(S, SS, i * SB + kk, lv);
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+                const int i = kk + 2 + wr + 8 * t;
+                if (i >= w) break;
+                const T a = lds<W>(S, SS, i * SB + kk);
+                if (pivot && lane == 0 && E::abs_gt(a, akk)) bad = true;
+                const T lv = E::mul(a, rinv);
+                if (j < w)
+                    sts<W>(S, SS, i * SB + j, E::sub(lds<W>(S, SS, i * SB + j), E::mul(lv, lds<W>(S, SS, kk * SB + j))));
+                __syncwarp();
+                if (lane == 0) sts<W>(S, SS, i * SB + kk, lv);
+            }
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < w * w; e += NT) {
+        const int i = e / w, jj = e % w;
+        stA<W>(A, n, p0 + i, p0 + jj, lds<W>(S, SS, i * SB + jj));
+    }
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(miss, 1);
+}
+
+template <int W> struct SubBelow {
+    static constexpr int RW = 1;                   // rows per warp
+    static constexpr int NT = 128;
+    static constexpr int ROWS = RW * (NT / 32);    // rows per CTA
+};
+
+// B: rows [r0, r0 + rows) x columns [p0, p0 + w): column elimination with the U rows and
+// reciprocals of the sub-panel's diagonal block (staged whole in shared memory)
+template <int W>
+__global__ void __launch_bounds__(SubBelow<W>::NT) lu_subbelow_kernel(double *A, int64_t n, int64_t p0, int w,
+                                                                      int pivot, int *miss, int64_t r0,
+                                                                      int64_t rows, const double *rv_in) {
+    using E = elem<W>;
+    using T = typename E::T;
+    constexpr int SB = kSubSB, NS = SB / 32, SS = SB * SB, RW = SubBelow<W>::RW, NT = SubBelow<W>::NT;
+    if (__ldcg(miss)) return;
+    __shared__ double U[W * SS];        // [W][SB][SB]
+    __shared__ double Rv[W * SB];       // [W][SB]
+    const int tid = threadIdx.x, lane = tid & 31, wrp = tid >> 5;
+    {
+        T v[SS / NT];
+#pragma unroll
+        for (int it = 0; it < SS / NT; it++) {
+            const int e = tid + NT * it, i = e / SB, j = e % SB;
+            v[it] = (j >= i && i < w && j < w) ? ldA<W>(A, n, p0 + i, p0 + j) : E::zero();
+        }
+#pragma unroll
+        for (int it = 0; it < SS / NT; it++) sts<W>(U, SS, tid + NT * it, v[it]);
+    }
+    __syncthreads();
+    if (tid < W * SB) Rv[tid] = rv_in[tid];   // D's reciprocals 1 / u_kk (the same bits)
+    const int64_t rb = r0 + (int64_t)blockIdx.x * SubBelow<W>::ROWS + (int64_t)wrp * RW;
+    T acc[RW][NS];
+#pragma unroll
+    for (int r = 0; r < RW; r++)
+#pragma unroll
+        for (int t = 0; t < NS; t++) {
+            const int j = lane + 32 * t;
+            acc[r][t] = (rb + r < r0 + rows && j < w) ? ldA<W>(A, n, rb + r, p0 + j) : E::zero();
+        }
+    __syncthreads();
+    bool bad = false;
+#pragma unroll
+    for (int s = 0; s < NS; s++) {
+        if (32 * s >= w) break;
+        for (int kl = 0; kl < 32; kl++) {
+            const int k = 32 * s + kl;
+            if (k >= w) break;
+            const T ukk = lds<W>(U, SS, k * SB + k);
+            const T rinv = lds<W>(Rv, SB, k);
+            T u[NS];
+#pragma unroll
+            for (int t = s; t < NS; t++) u[t] = lds<W>(U, SS, k * SB + lane + 32 * t);
+#pragma unroll
+            for (int r = 0; r < RW; r++) {
+                T a;
+#pragma unroll
+                for (int ww = 0; ww < W; ww++) E::set_word(a, ww, __shfl_sync(0xffffffffu, E::word(acc[r][s], ww), kl));
+                if (pivot && rb + r < r0 + rows && E::abs_gt(a, ukk)) bad = true;
+                const T lv = E::mul(a, rinv);
+                {
+                    const int j = lane + 32 * s;
+                    const T nv = E::sub(acc[r][s], E::mul(lv, u[s]));
+                    if (lane == kl) acc[r][s] = lv;
+                    else if (lane > kl && j < w) acc[r][s] = nv;
+                }
+#pragma unroll
+                for (int t = s + 1; t < NS; t++)
+                    if (lane + 32 * t < w) acc[r][t] = E::sub(acc[r][t], E::mul(lv, u[t]));
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < RW; r++)
+        if (rb + r < r0 + rows)
+#pragma unroll
+            for (int t = 0; t < NS; t++) {
+                const int j = lane + 32 * t;
+                if (j < w) stA<W>(A, n, rb + r, p0 + j, acc[r][t]);
+            }
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(miss, 1);
+}
+
+// G: rows [r0, r0 + rows) x columns [c0, c0 + cols): a_ij := a_ij - l_ik u_kj for
+// k = p0 .. p0+w-1 ascending (w <= 32; l from columns [p0, p0 + w), u from rows [p0, p0 + w));
+// 32 x 32 tiles, 128 threads with 2 x 4 outputs each
+template <int W>
+__global__ void __launch_bounds__(128) lu_subgemm_kernel(double *A, int64_t n, int64_t p0, int w, int64_t r0,
+                                                         int64_t rows, int64_t c0, int64_t cols, const int *miss) {
+    using E = elem<W>;
+    using T = typename E::T;
+    constexpr int BM = 32, BN = 32, BK = kSubSB, LDL = BK + 1;
+    if (__ldcg(miss)) return;
+    __shared__ double Ls[W * BM * LDL];   // [W][BM][LDL]
+    __shared__ double Us[W * BK * BN];    // [W][BK][BN]
+    const int tid = threadIdx.x, tx = tid % 8, ty = tid / 8;
+    const int64_t i0 = r0 + (int64_t)blockIdx.y * BM, j0 = c0 + (int64_t)blockIdx.x * BN;
+    // compile-time trip counts: every load of the two tiles is in flight at once (the small
+    // grids of the next sub-panel's rows, Ga, sit on the critical path)
+    {
+        T lt[BM * BK / 128], ut[BK * BN / 128];
+#pragma unroll
+        for (int it = 0; it < BM * BK / 128; it++) {
+            const int e = tid + 128 * it, r = e / BK, k = e % BK;
+            const int64_t i = i0 + r;
+            lt[it] = (i < r0 + rows && k < w) ? ldA<W>(A, n, i, p0 + k) : E::zero();
+        }
+#pragma unroll
+        for (int it = 0; it < BK * BN / 128; it++) {
+            const int e = tid + 128 * it, k = e / BN, c = e % BN;
+            const int64_t j = j0 + c;
+            ut[it] = (j < c0 + cols && k < w) ? ldA<W>(A, n, p0 + k, j) : E::zero();
+        }
+#pragma unroll
+        for (int it = 0; it < BM * BK / 128; it++) {
+            const int e = tid + 128 * it;
+            sts<W>(Ls, BM * LDL, (e / BK) * LDL + e % BK, lt[it]);
+        }
+#pragma unroll
+        for (int it = 0; it < BK * BN / 128; it++) sts<W>(Us, BK * BN, tid + 128 * it, ut[it]);
+    }
+    T acc[2][4];
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            const int64_t i = i0 + ty + 16 * a, j = j0 + tx + 8 * b;
+            acc[a][b] = (i < r0 + rows && j < c0 + cols) ? ldA<W>(A, n, i, j) : E::zero();
+        }
+    __syncthreads();
+    for (int k = 0; k < w; k++) {
+        T lv[2], uv[4];
+#pragma unroll
+        for (int a = 0; a < 2; a++) lv[a] = lds<W>(Ls, BM * LDL, (ty + 16 * a) * LDL + k);
+#pragma unroll
+        for (int b = 0; b < 4; b++) uv[b] = lds<W>(Us, BK * BN, k * BN + tx + 8 * b);
+#pragma unroll
+        for (int a = 0; a < 2; a++)
+#pragma unroll
+            for (int b = 0; b < 4; b++) acc[a][b] = E::sub(acc[a][b], E::mul(lv[a], uv[b]));
+    }
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            const int64_t i = i0 + ty + 16 * a, j = j0 + tx + 8 * b;
+            if (i < r0 + rows && j < c0 + cols) stA<W>(A, n, i, j, acc[a][b]);
+        }
+}
+
+// dir 0: panel rows [p, n) x columns [p, p + kb) of A -> snapshot; dir 1: after the sub-panels,
+// restore the snapshot if a row missed, else write ipiv = identity for the panel
+__global__ void __launch_bounds__(256) lu_snap_kernel(double *A, int W, int64_t n, int64_t p, int kb, double *snap,
+                                                      int64_t *ipiv, const int *miss, int dir) {
+    if (dir == 1 && !__ldcg(miss)) {
+        if (blockIdx.x == 0)
+            for (int j = threadIdx.x; j < kb; j += blockDim.x) ipiv[p + j] = p + j;
+        return;
+    }
+    const int64_t R = n - p, total = (int64_t)W * R * kb;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ww = e / (R * kb), rem = e % (R * kb), r = rem / kb, j = rem % kb;
+        double *a = A + ww * n * n + (p + r) * n + p + j;
+        if (dir == 0) snap[e] = *a;
+        else *a = snap[e];
+    }
+}
+
 // Apply the panel's interchanges (in order) to the columns outside the panel.
 __global__ void __launch_bounds__(256) lu_laswp_kernel(double *A, int W, int64_t n, int64_t p, int64_t kb,
                                                        const int64_t *ipiv) {
@@ -748,15 +1015,15 @@ template <int W> struct TrsmWpb { static constexpr int v = W == 2 ? 16 : 8; };
 template <int W> struct TrsmCh { static constexpr int v = W == 2 ? 16 : 8; };   // 2 x 64 KB ring
 
 
-template <int W, int RPL>
-__global__ void __launch_bounds__(TrsmWpb<W>::v * 32) lu_trsm_warp_kernel(double *A, int64_t n, int64_t p,
-                                                                     int kb, int64_t c0, int64_t ncols) {
+template <int W, int RPL, int WPB = TrsmWpb<W>::v>
+__global__ void __launch_bounds__(WPB * 32) lu_trsm_warp_kernel(double *A, int64_t n, int64_t p,
+                                                               int kb, int64_t c0, int64_t ncols) {
     using E = elem<W>;
     using T = typename E::T;
     constexpr int CH = TrsmCh<W>::v;
     extern __shared__ double Ls[];   // [2][W][CH][kb]: word w of l_{p+r, p+i0+ii} at [b][w][ii][r]
     const int lane = threadIdx.x & 31, wrp = threadIdx.x >> 5;
-    const int64_t col = c0 + (int64_t)blockIdx.x * TrsmWpb<W>::v + wrp;
+    const int64_t col = c0 + (int64_t)blockIdx.x * WPB + wrp;
     const bool active = col < c0 + ncols;
     const int SS = CH * kb, BUF = W * SS;
     const int nst = (kb + CH - 1) / CH;
@@ -1378,7 +1645,8 @@ static int spec_mode() {
 // returns 1 if the cooperative path was launched, 0 if the caller should use the per-column path
 template <int W>
 static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot, int64_t *ipiv, LuAux *aux,
-                          double *scr, size_t scr_bytes, cudaStream_t s, int *rc, cudaEvent_t pre_swap) {
+                          double *scr, size_t scr_bytes, cudaStream_t s, int *rc, cudaEvent_t pre_swap,
+                          const int *gate = nullptr, bool probe_only = false) {
     *rc = DDQD_OK;
     const int64_t R = n - p;
     const int dv = current_device();
@@ -1418,6 +1686,7 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
     }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lu_panel_coop_kernel<W>, nthr, smem);
     if (occ < 1 || G > occ * nsm) return 0;
+    if (probe_only) return 1;   // (the split path asks whether its fallback can launch)
     int kbi = (int)kb;
     int piv = pivot;
     static int probe = -1;   // DDQD_LU_PROBE=1: per-phase clock64 report (timing experiments)
@@ -1425,9 +1694,10 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
         const char *e = getenv("DDQD_LU_PROBE");
         probe = (e && e[0] == '1') ? 1 : 0;
     }
-    int spec = spec_mode();
+    int spec = gate ? 0 : spec_mode();   // the split path's fallback: straight to the full search
     double *fscr = scr + 2 * per_buf;
-    void *args[] = {&A, &n, &p, &kbi, (void *)&rows_per, &piv, &ipiv, &aux, &scr, &probe, &spec, &fscr};
+    void *args[] = {&A, &n, &p, &kbi, (void *)&rows_per, &piv, &ipiv, &aux, &scr, &probe, &spec, &fscr,
+                    (void *)&gate};
     cudaError_t e = cudaLaunchCooperativeKernel((void *)lu_panel_coop_kernel<W>, dim3(G), dim3(nthr), args, smem, s);
     count_launch();
     if (e != cudaSuccess) {
@@ -1451,6 +1721,137 @@ static int try_panel_coop(double *A, int64_t n, int64_t p, int64_t kb, int pivot
     return 1;
 }
 
+// DDQD_LU_SPLIT=0 keeps the cooperative panel for the speculated path (A/B measurements)
+static bool split_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_LU_SPLIT");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// DDQD_LU_SUB_OVERLAP=0 runs every sub-panel kernel on the one stream (A/B measurements)
+static bool sub_overlap_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_LU_SUB_OVERLAP");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// returns 1 if the blocked speculated panel (+ its gated cooperative fallback and the
+// interchanges) was launched, 0 if the caller should use the cooperative/per-column path
+template <int W>
+static int try_panel_split(double *A, int64_t n, int64_t p, int64_t kb, int pivot, int64_t *ipiv, LuAux *aux,
+                           double *scr, size_t scr_bytes, double *pout, cudaStream_t s, int *rc,
+                           cudaEvent_t pre_swap) {
+    *rc = DDQD_OK;
+    if constexpr (W != 2) {   // (DD only: the QD tiles would spill; QD keeps the cooperative panel)
+        return 0;
+    } else {
+    if (!pout || !split_enabled() || spec_mode() != 2 || kb > 256 || kb < 1) return 0;
+    // the fallback must be able to run (cooperative launch with the slab in shared memory)
+    int frc = DDQD_OK;
+    if (!try_panel_coop<W>(A, n, p, kb, pivot, ipiv, aux, scr, scr_bytes, s, &frc, nullptr, nullptr, true)) return 0;
+    constexpr int SB = kSubSB;
+    const int dv = current_device();
+    const size_t tsm = sizeof(double) * 2 * W * (size_t)TrsmCh<W>::v * SB;
+    const int kbi = (int)kb;
+    const int64_t R = n - p;
+    int *miss = &aux->miss;
+    const unsigned cgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(((int64_t)W * R * kb + 255) / 256,
+                                                                             (int64_t)sm_count() * 8));
+    DDQD_CUDA_CHECK(cudaMemsetAsync(miss, 0, sizeof(int), s));
+    lu_snap_kernel<<<cgrid, 256, 0, s>>>(A, W, n, p, kbi, pout, ipiv, miss, 0);
+    DDQD_LAUNCH_CHECK();
+    // Two streams (not under graph capture): the latency-bound diagonal blocks D and the column
+    // TRSMs T on a side stream, the row eliminations B and the updates G on s. G of sub-panel q
+    // is split into Ga (the next sub-panel's rows, all columns right) and Gb (the rows below):
+    // D_{q+1} and T_{q+1} need only Ga, so they run while Gb does. Dependencies (events):
+    //   D_q, T_q  after Ga_{q-1} (side);  B_q after D_q and Gb_{q-1} (s);
+    //   Ga_q, Gb_q after B_q (s) and T_q (side).
+    cudaStream_t s2 = s;
+    cudaEvent_t evA = nullptr, evD = nullptr, evT = nullptr;
+    {
+        cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(s, &cst) != cudaSuccess) { cudaGetLastError(); cst = cudaStreamCaptureStatusActive; }
+        static thread_local cudaStream_t side[64];
+        static thread_local cudaEvent_t evs[64][3];
+        if (cst == cudaStreamCaptureStatusNone && sub_overlap_enabled()) {
+            if (!side[dv]) {
+                int lo = 0, hi = 0;
+                DDQD_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+                DDQD_CUDA_CHECK(cudaStreamCreateWithPriority(&side[dv], cudaStreamNonBlocking, hi));
+                for (int e = 0; e < 3; e++) DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&evs[dv][e], cudaEventDisableTiming));
+            }
+            s2 = side[dv];
+            evA = evs[dv][0]; evD = evs[dv][1]; evT = evs[dv][2];
+        }
+    }
+    const bool two = s2 != s;
+    if (two) {   // the side stream starts after the snapshot
+        DDQD_CUDA_CHECK(cudaEventRecord(evA, s));
+        DDQD_CUDA_CHECK(cudaStreamWaitEvent(s2, evA, 0));
+    }
+    constexpr int WPB = 4;   // TRSM: 4 columns per CTA (each column is a 32-step chain: spread them)
+    // D -> B reciprocals, one [W][SB] slot per sub-panel (after the snapshot in pout)
+    double *const rv_base = pout + (size_t)W * (size_t)n * 256;
+    for (int q0 = 0; q0 < kbi; q0 += SB) {
+        const int w = std::min(SB, kbi - q0);
+        const int64_t p0 = p + q0;
+        const int64_t rows = n - (p0 + w);            // rows below the diagonal block
+        const int64_t cols = p + kb - (p0 + w);       // columns right of it (inside the panel)
+        double *const rvb = rv_base + (size_t)(q0 / SB) * W * SB;
+        lu_subdiag_kernel<W><<<1, kSubDiagNT, 0, s2>>>(A, n, p0, w, pivot, miss, rvb);
+        DDQD_LAUNCH_CHECK();
+        if (two) DDQD_CUDA_CHECK(cudaEventRecord(evD, s2));
+        if (cols > 0) {
+            lu_trsm_warp_kernel<W, 1, WPB><<<(unsigned)((cols + WPB - 1) / WPB), WPB * 32, tsm, s2>>>(A, n, p0, w, p0 + w,
+                                                                                                    cols);
+            DDQD_LAUNCH_CHECK();
+            if (two) DDQD_CUDA_CHECK(cudaEventRecord(evT, s2));
+        }
+        if (two) DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, evD, 0));
+        if (rows > 0) {
+            lu_subbelow_kernel<W><<<(unsigned)((rows + SubBelow<W>::ROWS - 1) / SubBelow<W>::ROWS), SubBelow<W>::NT, 0,
+                                    s>>>(A, n, p0, w, pivot, miss, p0 + w, rows, rvb);
+            DDQD_LAUNCH_CHECK();
+        }
+        if (cols > 0 && rows > 0) {
+            if (two) DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, evT, 0));
+            const int64_t ra = std::min<int64_t>(rows, SB);   // Ga: the next sub-panel's rows
+            dim3 ga((unsigned)((cols + 31) / 32), (unsigned)((ra + 31) / 32));
+            lu_subgemm_kernel<W><<<ga, 128, 0, s>>>(A, n, p0, w, p0 + w, ra, p0 + w, cols, miss);
+            DDQD_LAUNCH_CHECK();
+            if (two) {
+                DDQD_CUDA_CHECK(cudaEventRecord(evA, s));
+                DDQD_CUDA_CHECK(cudaStreamWaitEvent(s2, evA, 0));
+            }
+            if (rows > ra) {
+                dim3 gb((unsigned)((cols + 31) / 32), (unsigned)((rows - ra + 31) / 32));
+                lu_subgemm_kernel<W><<<gb, 128, 0, s>>>(A, n, p0, w, p0 + w + ra, rows - ra, p0 + w, cols, miss);
+                DDQD_LAUNCH_CHECK();
+            }
+        }
+    }
+    if (two) {   // join: the last D / T
+        DDQD_CUDA_CHECK(cudaEventRecord(evD, s2));
+        DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, evD, 0));
+    }
+    lu_snap_kernel<<<cgrid, 256, 0, s>>>(A, W, n, p, kbi, pout, ipiv, miss, 1);
+    DDQD_LAUNCH_CHECK();
+    // the fallback (full pivot search from the restored panel) runs only on a miss; then the
+    // interchanges of the other columns, as after the cooperative kernel
+    if (!try_panel_coop<W>(A, n, p, kb, pivot, ipiv, aux, scr, scr_bytes, s, rc, pre_swap, miss)) {
+        set_error("split panel: the cooperative fallback could not be launched");
+        *rc = DDQD_ECUDA;
+    }
+    return 1;
+    }
+}
+
 // DDQD_LU_TRSM=strip selects the row-parallel strip kernel (one CTA barrier per step) for
 // every panel width, =warp the warp-per-column kernel; default: the blocked kernel for
 // 256-wide panels (c4's), the warp-per-column kernel for other widths <= 256.
@@ -1467,14 +1868,18 @@ static int trsm_mode() {
 // the per-column pair), interchanges of the other columns, U12 := L11^{-1} A12.
 template <int W>
 static int lu_panel_w(int64_t n, int pivot, double *A, int64_t *ipiv, int64_t p, int64_t kb, LuAux *aux,
-                      double *scr, size_t scr_bytes, cudaStream_t s, cudaEvent_t pre_swap = nullptr) {
+                      double *scr, size_t scr_bytes, cudaStream_t s, cudaEvent_t pre_swap = nullptr,
+                      double *pout = nullptr) {
     NvtxRange nv("LU panel + TRSM");
     prof_begin(3, s);
     int crc = DDQD_OK;
     // the per-column kernels swap whole rows as they go: order them after the reader up front
     if (pre_swap && !use_coop_panel()) DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, pre_swap, 0));
-    const bool coop = use_coop_panel() && try_panel_coop<W>(A, n, p, kb, pivot, ipiv, aux, scr, scr_bytes, s, &crc,
-                                                            pre_swap);
+    const bool split = use_coop_panel() && try_panel_split<W>(A, n, p, kb, pivot, ipiv, aux, scr, scr_bytes, pout, s,
+                                                              &crc, pre_swap);
+    if (crc) return crc;
+    const bool coop = split || (use_coop_panel() && try_panel_coop<W>(A, n, p, kb, pivot, ipiv, aux, scr, scr_bytes,
+                                                                      s, &crc, pre_swap));
     if (crc) return crc;
     if (!coop && pre_swap && use_coop_panel()) DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, pre_swap, 0));
     for (int64_t k = p; !coop && k < p + kb; k++) {
@@ -1489,7 +1894,8 @@ static int lu_panel_w(int64_t n, int pivot, double *A, int64_t *ipiv, int64_t p,
         }
     }
     prof_end(3, (double)kb * (double)(n - p) * (double)kb / 2.0, s,   // panel madds (approx.)
-             coop ? "lu_panel_coop_kernel (+ lu_laswp_kernel)" : "lu_pivot_kernel + lu_rank1_kernel");
+             split ? "lu split panel (lu_subdiag/subbelow/trsm_warp/subgemm kernels)"
+                   : coop ? "lu_panel_coop_kernel (+ lu_laswp_kernel)" : "lu_pivot_kernel + lu_rank1_kernel");
     const int64_t n2 = n - p - kb;
     if (n2 <= 0) return DDQD_OK;
     // one CTA per SM when possible: cw = ceil(n2 / #SMs), capped by shared memory
@@ -1637,6 +2043,7 @@ struct LuMem {
     LuAux *aux;
     double *y, *scr;
     size_t scr_bytes;
+    double *pout;   // split panel: [W][n - p][K] factors + [W][K] reciprocals
 };
 static int lu_mem(int W, int64_t n, int64_t K, LuMem *m) {
     int st = DDQD_OK;
@@ -1645,11 +2052,14 @@ static int lu_mem(int W, int64_t n, int64_t K, LuMem *m) {
     const size_t G = (size_t)std::max(sm_count(), 1);
     m->scr_bytes = sizeof(double) * (2 * (G * ((W + 1) * kLuCrep + W * (size_t)K) + W * (size_t)K) +
                                      2 * (size_t)kLuRrep * W * (K + 1) + (size_t)K + 2);
-    char *mem = static_cast<char *>(aux_get(256 + ybytes + m->scr_bytes, &st));
+    const size_t sb = (m->scr_bytes + 255) & ~size_t(255);
+    const size_t pbytes = K <= 256 ? sizeof(double) * W * ((size_t)n * 256 + 256) : 0;   // snapshot + reciprocals
+    char *mem = static_cast<char *>(aux_get(256 + ybytes + sb + pbytes, &st));
     if (st) return st;
     m->aux = reinterpret_cast<LuAux *>(mem);
     m->y = reinterpret_cast<double *>(mem + 256);
     m->scr = reinterpret_cast<double *>(mem + 256 + ybytes);
+    m->pout = pbytes ? reinterpret_cast<double *>(mem + 256 + ybytes + sb) : nullptr;
     return DDQD_OK;
 }
 
@@ -1712,7 +2122,7 @@ static int lu_solve_w(int64_t n, int pivot, double *A, const double *b, double *
     for (int64_t p = 0; p < n; p += K) {
         const int64_t kb = std::min(K, n - p);
         if ((rc = lu_panel_w<W>(n, pivot, A, ipiv, p, kb, mem.aux, mem.scr, mem.scr_bytes, s,
-                                side_pending ? sd->done : nullptr))) return rc;
+                                side_pending ? sd->done : nullptr, mem.pout))) return rc;
         if (overlap) {
             DDQD_CUDA_CHECK(cudaEventRecord(sd->panel, s));
             DDQD_CUDA_CHECK(cudaStreamWaitEvent(sd->ss, sd->panel, 0));
@@ -1755,8 +2165,8 @@ int lu_panel_impl(int W, int pivot, int64_t n, double *A, int64_t *ipiv, int64_t
     int rc = lu_mem(W, n, kb, &mem);
     if (rc) return rc;
     DDQD_CUDA_CHECK(cudaMemsetAsync(mem.aux, 0, sizeof(LuAux), s));
-    rc = W == 2 ? lu_panel_w<2>(n, pivot, A, ipiv, p, kb, mem.aux, mem.scr, mem.scr_bytes, s)
-                : lu_panel_w<4>(n, pivot, A, ipiv, p, kb, mem.aux, mem.scr, mem.scr_bytes, s);
+    rc = W == 2 ? lu_panel_w<2>(n, pivot, A, ipiv, p, kb, mem.aux, mem.scr, mem.scr_bytes, s, nullptr, mem.pout)
+                : lu_panel_w<4>(n, pivot, A, ipiv, p, kb, mem.aux, mem.scr, mem.scr_bytes, s, nullptr, mem.pout);
     if (rc) return rc;
     int info_h = 0;
     DDQD_CUDA_CHECK(cudaMemcpyAsync(&info_h, &mem.aux->info, sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -2,6 +2,7 @@
 oracle on the same seeded inputs. Bit-exact wherever the kernel reproduces the oracle's
 summation order (everything here: docs/numerics.md), plus exact-error bounds (BJ:5) at
 the BASELINE.json full sizes where only sampled entries are checkable."""
+import json
 import os
 
 import numpy as np
@@ -1323,3 +1324,55 @@ def test_row_pair_tma_leaf_bitwise(orc, m, l):
     got = np_(C)
     for b in range(0, batch, 9):
         assert same(got[b], orc.gemm(A[b], B[b], "block")), b
+
+
+def test_lu_split_panel_bitwise(orc, tmp_path):
+    """The split panel (the diagonal block on one thread-block cluster, the rows below
+    eliminated warp by warp, committed only when the speculated pivots all hold) gives the
+    bits of the cooperative panel (DDQD_LU_SPLIT=0) and of the oracle: panels where the
+    speculation holds and panels where it misses in the same solve (the gated fallback factors
+    those), a ragged last panel, K < 256, QD (16-CTA cluster), pivot-free, and an exactly zero
+    pivot (info). Subprocesses: the switch is read once per process."""
+    import subprocess
+    import sys
+    code = (
+        "import json, numpy as np, torch, ddqd_inputs as gen, paper_1510_08642_b200 as d\n"
+        "def dom_first(W, n, seed, cols):\n"
+        "    A = gen.matrix(W, n, n, seed, 0); A[0, np.arange(cols), np.arange(cols)] += n; return A\n"
+        "cases = [(2, dom_first(2, 600, 31, 256), 256, 'strassen', 64, True),\n"
+        "         (2, gen.lu_matrix(700, 5), 256, 'winograd', 64, True),\n"
+        "         (4, dom_first(4, 400, 32, 400), 256, 'strassen', 64, True),\n"
+        "         (2, gen.dd_matrix(300, 300, 33, 0), 128, 'block', 1, False),\n"
+        "         (2, gen.dd_matrix(300, 300, 34, 0), 100, 'winograd', 32, True)]\n"
+        "z = gen.lu_matrix(100, 6); z[:, :, 7] = 0.0\n"
+        "cases.append((2, z, 64, 'strassen', 16, True))\n"
+        "out, infos = [], []\n"
+        "d.profile_start()\n"
+        "for W, A, K, algo, T, piv in cases:\n"
+        "    n = A.shape[1]; b = gen.matrix(W, 1, n, 35, 1)[:, 0, :].copy()\n"
+        "    x, LU, p, info = d.lu_solve(torch.from_numpy(A).cuda(), torch.from_numpy(b).cuda(), panel=K, algo=algo,\n"
+        "                                threshold=T, pivot=piv)\n"
+        "    out += [LU.cpu().numpy().ravel(), x.cpu().numpy().ravel(), p.cpu().numpy().astype(np.float64)]\n"
+        "    infos.append(int(info))\n"
+        "d.profile_stop()\n"
+        "np.save(r'%s', np.concatenate(out))\n"
+        "json.dump({'info': infos, 'kernels': sorted(d.profile_kernels())}, open(r'%s.json', 'w'))\n")
+    outs, meta = [], []
+    for mode in ("1", "0"):
+        f = tmp_path / f"s{mode}.npy"
+        subprocess.check_call([sys.executable, "-c", code % (f, f)], env=dict(os.environ, DDQD_LU_SPLIT=mode), cwd=ROOT)
+        outs.append(np.load(f))
+        meta.append(json.load(open(f"{f}.json")))
+    assert same(outs[0], outs[1])
+    assert meta[0]["info"] == meta[1]["info"] and meta[0]["info"][-1] == 8 and meta[0]["info"][:-1] == [0] * 5
+    assert any("split panel" in k for k in meta[0]["kernels"])
+    assert not any("split panel" in k for k in meta[1]["kernels"])
+    # the first case (speculation holds in panel 0, misses later) and the QD case vs the oracle
+    v, k = outs[0], 0
+    A1 = gen.matrix(2, 600, 600, 31, 0); A1[0, np.arange(256), np.arange(256)] += 600
+    b1 = gen.matrix(2, 1, 600, 35, 1)[:, 0, :].copy()
+    x_ref, LU_ref, piv_ref, _ = orc.solve(A1, b1, panel=256, algo="strassen", threshold=64)
+    assert np.any(piv_ref[256:] != np.arange(256, 600)) and np.array_equal(piv_ref[:256], np.arange(256))
+    assert same(v[k:k + LU_ref.size], LU_ref.ravel()); k += LU_ref.size
+    assert same(v[k:k + x_ref.size], x_ref.ravel()); k += x_ref.size
+    assert np.array_equal(v[k:k + 600], piv_ref.astype(np.float64))
