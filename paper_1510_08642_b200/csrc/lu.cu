@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "common.cuh"
 #include "cp_async.cuh"
@@ -689,15 +690,19 @@ __global__ void __launch_bounds__(512) lu_panel_coop_kernel(double *A, int64_t n
 // first; after a miss the later kernels return at once, the snapshot is restored and the gated
 // cooperative kernel factors the panel with the full pivot search.
 constexpr int kSubSB = 32;     // sub-panel width
-constexpr int kSubDiagNT = 288; // 8 bulk warps + the chain warp
+constexpr int kSubDiagPad = 180 * 1024;   // D's SM to itself (see the launch)
+constexpr int kSubDiagNT = 384; // 12 warps: the chain warp 0 alone on SM sub-partition 0, 9 bulk warps on 1-3
 
-// D: the w x w (w <= 32) diagonal block of sub-panel [p0, p0 + w). Warp 8 (the chain warp) owns
+// D: the w x w (w <= 32) diagonal block of sub-panel [p0, p0 + w). Warp 0 (the chain warp) owns
 // row kk+1 in step kk: it scales it, updates it and forms the next reciprocal 1/u_{kk+1,kk+1}
-// (the dependent chain mul -> sub(mul) -> div of every column) while warps 0-7 update rows
-// kk+2.. (warp wr: rows kk+2+wr+8t; lane: column kk+1+lane); one CTA barrier per column.
+// (the dependent chain mul -> sub(mul) -> div of every column) while 9 bulk warps update rows
+// kk+2.. (bulk warp b: rows kk+2+b+9t; lane: column kk+1+lane); one CTA barrier per column.
+// Warps 4 and 8 idle: the chain warp has SM sub-partition 0 (warp % 4) to itself, so its
+// dependent chain is not queued behind the bulk warps' FP64 instructions (measured: the chain
+// took ~1.1k cycles per column sharing its sub-partition with two bulk warps).
 template <int W>
 __global__ void __launch_bounds__(kSubDiagNT, 1) lu_subdiag_kernel(double *A, int64_t n, int64_t p0, int w, int pivot,
-                                                                   int *miss, double *rv_out) {
+                                                                   int *miss, double *rv_out, int probe) {
     using E = elem<W>;
     using T = typename E::T;
     if (__ldcg(miss)) return;
@@ -720,7 +725,10 @@ __global__ void __launch_bounds__(kSubDiagNT, 1) lu_subdiag_kernel(double *A, in
     if (tid == 0) sts<W>(s_r, 1, 0, E::div(E::one(), lds<W>(S, SS, 0)));
     __syncthreads();
     bool bad = false;
+    long long pc0 = 0, pc1 = 0, pc2 = 0, tst = clock64();
+    const long long t_start = tst;
     for (int kk = 0; kk < w; kk++) {
+        if (probe) { const long long t = clock64(); pc2 += t - tst; tst = t; }
         const T akk = lds<W>(S, SS, kk * SB + kk);
         const T rinv = lds<W>(s_r + (kk & 1) * W, 1, 0);
         if (tid == 0) {
@@ -728,7 +736,8 @@ __global__ void __launch_bounds__(kSubDiagNT, 1) lu_subdiag_kernel(double *A, in
             for (int ww = 0; ww < W; ww++) rv_out[ww * SB + kk] = E::word(rinv, ww);   // for B
         }
         const int j = kk + 1 + lane;
-        if (wr == 8) {
+        const int bw = (wr >> 2) * 3 + (wr & 3) - 1;   // bulk warp index 0..8 (wr % 4 != 0)
+        if (wr == 0) {
             const int i = kk + 1;
             if (i < w) {
                 const T a = lds<W>(S, SS, i * SB + kk);
@@ -742,22 +751,43 @@ __global__ void __launch_bounds__(kSubDiagNT, 1) lu_subdiag_kernel(double *A, in
                 __syncwarp();
                 if (lane == 0) sts<W>(S, SS, i * SB + kk, lv);
             }
-        } else {
+            if (probe) { const long long t = clock64(); pc0 += t - tst; }
+        } else if ((wr & 3) != 0 && kk + 2 + bw < w) {
+            // this warp's rows kk+2+bw+9t (t < nr, warp-uniform count): the nr chains issued
+            // together (no branch between them), so only valid rows cost FP64 issue slots
+            const int nr = (w - (kk + 2 + bw) + 8) / 9;
+            const int jc = j < w ? j : kk;
+            const T u = lds<W>(S, SS, kk * SB + jc);
+            auto rows_go = [&](auto NRc) {
+                constexpr int NR = decltype(NRc)::value;
+                T lv[NR], nv[NR];
 #pragma unroll
-            for (int t = 0; t < 4; t++) {
-                const int i = kk + 2 + wr + 8 * t;
-                if (i >= w) break;
-                const T a = lds<W>(S, SS, i * SB + kk);
-                if (pivot && lane == 0 && E::abs_gt(a, akk)) bad = true;
-                const T lv = E::mul(a, rinv);
+                for (int t = 0; t < NR; t++) {
+                    const int i = kk + 2 + bw + 9 * t;
+                    const T a = lds<W>(S, SS, i * SB + kk);
+                    if (pivot && lane == 0 && E::abs_gt(a, akk)) bad = true;
+                    lv[t] = E::mul(a, rinv);
+                    nv[t] = E::sub(lds<W>(S, SS, i * SB + jc), E::mul(lv[t], u));
+                }
                 if (j < w)
-                    sts<W>(S, SS, i * SB + j, E::sub(lds<W>(S, SS, i * SB + j), E::mul(lv, lds<W>(S, SS, kk * SB + j))));
+#pragma unroll
+                    for (int t = 0; t < NR; t++) sts<W>(S, SS, (kk + 2 + bw + 9 * t) * SB + j, nv[t]);
                 __syncwarp();
-                if (lane == 0) sts<W>(S, SS, i * SB + kk, lv);
-            }
+                if (lane == 0)
+#pragma unroll
+                    for (int t = 0; t < NR; t++) sts<W>(S, SS, (kk + 2 + bw + 9 * t) * SB + kk, lv[t]);
+            };
+            if (nr >= 4) rows_go(std::integral_constant<int, 4>{});
+            else if (nr == 3) rows_go(std::integral_constant<int, 3>{});
+            else if (nr == 2) rows_go(std::integral_constant<int, 2>{});
+            else rows_go(std::integral_constant<int, 1>{});
+            if (probe) { const long long t = clock64(); pc1 += t - tst; }
         }
         __syncthreads();
     }
+    if (probe && (tid == 0 || tid == 32) && p0 < 64)
+        printf("LUSUBPROBE p0=%lld tid=%d chain %lld bulk %lld step %lld total %lld\n", (long long)p0, tid, pc0, pc1, pc2,
+               clock64() - t_start);
     for (int e = tid; e < w * w; e += NT) {
         const int i = e / w, jj = e % w;
         stA<W>(A, n, p0 + i, p0 + jj, lds<W>(S, SS, i * SB + jj));
@@ -766,24 +796,29 @@ __global__ void __launch_bounds__(kSubDiagNT, 1) lu_subdiag_kernel(double *A, in
 }
 
 template <int W> struct SubBelow {
-    static constexpr int RW = 1;                   // rows per warp
-    static constexpr int NT = 128;
-    static constexpr int ROWS = RW * (NT / 32);    // rows per CTA
+    static constexpr int TPR = 4;                  // threads per row
+    static constexpr int NT = 128;                 // 4 warps: one per SM sub-partition
+    static constexpr int ROWS = NT / TPR;          // rows per CTA
 };
 
 // B: rows [r0, r0 + rows) x columns [p0, p0 + w): column elimination with the U rows and
-// reciprocals of the sub-panel's diagonal block (staged whole in shared memory)
+// reciprocals of the sub-panel's diagonal block (U staged in shared memory, the reciprocals
+// from D). Four threads per row, thread t holding columns t + 4c (c < 8) in registers: the
+// column loop is unrolled, so at step k a thread only issues the slots that still have
+// columns > k (no idle lanes beyond the partial slot), and the multiplier's source a_ik is one
+// shuffle inside the row's 4-lane group.
 template <int W>
 __global__ void __launch_bounds__(SubBelow<W>::NT) lu_subbelow_kernel(double *A, int64_t n, int64_t p0, int w,
                                                                       int pivot, int *miss, int64_t r0,
-                                                                      int64_t rows, const double *rv_in) {
+                                                                      int64_t rows, const double *rv_in, int probe) {
     using E = elem<W>;
     using T = typename E::T;
-    constexpr int SB = kSubSB, NS = SB / 32, SS = SB * SB, RW = SubBelow<W>::RW, NT = SubBelow<W>::NT;
+    constexpr int SB = kSubSB, SS = SB * SB, TPR = SubBelow<W>::TPR, NC = SB / TPR, NT = SubBelow<W>::NT;
+    const long long tb0 = clock64();
     if (__ldcg(miss)) return;
     __shared__ double U[W * SS];        // [W][SB][SB]
     __shared__ double Rv[W * SB];       // [W][SB]
-    const int tid = threadIdx.x, lane = tid & 31, wrp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, t = tid % TPR;
     {
         T v[SS / NT];
 #pragma unroll
@@ -794,58 +829,53 @@ __global__ void __launch_bounds__(SubBelow<W>::NT) lu_subbelow_kernel(double *A,
 #pragma unroll
         for (int it = 0; it < SS / NT; it++) sts<W>(U, SS, tid + NT * it, v[it]);
     }
-    __syncthreads();
     if (tid < W * SB) Rv[tid] = rv_in[tid];   // D's reciprocals 1 / u_kk (the same bits)
-    const int64_t rb = r0 + (int64_t)blockIdx.x * SubBelow<W>::ROWS + (int64_t)wrp * RW;
-    T acc[RW][NS];
+    const int64_t i = r0 + (int64_t)blockIdx.x * SubBelow<W>::ROWS + tid / TPR;
+    const bool valid = i < r0 + rows;
+    T acc[NC];
 #pragma unroll
-    for (int r = 0; r < RW; r++)
-#pragma unroll
-        for (int t = 0; t < NS; t++) {
-            const int j = lane + 32 * t;
-            acc[r][t] = (rb + r < r0 + rows && j < w) ? ldA<W>(A, n, rb + r, p0 + j) : E::zero();
-        }
+    for (int c = 0; c < NC; c++) {
+        const int j = t + TPR * c;
+        acc[c] = (valid && j < w) ? ldA<W>(A, n, i, p0 + j) : E::zero();
+    }
     __syncthreads();
+    const long long tb1 = clock64();
     bool bad = false;
+    const int gl = lane & ~(TPR - 1);
 #pragma unroll
-    for (int s = 0; s < NS; s++) {
-        if (32 * s >= w) break;
-        for (int kl = 0; kl < 32; kl++) {
-            const int k = 32 * s + kl;
-            if (k >= w) break;
-            const T ukk = lds<W>(U, SS, k * SB + k);
-            const T rinv = lds<W>(Rv, SB, k);
-            T u[NS];
+    for (int k = 0; k < SB; k++) {
+        if (k >= w) break;
+        const int ck = k / TPR, tk = k % TPR;
+        T a;
 #pragma unroll
-            for (int t = s; t < NS; t++) u[t] = lds<W>(U, SS, k * SB + lane + 32 * t);
+        for (int ww = 0; ww < W; ww++) E::set_word(a, ww, __shfl_sync(0xffffffffu, E::word(acc[ck], ww), gl | tk));
+        const T ukk = lds<W>(U, SS, k * SB + k);
+        if (pivot && valid && E::abs_gt(a, ukk)) bad = true;
+        const T lv = E::mul(a, lds<W>(Rv, SB, k));
+        // branch-free (selects, not branches), so the slots' chains interleave; U is zero past w
+        {
+            const int j = t + TPR * ck;
+            const T nv = E::sub(acc[ck], E::mul(lv, lds<W>(U, SS, k * SB + j)));
+            acc[ck] = t == tk ? lv : ((t > tk && j < w) ? nv : acc[ck]);
+        }
 #pragma unroll
-            for (int r = 0; r < RW; r++) {
-                T a;
-#pragma unroll
-                for (int ww = 0; ww < W; ww++) E::set_word(a, ww, __shfl_sync(0xffffffffu, E::word(acc[r][s], ww), kl));
-                if (pivot && rb + r < r0 + rows && E::abs_gt(a, ukk)) bad = true;
-                const T lv = E::mul(a, rinv);
-                {
-                    const int j = lane + 32 * s;
-                    const T nv = E::sub(acc[r][s], E::mul(lv, u[s]));
-                    if (lane == kl) acc[r][s] = lv;
-                    else if (lane > kl && j < w) acc[r][s] = nv;
-                }
-#pragma unroll
-                for (int t = s + 1; t < NS; t++)
-                    if (lane + 32 * t < w) acc[r][t] = E::sub(acc[r][t], E::mul(lv, u[t]));
-            }
+        for (int c = ck + 1; c < NC; c++) {
+            const int j = t + TPR * c;
+            const T nv = E::sub(acc[c], E::mul(lv, lds<W>(U, SS, k * SB + j)));
+            acc[c] = j < w ? nv : acc[c];
         }
     }
+    const long long tb2 = clock64();
+    if (valid)
 #pragma unroll
-    for (int r = 0; r < RW; r++)
-        if (rb + r < r0 + rows)
-#pragma unroll
-            for (int t = 0; t < NS; t++) {
-                const int j = lane + 32 * t;
-                if (j < w) stA<W>(A, n, rb + r, p0 + j, acc[r][t]);
-            }
+        for (int c = 0; c < NC; c++) {
+            const int j = t + TPR * c;
+            if (j < w) stA<W>(A, n, i, p0 + j, acc[c]);
+        }
     if (__syncthreads_or(bad) && tid == 0) atomicOr(miss, 1);
+    if (probe && tid == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x / 2) && p0 < 64)
+        printf("LUBELOWPROBE p0=%lld cta=%d grid=%d prologue %lld steps %lld\n", (long long)p0, blockIdx.x, gridDim.x,
+               tb1 - tb0, tb2 - tb1);
 }
 
 // G: rows [r0, r0 + rows) x columns [c0, c0 + cols): a_ij := a_ij - l_ik u_kj for
@@ -1731,6 +1761,15 @@ static bool split_enabled() {
     return v == 1;
 }
 
+static int sub_probe() {   // DDQD_LU_PROBE=1: per-phase clock64 of the sub-panel diagonal kernel
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DDQD_LU_PROBE");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v;
+}
+
 // DDQD_LU_SUB_OVERLAP=0 runs every sub-panel kernel on the one stream (A/B measurements)
 static bool sub_overlap_enabled() {
     static int v = -1;
@@ -1758,6 +1797,11 @@ static int try_panel_split(double *A, int64_t n, int64_t p, int64_t kb, int pivo
     constexpr int SB = kSubSB;
     const int dv = current_device();
     const size_t tsm = sizeof(double) * 2 * W * (size_t)TrsmCh<W>::v * SB;
+    static bool dattr[64];
+    if (!dattr[dv]) {
+        DDQD_CUDA_CHECK(cudaFuncSetAttribute(lu_subdiag_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSubDiagPad));
+        dattr[dv] = true;
+    }
     const int kbi = (int)kb;
     const int64_t R = n - p;
     int *miss = &aux->miss;
@@ -1804,7 +1848,9 @@ static int try_panel_split(double *A, int64_t n, int64_t p, int64_t kb, int pivo
         const int64_t rows = n - (p0 + w);            // rows below the diagonal block
         const int64_t cols = p + kb - (p0 + w);       // columns right of it (inside the panel)
         double *const rvb = rv_base + (size_t)(q0 / SB) * W * SB;
-        lu_subdiag_kernel<W><<<1, kSubDiagNT, 0, s2>>>(A, n, p0, w, pivot, miss, rvb);
+        // (dynamic shared memory it does not use: the SM is D's alone, no update CTA shares its
+        // FP64 pipe -- measured 36.6k vs 47.5k cycles per D beside the concurrent update)
+        lu_subdiag_kernel<W><<<1, kSubDiagNT, kSubDiagPad, s2>>>(A, n, p0, w, pivot, miss, rvb, sub_probe());
         DDQD_LAUNCH_CHECK();
         if (two) DDQD_CUDA_CHECK(cudaEventRecord(evD, s2));
         if (cols > 0) {
@@ -1816,7 +1862,7 @@ static int try_panel_split(double *A, int64_t n, int64_t p, int64_t kb, int pivo
         if (two) DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, evD, 0));
         if (rows > 0) {
             lu_subbelow_kernel<W><<<(unsigned)((rows + SubBelow<W>::ROWS - 1) / SubBelow<W>::ROWS), SubBelow<W>::NT, 0,
-                                    s>>>(A, n, p0, w, pivot, miss, p0 + w, rows, rvb);
+                                    s>>>(A, n, p0, w, pivot, miss, p0 + w, rows, rvb, sub_probe());
             DDQD_LAUNCH_CHECK();
         }
         if (cols > 0 && rows > 0) {
