@@ -387,15 +387,17 @@ def lu_bench(args, wl, rank, world, local):
     pan_ach = 20.0 * pan_madds / (pan_ms * 1e-3) / 1e12 if pan_ms else 0.0
     roof_pan = {"bound": "alu", "achieved": pan_ach, "peak": peak / 1e12, "unit": "TFLOP/s",
                 "frac": pan_ach / (peak / 1e12) if peak else None,
-                "kernel": "lu_panel_coop_kernel (+ lu_laswp_kernel)", "launches": int(pan_n),
+                "kernel": max((k for k, v in kern.items() if v[0] == 3), key=lambda k: kern[k][1],
+                              default="lu panel"), "launches": int(pan_n),
                 "share_of_step": shares["lu_panel"], "traffic": None,
-                "latency_bound": "one grid barrier + candidate exchange per column, ~14k cycles per "
-                                 "pivot step x 4096 steps (DESIGN.md s.7, profiles/r01/lu_panel_phase_probe_*)",
+                "latency_bound": "the 4096-column pivot chain (l = a * r, u = a - l * u, r = 1 / u: ~0.8k "
+                                 "cycles per column in the one-CTA diagonal blocks of the 32-column "
+                                 "sub-panels) and the 32-step row-elimination chains (DESIGN.md s.7)",
                 "work_def": "rank-1 panel updates R*K^2/2 DD madds x 20 FP64 lane-ops",
                 "algorithmic_bytes_per_launch": 16.0 * K * (n - K * (n // K - 1) / 2.0) * 2,
                 "traffic_note": "one panel launch reads its slab once (R x K DD) and writes it back "
                                 "(the write stays in the 126 MB L2 within the launch)"}
-    tr, src = ncu_panel_traffic()
+    tr, src = ncu_panel_traffic() if "coop" in roof_pan["kernel"] else (None, None)
     if tr is not None:
         roof_pan["traffic"] = tr
         roof_pan["traffic_source"] = src

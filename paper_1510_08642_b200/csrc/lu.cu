@@ -887,7 +887,7 @@ __global__ void __launch_bounds__(128) lu_subgemm_kernel(double *A, int64_t n, i
     using E = elem<W>;
     using T = typename E::T;
     constexpr int BM = 32, BN = 32, BK = kSubSB, LDL = BK + 1;
-    if (__ldcg(miss)) return;
+    if (miss && __ldcg(miss)) return;
     __shared__ double Ls[W * BM * LDL];   // [W][BM][LDL]
     __shared__ double Us[W * BK * BN];    // [W][BK][BN]
     const int tid = threadIdx.x, tx = tid % 8, ty = tid / 8;
@@ -1905,7 +1905,8 @@ static int trsm_mode() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("DDQD_LU_TRSM");
-        v = (e && std::string(e) == "strip") ? 0 : (e && std::string(e) == "warp") ? 1 : 2;
+        v = (e && std::string(e) == "strip") ? 0 : (e && std::string(e) == "warp") ? 1
+          : (e && std::string(e) == "sub") ? 3 : 2;
     }
     return v;
 }
@@ -1953,7 +1954,35 @@ static int lu_panel_w(int64_t n, int pivot, double *A, int64_t *ipiv, int64_t p,
                                              (int)smem));
     if (kb > 1024) { set_error("panel > 1024 not supported by the TRSM kernel"); return DDQD_ENOTSUP; }
     prof_begin(4, s);
-    if (kb == 256 && trsm_mode() == 2) {
+    bool trsm_done = false;
+    if constexpr (W == 2) {
+    if (trsm_mode() == 3) {
+        trsm_done = true;
+        // DDQD_LU_TRSM=sub (DD): blocked by 32 rows of L11 -- the 32-row diagonal block's triangle solve
+        // over all n2 columns (the warp TRSM, a 32-step chain per column), then the rows below
+        // it inside the panel take that block's 32 updates (the k-ascending update kernel of
+        // the blocked panel). Each U12 element still receives a_rj -= l_ri u_ij for i ascending
+        // (numerics.md s.5 step 2), so the bits are those of the one-pass kernels. Measured on
+        // c4: 36.8 ms vs 36.0 with the one-pass strip kernel (TRSM 10.1% vs 8.2% of the solve:
+        // the 8 launches per panel re-read L11 and U12 from L2), so it stays opt-in.
+        constexpr int SB = kSubSB, WPB = 4;
+        const size_t tsm = sizeof(double) * 2 * W * (size_t)TrsmCh<W>::v * SB;
+        for (int64_t b0 = 0; b0 < kb; b0 += SB) {
+            const int w = (int)std::min<int64_t>(SB, kb - b0);
+            lu_trsm_warp_kernel<W, 1, WPB><<<(unsigned)((n2 + WPB - 1) / WPB), WPB * 32, tsm, s>>>(A, n, p + b0, w,
+                                                                                                  p + kb, n2);
+            DDQD_LAUNCH_CHECK();
+            const int64_t rows = kb - b0 - w;
+            if (rows > 0) {
+                dim3 g((unsigned)((n2 + 31) / 32), (unsigned)((rows + 31) / 32));
+                lu_subgemm_kernel<W><<<g, 128, 0, s>>>(A, n, p + b0, w, p + b0 + w, rows, p + kb, n2, nullptr);
+                DDQD_LAUNCH_CHECK();
+            }
+        }
+    }
+    }
+    if (trsm_done) {
+    } else if (kb == 256 && trsm_mode() >= 2) {
         // 16-column strips while they fill ~1.5 waves of the SMs, else 8 (twice the CTAs, each
         // with half the chain): the per-CTA chain, not the FP64 rate, bounds small panels
         static bool battr[2][64] = {};
