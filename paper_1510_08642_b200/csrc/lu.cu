@@ -888,8 +888,9 @@ __global__ void __launch_bounds__(128) lu_subgemm_kernel(double *A, int64_t n, i
     using T = typename E::T;
     constexpr int BM = 32, BN = 32, BK = kSubSB, LDL = BK + 1;
     if (miss && __ldcg(miss)) return;
-    __shared__ double Ls[W * BM * LDL];   // [W][BM][LDL]
-    __shared__ double Us[W * BK * BN];    // [W][BK][BN]
+    extern __shared__ double sm[];
+    double *Ls = sm;                      // [W][BM][LDL]
+    double *Us = sm + W * BM * LDL;       // [W][BK][BN]
     const int tid = threadIdx.x, tx = tid % 8, ty = tid / 8;
     const int64_t i0 = r0 + (int64_t)blockIdx.y * BM, j0 = c0 + (int64_t)blockIdx.x * BN;
     // compile-time trip counts: every load of the two tiles is in flight at once (the small
@@ -944,6 +945,8 @@ __global__ void __launch_bounds__(128) lu_subgemm_kernel(double *A, int64_t n, i
             if (i < r0 + rows && j < c0 + cols) stA<W>(A, n, i, j, acc[a][b]);
         }
 }
+
+template <int W> static size_t sub_gemm_smem() { return sizeof(double) * W * (32 * (kSubSB + 1) + kSubSB * 32); }
 
 // dir 0: panel rows [p, n) x columns [p, p + kb) of A -> snapshot; dir 1: after the sub-panels,
 // restore the snapshot if a row missed, else write ipiv = identity for the panel
@@ -1787,7 +1790,11 @@ static int try_panel_split(double *A, int64_t n, int64_t p, int64_t kb, int pivo
                            double *scr, size_t scr_bytes, double *pout, cudaStream_t s, int *rc,
                            cudaEvent_t pre_swap) {
     *rc = DDQD_OK;
-    if constexpr (W != 2) {   // (DD only: the QD tiles would spill; QD keeps the cooperative panel)
+    // DD only. QD measured slower (n = 1024 / 2048, panel 256: 26.5 / 77.8 ms vs 19.7 / 62.8 ms
+    // with the cooperative panel): QD arithmetic is ~10x DD's, so the one-CTA diagonal blocks
+    // and the rank-32 updates become FP64-bound where the cooperative kernel spreads the panel
+    // over every SM.
+    if constexpr (W != 2) {
         return 0;
     } else {
     if (!pout || !split_enabled() || spec_mode() != 2 || kb > 256 || kb < 1) return 0;
@@ -1797,9 +1804,11 @@ static int try_panel_split(double *A, int64_t n, int64_t p, int64_t kb, int pivo
     constexpr int SB = kSubSB;
     const int dv = current_device();
     const size_t tsm = sizeof(double) * 2 * W * (size_t)TrsmCh<W>::v * SB;
+    const size_t gsm = sub_gemm_smem<W>();
     static bool dattr[64];
     if (!dattr[dv]) {
         DDQD_CUDA_CHECK(cudaFuncSetAttribute(lu_subdiag_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSubDiagPad));
+        DDQD_CUDA_CHECK(cudaFuncSetAttribute(lu_subgemm_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
         dattr[dv] = true;
     }
     const int kbi = (int)kb;
@@ -1869,7 +1878,7 @@ static int try_panel_split(double *A, int64_t n, int64_t p, int64_t kb, int pivo
             if (two) DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, evT, 0));
             const int64_t ra = std::min<int64_t>(rows, SB);   // Ga: the next sub-panel's rows
             dim3 ga((unsigned)((cols + 31) / 32), (unsigned)((ra + 31) / 32));
-            lu_subgemm_kernel<W><<<ga, 128, 0, s>>>(A, n, p0, w, p0 + w, ra, p0 + w, cols, miss);
+            lu_subgemm_kernel<W><<<ga, 128, gsm, s>>>(A, n, p0, w, p0 + w, ra, p0 + w, cols, miss);
             DDQD_LAUNCH_CHECK();
             if (two) {
                 DDQD_CUDA_CHECK(cudaEventRecord(evA, s));
@@ -1877,7 +1886,7 @@ static int try_panel_split(double *A, int64_t n, int64_t p, int64_t kb, int pivo
             }
             if (rows > ra) {
                 dim3 gb((unsigned)((cols + 31) / 32), (unsigned)((rows - ra + 31) / 32));
-                lu_subgemm_kernel<W><<<gb, 128, 0, s>>>(A, n, p0, w, p0 + w + ra, rows - ra, p0 + w, cols, miss);
+                lu_subgemm_kernel<W><<<gb, 128, gsm, s>>>(A, n, p0, w, p0 + w + ra, rows - ra, p0 + w, cols, miss);
                 DDQD_LAUNCH_CHECK();
             }
         }
@@ -1975,7 +1984,7 @@ static int lu_panel_w(int64_t n, int pivot, double *A, int64_t *ipiv, int64_t p,
             const int64_t rows = kb - b0 - w;
             if (rows > 0) {
                 dim3 g((unsigned)((n2 + 31) / 32), (unsigned)((rows + 31) / 32));
-                lu_subgemm_kernel<W><<<g, 128, 0, s>>>(A, n, p + b0, w, p + b0 + w, rows, p + kb, n2, nullptr);
+                lu_subgemm_kernel<W><<<g, 128, sub_gemm_smem<W>(), s>>>(A, n, p + b0, w, p + b0 + w, rows, p + kb, n2, nullptr);
                 DDQD_LAUNCH_CHECK();
             }
         }
