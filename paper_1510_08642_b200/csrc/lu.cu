@@ -795,18 +795,21 @@ __global__ void __launch_bounds__(kSubDiagNT, 1) lu_subdiag_kernel(double *A, in
     if (__syncthreads_or(bad) && tid == 0) atomicOr(miss, 1);
 }
 
+#ifndef LU_BELOW_TPR
+#define LU_BELOW_TPR 8   // c4: 35.78 ms vs 35.92 with 4 threads per row (4 columns per thread)
+#endif
 template <int W> struct SubBelow {
-    static constexpr int TPR = 4;                  // threads per row
+    static constexpr int TPR = LU_BELOW_TPR;       // threads per row
     static constexpr int NT = 128;                 // 4 warps: one per SM sub-partition
     static constexpr int ROWS = NT / TPR;          // rows per CTA
 };
 
 // B: rows [r0, r0 + rows) x columns [p0, p0 + w): column elimination with the U rows and
 // reciprocals of the sub-panel's diagonal block (U staged in shared memory, the reciprocals
-// from D). Four threads per row, thread t holding columns t + 4c (c < 8) in registers: the
+// from D). TPR threads per row, thread t holding columns t + TPR c in registers: the
 // column loop is unrolled, so at step k a thread only issues the slots that still have
 // columns > k (no idle lanes beyond the partial slot), and the multiplier's source a_ik is one
-// shuffle inside the row's 4-lane group.
+// shuffle inside the row's TPR-lane group.
 template <int W>
 __global__ void __launch_bounds__(SubBelow<W>::NT) lu_subbelow_kernel(double *A, int64_t n, int64_t p0, int w,
                                                                       int pivot, int *miss, int64_t r0,
