@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <string>
 #include <type_traits>
+#include <vector>
 
 #include "common.cuh"
 #include "cp_async.cuh"
@@ -949,6 +950,43 @@ __global__ void __launch_bounds__(128) lu_subgemm_kernel(double *A, int64_t n, i
         }
 }
 
+// Ga (the next sub-panel's 32 rows: a short grid on the pivot chain): 8 x 8 tiles of 64 threads,
+// ONE output per thread, so each thread's 32-step chain is latency- not issue-bound and the
+// grid spreads over ~4x as many SMs as the 32 x 32 tiles (measured 13.5 us per Ga with those).
+template <int W>
+__global__ void __launch_bounds__(64) lu_subgemm_small_kernel(double *A, int64_t n, int64_t p0, int w, int64_t r0,
+                                                              int64_t rows, int64_t c0, int64_t cols,
+                                                              const int *miss) {
+    using E = elem<W>;
+    using T = typename E::T;
+    constexpr int BK = kSubSB, LDL = BK + 1;
+    if (miss && __ldcg(miss)) return;
+    __shared__ double Ls[W * 8 * LDL];
+    __shared__ double Us[W * BK * 8];
+    const int tid = threadIdx.x, tx = tid % 8, ty = tid / 8;
+    const int64_t i0 = r0 + (int64_t)blockIdx.y * 8, j0 = c0 + (int64_t)blockIdx.x * 8;
+    T lt[4], ut[4];
+#pragma unroll
+    for (int it = 0; it < 4; it++) {
+        const int e = tid + 64 * it;   // 256 = 8 rows x 32 k  /  32 k x 8 cols
+        const int r = e / BK, k = e % BK, kk = e / 8, c = e % 8;
+        lt[it] = (i0 + r < r0 + rows && k < w) ? ldA<W>(A, n, i0 + r, p0 + k) : E::zero();
+        ut[it] = (j0 + c < c0 + cols && kk < w) ? ldA<W>(A, n, p0 + kk, j0 + c) : E::zero();
+    }
+    const int64_t i = i0 + ty, j = j0 + tx;
+    const bool ok = i < r0 + rows && j < c0 + cols;
+    T acc = ok ? ldA<W>(A, n, i, j) : E::zero();
+#pragma unroll
+    for (int it = 0; it < 4; it++) {
+        const int e = tid + 64 * it;
+        sts<W>(Ls, 8 * LDL, (e / BK) * LDL + e % BK, lt[it]);
+        sts<W>(Us, BK * 8, e, ut[it]);
+    }
+    __syncthreads();
+    for (int k = 0; k < w; k++) acc = E::sub(acc, E::mul(lds<W>(Ls, 8 * LDL, ty * LDL + k), lds<W>(Us, BK * 8, k * 8 + tx)));
+    if (ok) stA<W>(A, n, i, j, acc);
+}
+
 template <int W> static size_t sub_gemm_smem() { return sizeof(double) * W * (32 * (kSubSB + 1) + kSubSB * 32); }
 
 // dir 0: panel rows [p, n) x columns [p, p + kb) of A -> snapshot; dir 1: after the sub-panels,
@@ -1776,6 +1814,22 @@ static int sub_probe() {   // DDQD_LU_PROBE=1: per-phase clock64 of the sub-pane
     return v;
 }
 
+// DDQD_LU_TIMELINE=p0,p1,...: for those panel starts (columns), record CUDA events around every
+// blocked-panel kernel on its stream and print a start/end timeline (us from the panel's start;
+// a diagnostic: it synchronises after the panel)
+static bool timeline_panel(int64_t p) {
+    static std::string v = [] { const char *e = getenv("DDQD_LU_TIMELINE"); return std::string(e ? e : ""); }();
+    if (v.empty()) return false;
+    size_t a = 0;
+    while (a <= v.size()) {
+        size_t b = v.find(',', a);
+        if (b == std::string::npos) b = v.size();
+        if (b > a && std::atoll(v.substr(a, b - a).c_str()) == (long long)p) return true;
+        a = b + 1;
+    }
+    return false;
+}
+
 // DDQD_LU_SUB_OVERLAP=0 runs every sub-panel kernel on the one stream (A/B measurements)
 static bool sub_overlap_enabled() {
     static int v = -1;
@@ -1847,6 +1901,23 @@ static int try_panel_split(double *A, int64_t n, int64_t p, int64_t kb, int pivo
         }
     }
     const bool two = s2 != s;
+    struct TlRec { const char *nm; int q; bool side; cudaEvent_t e0, e1; };
+    std::vector<TlRec> tlr;
+    const bool tl = timeline_panel(p);
+    cudaEvent_t tl_base = nullptr;
+    if (tl) { cudaEventCreate(&tl_base); cudaEventRecord(tl_base, s); }
+    auto tl0 = [&](cudaStream_t st) -> cudaEvent_t {
+        cudaEvent_t e = nullptr;
+        if (tl) { cudaEventCreate(&e); cudaEventRecord(e, st); }
+        return e;
+    };
+    auto tl1 = [&](const char *nm, int q, cudaStream_t st, cudaEvent_t e0) {
+        if (!tl) return;
+        cudaEvent_t e1;
+        cudaEventCreate(&e1);
+        cudaEventRecord(e1, st);
+        tlr.push_back({nm, q, two && st == s2, e0, e1});
+    };
     if (two) {   // the side stream starts after the snapshot
         DDQD_CUDA_CHECK(cudaEventRecord(evA, s));
         DDQD_CUDA_CHECK(cudaStreamWaitEvent(s2, evA, 0));
@@ -1854,43 +1925,68 @@ static int try_panel_split(double *A, int64_t n, int64_t p, int64_t kb, int pivo
     constexpr int WPB = 4;   // TRSM: 4 columns per CTA (each column is a 32-step chain: spread them)
     // D -> B reciprocals, one [W][SB] slot per sub-panel (after the snapshot in pout)
     double *const rv_base = pout + (size_t)W * (size_t)n * 256;
+    // The pivot chain D_q -> B_q -> Ga_q -> D_{q+1} stays on ONE stream (s2, high priority): a
+    // same-stream hop costs ~2.6 us, a cross-stream one ~5.7 us (DDQD_LU_TIMELINE). The bulk
+    // (T_q, then Gb_q) runs on s; the cross-stream waits are on work that normally finished
+    // already: B_q waits for Gb_{q-1} (its rows), Ga_q for T_q (its U rows), T_q for D_q, Gb_q
+    // for B_q.
+    cudaEvent_t evB = evT;   // (the three events: evA = Gb done, evD = D done, evT = T done; evB below)
+    static thread_local cudaEvent_t evBs[64];
+    if (two) {
+        if (!evBs[dv]) DDQD_CUDA_CHECK(cudaEventCreateWithFlags(&evBs[dv], cudaEventDisableTiming));
+        evB = evBs[dv];
+    }
+    bool gb_pending = false;   // evA holds a Gb of an earlier sub-panel
     for (int q0 = 0; q0 < kbi; q0 += SB) {
         const int w = std::min(SB, kbi - q0);
         const int64_t p0 = p + q0;
         const int64_t rows = n - (p0 + w);            // rows below the diagonal block
         const int64_t cols = p + kb - (p0 + w);       // columns right of it (inside the panel)
         double *const rvb = rv_base + (size_t)(q0 / SB) * W * SB;
-        // (dynamic shared memory it does not use: the SM is D's alone, no update CTA shares its
-        // FP64 pipe -- measured 36.6k vs 47.5k cycles per D beside the concurrent update)
+        cudaEvent_t t0 = tl0(s2);
         lu_subdiag_kernel<W><<<1, kSubDiagNT, kSubDiagPad, s2>>>(A, n, p0, w, pivot, miss, rvb, sub_probe());
         DDQD_LAUNCH_CHECK();
-        if (two) DDQD_CUDA_CHECK(cudaEventRecord(evD, s2));
+        tl1("D", q0 / SB, s2, t0);
         if (cols > 0) {
-            lu_trsm_warp_kernel<W, 1, WPB><<<(unsigned)((cols + WPB - 1) / WPB), WPB * 32, tsm, s2>>>(A, n, p0, w, p0 + w,
-                                                                                                    cols);
+            if (two) {
+                DDQD_CUDA_CHECK(cudaEventRecord(evD, s2));
+                DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, evD, 0));
+            }
+            t0 = tl0(s);
+            lu_trsm_warp_kernel<W, 1, WPB><<<(unsigned)((cols + WPB - 1) / WPB), WPB * 32, tsm, s>>>(A, n, p0, w, p0 + w,
+                                                                                                   cols);
             DDQD_LAUNCH_CHECK();
-            if (two) DDQD_CUDA_CHECK(cudaEventRecord(evT, s2));
+            tl1("T", q0 / SB, s, t0);
+            if (two) DDQD_CUDA_CHECK(cudaEventRecord(evT, s));
         }
-        if (two) DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, evD, 0));
         if (rows > 0) {
+            if (two && gb_pending) DDQD_CUDA_CHECK(cudaStreamWaitEvent(s2, evA, 0));
+            t0 = tl0(s2);
             lu_subbelow_kernel<W><<<(unsigned)((rows + SubBelow<W>::ROWS - 1) / SubBelow<W>::ROWS), SubBelow<W>::NT, 0,
-                                    s>>>(A, n, p0, w, pivot, miss, p0 + w, rows, rvb, sub_probe());
+                                    s2>>>(A, n, p0, w, pivot, miss, p0 + w, rows, rvb, sub_probe());
             DDQD_LAUNCH_CHECK();
+            tl1("B", q0 / SB, s2, t0);
         }
         if (cols > 0 && rows > 0) {
-            if (two) DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, evT, 0));
-            const int64_t ra = std::min<int64_t>(rows, SB);   // Ga: the next sub-panel's rows
-            dim3 ga((unsigned)((cols + 31) / 32), (unsigned)((ra + 31) / 32));
-            lu_subgemm_kernel<W><<<ga, 128, gsm, s>>>(A, n, p0, w, p0 + w, ra, p0 + w, cols, miss);
-            DDQD_LAUNCH_CHECK();
             if (two) {
-                DDQD_CUDA_CHECK(cudaEventRecord(evA, s));
-                DDQD_CUDA_CHECK(cudaStreamWaitEvent(s2, evA, 0));
+                DDQD_CUDA_CHECK(cudaEventRecord(evB, s2));
+                DDQD_CUDA_CHECK(cudaStreamWaitEvent(s2, evT, 0));
             }
+            const int64_t ra = std::min<int64_t>(rows, SB);   // Ga: the next sub-panel's rows
+            dim3 ga((unsigned)((cols + 7) / 8), (unsigned)((ra + 7) / 8));
+            t0 = tl0(s2);
+            lu_subgemm_small_kernel<W><<<ga, 64, 0, s2>>>(A, n, p0, w, p0 + w, ra, p0 + w, cols, miss);
+            DDQD_LAUNCH_CHECK();
+            tl1("Ga", q0 / SB, s2, t0);
             if (rows > ra) {
+                if (two) DDQD_CUDA_CHECK(cudaStreamWaitEvent(s, evB, 0));
                 dim3 gb((unsigned)((cols + 31) / 32), (unsigned)((rows - ra + 31) / 32));
+                t0 = tl0(s);
                 lu_subgemm_kernel<W><<<gb, 128, gsm, s>>>(A, n, p0, w, p0 + w + ra, rows - ra, p0 + w, cols, miss);
                 DDQD_LAUNCH_CHECK();
+                tl1("Gb", q0 / SB, s, t0);
+                if (two) DDQD_CUDA_CHECK(cudaEventRecord(evA, s));
+                gb_pending = true;
             }
         }
     }
@@ -1900,6 +1996,19 @@ static int try_panel_split(double *A, int64_t n, int64_t p, int64_t kb, int pivo
     }
     lu_snap_kernel<<<cgrid, 256, 0, s>>>(A, W, n, p, kbi, pout, ipiv, miss, 1);
     DDQD_LAUNCH_CHECK();
+    if (tl) {
+        cudaStreamSynchronize(s);
+        for (const TlRec &r : tlr) {
+            float a = 0.f, b = 0.f;
+            cudaEventElapsedTime(&a, tl_base, r.e0);
+            cudaEventElapsedTime(&b, tl_base, r.e1);
+            printf("LUTIMELINE p=%lld q=%d kernel=%s stream=%s start_us=%.2f end_us=%.2f\n", (long long)p, r.q, r.nm,
+                   r.side ? "side" : "main", a * 1e3f, b * 1e3f);
+            cudaEventDestroy(r.e0);
+            cudaEventDestroy(r.e1);
+        }
+        cudaEventDestroy(tl_base);
+    }
     // the fallback (full pivot search from the restored panel) runs only on a miss; then the
     // interchanges of the other columns, as after the cooperative kernel
     if (!try_panel_coop<W>(A, n, p, kb, pivot, ipiv, aux, scr, scr_bytes, s, rc, pre_swap, miss)) {
