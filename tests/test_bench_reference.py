@@ -33,6 +33,20 @@ def test_reference_arm_custom_workload():
     assert d["config"]["algo"] == "strassen" and d["value"] > 0
 
 
+def test_reference_arm_under_torchrun_two_ranks():
+    """The driver launches the reference arm like ours (torchrun, one rank per GPU): rank 0
+    alone runs the oracle sample and prints the one line; the other rank exits 0 without work."""
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29547", os.path.join(ROOT, "bench.py"),
+                        "--impl", "reference", "--workload", "c1", "--gpus", "2", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, cwd=ROOT, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["config"]["m"] == 1024
+
+
 import pytest  # noqa: E402
 
 

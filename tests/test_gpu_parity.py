@@ -1376,3 +1376,20 @@ def test_lu_split_panel_bitwise(orc, tmp_path):
     assert same(v[k:k + LU_ref.size], LU_ref.ravel()); k += LU_ref.size
     assert same(v[k:k + x_ref.size], x_ref.ravel()); k += x_ref.size
     assert np.array_equal(v[k:k + 600], piv_ref.astype(np.float64))
+
+
+@pytest.mark.parametrize("W,n,K", [(2, 1000, 128), (4, 800, 256), (2, 1280, 256)])
+def test_lu_backward_lookahead_bitwise(orc, W, n, K):
+    """The backward solve's look-ahead (block J's columns folded into the next diagonal block's
+    rows on the caller's stream, into the rows above on a side stream; DDQD_LU_BWD_OVERLAP) on
+    several 256-row blocks: a ragged bottom block (n = 1000: 232 rows, the per-element path),
+    a 32-row bottom block (QD n = 800), whole blocks (n = 1280); non-dominant random matrices
+    so the rows are interchanged. Bit-exact vs the oracle's factors and solution."""
+    A = gen.matrix(W, n, n, 41 + n, 0)
+    b = gen.matrix(W, 1, n, 42 + n, 1)[:, 0, :].copy()
+    x_ref, LU_ref, piv_ref, info_ref = orc.solve(A, b, panel=K, algo="strassen", threshold=64)
+    x, LU, piv, info = ddqd.lu_solve(cu(A), cu(b), panel=K, algo="strassen", threshold=64)
+    assert info == info_ref == 0
+    assert np.any(piv_ref != np.arange(n))
+    assert np.array_equal(np_(piv), piv_ref)
+    assert same(np_(LU), LU_ref) and same(np_(x), x_ref)
