@@ -1482,6 +1482,7 @@ __global__ void __launch_bounds__(288) trsv_diag_blk(const double *A, int64_t n,
     using T = typename E::T;
     constexpr int PL = W == 2 ? 32 : 8;   // multipliers preloaded per chunk (registers)
     __shared__ double ys[W * 256];   // the block's y (forward) / x (backward) values
+    extern __shared__ double dyn_smem[];   // DD: 8 warps x [W][32][33] multiplier tiles
     const int tid = threadIdx.x, lane = tid & 31, wrp = tid >> 5;
     if (tid < nb) sts<W>(ys, 256, tid, ldv<W>(y, n, J + tid));
     const int nsb = nb / 32;
@@ -1498,15 +1499,32 @@ __global__ void __launch_bounds__(288) trsv_diag_blk(const double *A, int64_t n,
 #pragma unroll
             for (int i = 0; i < 32; i++) l[i] = ldA<W>(A, n, J + 32 * sb + lane, J + 32 * sb + i);
         };
+        // A row-owning warp's 32 rows x 32 multipliers, read coalesced (lane = column: one
+        // 256-byte row segment per load instead of 32 rows' sectors per load, which kept the
+        // LSU busy ~16k cycles per sub-block) and transposed through a padded per-warp tile.
+        // The warps are row-uniform (nb % 32 == 0), so whole warps own rows or none.
+        double *tile = dyn_smem + wrp * (W * 32 * 33);
+        auto rows_load = [&](int b0) {
+#pragma unroll 8
+            for (int q = 0; q < 32; q++) {
+                const int64_t g = (J + 32 * wrp + q) * n + (J + b0 + lane);
+#pragma unroll
+                for (int w = 0; w < W; w++) tile[w * 32 * 33 + q * 33 + lane] = A[g + (int64_t)w * n * n];
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+#pragma unroll
+                for (int w = 0; w < W; w++) E::set_word(l[i], w, tile[w * 32 * 33 + lane * 33 + i]);
+            }
+            __syncwarp();
+        };
         if (solver) tri_load(FWD ? 0 : nsb - 1);
         for (int k = 0; k < nsb; k++) {
             const int sb = FWD ? k : nsb - 1 - k;
             const int b0 = 32 * sb;
-            if (mine(b0)) {
-#pragma unroll
-                for (int i = 0; i < 32; i++) l[i] = ldA<W>(A, n, J + tid, J + b0 + i);
-            }
             __syncthreads();   // ys of the previous sub-block complete
+            if (!solver && mine(b0)) rows_load(b0);   // alongside the triangle (a barrier-free phase)
             if (solver) {
                 T v = lds<W>(ys, 256, b0 + lane);
 #pragma unroll
@@ -2149,10 +2167,18 @@ static bool trsv_fast_enabled() {
 
 // shared-memory sizes / attributes of the solve kernels (set once per device)
 template <int W>
+static size_t trsv_diag_smem() { return W == 2 ? sizeof(double) * 8 * W * 32 * 33 : 0; }
+template <int W>
 static int trsv_setup(size_t *usm_out) {
     const size_t usm = sizeof(double) * W * (256 + 2 * (size_t)TuCc<W>::v * TU_LD);
     static bool tattr[64] = {};
     if (trsv_fast_enabled() && !tattr[current_device()]) {
+        if (W == 2) {
+            DDQD_CUDA_CHECK(cudaFuncSetAttribute(trsv_diag_blk<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)trsv_diag_smem<W>()));
+            DDQD_CUDA_CHECK(cudaFuncSetAttribute(trsv_diag_blk<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)trsv_diag_smem<W>()));
+        }
         DDQD_CUDA_CHECK(cudaFuncSetAttribute(trsv_update_co<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
         DDQD_CUDA_CHECK(cudaFuncSetAttribute(trsv_update_co<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
         tattr[current_device()] = true;
@@ -2166,7 +2192,7 @@ template <int W>
 static int trsv_fwd_block(int64_t n, const double *A, double *y, int64_t J, int nb, size_t usm, cudaStream_t s) {
     const int64_t rows = n - J - nb;
     if (trsv_fast_enabled() && nb % 32 == 0) {
-        trsv_diag_blk<W, true><<<1, W == 2 ? 288 : 256, 0, s>>>(A, n, y, nullptr, J, nb);
+        trsv_diag_blk<W, true><<<1, W == 2 ? 288 : 256, trsv_diag_smem<W>(), s>>>(A, n, y, nullptr, J, nb);
         DDQD_LAUNCH_CHECK();
         if (rows > 0) {
             trsv_update_co<W, true><<<(unsigned)((rows + TU_ROWS - 1) / TU_ROWS), TU_ROWS, usm, s>>>(A, n, y, nullptr, J, nb);
@@ -2192,7 +2218,7 @@ static int trsv_bwd_all(int64_t n, const double *A, double *y, double *x, size_t
     for (int64_t J = last; J >= 0; J -= NB) {
         const int nb = (int)std::min<int64_t>(NB, n - J);
         if (fast && nb % 32 == 0) {
-            trsv_diag_blk<W, false><<<1, W == 2 ? 288 : 256, 0, s>>>(A, n, y, x, J, nb);
+            trsv_diag_blk<W, false><<<1, W == 2 ? 288 : 256, trsv_diag_smem<W>(), s>>>(A, n, y, x, J, nb);
             DDQD_LAUNCH_CHECK();
             if (J > 0) {
                 trsv_update_co<W, false><<<(unsigned)((J + TU_ROWS - 1) / TU_ROWS), TU_ROWS, usm, s>>>(A, n, y, x, J, nb);
